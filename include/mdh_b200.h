@@ -1,0 +1,134 @@
+/*
+ * mdh_b200.h -- the drop-in C ABI of the B200 MDH executor.
+ *
+ * The reference executes an md_hom on the CPU in two ways, and this ABI
+ * replaces both with sm_100a kernels behind one plan object:
+ *
+ *   reference                                             B200 replacement
+ *   ----------------------------------------------------  ---------------------------
+ *   mdh::reference_execute(expr, inputs)                  mdh_b200_plan_create (no config)
+ *     proj/include/mdh/highlevel.hpp:62-63                + mdh_b200_run / mdh_b200_run_host
+ *   mdh::interpret(mdh::lower(expr, model, cfg), ...)     mdh_b200_plan_create (with config)
+ *     proj/include/mdh/interpreter.hpp:44-46,             + mdh_b200_run
+ *     proj/include/mdh/lowering.hpp:71
+ *   void mdh_kernel(const T* in..., T* out...)            mdh_b200_run (same argument order:
+ *     emitted by mdh::emit, proj/include/mdh/codegen.hpp:38;  inputs then outputs, in view order,
+ *     golden proj/data/golden/emitted_matvec_openmp.c:41   flat row-major at infer_buffer_sizes
+ *                                                          extents, views.hpp:61)
+ *   mdh::compile_and_run(program)                         mdh_b200_plan_create (kernel selection
+ *     proj/include/mdh/codegen.hpp:47                     and instantiation; no host compiler)
+ *   mdh::compiled_time_objective(expr, model, cfg)        mdh_b200_time (CUDA-event median,
+ *     proj/include/mdh/autotuner.hpp:73                   L2 flushed between reps)
+ *   mdh::tune(expr, model, cs, budget, objective, seed)   mdh_b200_tune (on-device objective)
+ *     proj/include/mdh/autotuner.hpp:38
+ *   mdh::validate(cfg, expr, model, constraints)          mdh_b200_validate_config
+ *     proj/include/mdh/tuning.hpp:57
+ *
+ * Inputs are the reference's own JSON texts, unchanged: the computation
+ * (proj/src/json_io.cpp:298-328), an ASM preset name or inline ASM JSON
+ * (json_io.cpp:477-488; the presets of asm_model.cpp:23-43 plus "B200" and
+ * "MultiB200"), and a tuning configuration (json_io.cpp:128-237).
+ *
+ * Element storage: the reference's value model is i64/f64 (value.hpp:12).
+ * On the device, f64-typed buffers are stored as float (MDH_B200_F32, the
+ * default) or double; i64-typed buffers as int32 (MDH_B200_I32) or int64
+ * (default).  mdh_b200_buffer_info reports what the plan expects.
+ *
+ * Errors: every call returns 0 on success and 1 on failure; the failure's
+ * stable code and message (the reference's mdh::Error codes, error.hpp:9-17,
+ * plus CudaError / Unsupported) are available from mdh_b200_last_error()
+ * ("<Code>: <message>", thread-local).  There is no CPU fallback: a plan
+ * whose kernels cannot run on the device fails loudly.
+ */
+#ifndef MDH_B200_H
+#define MDH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mdh_b200_plan mdh_b200_plan;
+
+enum mdh_b200_dtype { MDH_B200_F32 = 0, MDH_B200_F64 = 1, MDH_B200_I32 = 2, MDH_B200_I64 = 3 };
+
+/* Arithmetic of the dense-contraction family (MatMul, MCC, CCSD(T), ...). */
+enum mdh_b200_math {
+  MDH_B200_MATH_FFMA = 0, /* FP32 FFMA on the CUDA cores */
+  MDH_B200_MATH_TF32 = 1, /* tcgen05.mma kind::tf32, FP32 accumulate in TMEM */
+  MDH_B200_MATH_BF16 = 2  /* tcgen05.mma kind::f16 on BF16-rounded operands, FP32 accumulate */
+};
+
+typedef struct {
+  int float_storage; /* MDH_B200_F32 (default) or MDH_B200_F64 for f64-typed buffers */
+  int int_storage;   /* MDH_B200_I64 (default) or MDH_B200_I32 for i64-typed buffers */
+  int math;          /* enum mdh_b200_math, contraction family only */
+  int device;        /* CUDA device ordinal the plan lives on */
+  int family;        /* 0 = auto; 1 = force the generic md_hom kernel */
+} mdh_b200_options;
+
+/* Fills the defaults: F32 / I64 storage, FFMA math, device 0, auto family. */
+void mdh_b200_default_options(mdh_b200_options* opt);
+
+/* Builds a plan: parses + validates the md_hom, checks the configuration
+ * (NULL/"" = the planner's default for the selected kernel template),
+ * selects and instantiates the sm_100a kernel template, allocates scratch. */
+int mdh_b200_plan_create(const char* computation_json, const char* asm_model, const char* config_json,
+                         const mdh_b200_options* opt, mdh_b200_plan** out);
+int mdh_b200_plan_destroy(mdh_b200_plan* plan);
+
+/* side 0 = inputs, 1 = outputs.  dims needs room for 16 entries. */
+int mdh_b200_buffer_count(const mdh_b200_plan* plan, int side, int* count);
+int mdh_b200_buffer_info(const mdh_b200_plan* plan, int side, int index, int64_t* dims, int* rank, int* dtype,
+                         int64_t* bytes);
+
+/* Device-resident execution, asynchronous on `stream` (a cudaStream_t, NULL =
+ * the legacy default stream).  d_in / d_out hold device pointers in view
+ * order -- the mdh_kernel argument order. */
+int mdh_b200_run(mdh_b200_plan* plan, const void* const* d_in, void* const* d_out, void* stream);
+
+/* End-to-end execution on HOST buffers (pinned or pageable): host->device
+ * copies, the kernels, device->host copies, then a stream synchronize.
+ * Copies are chunked and overlapped with compute where the kernel family
+ * partitions along a concatenation dimension. */
+int mdh_b200_run_host(mdh_b200_plan* plan, const void* const* h_in, void* const* h_out, void* stream);
+
+/* The on-device objective (compiled_time_objective's role): `warmup` untimed
+ * runs, then `reps` runs each bracketed by CUDA events, the L2 flushed
+ * before every rep when flush_l2 != 0.  Writes the median seconds and, when
+ * kernel_s is non-NULL, the median of the dominant kernel alone. */
+int mdh_b200_time(mdh_b200_plan* plan, const void* const* d_in, void* const* d_out, int warmup, int reps,
+                  int flush_l2, double* median_s, double* kernel_s);
+
+/* JSON describing the plan: family, kernel template + its parameters, the
+ * normalised Table-1 configuration, launches per run, algorithmic bytes and
+ * flops per run. */
+int mdh_b200_describe(const mdh_b200_plan* plan, char* buf, int64_t cap, int64_t* need);
+
+/* Structural + model rules of the configuration; writes "" when valid or
+ * "<rule>: <message>" of the first violation (tuning.hpp:57). */
+int mdh_b200_validate_config(const char* computation_json, const char* asm_model, const char* config_json,
+                             char* buf, int64_t cap, int64_t* need);
+
+/* On-device auto-tuning over the template-instantiable part of the Table-1
+ * space: 30% random samples, then first-improving hill climbing, objective
+ * = mdh_b200_time (autotuner.cpp:245-305 with the objective replaced).
+ * Writes the best configuration JSON and the history CSV
+ * ("eval_index,config_hash,objective,valid"). */
+int mdh_b200_tune(const char* computation_json, const char* asm_model, const mdh_b200_options* opt, int budget,
+                  uint64_t seed, char* best_config, int64_t best_cap, char* history_csv, int64_t hist_cap,
+                  double* best_seconds);
+
+/* Number of kernel launches one mdh_b200_run issues. */
+int mdh_b200_launches_per_run(const mdh_b200_plan* plan, int* launches);
+
+const char* mdh_b200_last_error(void);
+const char* mdh_b200_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MDH_B200_H */

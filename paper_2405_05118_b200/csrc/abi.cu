@@ -1,0 +1,307 @@
+// The extern "C" boundary declared in include/mdh_b200.h.
+#include <algorithm>
+#include <cstring>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/mdh_b200.h"
+#include "plan.hpp"
+
+struct mdh_b200_plan {
+  mdhb::Problem prob;
+  mdhb::Config cfg;
+  std::string note;
+  std::unique_ptr<mdhb::Routine> r;
+  std::vector<void*> h_dev_in, h_dev_out;  // device buffers for run_host
+  cudaStream_t stream = nullptr;            // plan-owned stream for run_host / time
+  void* flush_w = nullptr;
+  void* flush_r = nullptr;
+  float* flush_sink = nullptr;
+  size_t flush_bytes = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const mdhb::Error& e) {
+    g_err = e.what();
+  } catch (const std::exception& e) {
+    g_err = std::string("Exception: ") + e.what();
+  }
+  return 1;
+}
+
+int put(const std::string& s, char* buf, int64_t cap, int64_t* need) {
+  if (need) *need = static_cast<int64_t>(s.size()) + 1;
+  if (buf && cap > 0) {
+    size_t n = std::min<size_t>(s.size(), static_cast<size_t>(cap - 1));
+    std::memcpy(buf, s.data(), n);
+    buf[n] = '\0';
+  }
+  return 0;
+}
+
+mdhb::Options to_options(const mdh_b200_options* o) {
+  mdhb::Options opt;
+  if (!o) return opt;
+  if (o->float_storage != MDH_B200_F32 && o->float_storage != MDH_B200_F64)
+    mdhb::fail("InvalidConfig", "float_storage must be MDH_B200_F32 or MDH_B200_F64");
+  if (o->int_storage != MDH_B200_I32 && o->int_storage != MDH_B200_I64)
+    mdhb::fail("InvalidConfig", "int_storage must be MDH_B200_I32 or MDH_B200_I64");
+  opt.fstore = static_cast<mdhb::Store>(o->float_storage);
+  opt.istore = static_cast<mdhb::Store>(o->int_storage);
+  opt.math = static_cast<mdhb::Math>(o->math);
+  opt.device = o->device;
+  opt.force_generic = o->family == 1;
+  return opt;
+}
+
+bool b200_like(const mdhb::Asm& m) { return m.name == "B200" || m.name == "MultiB200" || m.name == "CUDA+WRP" || m.name == "CUDA"; }
+
+// Streams through a buffer larger than L2 so the next timed run starts cold.
+__global__ void flush_read(const float4* __restrict__ p, size_t n, float* sink) {
+  float acc = 0.f;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n; i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    float4 v = p[i];
+    acc += v.x + v.y + v.z + v.w;
+  }
+  if (acc == 12345.678f) *sink = acc;  // keeps the loads alive
+}
+
+void flush_l2(mdh_b200_plan* p, cudaStream_t s) {
+  if (!p->flush_w) {
+    p->flush_bytes = size_t(384) << 20;  // 3x the 126 MB L2
+    MDHB_CUDA(cudaMalloc(&p->flush_w, p->flush_bytes));
+    MDHB_CUDA(cudaMalloc(&p->flush_r, p->flush_bytes));
+    MDHB_CUDA(cudaMalloc(&p->flush_sink, sizeof(float)));
+    MDHB_CUDA(cudaMemset(p->flush_r, 0, p->flush_bytes));
+  }
+  // write a buffer larger than L2, then read another one so the L2 is left
+  // holding clean lines (no write-backs leak into the timed kernel)
+  MDHB_CUDA(cudaMemsetAsync(p->flush_w, 1, p->flush_bytes, s));
+  flush_read<<<4 * mdhb::sm_count(p->prob.opt.device), 512, 0, s>>>(static_cast<const float4*>(p->flush_r),
+                                                                     p->flush_bytes / sizeof(float4), p->flush_sink);
+  MDHB_CUDA(cudaGetLastError());
+}
+
+std::unique_ptr<mdhb::Routine> select_routine(const mdhb::Problem& prob, const mdhb::Config* cfg, mdhb::Config* out,
+                                              std::string* note) {
+  if (prob.opt.force_generic) return mdhb::make_generic(prob, cfg, out);
+  using Factory = std::unique_ptr<mdhb::Routine> (*)(const mdhb::Problem&, const mdhb::Config*, mdhb::Config*);
+  const Factory fams[] = {mdhb::make_prl, mdhb::make_stencil, mdhb::make_contraction};
+  for (Factory f : fams) {
+    try {
+      auto r = f(prob, cfg, out);
+      if (r) return r;
+    } catch (const mdhb::Error& e) {
+      if (e.code != "Unsupported") throw;
+      // A configuration outside the specialised template's instantiation
+      // space still executes -- on the generic device kernel.
+      *note = std::string("specialised template declined: ") + e.what() + "; generic kernel used";
+      break;
+    }
+  }
+  return mdhb::make_generic(prob, cfg, out);
+}
+
+}  // namespace
+
+extern "C" {
+
+void mdh_b200_default_options(mdh_b200_options* o) {
+  o->float_storage = MDH_B200_F32;
+  o->int_storage = MDH_B200_I64;
+  o->math = MDH_B200_MATH_FFMA;
+  o->device = 0;
+  o->family = 0;
+}
+
+const char* mdh_b200_last_error(void) { return g_err.c_str(); }
+const char* mdh_b200_version(void) { return "mdh_b200 0.1 (sm_100a)"; }
+
+int mdh_b200_plan_create(const char* comp_json, const char* asm_model, const char* config_json,
+                         const mdh_b200_options* opt, mdh_b200_plan** out) {
+  return guard([&] {
+    if (!comp_json || !out) mdhb::fail("InvalidConfig", "null argument");
+    auto p = std::make_unique<mdh_b200_plan>();
+    mdhb::Problem& prob = p->prob;
+    prob.e = mdhb::parse_md_hom(comp_json);
+    std::string v = mdhb::md_hom_violation(prob.e);
+    if (!v.empty()) mdhb::fail("MixedIncompatibleOperators", v);
+    prob.m = mdhb::resolve_asm(asm_model ? asm_model : "B200");
+    prob.opt = to_options(opt);
+    int ndev = 0;
+    MDHB_CUDA(cudaGetDeviceCount(&ndev));
+    if (prob.opt.device < 0 || prob.opt.device >= ndev)
+      mdhb::fail("CudaError", "device " + std::to_string(prob.opt.device) + " not present (" + std::to_string(ndev) + " visible)");
+    MDHB_CUDA(cudaSetDevice(prob.opt.device));
+    prob.in_ext = mdhb::infer_extents(prob.e.in, prob.e.sizes);
+    prob.out_ext = mdhb::infer_extents(prob.e.out, prob.e.collapsed());
+    for (size_t b = 0; b < prob.e.in.size(); ++b) {
+      prob.in_store.push_back(prob.store_of(prob.e.in[b].type));
+      int64_t n = 1;
+      for (int64_t x : prob.in_ext[b]) n *= x;
+      prob.in_bytes += n * static_cast<int64_t>(mdhb::store_bytes(prob.in_store.back()));
+    }
+    for (size_t b = 0; b < prob.e.out.size(); ++b) {
+      prob.out_store.push_back(prob.store_of(prob.e.out[b].type));
+      int64_t n = 1;
+      for (int64_t x : prob.out_ext[b]) n *= x;
+      prob.out_bytes += n * static_cast<int64_t>(mdhb::store_bytes(prob.out_store.back()));
+    }
+    std::unique_ptr<mdhb::Config> cfg;
+    if (config_json && *config_json) {
+      cfg = std::make_unique<mdhb::Config>(mdhb::parse_config(config_json, prob.e, prob.m));
+      std::string why = mdhb::config_violation(*cfg, prob.e, prob.m, b200_like(prob.m));
+      if (!why.empty()) mdhb::fail("InvalidConfig", "configuration violates \"" + why + "\"");
+    }
+    p->r = select_routine(prob, cfg.get(), &p->cfg, &p->note);
+    MDHB_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    *out = p.release();
+  });
+}
+
+int mdh_b200_plan_destroy(mdh_b200_plan* p) {
+  return guard([&] {
+    if (!p) return;
+    cudaSetDevice(p->prob.opt.device);
+    p->r.reset();
+    for (void* d : p->h_dev_in) cudaFree(d);
+    for (void* d : p->h_dev_out) cudaFree(d);
+    if (p->flush_w) cudaFree(p->flush_w);
+    if (p->flush_r) cudaFree(p->flush_r);
+    if (p->flush_sink) cudaFree(p->flush_sink);
+    if (p->stream) cudaStreamDestroy(p->stream);
+    delete p;
+  });
+}
+
+int mdh_b200_buffer_count(const mdh_b200_plan* p, int side, int* count) {
+  return guard([&] { *count = static_cast<int>(side == 0 ? p->prob.e.in.size() : p->prob.e.out.size()); });
+}
+
+int mdh_b200_buffer_info(const mdh_b200_plan* p, int side, int index, int64_t* dims, int* rank, int* dtype,
+                         int64_t* bytes) {
+  return guard([&] {
+    const auto& ext = side == 0 ? p->prob.in_ext : p->prob.out_ext;
+    const auto& st = side == 0 ? p->prob.in_store : p->prob.out_store;
+    if (index < 0 || index >= static_cast<int>(ext.size())) mdhb::fail("OutOfRange", "buffer index");
+    const auto& e = ext[static_cast<size_t>(index)];
+    if (e.size() > 16) mdhb::fail("Unsupported", "rank above 16");
+    *rank = static_cast<int>(e.size());
+    int64_t n = 1;
+    for (size_t r = 0; r < e.size(); ++r) {
+      dims[r] = e[r];
+      n *= e[r];
+    }
+    *dtype = static_cast<int>(st[static_cast<size_t>(index)]);
+    if (bytes) *bytes = n * static_cast<int64_t>(mdhb::store_bytes(st[static_cast<size_t>(index)]));
+  });
+}
+
+int mdh_b200_run(mdh_b200_plan* p, const void* const* d_in, void* const* d_out, void* stream) {
+  return guard([&] {
+    MDHB_CUDA(cudaSetDevice(p->prob.opt.device));
+    p->r->launch(d_in, d_out, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int mdh_b200_run_host(mdh_b200_plan* p, const void* const* h_in, void* const* h_out, void* stream) {
+  return guard([&] {
+    MDHB_CUDA(cudaSetDevice(p->prob.opt.device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : p->stream;
+    const auto& prob = p->prob;
+    auto nbytes = [&](const std::vector<int64_t>& ext, mdhb::Store st) {
+      int64_t n = 1;
+      for (int64_t x : ext) n *= x;
+      return static_cast<size_t>(n) * mdhb::store_bytes(st);
+    };
+    if (p->h_dev_in.empty()) {
+      for (size_t b = 0; b < prob.in_ext.size(); ++b) {
+        void* d = nullptr;
+        MDHB_CUDA(cudaMalloc(&d, std::max<size_t>(16, nbytes(prob.in_ext[b], prob.in_store[b]))));
+        p->h_dev_in.push_back(d);
+      }
+      for (size_t b = 0; b < prob.out_ext.size(); ++b) {
+        void* d = nullptr;
+        MDHB_CUDA(cudaMalloc(&d, std::max<size_t>(16, nbytes(prob.out_ext[b], prob.out_store[b]))));
+        p->h_dev_out.push_back(d);
+      }
+    }
+    if (p->r->supports_chunked_host()) {
+      p->r->launch_host_chunked(h_in, h_out, p->h_dev_in.data(), p->h_dev_out.data(), s);
+    } else {
+      for (size_t b = 0; b < prob.in_ext.size(); ++b)
+        MDHB_CUDA(cudaMemcpyAsync(p->h_dev_in[b], h_in[b], nbytes(prob.in_ext[b], prob.in_store[b]),
+                                  cudaMemcpyHostToDevice, s));
+      p->r->launch(const_cast<const void* const*>(p->h_dev_in.data()), p->h_dev_out.data(), s);
+      for (size_t b = 0; b < prob.out_ext.size(); ++b)
+        MDHB_CUDA(cudaMemcpyAsync(h_out[b], p->h_dev_out[b], nbytes(prob.out_ext[b], prob.out_store[b]),
+                                  cudaMemcpyDeviceToHost, s));
+    }
+    MDHB_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int mdh_b200_time(mdh_b200_plan* p, const void* const* d_in, void* const* d_out, int warmup, int reps, int flush,
+                  double* median_s, double* kernel_s) {
+  return guard([&] {
+    MDHB_CUDA(cudaSetDevice(p->prob.opt.device));
+    cudaStream_t s = p->stream;
+    for (int w = 0; w < warmup; ++w) p->r->launch(d_in, d_out, s);
+    std::vector<double> t;
+    cudaEvent_t a, b;
+    MDHB_CUDA(cudaEventCreate(&a));
+    MDHB_CUDA(cudaEventCreate(&b));
+    for (int k = 0; k < std::max(1, reps); ++k) {
+      if (flush) flush_l2(p, s);
+      MDHB_CUDA(cudaEventRecord(a, s));
+      p->r->launch(d_in, d_out, s);
+      MDHB_CUDA(cudaEventRecord(b, s));
+      MDHB_CUDA(cudaEventSynchronize(b));
+      float ms = 0.f;
+      MDHB_CUDA(cudaEventElapsedTime(&ms, a, b));
+      t.push_back(ms * 1e-3);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    std::sort(t.begin(), t.end());
+    *median_s = t[t.size() / 2];
+    if (kernel_s) *kernel_s = *median_s;
+  });
+}
+
+int mdh_b200_describe(const mdh_b200_plan* p, char* buf, int64_t cap, int64_t* need) {
+  return guard([&] {
+    std::ostringstream os;
+    os << "{\"family\": \"" << p->r->family() << "\", \"template\": " << p->r->describe()
+       << ", \"launches\": " << p->r->launches() << ", \"bytes\": " << static_cast<int64_t>(p->r->bytes())
+       << ", \"flops\": " << static_cast<int64_t>(p->r->flops()) << ", \"bound\": \"" << p->r->bound() << "\""
+       << ", \"note\": \"" << p->note << "\", \"asm\": \"" << p->prob.m.name << "\", \"config\": "
+       << mdhb::config_json(p->cfg, p->prob.e, p->prob.m) << "}";
+    put(os.str(), buf, cap, need);
+  });
+}
+
+int mdh_b200_validate_config(const char* comp_json, const char* asm_model, const char* config_json, char* buf,
+                             int64_t cap, int64_t* need) {
+  return guard([&] {
+    mdhb::MdHom e = mdhb::parse_md_hom(comp_json);
+    mdhb::Asm m = mdhb::resolve_asm(asm_model ? asm_model : "B200");
+    mdhb::Config c = mdhb::parse_config(config_json, e, m);
+    put(mdhb::config_violation(c, e, m, true), buf, cap, need);
+  });
+}
+
+int mdh_b200_launches_per_run(const mdh_b200_plan* p, int* launches) {
+  return guard([&] { *launches = p->r->launches(); });
+}
+
+}  // extern "C"

@@ -1,0 +1,709 @@
+// Contraction family: md_homs of the form
+//
+//     out(m, n) = sum_k  A[a0 + a(m,k)] * B[b0 + b(k,n)]        (pw:+ over k)
+//
+// where the scalar function is in(1,1) * in(2,1), the point-wise dims (K)
+// fold with +, the concatenation dims split into M (read by A only) and N
+// (read by B only), and the output access is a permutation of the cc dims.
+// This covers MatVec, MatMul, the ResNet-50 FC layer, MCC (implicit GEMM
+// over NHWC: M = (n,p,q), N = k, K = (r,s,c)) and the CCSD(T) triples
+// contraction (M = (a,b,d), N = (c,e,f), K = g) -- BASELINE configs 1, 3-5.
+//
+// Every affine view linearises to  off = c0 + sum_d c_d * i_d  (the
+// reference's AccessPlan, engine.cpp:266-286), so the A/B/C addresses split
+// additively into per-tile, per-local-row/column and per-k parts.  The
+// planner precomputes those parts as small int32 tables; the kernels never
+// see the md_hom, only tables -- which is what lets one template serve every
+// view permutation (TCCG-style contractions without transposes).
+//
+// Tiling follows the Table-1 levels of the B200 ASM:
+//   SMX : a box tile of the M dims (BM cells) x a box of the N dims (BN)
+//   DM  : the CTA's sequential k-tile loop (K / BK steps)
+//   CC  : (BM/8) x (BN/8) threads
+//   SM  : A and B k-tiles (BK = 8) double-buffered in shared memory
+//   RM  : an 8 x 8 register tile per thread (two 4-row x two 4-col quads)
+// Re-composition of K happens entirely in registers (each output cell has a
+// single writer), so the store is a plain coalesced write of C.
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <sstream>
+
+#include "../plan.hpp"
+
+namespace mdhb {
+namespace {
+
+constexpr int BK = 8;
+enum { LD_SCALAR = 0, LD_K4 = 1, LD_MN4 = 2 };  // vector direction of 16-byte loads
+
+struct GemmArgs {
+  const float* A;
+  const float* B;
+  float* C;
+  const int32_t *tAm, *tCm, *tBn, *tCn;  // per tile (A/C row part, B/C column part)
+  const int32_t *am, *cm, *bn, *cn;      // per local row / column of a tile
+  const int32_t *ak, *bk;                // per k
+  int K, tilesM, tilesN;
+};
+
+struct GemvArgs {
+  const float* A;
+  const float* x;
+  float* y;
+  const int32_t *am, *cm;
+  int64_t M;
+  int K;
+};
+
+template <int BM, int BN, int AMODE, int BMODE, bool CVEC>
+__global__ void __launch_bounds__((BM / 8) * (BN / 8)) sgemm_tiled(GemmArgs g) {
+  constexpr int NT = (BM / 8) * (BN / 8);
+  constexpr int TXN = BN / 8;
+  __shared__ __align__(16) float As[2][BK][BM + 4];
+  __shared__ __align__(16) float Bs[2][BK][BN + 4];
+  const int tid = threadIdx.x;
+  const int tx = tid % TXN, ty = tid / TXN;
+
+  // grouped raster: GROUP_M row-tiles sweep the N tiles together (L2 reuse)
+  constexpr int GROUP_M = 8;
+  const int x = blockIdx.x;
+  const int per_group = GROUP_M * g.tilesN;
+  const int first_m = (x / per_group) * GROUP_M;
+  const int gsz = min(g.tilesM - first_m, GROUP_M);
+  const int tm = first_m + (x % per_group) % gsz;
+  const int tn = (x % per_group) / gsz;
+
+  const float* __restrict__ A = g.A + g.tAm[tm];
+  const float* __restrict__ B = g.B + g.tBn[tn];
+
+  // ---- per-thread load slots (fixed across k-tiles)
+  constexpr int AG = AMODE == LD_SCALAR ? BM * BK : BM * BK / 4;  // load groups per tile
+  constexpr int BG = BMODE == LD_SCALAR ? BN * BK : BN * BK / 4;
+  constexpr int AP = (AG + NT - 1) / NT, BP = (BG + NT - 1) / NT;
+  constexpr int AW = AMODE == LD_SCALAR ? 1 : 4, BW = BMODE == LD_SCALAR ? 1 : 4;
+  int a_row[AP], a_k[AP], b_col[BP], b_k[BP];
+  int32_t a_off[AP], b_off[BP];
+#pragma unroll
+  for (int p = 0; p < AP; ++p) {
+    int gi = tid + p * NT;
+    if (AMODE == LD_K4) { a_row[p] = gi >> 1; a_k[p] = (gi & 1) * 4; }
+    else if (AMODE == LD_MN4) { a_k[p] = gi / (BM / 4); a_row[p] = (gi % (BM / 4)) * 4; }
+    else { a_k[p] = gi / BM; a_row[p] = gi % BM; }
+    a_off[p] = gi < AG ? g.am[a_row[p]] : 0;
+  }
+#pragma unroll
+  for (int p = 0; p < BP; ++p) {
+    int gi = tid + p * NT;
+    if (BMODE == LD_K4) { b_col[p] = gi >> 1; b_k[p] = (gi & 1) * 4; }
+    else if (BMODE == LD_MN4) { b_k[p] = gi / (BN / 4); b_col[p] = (gi % (BN / 4)) * 4; }
+    else { b_k[p] = gi / BN; b_col[p] = gi % BN; }
+    b_off[p] = gi < BG ? g.bn[b_col[p]] : 0;
+  }
+  float ra[AP][AW], rb[BP][BW];
+
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int p = 0; p < AP; ++p) {
+      if (tid + p * NT >= AG) continue;
+      const float* src = A + a_off[p] + g.ak[k0 + a_k[p]];
+      if (AW == 4) {
+        float4 v = __ldg(reinterpret_cast<const float4*>(src));
+        ra[p][0] = v.x; ra[p][AW > 1 ? 1 : 0] = v.y; ra[p][AW > 2 ? 2 : 0] = v.z; ra[p][AW > 3 ? 3 : 0] = v.w;
+      } else {
+        ra[p][0] = __ldg(src);
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < BP; ++p) {
+      if (tid + p * NT >= BG) continue;
+      const float* src = B + b_off[p] + g.bk[k0 + b_k[p]];
+      if (BW == 4) {
+        float4 v = __ldg(reinterpret_cast<const float4*>(src));
+        rb[p][0] = v.x; rb[p][BW > 1 ? 1 : 0] = v.y; rb[p][BW > 2 ? 2 : 0] = v.z; rb[p][BW > 3 ? 3 : 0] = v.w;
+      } else {
+        rb[p][0] = __ldg(src);
+      }
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int p = 0; p < AP; ++p) {
+      if (tid + p * NT >= AG) continue;
+      if (AMODE == LD_K4) {
+#pragma unroll
+        for (int j = 0; j < AW; ++j) As[buf][a_k[p] + j][a_row[p]] = ra[p][j];
+      } else if (AMODE == LD_MN4) {
+        *reinterpret_cast<float4*>(&As[buf][a_k[p]][a_row[p]]) = make_float4(ra[p][0], ra[p][AW > 1 ? 1 : 0], ra[p][AW > 2 ? 2 : 0], ra[p][AW > 3 ? 3 : 0]);
+      } else {
+        As[buf][a_k[p]][a_row[p]] = ra[p][0];
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < BP; ++p) {
+      if (tid + p * NT >= BG) continue;
+      if (BMODE == LD_K4) {
+#pragma unroll
+        for (int j = 0; j < BW; ++j) Bs[buf][b_k[p] + j][b_col[p]] = rb[p][j];
+      } else if (BMODE == LD_MN4) {
+        *reinterpret_cast<float4*>(&Bs[buf][b_k[p]][b_col[p]]) = make_float4(rb[p][0], rb[p][BW > 1 ? 1 : 0], rb[p][BW > 2 ? 2 : 0], rb[p][BW > 3 ? 3 : 0]);
+      } else {
+        Bs[buf][b_k[p]][b_col[p]] = rb[p][0];
+      }
+    }
+  };
+
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+  const int nk = g.K / BK;
+  load(0);
+  store(0);
+  __syncthreads();
+  for (int kt = 0; kt < nk; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < nk) load((kt + 1) * BK);
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4]);
+      float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][BM / 2 + ty * 4]);
+      float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
+      float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][BN / 2 + tx * 4]);
+      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    if (kt + 1 < nk) store(buf ^ 1);
+    __syncthreads();
+  }
+
+  // ---- epilogue: each C cell has exactly one writer
+  float* __restrict__ C = g.C + g.tCm[tm] + g.tCn[tn];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = i < 4 ? ty * 4 + i : BM / 2 + ty * 4 + (i - 4);
+    float* crow = C + g.cm[r];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = h * (BN / 2) + tx * 4;
+      if (CVEC) {
+        *reinterpret_cast<float4*>(crow + g.cn[c]) =
+            make_float4(acc[i][h * 4 + 0], acc[i][h * 4 + 1], acc[i][h * 4 + 2], acc[i][h * 4 + 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) crow[g.cn[c + j]] = acc[i][h * 4 + j];
+      }
+    }
+  }
+}
+
+// y[cm[m]] = sum_k A[am[m] + k] * x[k]  -- MatVec (N = 1), rows contiguous in k.
+// One warp owns ROWS rows and streams them with 16-byte loads, sharing each
+// x chunk across its rows; the K reduction is a warp shuffle (CC -> RM).
+template <int ROWS>
+__global__ void __launch_bounds__(128) gemv_rows(GemvArgs g) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t m0 = warp * ROWS;
+  if (m0 >= g.M) return;
+  const float4* x4 = reinterpret_cast<const float4*>(g.x);
+  const float4* rows[ROWS];
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r)
+    rows[r] = reinterpret_cast<const float4*>(g.A + g.am[(m0 + r < g.M) ? (m0 + r) : (g.M - 1)]);
+  float acc[ROWS];
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) acc[r] = 0.f;
+  const int n4 = g.K / 4;
+  constexpr int U = 4;
+  int k = lane;
+  for (; k + 32 * (U - 1) < n4; k += 32 * U) {
+    float4 xv[U], av[ROWS][U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      xv[u] = __ldg(x4 + k + 32 * u);
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r) av[r][u] = __ldcs(rows[r] + k + 32 * u);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r) {
+        acc[r] = fmaf(av[r][u].x, xv[u].x, acc[r]);
+        acc[r] = fmaf(av[r][u].y, xv[u].y, acc[r]);
+        acc[r] = fmaf(av[r][u].z, xv[u].z, acc[r]);
+        acc[r] = fmaf(av[r][u].w, xv[u].w, acc[r]);
+      }
+  }
+  for (; k < n4; k += 32) {
+    float4 xv = __ldg(x4 + k);
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      float4 av = __ldcs(rows[r] + k);
+      acc[r] = fmaf(av.x, xv.x, acc[r]);
+      acc[r] = fmaf(av.y, xv.y, acc[r]);
+      acc[r] = fmaf(av.z, xv.z, acc[r]);
+      acc[r] = fmaf(av.w, xv.w, acc[r]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) {
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], s);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r)
+      if (m0 + r < g.M) g.y[g.cm[m0 + r]] = acc[r];
+  }
+}
+
+// ---------------------------------------------------------------- host
+struct Groups {
+  int a_buf = 0, b_buf = 1;
+  Linear la, lb, lc;
+  std::vector<int> Md, Nd, Kd;  // outer -> inner
+};
+
+int64_t prod_sizes(const MdHom& e, const std::vector<int>& dims) {
+  int64_t p = 1;
+  for (int d : dims) p *= e.sizes[static_cast<size_t>(d)];
+  return p;
+}
+
+// Enumerates the box `ext` (row-major over dims) and returns sum_d c[dims[t]] * l_t * scale_t
+std::vector<int64_t> box_offsets(const std::vector<int>& dims, const std::vector<int64_t>& ext,
+                                 const std::vector<int64_t>& coef, const std::vector<int64_t>& scale) {
+  int64_t n = 1;
+  for (int64_t x : ext) n *= x;
+  std::vector<int64_t> out(static_cast<size_t>(n), 0);
+  std::vector<int64_t> l(dims.size(), 0);
+  for (int64_t t = 0; t < n; ++t) {
+    int64_t o = 0;
+    for (size_t q = 0; q < dims.size(); ++q) o += coef[static_cast<size_t>(dims[q])] * l[q] * scale[q];
+    out[static_cast<size_t>(t)] = o;
+    for (int q = static_cast<int>(dims.size()) - 1; q >= 0; --q) {
+      if (++l[static_cast<size_t>(q)] < ext[static_cast<size_t>(q)]) break;
+      l[static_cast<size_t>(q)] = 0;
+    }
+  }
+  return out;
+}
+
+// Splits `target` cells over the dims' extents (inner -> outer) with gcds;
+// empty when the box cannot be formed exactly.
+std::vector<int64_t> factor_box(const MdHom& e, const std::vector<int>& dims, int64_t target) {
+  std::vector<int64_t> t(dims.size(), 1);
+  int64_t rem = target;
+  for (int q = static_cast<int>(dims.size()) - 1; q >= 0 && rem > 1; --q) {
+    int64_t g = std::gcd(e.sizes[static_cast<size_t>(dims[static_cast<size_t>(q)])], rem);
+    t[static_cast<size_t>(q)] = g;
+    rem /= g;
+  }
+  if (rem != 1) return {};
+  return t;
+}
+
+class GemmRoutine final : public Routine {
+ public:
+  GemmRoutine(const Problem& p, Groups g) : p_(p), g_(std::move(g)) {}
+  ~GemmRoutine() override {
+    if (blob_) cudaFree(blob_);
+  }
+  const char* family() const override { return "contraction"; }
+  double flops() const override { return 2.0 * static_cast<double>(M_) * static_cast<double>(N_) * static_cast<double>(K_); }
+  double bytes() const override { return static_cast<double>(p_.in_bytes + p_.out_bytes); }
+  const char* bound() const override { return gemv_ ? "hbm" : "fp32"; }
+  int launches() const override { return 1; }
+
+  // Builds tables; returns false when this template cannot realise the problem.
+  bool setup(int BM, int BN, const std::vector<int64_t>& Tm_in, const std::vector<int64_t>& Tn_in) {
+    const MdHom& e = p_.e;
+    M_ = prod_sizes(e, g_.Md);
+    N_ = prod_sizes(e, g_.Nd);
+    K_ = prod_sizes(e, g_.Kd);
+    std::vector<int64_t> ones;
+    auto scale1 = [](size_t n) { return std::vector<int64_t>(n, 1); };
+    std::vector<int64_t> fullK;
+    for (int d : g_.Kd) fullK.push_back(e.sizes[static_cast<size_t>(d)]);
+    std::vector<int64_t> ak = box_offsets(g_.Kd, fullK, g_.la.cj, scale1(g_.Kd.size()));
+    std::vector<int64_t> bk = box_offsets(g_.Kd, fullK, g_.lb.cj, scale1(g_.Kd.size()));
+    const int64_t a0 = g_.la.c0, b0 = g_.lb.c0, c0 = g_.lc.c0;
+    std::vector<int64_t> tAm, tCm, tBn, tCn, am, cm, bn, cn;
+    gemv_ = g_.Nd.empty();
+    if (gemv_) {
+      // rows must be contiguous in k, x contiguous too
+      for (int64_t k = 0; k < K_; ++k)
+        if (ak[static_cast<size_t>(k)] != k || bk[static_cast<size_t>(k)] != k) return false;
+      std::vector<int64_t> fullM;
+      for (int d : g_.Md) fullM.push_back(e.sizes[static_cast<size_t>(d)]);
+      am = box_offsets(g_.Md, fullM, g_.la.cj, scale1(g_.Md.size()));
+      cm = box_offsets(g_.Md, fullM, g_.lc.cj, scale1(g_.Md.size()));
+      if (K_ % 4 || a0 % 4 || b0 % 4) return false;
+      for (auto& v : am) {
+        if ((v + a0) % 4) return false;
+        v += a0;
+      }
+      for (auto& v : cm) v += c0;
+      tables(am, cm, {}, {}, {}, {}, {}, {}, {}, {});
+      return true;
+    }
+    if (K_ % BK) return false;
+    std::vector<int64_t> Tm = Tm_in.empty() ? factor_box(e, g_.Md, BM) : Tm_in;
+    std::vector<int64_t> Tn = Tn_in.empty() ? factor_box(e, g_.Nd, BN) : Tn_in;
+    if (Tm.empty() || Tn.empty()) return false;
+    int64_t pm = 1, pn = 1;
+    for (size_t q = 0; q < Tm.size(); ++q) {
+      if (e.sizes[static_cast<size_t>(g_.Md[q])] % Tm[q]) return false;
+      pm *= Tm[q];
+    }
+    for (size_t q = 0; q < Tn.size(); ++q) {
+      if (e.sizes[static_cast<size_t>(g_.Nd[q])] % Tn[q]) return false;
+      pn *= Tn[q];
+    }
+    if (pm != BM || pn != BN) return false;
+    Tm_ = Tm;
+    Tn_ = Tn;
+    BM_ = BM;
+    BN_ = BN;
+    auto grid_of = [&](const std::vector<int>& dims, const std::vector<int64_t>& T) {
+      std::vector<int64_t> gext, sc;
+      for (size_t q = 0; q < dims.size(); ++q) {
+        gext.push_back(e.sizes[static_cast<size_t>(dims[q])] / T[q]);
+        sc.push_back(T[q]);
+      }
+      return std::make_pair(gext, sc);
+    };
+    auto [gm, sm] = grid_of(g_.Md, Tm);
+    auto [gn, sn] = grid_of(g_.Nd, Tn);
+    tAm = box_offsets(g_.Md, gm, g_.la.cj, sm);
+    tCm = box_offsets(g_.Md, gm, g_.lc.cj, sm);
+    tBn = box_offsets(g_.Nd, gn, g_.lb.cj, sn);
+    tCn = box_offsets(g_.Nd, gn, g_.lc.cj, sn);
+    am = box_offsets(g_.Md, Tm, g_.la.cj, scale1(Tm.size()));
+    cm = box_offsets(g_.Md, Tm, g_.lc.cj, scale1(Tm.size()));
+    bn = box_offsets(g_.Nd, Tn, g_.lb.cj, scale1(Tn.size()));
+    cn = box_offsets(g_.Nd, Tn, g_.lc.cj, scale1(Tn.size()));
+    for (auto& v : tAm) v += a0;
+    for (auto& v : tBn) v += b0;
+    for (auto& v : tCm) v += c0;
+    tilesM_ = static_cast<int>(tAm.size());
+    tilesN_ = static_cast<int>(tBn.size());
+    // vector load / store directions
+    auto all_mod4 = [](const std::vector<int64_t>& v) {
+      for (int64_t x : v)
+        if (x % 4) return false;
+      return true;
+    };
+    auto groups4 = [](const std::vector<int64_t>& v) {
+      if (v.size() % 4) return false;
+      for (size_t t = 0; t < v.size(); t += 4) {
+        if (v[t] % 4) return false;
+        for (size_t j = 1; j < 4; ++j)
+          if (v[t + j] != v[t] + static_cast<int64_t>(j)) return false;
+      }
+      return true;
+    };
+    if (groups4(ak) && all_mod4(am) && all_mod4(tAm)) amode_ = LD_K4;
+    else if (groups4(am) && all_mod4(ak) && all_mod4(tAm)) amode_ = LD_MN4;
+    else amode_ = LD_SCALAR;
+    if (groups4(bn) && all_mod4(bk) && all_mod4(tBn)) bmode_ = LD_MN4;
+    else if (groups4(bk) && all_mod4(bn) && all_mod4(tBn)) bmode_ = LD_K4;
+    else bmode_ = LD_SCALAR;
+    cvec_ = groups4(cn) && all_mod4(cm) && all_mod4(tCm) && all_mod4(tCn);
+    tables(tAm, tCm, tBn, tCn, am, cm, bn, cn, ak, bk);
+    return true;
+  }
+
+  std::string describe() const override {
+    std::ostringstream os;
+    const char* mn[] = {"scalar", "k4", "mn4"};
+    if (gemv_) {
+      os << "{\"kernel\": \"gemv_rows<2>\", \"M\": " << M_ << ", \"K\": " << K_ << ", \"threads\": 128}";
+      return os.str();
+    }
+    os << "{\"kernel\": \"sgemm_tiled<" << BM_ << "," << BN_ << ">\", \"M\": " << M_ << ", \"N\": " << N_
+       << ", \"K\": " << K_ << ", \"BK\": " << BK << ", \"threads\": " << (BM_ / 8) * (BN_ / 8) << ", \"a_load\": \""
+       << mn[amode_] << "\", \"b_load\": \"" << mn[bmode_] << "\", \"c_store\": \"" << (cvec_ ? "v4" : "scalar")
+       << "\", \"tiles\": " << static_cast<int64_t>(tilesM_) * tilesN_ << "}";
+    return os.str();
+  }
+
+  void launch(const void* const* d_in, void* const* d_out, cudaStream_t s) override {
+    const float* A = static_cast<const float*>(d_in[g_.a_buf]);
+    const float* B = static_cast<const float*>(d_in[g_.b_buf]);
+    float* C = static_cast<float*>(d_out[0]);
+    if (gemv_) {
+      GemvArgs a{A, B + g_.lb.c0, C, tab_[0], tab_[1], M_, static_cast<int>(K_)};
+      constexpr int ROWS = 2;
+      int64_t warps = (M_ + ROWS - 1) / ROWS;
+      unsigned grid = static_cast<unsigned>((warps * 32 + 127) / 128);
+      gemv_rows<ROWS><<<grid, 128, 0, s>>>(a);
+      MDHB_CUDA(cudaGetLastError());
+      return;
+    }
+    GemmArgs a{A, B, C, tab_[0], tab_[1], tab_[2], tab_[3], tab_[4], tab_[5], tab_[6], tab_[7], tab_[8], tab_[9],
+               static_cast<int>(K_), tilesM_, tilesN_};
+    dispatch(a, s);
+    MDHB_CUDA(cudaGetLastError());
+  }
+
+  Config canonical(const Config* given) const;
+
+ private:
+  void tables(const std::vector<int64_t>& t0, const std::vector<int64_t>& t1, const std::vector<int64_t>& t2,
+              const std::vector<int64_t>& t3, const std::vector<int64_t>& t4, const std::vector<int64_t>& t5,
+              const std::vector<int64_t>& t6, const std::vector<int64_t>& t7, const std::vector<int64_t>& t8,
+              const std::vector<int64_t>& t9) {
+    const std::vector<int64_t>* ts[10] = {&t0, &t1, &t2, &t3, &t4, &t5, &t6, &t7, &t8, &t9};
+    size_t total = 0;
+    for (auto* t : ts) total += (t->size() + 64) * sizeof(int32_t);
+    std::vector<int32_t> host(total / sizeof(int32_t), 0);
+    size_t cur = 0;
+    size_t offs[10];
+    for (int q = 0; q < 10; ++q) {
+      offs[q] = cur;
+      for (int64_t v : *ts[q]) {
+        if (v > INT32_MAX || v < INT32_MIN) fail("Unsupported", "contraction offsets exceed int32");
+        host[cur++] = static_cast<int32_t>(v);
+      }
+      cur = (cur + 64) / 64 * 64;
+    }
+    MDHB_CUDA(cudaSetDevice(p_.opt.device));
+    MDHB_CUDA(cudaMalloc(&blob_, std::max<size_t>(cur, 64) * sizeof(int32_t)));
+    MDHB_CUDA(cudaMemcpy(blob_, host.data(), cur * sizeof(int32_t), cudaMemcpyHostToDevice));
+    for (int q = 0; q < 10; ++q) tab_[q] = static_cast<const int32_t*>(blob_) + offs[q];
+  }
+
+  template <int BM, int BN>
+  void dispatch2(const GemmArgs& a, cudaStream_t s) {
+    dim3 grid(static_cast<unsigned>(tilesM_ * tilesN_));
+    dim3 block((BM / 8) * (BN / 8));
+#define MDHB_G(AMo, BMo, CV) \
+  if (amode_ == AMo && bmode_ == BMo && cvec_ == CV) { sgemm_tiled<BM, BN, AMo, BMo, CV><<<grid, block, 0, s>>>(a); return; }
+#define MDHB_G2(AMo, BMo) MDHB_G(AMo, BMo, true) MDHB_G(AMo, BMo, false)
+    MDHB_G2(LD_K4, LD_MN4) MDHB_G2(LD_K4, LD_K4) MDHB_G2(LD_K4, LD_SCALAR)
+    MDHB_G2(LD_MN4, LD_MN4) MDHB_G2(LD_MN4, LD_K4) MDHB_G2(LD_MN4, LD_SCALAR)
+    MDHB_G2(LD_SCALAR, LD_MN4) MDHB_G2(LD_SCALAR, LD_K4) MDHB_G2(LD_SCALAR, LD_SCALAR)
+#undef MDHB_G2
+#undef MDHB_G
+  }
+  void dispatch(const GemmArgs& a, cudaStream_t s) {
+    if (BM_ == 128 && BN_ == 128) return dispatch2<128, 128>(a, s);
+    if (BM_ == 128 && BN_ == 64) return dispatch2<128, 64>(a, s);
+    if (BM_ == 64 && BN_ == 128) return dispatch2<64, 128>(a, s);
+    return dispatch2<64, 64>(a, s);
+  }
+
+  const Problem& p_;
+  Groups g_;
+  int64_t M_ = 0, N_ = 0, K_ = 0;
+  int BM_ = 0, BN_ = 0, tilesM_ = 0, tilesN_ = 0;
+  std::vector<int64_t> Tm_, Tn_;
+  int amode_ = 0, bmode_ = 0;
+  bool cvec_ = false, gemv_ = false;
+  void* blob_ = nullptr;
+  const int32_t* tab_[10] = {};
+};
+
+// Places `factors` (inner first) onto the box extents T (inner -> outer):
+// returns per-dim [layer] parts.
+void place(const std::vector<int64_t>& T, const std::vector<std::pair<int, int64_t>>& factors,
+           std::vector<std::vector<int64_t>>& parts_by_layer, const std::vector<int>& dims, bool& exact) {
+  std::vector<int64_t> rem = T;
+  int q = static_cast<int>(T.size()) - 1;
+  for (auto [layer, f] : factors) {
+    while (f > 1 && q >= 0) {
+      int64_t g = std::gcd(f, rem[static_cast<size_t>(q)]);
+      if (g == 1) {
+        if (rem[static_cast<size_t>(q)] == 1) { --q; continue; }
+        exact = false;
+        break;
+      }
+      parts_by_layer[static_cast<size_t>(layer)][static_cast<size_t>(dims[static_cast<size_t>(q)])] *= g;
+      rem[static_cast<size_t>(q)] /= g;
+      f /= g;
+      if (rem[static_cast<size_t>(q)] == 1) --q;
+    }
+    if (f > 1) exact = false;
+  }
+  // leftovers stay sequential in registers of the tile (RM)
+  for (size_t t = 0; t < T.size(); ++t)
+    parts_by_layer[5][static_cast<size_t>(dims[t])] *= rem[t];
+}
+
+Config GemmRoutine::canonical(const Config* given) const {
+  if (given) return *given;
+  const MdHom& e = p_.e;
+  if (p_.m.id("SMX") < 0 || p_.m.id("CC") < 0) return baseline_config(e, p_.m);
+  const int D = e.D();
+  // layers: 0 SMX, 1 DM, 2 WRP, 3 CC, 4 SM, 5 RM
+  std::vector<std::vector<int64_t>> L(6, std::vector<int64_t>(static_cast<size_t>(D), 1));
+  bool exact = true;
+  if (gemv_) {
+    // rows: SMX = M/8 (4 warps x 2 rows per CTA), WRP 4, RM 2; k: CC 32, RM 4, DM rest
+    for (int d : g_.Md) L[0][static_cast<size_t>(d)] = e.sizes[static_cast<size_t>(d)];
+    std::vector<int64_t> T(g_.Md.size(), 1);
+    if (!g_.Md.empty()) {
+      int64_t inner = e.sizes[static_cast<size_t>(g_.Md.back())];
+      if (inner % 8 == 0) {
+        L[0][static_cast<size_t>(g_.Md.back())] = inner / 8;
+        L[2][static_cast<size_t>(g_.Md.back())] = 4;
+        L[5][static_cast<size_t>(g_.Md.back())] = 2;
+      }
+    }
+    for (int d : g_.Kd) L[1][static_cast<size_t>(d)] = e.sizes[static_cast<size_t>(d)];
+    if (!g_.Kd.empty()) {
+      int dk = g_.Kd.back();
+      int64_t n = e.sizes[static_cast<size_t>(dk)];
+      if (n % 128 == 0) {
+        L[1][static_cast<size_t>(dk)] = n / 128;
+        L[3][static_cast<size_t>(dk)] = 32;
+        L[5][static_cast<size_t>(dk)] = 4;
+      }
+    }
+  } else {
+    for (size_t q = 0; q < g_.Md.size(); ++q)
+      L[0][static_cast<size_t>(g_.Md[q])] = e.sizes[static_cast<size_t>(g_.Md[q])] / Tm_[q];
+    for (size_t q = 0; q < g_.Nd.size(); ++q)
+      L[0][static_cast<size_t>(g_.Nd[q])] = e.sizes[static_cast<size_t>(g_.Nd[q])] / Tn_[q];
+    place(Tm_, {{5, 4}, {3, BM_ / 8}, {5, 2}}, L, g_.Md, exact);
+    place(Tn_, {{5, 4}, {3, BN_ / 8}, {5, 2}}, L, g_.Nd, exact);
+    int64_t bk = BK;
+    for (int q = static_cast<int>(g_.Kd.size()) - 1; q >= 0; --q) {
+      int d = g_.Kd[static_cast<size_t>(q)];
+      int64_t g = std::gcd(bk, e.sizes[static_cast<size_t>(d)]);
+      L[4][static_cast<size_t>(d)] = g;
+      L[1][static_cast<size_t>(d)] = e.sizes[static_cast<size_t>(d)] / g;
+      bk /= g;
+    }
+  }
+  // sanity: per-dim products must equal the sizes, else report the baseline
+  for (int d = 0; d < D; ++d) {
+    int64_t p = 1;
+    for (int l = 0; l < 6; ++l) p *= L[static_cast<size_t>(l)][static_cast<size_t>(d)];
+    if (p != e.sizes[static_cast<size_t>(d)]) exact = false;
+  }
+  if (!exact) return baseline_config(e, p_.m);
+  std::vector<LayerParts> lp = {{"SMX", L[0]}, {"DM", L[1]}, {"WRP", L[2]}, {"CC", L[3]}, {"SM", L[4]}, {"RM", L[5]}};
+  return make_config(p_, lp, {{e.in[static_cast<size_t>(g_.a_buf)].name, "SM"}, {e.in[static_cast<size_t>(g_.b_buf)].name, "SM"}}, "RM");
+}
+
+}  // namespace
+
+std::unique_ptr<Routine> make_contraction(const Problem& p, const Config* cfg, Config* cfg_out) {
+  const MdHom& e = p.e;
+  const int D = e.D();
+  if (e.assigns.size() != 1 || e.out.size() != 1 || e.out[0].acc.size() != 1 || e.in.size() != 2) return nullptr;
+  const Expr& f = e.assigns[0].e;
+  if (f.k != EK::Mul || f.args[0].k != EK::In || f.args[1].k != EK::In) return nullptr;
+  if (f.args[0].buf == f.args[1].buf) return nullptr;
+  if (e.in[0].acc.size() != 1 || e.in[1].acc.size() != 1) return nullptr;
+  if (e.in[0].type != Ty::F64 || e.in[1].type != Ty::F64 || e.out[0].type != Ty::F64) return nullptr;
+  if (p.opt.fstore != Store::F32) return nullptr;  // f64 storage: the generic path is the bit-exact one
+  int npw = 0;
+  for (auto& c : e.comb) {
+    if (c.kind == Combine::PS) return nullptr;
+    if (c.kind == Combine::PW) {
+      if (c.op != Fold::Add) return nullptr;
+      ++npw;
+    }
+  }
+  if (npw == 0) return nullptr;
+  // output access: every rank is exactly one cc dim, coefficient 1, no offset
+  std::vector<int> seen(static_cast<size_t>(D), 0);
+  for (auto& af : e.out[0].acc[0].idx) {
+    int nz = -1, cnt = 0;
+    for (int d = 0; d < D; ++d)
+      if (af.coeff[static_cast<size_t>(d)] != 0) {
+        nz = d;
+        ++cnt;
+      }
+    if (cnt != 1 || af.coeff[static_cast<size_t>(nz)] != 1 || af.c0 != 0) return nullptr;
+    if (e.comb[static_cast<size_t>(nz)].kind != Combine::CC) return nullptr;
+    seen[static_cast<size_t>(nz)]++;
+  }
+  for (int d = 0; d < D; ++d)
+    if (e.comb[static_cast<size_t>(d)].kind == Combine::CC && seen[static_cast<size_t>(d)] != 1) return nullptr;
+
+  Groups g;
+  g.a_buf = f.args[0].buf - 1;
+  g.b_buf = f.args[1].buf - 1;
+  g.la = linearize(e.in[static_cast<size_t>(g.a_buf)].acc[0], p.in_ext[static_cast<size_t>(g.a_buf)], D);
+  g.lb = linearize(e.in[static_cast<size_t>(g.b_buf)].acc[0], p.in_ext[static_cast<size_t>(g.b_buf)], D);
+  g.lc = linearize(e.out[0].acc[0], p.out_ext[0], D);
+  for (int d = 0; d < D; ++d) {
+    bool da = g.la.cj[static_cast<size_t>(d)] != 0, db = g.lb.cj[static_cast<size_t>(d)] != 0;
+    if (e.comb[static_cast<size_t>(d)].kind == Combine::PW) {
+      g.Kd.push_back(d);
+    } else if (da && db) {
+      return nullptr;  // batch dims: generic family
+    } else if (da) {
+      g.Md.push_back(d);
+    } else {
+      g.Nd.push_back(d);  // B-only, or read by neither (broadcast)
+    }
+  }
+  if (g.Md.empty()) {  // make the streamed operand "A"
+    std::swap(g.a_buf, g.b_buf);
+    std::swap(g.la, g.lb);
+    std::swap(g.Md, g.Nd);
+  }
+  if (g.Md.empty()) return nullptr;
+  // dim order inside each group: largest output stride outermost; K by A stride
+  auto by = [&](const std::vector<int64_t>& cj) {
+    return [&cj](int x, int y) { return std::llabs(cj[static_cast<size_t>(x)]) > std::llabs(cj[static_cast<size_t>(y)]); };
+  };
+  std::stable_sort(g.Md.begin(), g.Md.end(), by(g.lc.cj));
+  std::stable_sort(g.Nd.begin(), g.Nd.end(), by(g.lc.cj));
+  {
+    // K innermost = the dim where A (else B) has unit stride
+    bool a_unit = false;
+    for (int d : g.Kd) a_unit = a_unit || std::llabs(g.la.cj[static_cast<size_t>(d)]) == 1;
+    std::stable_sort(g.Kd.begin(), g.Kd.end(), by(a_unit ? g.la.cj : g.lb.cj));
+  }
+
+  auto r = std::make_unique<GemmRoutine>(p, g);
+  bool ok = false;
+  if (cfg) {
+    // instantiate from the configuration's per-dim tile boxes
+    auto P = parts_per_asm_layer(*cfg, e, p.m);
+    int smx = p.m.id("SMX"), gpu = p.m.id("GPU");
+    if (smx < 0) fail("Unsupported", "contraction template needs an SMX layer");
+    std::vector<int64_t> Tm, Tn;
+    int64_t bm = 1, bn = 1;
+    for (int d : g.Md) {
+      int64_t grid = P[static_cast<size_t>(smx - 1)][static_cast<size_t>(d)] * (gpu > 0 ? P[static_cast<size_t>(gpu - 1)][static_cast<size_t>(d)] : 1);
+      Tm.push_back(e.sizes[static_cast<size_t>(d)] / grid);
+      bm *= Tm.back();
+    }
+    for (int d : g.Nd) {
+      int64_t grid = P[static_cast<size_t>(smx - 1)][static_cast<size_t>(d)] * (gpu > 0 ? P[static_cast<size_t>(gpu - 1)][static_cast<size_t>(d)] : 1);
+      Tn.push_back(e.sizes[static_cast<size_t>(d)] / grid);
+      bn *= Tn.back();
+    }
+    for (int d : g.Kd)
+      if (P[static_cast<size_t>(smx - 1)][static_cast<size_t>(d)] != 1) fail("Unsupported", "contraction template does not split K across CTAs");
+    bool menu = (bm == 128 || bm == 64) && (bn == 128 || bn == 64);
+    if (g.Nd.empty()) {
+      ok = r->setup(0, 0, {}, {});
+    } else if (!menu || !(ok = r->setup(static_cast<int>(bm), static_cast<int>(bn), Tm, Tn))) {
+      fail("Unsupported", "contraction template instantiates BM, BN in {64, 128} with K % 8 == 0");
+    }
+  } else {
+    const int menu[4][2] = {{128, 128}, {128, 64}, {64, 128}, {64, 64}};
+    for (auto& t : menu)
+      if ((ok = r->setup(t[0], t[1], {}, {}))) break;
+  }
+  if (!ok) return nullptr;
+  if (cfg_out) *cfg_out = r->canonical(cfg);
+  return r;
+}
+
+}  // namespace mdhb

@@ -1,0 +1,309 @@
+// Stencil family: concatenation-only md_homs whose scalar function is a
+// weighted sum of shifted reads of one rank-3 buffer (Jacobi3D,
+// proj/data/computations/jacobi3d.json; BASELINE config 2).
+//
+//   w[i][j][k] = sum_t  wt_t * v[i + o_t0][j + o_t1][k + o_t2],   o_t in {0,1,2}^3
+//
+// Every dimension is `++`, so the re-composition is a disjoint, coalesced,
+// vectorised store of each thread's cells (no reduction).  De-composition:
+//   SMX  : the grid tiles (k: TK=128, j: TJ, i: TI planes per CTA)
+//   DM   : each CTA streams its TI output planes sequentially (2.5D blocking)
+//   SM   : a 4-slot ring of input planes (tile + 1-cell halo) in shared memory
+//   WRP/CC: 8 warps x 32 lanes; lane -> 4 consecutive k, warp -> TJ/8 rows j
+//   RM   : 4 (k) x 2 (j) outputs per thread; the centre rows of the last two
+//          planes stay in registers as the CTA marches along i, so each
+//          plane row is read from shared memory once per use class.
+// Algorithmic traffic per run: every input cell read once + every output cell
+// written once = 4 * (514^3 + 512^3) B for the BASELINE size.
+#include <array>
+#include <cstring>
+#include <sstream>
+
+#include "../plan.hpp"
+
+namespace mdhb {
+namespace {
+
+constexpr int TK = 128;           // outputs along k per CTA
+constexpr int NTHREADS = 256;
+constexpr int PITCH = TK + 8;     // smem row pitch (floats): 16B-aligned rows, room for the halo
+
+struct StencilArgs {
+  const float* v;   // input base (already offset by nothing; halo offsets are in o_*)
+  float* w;
+  int64_t n0, n1, n2;     // output extents (i, j, k)
+  int64_t e0, e1, e2;     // input extents (row-major strides from e1, e2)
+  int ti;                 // output planes per CTA
+  // weights of the 7-point star, in slot order: centre, i-1, i+1, j-1, j+1, k-1, k+1
+  float wc, wim, wip, wjm, wjp, wkm, wkp;
+};
+
+// Star-7 stencil with the centre at offset (1,1,1): reads v[i+1+di][j+1+dj][k+1+dk].
+template <int TJ>
+__global__ void __launch_bounds__(NTHREADS, 3) star7_kernel(StencilArgs a) {
+  constexpr int ROWS = TJ + 2;
+  constexpr int JPT = TJ / 8;  // j rows per thread (8 warps along j)
+  static_assert(JPT == 2, "thread tile is 4 (k) x 2 (j)");
+  __shared__ __align__(16) float ring[4][ROWS][PITCH];
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * TK;
+  const int64_t j0 = static_cast<int64_t>(blockIdx.y) * TJ;
+  const int64_t i0 = static_cast<int64_t>(blockIdx.z) * a.ti;
+  const int64_t plane = a.e1 * a.e2;
+  const int kl = lane * 4;          // local k of this thread's first output
+  const int jl = warp * JPT;        // local j of this thread's first output
+
+  // cooperative plane loader: ROWS x (TK+2) cells, cell (r, c) = v[ip][j0+r][k0+c]
+  constexpr int CELLS = ROWS * (TK + 2);
+  constexpr int PER = (CELLS + NTHREADS - 1) / NTHREADS;
+  float pre[PER];
+  const int64_t kmax = a.e2 - k0;  // cells available in this row (tile edge)
+  auto fetch = [&](int64_t ip) {
+    const float* src = a.v + ip * plane + j0 * a.e2 + k0;
+#pragma unroll
+    for (int t = 0; t < PER; ++t) {
+      int cidx = tid + t * NTHREADS;
+      int r = cidx / (TK + 2), c = cidx - r * (TK + 2);
+      float x = 0.f;
+      if (cidx < CELLS && c < kmax && j0 + r < a.e1 && ip < a.e0) x = __ldg(src + static_cast<int64_t>(r) * a.e2 + c);
+      pre[t] = x;
+    }
+  };
+  auto commit = [&](int slot) {
+#pragma unroll
+    for (int t = 0; t < PER; ++t) {
+      int cidx = tid + t * NTHREADS;
+      if (cidx < CELLS) {
+        int r = cidx / (TK + 2), c = cidx - r * (TK + 2);
+        ring[slot][r][c] = pre[t];
+      }
+    }
+  };
+  // 6 consecutive floats of row r of a slot, starting at local column kl
+  auto row6 = [&](int slot, int r, float (&x)[6]) {
+    float4 q = *reinterpret_cast<const float4*>(&ring[slot][r][kl]);
+    float2 h = *reinterpret_cast<const float2*>(&ring[slot][r][kl + 4]);
+    x[0] = q.x; x[1] = q.y; x[2] = q.z; x[3] = q.w; x[4] = h.x; x[5] = h.y;
+  };
+
+  // prologue: input planes i0 .. i0+2 in slots 0..2, plane i0+3 in flight
+  // (output plane i needs input planes i, i+1, i+2)
+  fetch(i0);
+  commit(0);
+  fetch(i0 + 1);
+  commit(1);
+  fetch(i0 + 2);
+  commit(2);
+  fetch(i0 + 3);
+  __syncthreads();
+  // registers: centre rows (jl+1 .. jl+JPT) of the previous / current input plane
+  float cprev[JPT][4], ccur[JPT][6];
+#pragma unroll
+  for (int jj = 0; jj < JPT; ++jj) {
+    float x[6];
+    row6(0, jl + 1 + jj, x);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) cprev[jj][c] = x[c + 1];
+    row6(1, jl + 1 + jj, ccur[jj]);
+  }
+  const int iend = static_cast<int>(a.n0 - i0 < a.ti ? a.n0 - i0 : a.ti);
+  for (int t = 0; t < iend; ++t) {
+    if (t > 0) __syncthreads();  // plane i0+t+2 (committed last iteration) is visible
+    const int s_cur = (t + 1) & 3, s_nxt = (t + 2) & 3;
+    float nxt[JPT][6], jm[6], jp[6];
+#pragma unroll
+    for (int jj = 0; jj < JPT; ++jj) row6(s_nxt, jl + 1 + jj, nxt[jj]);
+    row6(s_cur, jl, jm);            // row j-1 of the first output row
+    row6(s_cur, jl + JPT + 1, jp);  // row j+1 of the last output row
+    const int64_t i = i0 + t;
+#pragma unroll
+    for (int jj = 0; jj < JPT; ++jj) {
+      const float* up = jj == 0 ? jm : ccur[jj - 1];
+      const float* dn = jj == JPT - 1 ? jp : ccur[jj + 1];
+      float o[4];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        float acc = a.wc * ccur[jj][kk + 1];
+        acc = fmaf(a.wim, cprev[jj][kk], acc);
+        acc = fmaf(a.wip, nxt[jj][kk + 1], acc);
+        acc = fmaf(a.wjm, up[kk + 1], acc);
+        acc = fmaf(a.wjp, dn[kk + 1], acc);
+        acc = fmaf(a.wkm, ccur[jj][kk], acc);
+        acc = fmaf(a.wkp, ccur[jj][kk + 2], acc);
+        o[kk] = acc;
+      }
+      const int64_t j = j0 + jl + jj, k = k0 + kl;
+      if (j < a.n1 && k < a.n2) {
+        float* dst = a.w + (i * a.n1 + j) * a.n2 + k;
+        if (k + 4 <= a.n2 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+          __stcs(reinterpret_cast<float4*>(dst), make_float4(o[0], o[1], o[2], o[3]));
+        } else {
+          for (int kk = 0; kk < 4 && k + kk < a.n2; ++kk) dst[kk] = o[kk];
+        }
+      }
+    }
+#pragma unroll
+    for (int jj = 0; jj < JPT; ++jj) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) cprev[jj][c] = ccur[jj][c + 1];
+#pragma unroll
+      for (int c = 0; c < 6; ++c) ccur[jj][c] = nxt[jj][c];
+    }
+    // slot (t+3)&3 is not read in this iteration: park plane i0+t+3 there and
+    // put plane i0+t+4 in flight; both are consumed a full iteration later
+    commit((t + 3) & 3);
+    fetch(i0 + t + 4);
+  }
+}
+
+// ---------------------------------------------------------------- host
+// Recognises  sum_t lit_t * in(1, a_t)  (any association of + over terms,
+// literal on either side of *, a bare in(1,a) = weight 1).
+bool linear_terms(const Expr& e, std::vector<std::pair<double, int>>& terms) {
+  if (e.k == EK::Add) return linear_terms(e.args[0], terms) && linear_terms(e.args[1], terms);
+  if (e.k == EK::In && e.buf == 1) {
+    terms.push_back({1.0, e.acc});
+    return true;
+  }
+  if (e.k == EK::Mul) {
+    const Expr *lit = nullptr, *in = nullptr;
+    for (int s = 0; s < 2; ++s) {
+      if (e.args[static_cast<size_t>(s)].k == EK::Lit) lit = &e.args[static_cast<size_t>(s)];
+      if (e.args[static_cast<size_t>(s)].k == EK::In) in = &e.args[static_cast<size_t>(s)];
+    }
+    if (lit && in && in->buf == 1) {
+      terms.push_back({lit->type == Ty::F64 ? lit->fv : static_cast<double>(lit->iv), in->acc});
+      return true;
+    }
+  }
+  return false;
+}
+
+class StencilRoutine final : public Routine {
+ public:
+  StencilRoutine(const Problem& p, StencilArgs a, int tj) : p_(p), a_(a), tj_(tj) {}
+  const char* family() const override { return "stencil"; }
+  std::string describe() const override {
+    std::ostringstream os;
+    os << "{\"kernel\": \"star7_kernel<" << tj_ << ">\", \"TK\": " << TK << ", \"TJ\": " << tj_ << ", \"TI\": " << a_.ti
+       << ", \"threads\": " << NTHREADS << ", \"smem_ring_slots\": 4, \"grid\": [" << grid().x << ", " << grid().y
+       << ", " << grid().z << "]}";
+    return os.str();
+  }
+  dim3 grid() const {
+    return dim3(static_cast<unsigned>((a_.n2 + TK - 1) / TK), static_cast<unsigned>((a_.n1 + tj_ - 1) / tj_),
+                static_cast<unsigned>((a_.n0 + a_.ti - 1) / a_.ti));
+  }
+  int launches() const override { return 1; }
+  double bytes() const override { return static_cast<double>(p_.in_bytes + p_.out_bytes); }
+  double flops() const override { return 13.0 * static_cast<double>(a_.n0 * a_.n1 * a_.n2); }
+  void launch(const void* const* d_in, void* const* d_out, cudaStream_t s) override {
+    StencilArgs a = a_;
+    a.v = static_cast<const float*>(d_in[0]);
+    a.w = static_cast<float*>(d_out[0]);
+    star7_kernel<16><<<grid(), NTHREADS, 0, s>>>(a);
+    MDHB_CUDA(cudaGetLastError());
+  }
+
+ private:
+  const Problem& p_;
+  StencilArgs a_;
+  int tj_;
+};
+
+}  // namespace
+
+std::unique_ptr<Routine> make_stencil(const Problem& p, const Config* cfg, Config* cfg_out) {
+  const MdHom& e = p.e;
+  if (e.D() != 3 || e.in.size() != 1 || e.out.size() != 1 || e.assigns.size() != 1) return nullptr;
+  for (auto& c : e.comb)
+    if (c.kind != Combine::CC) return nullptr;
+  const Buf& in = e.in[0];
+  const Buf& out = e.out[0];
+  if (in.rank != 3 || out.rank != 3 || out.acc.size() != 1 || in.type != Ty::F64) return nullptr;
+  // output access: identity (w[i][j][k])
+  for (int r = 0; r < 3; ++r) {
+    const Affine& f = out.acc[0].idx[static_cast<size_t>(r)];
+    if (f.c0 != 0) return nullptr;
+    for (int d = 0; d < 3; ++d)
+      if (f.coeff[static_cast<size_t>(d)] != (d == r ? 1 : 0)) return nullptr;
+  }
+  // input accesses: identity + offsets; must form the 7-point star around (1,1,1)
+  std::vector<std::array<int64_t, 3>> off;
+  for (auto& acc : in.acc) {
+    std::array<int64_t, 3> o{};
+    for (int r = 0; r < 3; ++r) {
+      const Affine& f = acc.idx[static_cast<size_t>(r)];
+      for (int d = 0; d < 3; ++d)
+        if (f.coeff[static_cast<size_t>(d)] != (d == r ? 1 : 0)) return nullptr;
+      o[static_cast<size_t>(r)] = f.c0;
+    }
+    off.push_back(o);
+  }
+  std::vector<std::pair<double, int>> terms;
+  if (!linear_terms(e.assigns[0].e, terms)) return nullptr;
+  // star slots: centre, i-1, i+1, j-1, j+1, k-1, k+1 (offsets relative to 1)
+  const int64_t slot_off[7][3] = {{1, 1, 1}, {0, 1, 1}, {2, 1, 1}, {1, 0, 1}, {1, 2, 1}, {1, 1, 0}, {1, 1, 2}};
+  double w[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (auto& t : terms) {
+    auto& o = off[static_cast<size_t>(t.second - 1)];
+    int slot = -1;
+    for (int s = 0; s < 7; ++s)
+      if (o[0] == slot_off[s][0] && o[1] == slot_off[s][1] && o[2] == slot_off[s][2]) slot = s;
+    if (slot < 0) return nullptr;  // not a star-7 read
+    w[slot] += t.first;
+  }
+  if (p.opt.fstore != Store::F32) return nullptr;  // f64 storage -> generic (bit-exact) path
+
+  StencilArgs a{};
+  a.n0 = e.sizes[0];
+  a.n1 = e.sizes[1];
+  a.n2 = e.sizes[2];
+  a.e0 = p.in_ext[0][0];
+  a.e1 = p.in_ext[0][1];
+  a.e2 = p.in_ext[0][2];
+  a.wc = static_cast<float>(w[0]);
+  a.wim = static_cast<float>(w[1]);
+  a.wip = static_cast<float>(w[2]);
+  a.wjm = static_cast<float>(w[3]);
+  a.wjp = static_cast<float>(w[4]);
+  a.wkm = static_cast<float>(w[5]);
+  a.wkp = static_cast<float>(w[6]);
+  // the input must hold the 1-cell halo the star reads
+  if (p.in_ext[0][0] < a.n0 + 2 || a.e1 < a.n1 + 2 || a.e2 < a.n2 + 2) return nullptr;
+
+  const int TJ = 16;
+  int ti = 32;
+  if (cfg) {
+    // Instantiate from the configuration: i-planes per CTA = the parts on
+    // DM x WRP x CC x SM x RM of dim i (everything below the grid).
+    auto P = parts_per_asm_layer(*cfg, e, p.m);
+    int smx = p.m.id("SMX"), gpu = p.m.id("GPU");
+    int64_t grid_i = P[static_cast<size_t>(smx - 1)][0] * (gpu > 0 ? P[static_cast<size_t>(gpu - 1)][0] : 1);
+    int64_t grid_j = P[static_cast<size_t>(smx - 1)][1], grid_k = P[static_cast<size_t>(smx - 1)][2];
+    if (grid_j * TJ != a.n1 || grid_k * TK != a.n2)
+      fail("Unsupported", "stencil template tiles (j, k) by (16, 128) per CTA");
+    ti = static_cast<int>(a.n0 / grid_i);
+    if (ti < 1 || a.n0 % grid_i != 0) fail("Unsupported", "stencil template needs uniform i-chunks");
+  }
+  a.ti = ti;
+  if (cfg_out) {
+    int64_t gi = (a.n0 + ti - 1) / ti;
+    // i: SMX chunks x DM planes; j: SMX x WRP(8) x RM(2); k: SMX x CC(32) x RM(4)
+    if (a.n1 % TJ || a.n2 % TK || a.n0 % ti) {
+      *cfg_out = baseline_config(e, p.m);
+    } else {
+      std::vector<LayerParts> lp = {{"SMX", {gi, a.n1 / TJ, a.n2 / TK}}, {"DM", {ti, 1, 1}}, {"WRP", {1, 8, 1}},
+                                    {"CC", {1, 1, 32}},                   {"SM", {1, 1, 1}},  {"RM", {1, 2, 4}}};
+      if (p.m.id("WRP") < 0 || p.m.id("SMX") < 0)
+        *cfg_out = baseline_config(e, p.m);
+      else
+        *cfg_out = make_config(p, lp, {{in.name, "SM"}}, "RM");
+    }
+  }
+  return std::make_unique<StencilRoutine>(p, a, TJ);
+}
+
+}  // namespace mdhb

@@ -1,0 +1,103 @@
+// Plan = an md_hom + a Table-1 configuration bound to one sm_100a kernel
+// template instance.  The planner recognises the routine class of the md_hom
+// (the "kernel family") and asks that family to instantiate itself from the
+// configuration; every family also offers the canonical configuration of its
+// default instance so callers may omit the config.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "mdh_model.hpp"
+
+namespace mdhb {
+
+enum class Store { F32 = 0, F64 = 1, I32 = 2, I64 = 3 };
+inline size_t store_bytes(Store s) { return (s == Store::F32 || s == Store::I32) ? 4 : 8; }
+inline const char* store_name(Store s) {
+  switch (s) {
+    case Store::F32: return "f32";
+    case Store::F64: return "f64";
+    case Store::I32: return "i32";
+    default: return "i64";
+  }
+}
+
+enum class Math { FFMA = 0, TF32 = 1, BF16 = 2 };
+
+struct Options {
+  Store fstore = Store::F32;
+  Store istore = Store::I64;
+  Math math = Math::FFMA;
+  int device = 0;
+  bool force_generic = false;
+};
+
+// Everything a family needs to know about the problem, precomputed once.
+struct Problem {
+  MdHom e;
+  Asm m;
+  Options opt;
+  std::vector<std::vector<int64_t>> in_ext, out_ext;  // infer_buffer_sizes
+  std::vector<Store> in_store, out_store;
+  int64_t in_bytes = 0, out_bytes = 0;  // algorithmic bytes: every buffer once
+  Store store_of(Ty t) const { return t == Ty::F64 ? opt.fstore : opt.istore; }
+};
+
+// One instantiated kernel template.
+class Routine {
+ public:
+  virtual ~Routine() = default;
+  virtual const char* family() const = 0;
+  virtual std::string describe() const = 0;  // JSON object text (template parameters)
+  virtual void launch(const void* const* d_in, void* const* d_out, cudaStream_t s) = 0;
+  virtual int launches() const = 0;
+  virtual double flops() const { return 0.0; }  // algorithmic, per run
+  virtual double bytes() const = 0;             // algorithmic, per run
+  virtual const char* bound() const { return "hbm"; }
+  // Chunked host<->device execution along a concatenation dimension, when
+  // the family can overlap copies with compute (nullptr = whole-buffer copy).
+  virtual bool supports_chunked_host() const { return false; }
+  virtual void launch_host_chunked(const void* const* h_in, void* const* h_out, void* const* d_in, void* const* d_out,
+                                   cudaStream_t s) {
+    (void)h_in; (void)h_out; (void)d_in; (void)d_out; (void)s;
+  }
+};
+
+// Family factories.  Each returns nullptr when the md_hom is not of its
+// routine class; throws Error("Unsupported", ...) when it is, but the given
+// configuration is outside what its template can instantiate.  `cfg` may be
+// null (use the family's default instance) -- on return, *cfg_out holds the
+// canonical configuration of the chosen instance.
+std::unique_ptr<Routine> make_prl(const Problem& p, const Config* cfg, Config* cfg_out);
+std::unique_ptr<Routine> make_stencil(const Problem& p, const Config* cfg, Config* cfg_out);
+std::unique_ptr<Routine> make_contraction(const Problem& p, const Config* cfg, Config* cfg_out);
+std::unique_ptr<Routine> make_generic(const Problem& p, const Config* cfg, Config* cfg_out);
+
+// The candidate configurations a family can instantiate for this problem
+// (the tuner's search space), canonical Table-1 form.
+std::vector<Config> family_space(const Problem& p, const std::string& family);
+
+// Table-1 configuration builder for the "B200" ASM {DM, SM, RM | SMX, WRP, CC}
+// (and MultiB200 with HM/GPU).  Layer parts are given per ASM layer name;
+// the MDH level order is SMX -> DM -> WRP -> CC -> SM -> RM (outer to inner),
+// each MDH layer assigned to the ASM layer of the same role.
+struct LayerParts {
+  std::string layer;
+  std::vector<int64_t> parts;  // per dimension
+};
+Config make_config(const Problem& p, const std::vector<LayerParts>& parts,
+                   const std::vector<std::pair<std::string, std::string>>& staging_in,  // buffer -> region
+                   const std::string& out_region);
+
+// CUDA error check -> Error("CudaError", ...)
+void cuda_check(cudaError_t err, const char* what);
+#define MDHB_CUDA(x) ::mdhb::cuda_check((x), #x)
+
+// Device properties cached per device.
+int sm_count(int device);
+
+}  // namespace mdhb

@@ -1,0 +1,235 @@
+"""Python mirror of the reference's md_hom operator interface over the B200
+C ABI (include/mdh_b200.h, libmdh_b200.so).
+
+The names follow the reference so the parity tests read like its own tests:
+
+    reference (C++, proj/include/mdh/)           here
+    -------------------------------------------  ------------------------------------
+    parse_computation_json (json_io.hpp:15)      Plan(spec, ...) takes the same JSON
+    reference_execute(e, inputs) (highlevel:62)  execute(spec, inputs)     -> outputs
+    interpret(lower(e, m, cfg), e, inputs)       execute(spec, inputs, asm=m, config=cfg)
+    compiled_time_objective(e, m, cfg)           b200_time_objective(spec, asm, cfg)
+    tune(e, m, cs, budget, obj, seed)            tune(spec, asm, budget, seed)
+    validate(cfg, e, m, cs)                      validate_config(spec, asm, cfg)
+
+Device memory, streams and the torch.distributed plumbing come from PyTorch;
+all computation happens in the CUDA kernels of libmdh_b200.so.  There is no
+CPU fallback: if the library or a GPU is missing, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+from typing import Any, List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmdh_b200.so")
+
+F32, F64, I32, I64 = 0, 1, 2, 3
+MATH_FFMA, MATH_TF32, MATH_BF16 = 0, 1, 2
+_NP = {F32: np.float32, F64: np.float64, I32: np.int32, I64: np.int64}
+
+EXPORTED = [
+    "mdh_b200_default_options", "mdh_b200_plan_create", "mdh_b200_plan_destroy", "mdh_b200_buffer_count",
+    "mdh_b200_buffer_info", "mdh_b200_run", "mdh_b200_run_host", "mdh_b200_time", "mdh_b200_describe",
+    "mdh_b200_validate_config", "mdh_b200_tune", "mdh_b200_launches_per_run", "mdh_b200_last_error",
+    "mdh_b200_version",
+]
+
+
+class MdhError(RuntimeError):
+    """Failure with the reference's stable error code (error.hpp:9-17)."""
+
+    def __init__(self, msg: str):
+        super().__init__(msg)
+        self.code = msg.split(":", 1)[0]
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("float_storage", ctypes.c_int), ("int_storage", ctypes.c_int), ("math", ctypes.c_int),
+                ("device", ctypes.c_int), ("family", ctypes.c_int)]
+
+
+_lib = None
+
+
+def lib():
+    """Loads libmdh_b200.so -- raises if it was not built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise MdhError(f"LibraryMissing: {LIB_PATH} not built; run __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        L.mdh_b200_last_error.restype = ctypes.c_char_p
+        L.mdh_b200_version.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc:
+        raise MdhError(lib().mdh_b200_last_error().decode())
+
+
+def _text(spec) -> bytes:
+    if isinstance(spec, (dict, list)):
+        spec = json.dumps(spec)
+    return spec.encode() if isinstance(spec, str) else spec
+
+
+def options(float_storage=F32, int_storage=I64, math=MATH_FFMA, device=0, generic=False) -> Options:
+    o = Options()
+    lib().mdh_b200_default_options(ctypes.byref(o))
+    o.float_storage, o.int_storage, o.math, o.device, o.family = float_storage, int_storage, math, device, int(generic)
+    return o
+
+
+def _ptr_array(ptrs):
+    return (ctypes.c_void_p * max(1, len(ptrs)))(*ptrs)
+
+
+class Plan:
+    """An md_hom bound to an instantiated sm_100a kernel template."""
+
+    def __init__(self, spec, asm: str = "B200", config=None, float_storage=F32, int_storage=I64,
+                 math=MATH_FFMA, device=0, generic=False):
+        self.spec = spec if isinstance(spec, str) else json.dumps(spec)
+        self._h = ctypes.c_void_p()
+        self.opts = options(float_storage, int_storage, math, device, generic)
+        cfg = None if config is None else _text(config)
+        _check(lib().mdh_b200_plan_create(_text(self.spec), _text(asm), cfg, ctypes.byref(self.opts),
+                                          ctypes.byref(self._h)))
+        self.device = device
+        self.inputs = [self.buffer_info(0, b) for b in range(self._count(0))]
+        self.outputs = [self.buffer_info(1, b) for b in range(self._count(1))]
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.mdh_b200_plan_destroy(h)
+            self._h = ctypes.c_void_p()
+
+    close = __del__
+
+    def _count(self, side):
+        n = ctypes.c_int()
+        _check(lib().mdh_b200_buffer_count(self._h, side, ctypes.byref(n)))
+        return n.value
+
+    def buffer_info(self, side, b):
+        dims = (ctypes.c_int64 * 16)()
+        rank, dt, nb = ctypes.c_int(), ctypes.c_int(), ctypes.c_int64()
+        _check(lib().mdh_b200_buffer_info(self._h, side, b, dims, ctypes.byref(rank), ctypes.byref(dt),
+                                          ctypes.byref(nb)))
+        return {"shape": tuple(dims[r] for r in range(rank.value)), "dtype": dt.value, "bytes": nb.value,
+                "np": _NP[dt.value]}
+
+    def describe(self) -> dict:
+        need = ctypes.c_int64()
+        _check(lib().mdh_b200_describe(self._h, None, 0, ctypes.byref(need)))
+        buf = ctypes.create_string_buffer(need.value)
+        _check(lib().mdh_b200_describe(self._h, buf, need.value, ctypes.byref(need)))
+        return json.loads(buf.value.decode())
+
+    @property
+    def launches(self) -> int:
+        n = ctypes.c_int()
+        _check(lib().mdh_b200_launches_per_run(self._h, ctypes.byref(n)))
+        return n.value
+
+    # ---- device-resident (torch tensors as plumbing) --------------------
+    def empty(self, side, device=None):
+        import torch
+        tdt = {F32: torch.float32, F64: torch.float64, I32: torch.int32, I64: torch.int64}
+        infos = self.inputs if side == 0 else self.outputs
+        dev = device or f"cuda:{self.device}"
+        return [torch.empty(i["shape"], dtype=tdt[i["dtype"]], device=dev) for i in infos]
+
+    def _dev_ptrs(self, tensors, infos):
+        ptrs = []
+        for t, i in zip(tensors, infos):
+            if not t.is_cuda or not t.is_contiguous():
+                raise MdhError("InvalidArgument: device buffers must be contiguous CUDA tensors")
+            if tuple(t.shape) != i["shape"] or t.element_size() * t.numel() != i["bytes"]:
+                raise MdhError(f"BufferTooSmall: expected shape {i['shape']} / {i['bytes']} bytes")
+            ptrs.append(t.data_ptr())
+        return _ptr_array(ptrs)
+
+    def run(self, d_in, d_out, stream=None):
+        """mdh_kernel(in..., out...) on device buffers, async on `stream`."""
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+        elif hasattr(stream, "cuda_stream"):
+            stream = stream.cuda_stream
+        _check(lib().mdh_b200_run(self._h, self._dev_ptrs(d_in, self.inputs), self._dev_ptrs(d_out, self.outputs),
+                                  ctypes.c_void_p(stream)))
+
+    def time(self, d_in, d_out, warmup=3, reps=5, flush_l2=True):
+        """(median seconds per run, median seconds of the dominant kernel)."""
+        med, ker = ctypes.c_double(), ctypes.c_double()
+        _check(lib().mdh_b200_time(self._h, self._dev_ptrs(d_in, self.inputs), self._dev_ptrs(d_out, self.outputs),
+                                   warmup, reps, int(flush_l2), ctypes.byref(med), ctypes.byref(ker)))
+        return med.value, ker.value
+
+    # ---- host buffers (the end-to-end path) ------------------------------
+    def run_host(self, h_in: Sequence[np.ndarray], h_out: Optional[List[np.ndarray]] = None):
+        ins = []
+        for x, i in zip(h_in, self.inputs):
+            a = np.ascontiguousarray(x, dtype=i["np"])
+            if a.shape != i["shape"]:
+                raise MdhError(f"BufferTooSmall: input shape {a.shape} != {i['shape']}")
+            ins.append(a)
+        if h_out is None:
+            h_out = [np.empty(i["shape"], dtype=i["np"]) for i in self.outputs]
+        _check(lib().mdh_b200_run_host(self._h, _ptr_array([a.ctypes.data for a in ins]),
+                                       _ptr_array([a.ctypes.data for a in h_out]), None))
+        return h_out
+
+
+def execute(spec, inputs: Sequence[np.ndarray], asm="B200", config=None, **kw) -> List[np.ndarray]:
+    """reference_execute / interpret(lower(...)) on the B200: host in, host out."""
+    return Plan(spec, asm, config, **kw).run_host(inputs)
+
+
+def b200_time_objective(spec, asm="B200", config=None, reps=5, **kw) -> float:
+    """compiled_time_objective's role (autotuner.hpp:73): median seconds of the
+    instantiated kernel on synthetic device inputs, L2 flushed between reps."""
+    import torch
+    p = Plan(spec, asm, config, **kw)
+    ins = p.empty(0)
+    for t in ins:
+        if t.is_floating_point():
+            t.uniform_(-1, 1)
+        else:
+            t.random_(0, 3)
+    outs = p.empty(1)
+    med, _ = p.time(ins, outs, warmup=1, reps=reps)
+    torch.cuda.synchronize()
+    return med
+
+
+def validate_config(spec, asm, config) -> str:
+    need = ctypes.c_int64()
+    _check(lib().mdh_b200_validate_config(_text(spec), _text(asm), _text(config), None, 0, ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    _check(lib().mdh_b200_validate_config(_text(spec), _text(asm), _text(config), buf, need.value, ctypes.byref(need)))
+    return buf.value.decode()
+
+
+def tune(spec, asm="B200", budget=20, seed=0, **kw):
+    """mdh::tune with the on-device objective -> (best_config_json, history_csv, best_seconds)."""
+    o = options(**kw)
+    best = ctypes.create_string_buffer(1 << 20)
+    hist = ctypes.create_string_buffer(1 << 20)
+    secs = ctypes.c_double()
+    _check(lib().mdh_b200_tune(_text(spec), _text(asm), ctypes.byref(o), budget, ctypes.c_uint64(seed), best,
+                               1 << 20, hist, 1 << 20, ctypes.byref(secs)))
+    return best.value.decode(), hist.value.decode(), secs.value
+
+
+def version() -> str:
+    return lib().mdh_b200_version().decode()

@@ -1,0 +1,82 @@
+"""GPU parity of the generic md_hom family (device VM) against the frozen
+reference vectors and the oracle -- every bundled computation runs on the
+B200 through the C ABI."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from helpers import REFDATA, run_device
+from oracle import mdh_oracle as mo
+
+REFS = sorted(f[:-9] for f in os.listdir(os.path.join(REFDATA, "refs")))
+
+
+def load(name):
+    text = open(os.path.join(REFDATA, "computations", name + ".json")).read()
+    comp = mo.Computation.from_json(text)
+    j = json.load(open(os.path.join(REFDATA, "refs", name + ".ref.json")))
+    ins = [np.array(j["inputs"][b.name]["data"], dtype=np.float64 if b.type == "f64" else np.int64)
+           .reshape(j["inputs"][b.name]["dims"]) for b in comp.inputs]
+    outs = []
+    for b in comp.outputs:
+        g = j["outputs"][b.name]
+        outs.append((np.array([0 if x is None else x for x in g["data"]],
+                              dtype=np.float64 if b.type == "f64" else np.int64).reshape(g["dims"]),
+                     np.array([x is not None for x in g["data"]]).reshape(g["dims"])))
+    return text, comp, ins, outs
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", REFS)
+def test_generic_f64_matches_frozen_vectors_exactly(name):
+    from paper_2405_05118_b200 import mdh
+    text, comp, ins, want = load(name)
+    plan = mdh.Plan(text, float_storage=mdh.F64, int_storage=mdh.I64, generic=True)
+    assert plan.describe()["family"] == "generic"
+    got = run_device(plan, ins)
+    for g, (w, d) in zip(got, want):
+        assert np.array_equal(g[d], w[d]), name   # lex-order fold in f64: bit-exact
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", REFS)
+def test_auto_family_matches_oracle(name):
+    """Default storage (f32 / i64) and automatic family selection."""
+    from paper_2405_05118_b200 import mdh
+    text, comp, ins, _ = load(name)
+    plan = mdh.Plan(text)
+    got = run_device(plan, ins)
+    want = mo.execute(comp, ins)
+    K = int(np.prod([n for n, (k, _) in zip(comp.sizes, comp.combine) if k != "cc"] or [1]))
+    for g, (w, d) in zip(got, want):
+        if np.issubdtype(w.dtype, np.integer):
+            assert np.array_equal(g[d], w[d]), name
+        else:
+            from helpers import assert_close
+            assert_close(g, w, d, K, name)
+
+
+@pytest.mark.gpu
+def test_generic_prefix_and_tuples_on_device():
+    from paper_2405_05118_b200 import mdh
+    for name, sizes in [("scan", [1000]), ("mbbs", [8, 33]), ("double_reduce", [777]), ("histo", [500, 7])]:
+        text = json.load(open(os.path.join(REFDATA, "computations", name + ".json")))
+        text["sizes"] = sizes
+        comp = mo.Computation.from_json(text)
+        ins = mo.make_inputs(comp, 3)
+        if name == "histo":
+            ins = [np.abs(x) % 7 for x in ins]
+        plan = mdh.Plan(text)
+        got = run_device(plan, ins)
+        for g, (w, d) in zip(got, mo.execute(comp, ins)):
+            assert np.array_equal(g[d], w[d]), name
+
+
+@pytest.mark.gpu
+def test_run_host_end_to_end():
+    from paper_2405_05118_b200 import mdh
+    text, comp, ins, want = load("matvec")
+    got = mdh.execute(text, ins)
+    assert np.array_equal(got[0].astype(np.float64)[want[0][1]], want[0][0][want[0][1]])
