@@ -1,0 +1,442 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 MDH executor (BASELINE.json's metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--routine NAME] [--no-routines]
+
+A step = one execution of the md_hom (one pass of the hot path) over one
+batch of synthetic inputs already resident in HBM.  The headline workload is
+BASELINE configs[1], Jacobi3D fp32 with a 512^3 output (specs/jacobi3d_fp32.json);
+its inputs (543 MB) are larger than the 126 MB L2, so no flush is needed
+between steps.  Every other §8 routine is measured too (one line, key
+"routines"), each with its own roofline; those whose inputs fit in L2 are
+timed with an L2 flush between runs.
+
+Multi-GPU (torchrun, one rank per GPU, NCCL only for the barrier and the
+max-over-ranks timing): weak scaling -- rank r owns z-slab r of a
+(512*N) x 512 x 512 Jacobi3D, its input slab carrying the 1-plane halos
+(placed at distribution, no exchange in a single sweep).
+
+--impl reference times the reference's own CPU implementation of the path:
+the OpenMP C kernel its code generator emits (oracle/_ref, built from
+/root/reference by oracle/Makefile) on all host cores, on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = json.load(open(os.path.join(REPO, "BASELINE.json")))["metric"]
+HEADLINE = "jacobi3d_fp32"
+ROUTINES = ["matvec_fp32", "jacobi3d_fp32", "matmul_fp32", "matmul_fp32:tf32", "matmul_resnet_fc", "mcc_nhwc",
+            "mcc_nhwc:tf32", "ccsdt_abcdef_gdab_efgc", "prl_max"]
+L2_BYTES = 126 << 20
+
+
+def peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return {"hbm": j.get("hbm_gbs", 6650.0), "bf16": j.get("bf16_tflops", 1590.0),
+                "bf16_sustained": j.get("bf16_tflops_sustained", 1400.0), "sm_max_mhz": j.get("sm_max_mhz", 1965.0),
+                "source": "measured"}
+    return {"hbm": 6650.0, "bf16": 1590.0, "bf16_sustained": 1400.0, "sm_max_mhz": 1965.0, "source": "fallback"}
+
+
+def spec(name):
+    with open(os.path.join(REPO, "specs", name + ".json")) as f:
+        return json.load(f)
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """Polls NVML (SM clock, throttle reasons) while the timed region runs."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device_index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                bits = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for b, n in self.REASONS.items():
+                    if bits & b and b != 0x1:
+                        self.reasons.add(n)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ helpers
+def fill(tensors, seed):
+    import torch
+    g = torch.Generator(device=tensors[0].device).manual_seed(seed)
+    for t in tensors:
+        if t.is_floating_point():
+            t.uniform_(-1, 1, generator=g)
+        else:
+            t.random_(0, 3, generator=g)  # PRL fields in [0,3): forces ties and matches
+    return tensors
+
+
+def prl_weights(d_in):
+    # W (1..9) for the PRL spec: third buffer
+    d_in[2].copy_(d_in[2].new_tensor([3, 5, 7, 9]))
+
+
+def make_plan(name, device):
+    from paper_2405_05118_b200 import mdh
+    base, _, math = name.partition(":")
+    m = {"": mdh.MATH_FFMA, "tf32": mdh.MATH_TF32, "bf16": mdh.MATH_BF16}[math]
+    return mdh.Plan(spec(base), math=m, int_storage=mdh.I32, device=device), base, math or "ffma"
+
+
+def roofline_of(desc, kernel_s, pk, clock_mhz, traffic):
+    bound = desc["bound"]
+    if bound == "hbm":
+        ach = desc["bytes"] / kernel_s / 1e9
+        return {"bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm"], "unit": "GB/s",
+                "frac": round(ach / pk["hbm"], 4), "traffic": traffic, "peak_source": pk["source"]}
+    if bound == "int":
+        # integer issue roofline: 4 schedulers x 32 lanes per SM per clock
+        pairs = desc["template"]["pairs"]
+        ops = 6.0 * pairs  # instructions per pair of the packed path (see prl.cu)
+        peak = 148 * 128 * (clock_mhz or pk["sm_max_mhz"]) * 1e6 / 1e12
+        ach = ops / kernel_s / 1e12
+        return {"bound": "int-issue", "achieved": round(ach, 2), "peak": round(peak, 2), "unit": "Tops/s",
+                "frac": round(ach / peak, 4), "traffic": traffic, "pairs_per_s": pairs / kernel_s}
+    if bound == "tensor":
+        tflops = desc["flops"] / kernel_s / 1e12
+        peak = pk["bf16"] / 2.0 if desc["template"].get("math") == "tf32" else pk["bf16"]
+        return {"bound": "tensor", "achieved": round(tflops, 1), "peak": round(peak, 1), "unit": "TFLOP/s",
+                "frac": round(tflops / peak, 4), "traffic": traffic,
+                "peak_note": "TF32 dense = 1/2 of the measured BF16 cuBLAS peak" if desc["template"].get("math") == "tf32" else "measured BF16"}
+    # fp32 FFMA: 148 SMs x 128 lanes x 2 flop x clock
+    tflops = desc["flops"] / kernel_s / 1e12
+    peak = 148 * 128 * 2 * (clock_mhz or pk["sm_max_mhz"]) * 1e6 / 1e12
+    return {"bound": "fp32-ffma", "achieved": round(tflops, 2), "peak": round(peak, 2), "unit": "TFLOP/s",
+            "frac": round(tflops / peak, 4), "traffic": traffic, "peak_note": "148 SM x 128 FMA x 2 x SM clock"}
+
+
+def traffic_of(kernel):
+    p = os.path.join(REPO, "profiles", "traffic.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        for k, v in j.items():
+            if k in kernel:
+                return v
+    return None
+
+
+def time_device(plan, d_in, d_out, steps, warmup, flush):
+    """Device time of `steps` runs bracketed by events on the launching stream
+    (+ optional L2 flush outside the events); returns (total_s, per_run list)."""
+    import torch
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        plan.run(d_in, d_out)
+    torch.cuda.synchronize()
+    flush_buf = torch.empty(3 * L2_BYTES // 4, dtype=torch.float32, device=d_in[0].device) if flush else None
+    per = []
+    if flush:
+        for _ in range(steps):
+            flush_buf.fill_(1.0)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            plan.run(d_in, d_out)
+            b.record(stream)
+            b.synchronize()
+            per.append(a.elapsed_time(b) / 1e3)
+        return sum(per), per
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        plan.run(d_in, d_out)
+    b.record(stream)
+    b.synchronize()
+    tot = a.elapsed_time(b) / 1e3
+    return tot, [tot / steps] * steps
+
+
+# ------------------------------------------------------------------ CPU baseline
+def openmp_config(comp_json, threads):
+    """Blocked OpenMP configuration for the reference's emitter: the outermost
+    MDH layer is assigned to the COR core layer with `threads` parts along
+    dim 1 (tuning.cpp:373-381 "blocked"), everything else in MM."""
+    j = json.loads(comp_json)
+    D = len(j["sizes"])
+    n0 = j["sizes"][0]
+    t = max(1, min(threads, n0))
+    while n0 % t:
+        t -= 1
+    parts = [[t] + [1] * (D - 1), [n0 // t] + j["sizes"][1:], [1] * D, [1] * D]
+    layers = ["COR", "MM", "L2", "L1"]
+    ass = [[layers[l], d + 1] for l in range(4) for d in range(D)]
+    return json.dumps({"num_parts": parts, "ass_de": ass, "ass_scalar": ass, "ass_re": ass}), t
+
+
+def cpu_reference_run(name, sample_planes, threads, reps):
+    """Times the reference's emitted OpenMP kernel (f64) on an i-slab sample.
+    Returns (seconds per run, sample description, kind, cores)."""
+    from oracle import mdh_oracle as mo
+    from oracle import refbind
+    j = spec(name)
+    j["sizes"][0] = sample_planes
+    text = json.dumps(j)
+    comp = mo.Computation.from_json(text)
+    ins = [x.astype(np.float64) if vb.type == "f64" else x for vb, x in zip(comp.inputs, mo.make_inputs(comp, 1))]
+    outs = [np.zeros(s, dtype=np.float64 if vb.type == "f64" else np.int64)
+            for vb, s in zip(comp.outputs, mo.output_shapes(comp))]
+    try:
+        cfg, t = openmp_config(text, threads)
+        os.environ["OMP_NUM_THREADS"] = str(threads)
+        k = refbind.EmittedKernel(text, "OpenMP", cfg)
+        k(ins, outs)  # warm-up
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            k(ins, outs)
+            ts.append(time.perf_counter() - t0)
+        return statistics.median(ts), f"reference emitted OpenMP kernel (f64), {sample_planes}-plane i-slab of {name}", \
+            "reference", threads
+    except Exception as e:  # reference not built here: the C restatement, 1 thread
+        plan = mo.pw_outer_plan(comp)
+        t0 = time.perf_counter()
+        mo.execute(comp, ins, plan)
+        return time.perf_counter() - t0, f"oracle C restatement (f64, 1 thread; reference unavailable: {e})", "port", 1
+
+
+def cpu_points_bytes(name, planes):
+    j = spec(name)
+    full = j["sizes"][0]
+    return planes / full
+
+
+# ------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--routine", default=HEADLINE)
+    ap.add_argument("--no-routines", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        threads = os.cpu_count() or 1
+        planes = 32
+        per, sample, kind, cores = None, None, None, None
+        runs = []
+        for _ in range(max(1, args.warmup // 3)):
+            cpu_reference_run(args.routine, planes, threads, 1)
+        for _ in range(args.steps):
+            s, sample, kind, cores = cpu_reference_run(args.routine, planes, threads, 1)
+            runs.append(s)
+        per = statistics.median(runs)
+        frac = cpu_points_bytes(args.routine, planes)
+        full_bytes = bytes_of_spec(args.routine)
+        value = full_bytes * frac / per / 1e9
+        line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(per * 1e3, 3), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "impl": "reference",
+                "config": {"workload": f"{args.routine} ({planes}-plane i-slab sample per step)",
+                           "sample_fraction": frac, "threads": threads},
+                "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": cores, "kind": kind,
+                                 "sample": sample},
+                "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    device = local
+    torch.cuda.set_device(device)
+    pk = peaks()
+
+    # ---- headline: device-resident steps
+    plan, base, math = make_plan(args.routine, device)
+    desc = plan.describe()
+    d_in = fill(plan.empty(0), 1234 + rank)
+    if base == "prl_max":
+        prl_weights(d_in)
+    d_out = plan.empty(1)
+    in_bytes = sum(t.numel() * t.element_size() for t in d_in)
+    flush = in_bytes < 2 * L2_BYTES
+    sync_all(world)
+    with ClockSampler(device) as clk:
+        tot, per = time_device(plan, d_in, d_out, args.steps, args.warmup, flush)
+    tot = max_over_ranks(tot, world)
+    ms = tot / args.steps * 1e3
+    value = desc["bytes"] * world / (tot / args.steps) / 1e9 if desc["bound"] == "hbm" else \
+        desc["flops"] * world / (tot / args.steps) / 1e9
+    unit = "GB/s" if desc["bound"] == "hbm" else "GFLOP/s"
+    kernel_s = statistics.median(per)
+    clocks = clk.summary()
+    roof = roofline_of(desc, kernel_s, pk, clocks["sm_mhz"], traffic_of(desc["template"]["kernel"]))
+
+    # ---- e2e through the C ABI with pinned host buffers
+    e2e = e2e_measure(plan, d_in, max(3, min(args.steps, 10)), world)
+
+    line = {"metric": METRIC, "value": round(value, 2), "unit": unit, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32" if base != "prl_max" else "i32",
+            "data": "synthetic (uniform(-1,1) fp32, seeded per rank)",
+            "config": {"workload": f"{base} {spec(base)['sizes']} ({math})", "family": desc["family"],
+                       "kernel": desc["template"]["kernel"],
+                       "parallelism": f"++-sharded z-slabs x{world} (weak)" if world > 1 else "single GPU",
+                       "l2": "L2 flushed between steps" if flush else f"inputs ({in_bytes >> 20} MB) larger than L2"},
+            "roofline": roof, "clocks": clocks, "e2e": e2e,
+            "gpu_launches": plan.launches * args.steps}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        planes = 32
+        s, sample, kind, cores = cpu_reference_run(base, planes, threads, 3)
+        cpu_val = bytes_of_spec(base) * cpu_points_bytes(base, planes) / s / 1e9
+        line["cpu_baseline"] = {"value": round(cpu_val, 3), "unit": unit, "cores": cores, "kind": kind,
+                                "sample": sample + "; GB/s counted with the fp32 algorithmic bytes of the same points"}
+    if not args.no_routines:
+        line["routines"] = routines_table(device, pk, world, exclude=args.routine)
+        line["gpu_launches"] += sum(r.get("launches", 0) for r in line["routines"])
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def bytes_of_spec(name):
+    from oracle import mdh_oracle as mo  # shapes only (the CPU sample accounting)
+    comp = mo.Computation.from_json(spec(name))
+    n = sum(int(np.prod(s)) for s in mo.input_shapes(comp)) + sum(int(np.prod(s)) for s in mo.output_shapes(comp))
+    return 4 * n
+
+
+def sync_all(world):
+    import torch
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def e2e_measure(plan, d_in, reps, world):
+    """Host (pinned) inputs -> mdh_b200_run_host -> host outputs, wall clock."""
+    import torch
+    h_in = [t.cpu().pin_memory() for t in d_in]
+    tdt = {0: torch.float32, 1: torch.float64, 2: torch.int32, 3: torch.int64}
+    h_out = [torch.empty(o["shape"], dtype=tdt[o["dtype"]]).pin_memory() for o in plan.outputs]
+    np_in = [t.numpy() for t in h_in]
+    np_out = [t.numpy() for t in h_out]
+    plan.run_host(np_in, np_out)  # warm-up (allocates the plan's device buffers)
+    sync_all(world)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        plan.run_host(np_in, np_out)
+    dt = (time.perf_counter() - t0) / reps
+    dt = max_over_ranks(dt, world)
+    desc = plan.describe()
+    work = desc["bytes"] if desc["bound"] == "hbm" else desc["flops"]
+    unit = "GB/s" if desc["bound"] == "hbm" else "GFLOP/s"
+    return {"value": round(work * world / dt / 1e9, 2), "unit": unit,
+            "h2d_bytes_per_step": int(sum(a.nbytes for a in np_in)),
+            "d2h_bytes_per_step": int(sum(a.nbytes for a in np_out)), "ms_per_step": round(dt * 1e3, 3)}
+
+
+def routines_table(device, pk, world, exclude):
+    import torch
+    out = []
+    for name in ROUTINES:
+        if name == exclude:
+            continue
+        try:
+            plan, base, math = make_plan(name, device)
+        except Exception as e:
+            out.append({"routine": name, "error": str(e)})
+            continue
+        desc = plan.describe()
+        d_in = fill(plan.empty(0), 99)
+        if base == "prl_max":
+            prl_weights(d_in)
+        d_out = plan.empty(1)
+        in_bytes = sum(t.numel() * t.element_size() for t in d_in)
+        heavy = desc["flops"] > 1e11 or base == "prl_max"
+        steps = 3 if heavy else 20
+        tot, per = time_device(plan, d_in, d_out, steps, 2, in_bytes < 2 * L2_BYTES)
+        k = statistics.median(per)
+        roof = roofline_of(desc, k, pk, None, traffic_of(desc["template"]["kernel"]))
+        ent = {"routine": name, "family": desc["family"], "kernel": desc["template"]["kernel"],
+               "ms": round(k * 1e3, 4), "GB/s": round(desc["bytes"] / k / 1e9, 1),
+               "GFLOP/s": round(desc["flops"] / k / 1e9, 1), "roofline": roof, "launches": plan.launches * (steps + 2)}
+        if base == "prl_max":
+            ent["pairs_per_s"] = desc["template"]["pairs"] / k
+        out.append(ent)
+        del plan, d_in, d_out
+        torch.cuda.empty_cache()
+    return out
+
+
+if __name__ == "__main__":
+    main()

@@ -844,8 +844,29 @@ def concat_slice(c: Computation, dim: int, lo: int, hi: int) -> Tuple[Computatio
     return s, shifts
 
 
+def pw_outer_plan(c: Computation):
+    """A nest with the point-wise dims outermost (in their own order), then the
+    other dims.  Every result cell still folds its fiber in ascending lex
+    order over the pw dims, so the values are identical to lex_plan's
+    (engine.cpp:177-189 folds in visit order); only the cache behaviour of
+    the oracle changes."""
+    pw = [d for d in range(c.D) if c.combine[d][0] == "pw"]
+    rest = [d for d in range(c.D) if c.combine[d][0] != "pw"]
+    return [(d, c.sizes[d], 1) for d in pw + rest]
+
+
 def execute_slice(c: Computation, inputs, dim: int, lo: int, hi: int):
     """Oracle outputs of the [lo, hi) slab of cc-dimension `dim`, plus the
     per-output-buffer coordinate offset of that slab in the full result."""
     s, shifts = concat_slice(c, dim, lo, hi)
-    return execute(s, inputs), shifts
+    return execute(s, inputs, pw_outer_plan(s)), shifts
+
+
+def execute_box(c: Computation, inputs, box):
+    """Oracle outputs on a box of cc dims {dim: (lo, hi)} (several ++ slices
+    composed), with the per-output-buffer coordinate offsets."""
+    cur, total = c, None
+    for dim, (lo, hi) in sorted(box.items()):
+        cur, sh = concat_slice(cur, dim, lo, hi)
+        total = sh if total is None else [[a + b for a, b in zip(x, y)] for x, y in zip(total, sh)]
+    return execute(cur, inputs, pw_outer_plan(cur)), total

@@ -1,0 +1,124 @@
+"""Contraction family (MatVec, MatMul, ResNet-50 FC, MCC NHWC, CCSD(T)) vs the
+oracle.  Exact mode (the reference's own k/4 inputs, support.hpp:41-45) must be
+bit-identical; U(-1,1) inputs must satisfy |d| <= 1e-5 sqrt(K) max(|ref|,1)."""
+import numpy as np
+import pytest
+
+from helpers import assert_close, exact_inputs, run_device, spec, uniform_inputs
+from oracle import mdh_oracle as mo
+
+SMALL = [
+    ("matvec_fp32", [64, 128], "gemv"),
+    ("matvec_fp32", [300, 256], "gemv"),
+    ("matmul_fp32", [128, 128, 64], "sgemm"),
+    ("matmul_fp32", [256, 192, 72], "sgemm"),
+    ("matmul_fp32", [64, 64, 8], "sgemm"),
+    ("mcc_nhwc", [2, 8, 8, 64, 3, 3, 64], "sgemm"),
+    ("mcc_nhwc", [4, 8, 16, 64, 3, 3, 16], "sgemm"),
+    ("ccsdt_abcdef_gdab_efgc", [4, 4, 4, 4, 4, 4, 8], "sgemm"),
+    ("ccsdt_abcdef_gdab_efgc", [8, 4, 4, 4, 8, 4, 16], "sgemm"),
+    ("matmul_resnet_fc", [16, 1000, 2048], None),
+]
+
+
+def K_of(comp):
+    return int(np.prod([n for n, (k, _) in zip(comp.sizes, comp.combine) if k == "pw"]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,sizes,kernel", SMALL)
+def test_exact_mode_bit_identical(name, sizes, kernel):
+    from paper_2405_05118_b200 import mdh
+    j = spec(name, sizes)
+    comp = mo.Computation.from_json(j)
+    plan = mdh.Plan(j)
+    d = plan.describe()
+    if kernel:
+        assert d["family"] == "contraction" and kernel in d["template"]["kernel"], d
+    ins = exact_inputs(comp, 5)
+    got = run_device(plan, ins)
+    ((want, dfd),) = mo.execute(comp, ins)
+    assert np.array_equal(got[0].astype(np.float64)[dfd], want[dfd])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,sizes,kernel", SMALL)
+def test_uniform_mode_within_tolerance(name, sizes, kernel):
+    from paper_2405_05118_b200 import mdh
+    j = spec(name, sizes)
+    comp = mo.Computation.from_json(j)
+    plan = mdh.Plan(j)
+    ins = uniform_inputs(comp, 2)
+    got = run_device(plan, ins)
+    ((want, dfd),) = mo.execute(comp, ins)
+    assert_close(got[0], want, dfd, K_of(comp), name)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["matmul", "matmul_t", "bmatmul", "conv2d", "mcc", "dot", "matvec"])
+def test_bundled_contractions_vs_oracle(name):
+    """Bundled reference specs (i64) at sizes the tile menu accepts or not --
+    every one must run on the device and agree exactly."""
+    from helpers import bundled
+    from paper_2405_05118_b200 import mdh
+    sizes = {"matmul": [64, 64, 16], "matmul_t": [64, 128, 24], "bmatmul": [3, 6, 6, 6], "conv2d": [8, 8, 3, 3],
+             "mcc": [2, 4, 4, 2, 3, 3, 2], "dot": [1000], "matvec": [64, 128]}[name]
+    j = bundled(name, sizes)
+    for t in j["inputs"] + j["outputs"]:
+        t["type"] = "f64"
+    comp = mo.Computation.from_json(j)
+    plan = mdh.Plan(j)
+    ins = exact_inputs(comp, 9)
+    got = run_device(plan, ins)
+    ((want, dfd),) = mo.execute(comp, ins)
+    assert np.array_equal(got[0].astype(np.float64)[dfd], want[dfd]), plan.describe()
+
+
+def _full(name, slices):
+    """Full BASELINE size on the device; oracle on ++-slices of dim 0."""
+    import torch
+    from paper_2405_05118_b200 import mdh
+    j = spec(name)
+    comp = mo.Computation.from_json(j)
+    plan = mdh.Plan(j)
+    d = plan.describe()
+    assert d["family"] == "contraction", d
+    ins = exact_inputs(comp, 3)
+    d_in = plan.empty(0)
+    for t, x in zip(d_in, ins):
+        t.copy_(torch.from_numpy(x).to(t.dtype))
+    (out,) = plan.empty(1)
+    plan.run(d_in, [out])
+    torch.cuda.synchronize()
+    for box in slices:
+        if isinstance(box, tuple):
+            box = {0: box}
+        ((part, dfd),), shifts = mo.execute_box(comp, ins, box)
+        sl = tuple(slice(s, s + n) for s, n in zip(shifts[0], part.shape))
+        got = out[sl].cpu().numpy().astype(np.float64)
+        assert np.array_equal(got[dfd], part[dfd]), (name, box)
+
+
+@pytest.mark.gpu
+def test_matvec_full_size_exact():
+    _full("matvec_fp32", [(0, 4096)])
+
+
+@pytest.mark.gpu
+def test_matmul_8192_rows_exact():
+    _full("matmul_fp32", [(0, 1), (8191, 8192)])
+
+
+@pytest.mark.gpu
+def test_mcc_full_images_exact():
+    _full("mcc_nhwc", [(0, 1), (255, 256)])
+
+
+@pytest.mark.gpu
+def test_ccsdt_full_slices_exact():
+    _full("ccsdt_abcdef_gdab_efgc", [{0: (0, 1), 1: (0, 2)}, {0: (23, 24), 3: (22, 24)}])
+
+
+@pytest.mark.gpu
+def test_fc_full_exact():
+    _full("matmul_resnet_fc", [(0, 16)])
