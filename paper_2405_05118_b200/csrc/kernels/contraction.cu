@@ -30,9 +30,11 @@
 #include <sstream>
 
 #include "../plan.hpp"
+#include "contraction_common.hpp"
 
 namespace mdhb {
 namespace {
+using namespace ctr;
 
 constexpr int BK = 8;
 enum { LD_SCALAR = 0, LD_K4 = 1, LD_MN4 = 2 };  // vector direction of 16-byte loads
@@ -265,51 +267,6 @@ __global__ void __launch_bounds__(128) gemv_rows(GemvArgs g) {
 }
 
 // ---------------------------------------------------------------- host
-struct Groups {
-  int a_buf = 0, b_buf = 1;
-  Linear la, lb, lc;
-  std::vector<int> Md, Nd, Kd;  // outer -> inner
-};
-
-int64_t prod_sizes(const MdHom& e, const std::vector<int>& dims) {
-  int64_t p = 1;
-  for (int d : dims) p *= e.sizes[static_cast<size_t>(d)];
-  return p;
-}
-
-// Enumerates the box `ext` (row-major over dims) and returns sum_d c[dims[t]] * l_t * scale_t
-std::vector<int64_t> box_offsets(const std::vector<int>& dims, const std::vector<int64_t>& ext,
-                                 const std::vector<int64_t>& coef, const std::vector<int64_t>& scale) {
-  int64_t n = 1;
-  for (int64_t x : ext) n *= x;
-  std::vector<int64_t> out(static_cast<size_t>(n), 0);
-  std::vector<int64_t> l(dims.size(), 0);
-  for (int64_t t = 0; t < n; ++t) {
-    int64_t o = 0;
-    for (size_t q = 0; q < dims.size(); ++q) o += coef[static_cast<size_t>(dims[q])] * l[q] * scale[q];
-    out[static_cast<size_t>(t)] = o;
-    for (int q = static_cast<int>(dims.size()) - 1; q >= 0; --q) {
-      if (++l[static_cast<size_t>(q)] < ext[static_cast<size_t>(q)]) break;
-      l[static_cast<size_t>(q)] = 0;
-    }
-  }
-  return out;
-}
-
-// Splits `target` cells over the dims' extents (inner -> outer) with gcds;
-// empty when the box cannot be formed exactly.
-std::vector<int64_t> factor_box(const MdHom& e, const std::vector<int>& dims, int64_t target) {
-  std::vector<int64_t> t(dims.size(), 1);
-  int64_t rem = target;
-  for (int q = static_cast<int>(dims.size()) - 1; q >= 0 && rem > 1; --q) {
-    int64_t g = std::gcd(e.sizes[static_cast<size_t>(dims[static_cast<size_t>(q)])], rem);
-    t[static_cast<size_t>(q)] = g;
-    rem /= g;
-  }
-  if (rem != 1) return {};
-  return t;
-}
-
 class GemmRoutine final : public Routine {
  public:
   GemmRoutine(const Problem& p, Groups g) : p_(p), g_(std::move(g)) {}
@@ -431,7 +388,9 @@ class GemmRoutine final : public Routine {
     os << "{\"kernel\": \"sgemm_tiled<" << BM_ << "," << BN_ << ">\", \"M\": " << M_ << ", \"N\": " << N_
        << ", \"K\": " << K_ << ", \"BK\": " << BK << ", \"threads\": " << (BM_ / 8) * (BN_ / 8) << ", \"a_load\": \""
        << mn[amode_] << "\", \"b_load\": \"" << mn[bmode_] << "\", \"c_store\": \"" << (cvec_ ? "v4" : "scalar")
-       << "\", \"tiles\": " << static_cast<int64_t>(tilesM_) * tilesN_ << "}";
+       << "\", \"tiles\": " << static_cast<int64_t>(tilesM_) * tilesN_;
+    if (!note_.empty()) os << ", \"tc_declined\": \"" << note_ << "\"";
+    os << "}";
     return os.str();
   }
 
@@ -455,6 +414,7 @@ class GemmRoutine final : public Routine {
   }
 
   Config canonical(const Config* given) const;
+  bool is_gemv() const { return gemv_; }
 
  private:
   void tables(const std::vector<int64_t>& t0, const std::vector<int64_t>& t1, const std::vector<int64_t>& t2,
@@ -509,6 +469,11 @@ class GemmRoutine final : public Routine {
   int amode_ = 0, bmode_ = 0;
   bool cvec_ = false, gemv_ = false;
   void* blob_ = nullptr;
+
+ public:
+  std::string note_;  // why a requested tensor-core instance was declined
+
+ private:
   const int32_t* tab_[10] = {};
 };
 
@@ -597,25 +562,26 @@ Config GemmRoutine::canonical(const Config* given) const {
 
 }  // namespace
 
-std::unique_ptr<Routine> make_contraction(const Problem& p, const Config* cfg, Config* cfg_out) {
+// Recognises the contraction routine class and splits the dims into groups.
+bool analyze_contraction(const Problem& p, Groups& g) {
   const MdHom& e = p.e;
   const int D = e.D();
-  if (e.assigns.size() != 1 || e.out.size() != 1 || e.out[0].acc.size() != 1 || e.in.size() != 2) return nullptr;
+  if (e.assigns.size() != 1 || e.out.size() != 1 || e.out[0].acc.size() != 1 || e.in.size() != 2) return false;
   const Expr& f = e.assigns[0].e;
-  if (f.k != EK::Mul || f.args[0].k != EK::In || f.args[1].k != EK::In) return nullptr;
-  if (f.args[0].buf == f.args[1].buf) return nullptr;
-  if (e.in[0].acc.size() != 1 || e.in[1].acc.size() != 1) return nullptr;
-  if (e.in[0].type != Ty::F64 || e.in[1].type != Ty::F64 || e.out[0].type != Ty::F64) return nullptr;
-  if (p.opt.fstore != Store::F32) return nullptr;  // f64 storage: the generic path is the bit-exact one
+  if (f.k != EK::Mul || f.args[0].k != EK::In || f.args[1].k != EK::In) return false;
+  if (f.args[0].buf == f.args[1].buf) return false;
+  if (e.in[0].acc.size() != 1 || e.in[1].acc.size() != 1) return false;
+  if (e.in[0].type != Ty::F64 || e.in[1].type != Ty::F64 || e.out[0].type != Ty::F64) return false;
+  if (p.opt.fstore != Store::F32) return false;  // f64 storage: the generic path is the bit-exact one
   int npw = 0;
   for (auto& c : e.comb) {
-    if (c.kind == Combine::PS) return nullptr;
+    if (c.kind == Combine::PS) return false;
     if (c.kind == Combine::PW) {
-      if (c.op != Fold::Add) return nullptr;
+      if (c.op != Fold::Add) return false;
       ++npw;
     }
   }
-  if (npw == 0) return nullptr;
+  if (npw == 0) return false;
   // output access: every rank is exactly one cc dim, coefficient 1, no offset
   std::vector<int> seen(static_cast<size_t>(D), 0);
   for (auto& af : e.out[0].acc[0].idx) {
@@ -625,14 +591,13 @@ std::unique_ptr<Routine> make_contraction(const Problem& p, const Config* cfg, C
         nz = d;
         ++cnt;
       }
-    if (cnt != 1 || af.coeff[static_cast<size_t>(nz)] != 1 || af.c0 != 0) return nullptr;
-    if (e.comb[static_cast<size_t>(nz)].kind != Combine::CC) return nullptr;
+    if (cnt != 1 || af.coeff[static_cast<size_t>(nz)] != 1 || af.c0 != 0) return false;
+    if (e.comb[static_cast<size_t>(nz)].kind != Combine::CC) return false;
     seen[static_cast<size_t>(nz)]++;
   }
   for (int d = 0; d < D; ++d)
-    if (e.comb[static_cast<size_t>(d)].kind == Combine::CC && seen[static_cast<size_t>(d)] != 1) return nullptr;
+    if (e.comb[static_cast<size_t>(d)].kind == Combine::CC && seen[static_cast<size_t>(d)] != 1) return false;
 
-  Groups g;
   g.a_buf = f.args[0].buf - 1;
   g.b_buf = f.args[1].buf - 1;
   g.la = linearize(e.in[static_cast<size_t>(g.a_buf)].acc[0], p.in_ext[static_cast<size_t>(g.a_buf)], D);
@@ -643,7 +608,7 @@ std::unique_ptr<Routine> make_contraction(const Problem& p, const Config* cfg, C
     if (e.comb[static_cast<size_t>(d)].kind == Combine::PW) {
       g.Kd.push_back(d);
     } else if (da && db) {
-      return nullptr;  // batch dims: generic family
+      return false;  // batch dims: generic family
     } else if (da) {
       g.Md.push_back(d);
     } else {
@@ -655,7 +620,7 @@ std::unique_ptr<Routine> make_contraction(const Problem& p, const Config* cfg, C
     std::swap(g.la, g.lb);
     std::swap(g.Md, g.Nd);
   }
-  if (g.Md.empty()) return nullptr;
+  if (g.Md.empty()) return false;
   // dim order inside each group: largest output stride outermost; K by A stride
   auto by = [&](const std::vector<int64_t>& cj) {
     return [&cj](int x, int y) { return std::llabs(cj[static_cast<size_t>(x)]) > std::llabs(cj[static_cast<size_t>(y)]); };
@@ -669,7 +634,24 @@ std::unique_ptr<Routine> make_contraction(const Problem& p, const Config* cfg, C
     std::stable_sort(g.Kd.begin(), g.Kd.end(), by(a_unit ? g.la.cj : g.lb.cj));
   }
 
+  return true;
+}
+
+std::unique_ptr<Routine> make_contraction(const Problem& p, const Config* cfg, Config* cfg_out) {
+  Groups g;
+  if (!analyze_contraction(p, g)) return nullptr;
+  const MdHom& e = p.e;
+  std::string tc_why;
+  if (p.opt.math != Math::FFMA) {
+    if (p.opt.math == Math::TF32) {
+      auto tc = make_tc_contraction(p, g, cfg, cfg_out, &tc_why);
+      if (tc) return tc;
+    } else {
+      tc_why = "BF16 operands need a conversion pass (not instantiated)";
+    }
+  }
   auto r = std::make_unique<GemmRoutine>(p, g);
+  r->note_ = tc_why;
   bool ok = false;
   if (cfg) {
     // instantiate from the configuration's per-dim tile boxes
@@ -706,4 +688,23 @@ std::unique_ptr<Routine> make_contraction(const Problem& p, const Config* cfg, C
   return r;
 }
 
+}  // namespace mdhb
+
+namespace mdhb {
+// Tuning space of the FFMA contraction template: the (BM, BN) tile menu,
+// each instance reported through its canonical Table-1 configuration.
+std::vector<Config> contraction_space(const Problem& p) {
+  std::vector<Config> out;
+  Groups g;
+  if (!analyze_contraction(p, g)) return out;
+  const int menu[4][2] = {{128, 128}, {128, 64}, {64, 128}, {64, 64}};
+  for (auto& t : menu) {
+    GemmRoutine r(p, g);
+    if (!r.setup(t[0], t[1], {}, {})) continue;
+    Config c = r.canonical(nullptr);
+    if (config_violation(c, p.e, p.m, true).empty()) out.push_back(c);
+    if (r.is_gemv()) break;
+  }
+  return out;
+}
 }  // namespace mdhb

@@ -1,0 +1,68 @@
+// Shared host-side analysis of the contraction family (FFMA and tensor-core
+// templates): operand roles, dim groups and the additive offset tables.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <numeric>
+#include <vector>
+
+#include "../plan.hpp"
+
+namespace mdhb {
+namespace ctr {
+
+struct Groups {
+  int a_buf = 0, b_buf = 1;
+  Linear la, lb, lc;
+  std::vector<int> Md, Nd, Kd;  // outer -> inner
+};
+
+inline int64_t prod_sizes(const MdHom& e, const std::vector<int>& dims) {
+  int64_t p = 1;
+  for (int d : dims) p *= e.sizes[static_cast<size_t>(d)];
+  return p;
+}
+
+// Enumerates the box `ext` (row-major over dims) and returns sum_d c[dims[t]] * l_t * scale_t
+inline std::vector<int64_t> box_offsets(const std::vector<int>& dims, const std::vector<int64_t>& ext,
+                                 const std::vector<int64_t>& coef, const std::vector<int64_t>& scale) {
+  int64_t n = 1;
+  for (int64_t x : ext) n *= x;
+  std::vector<int64_t> out(static_cast<size_t>(n), 0);
+  std::vector<int64_t> l(dims.size(), 0);
+  for (int64_t t = 0; t < n; ++t) {
+    int64_t o = 0;
+    for (size_t q = 0; q < dims.size(); ++q) o += coef[static_cast<size_t>(dims[q])] * l[q] * scale[q];
+    out[static_cast<size_t>(t)] = o;
+    for (int q = static_cast<int>(dims.size()) - 1; q >= 0; --q) {
+      if (++l[static_cast<size_t>(q)] < ext[static_cast<size_t>(q)]) break;
+      l[static_cast<size_t>(q)] = 0;
+    }
+  }
+  return out;
+}
+
+// Splits `target` cells over the dims' extents (inner -> outer) with gcds;
+// empty when the box cannot be formed exactly.
+inline std::vector<int64_t> factor_box(const MdHom& e, const std::vector<int>& dims, int64_t target) {
+  std::vector<int64_t> t(dims.size(), 1);
+  int64_t rem = target;
+  for (int q = static_cast<int>(dims.size()) - 1; q >= 0 && rem > 1; --q) {
+    int64_t g = std::gcd(e.sizes[static_cast<size_t>(dims[static_cast<size_t>(q)])], rem);
+    t[static_cast<size_t>(q)] = g;
+    rem /= g;
+  }
+  if (rem != 1) return {};
+  return t;
+}
+
+// Tensor-core (tcgen05, TF32) instance of the contraction template for the
+// same groups; nullptr (and the reason in *why) when the operands cannot be
+// described as TMA boxes -- the caller then keeps the FFMA template.
+std::unique_ptr<Routine> make_tc_contraction(const Problem& p, const Groups& g, const Config* cfg, Config* cfg_out,
+                                             std::string* why);
+
+}  // namespace ctr
+}  // namespace mdhb

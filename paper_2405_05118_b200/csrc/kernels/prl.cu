@@ -434,3 +434,30 @@ std::unique_ptr<Routine> make_prl(const Problem& p, const Config* cfg, Config* c
 }
 
 }  // namespace mdhb
+
+namespace mdhb {
+// Tuning space of the PRL template: queries per thread (RM parts of q) x
+// record splits (SMX parts of r, combined in DM by atomicMax).
+std::vector<Config> prl_space(const Problem& p) {
+  std::vector<Config> out;
+  const MdHom& e = p.e;
+  if (p.m.id("SMX") < 0 || p.m.id("WRP") < 0 || e.D() != 2) return out;
+  int rdim = e.comb[0].kind == Combine::PW ? 0 : 1, qdim = 1 - rdim;
+  int64_t nq = e.sizes[static_cast<size_t>(qdim)], nr = e.sizes[static_cast<size_t>(rdim)];
+  for (int64_t qt : {4, 8, 16})
+    for (int64_t rs : {16, 32, 64, 128, 256}) {
+      int64_t qtile = 256 * qt;
+      if (nq % qtile || nr % rs || (nr / rs) % 2048) continue;
+      std::vector<int64_t> smx(2), dm(2, 1), wrp(2, 1), cc(2, 1), sm(2, 1), rm(2, 1);
+      smx[static_cast<size_t>(qdim)] = nq / qtile;
+      smx[static_cast<size_t>(rdim)] = rs;
+      dm[static_cast<size_t>(rdim)] = nr / rs / 2048;
+      wrp[static_cast<size_t>(qdim)] = 8;
+      cc[static_cast<size_t>(qdim)] = 32;
+      sm[static_cast<size_t>(rdim)] = 2048;
+      rm[static_cast<size_t>(qdim)] = qt;
+      out.push_back(make_config(p, {{"SMX", smx}, {"DM", dm}, {"WRP", wrp}, {"CC", cc}, {"SM", sm}, {"RM", rm}}, {}, "RM"));
+    }
+  return out;
+}
+}  // namespace mdhb

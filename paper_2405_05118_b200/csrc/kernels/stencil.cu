@@ -307,3 +307,19 @@ std::unique_ptr<Routine> make_stencil(const Problem& p, const Config* cfg, Confi
 }
 
 }  // namespace mdhb
+
+namespace mdhb {
+// Tuning space of the stencil template: i-planes per CTA (the DM parts of i).
+std::vector<Config> stencil_space(const Problem& p) {
+  std::vector<Config> out;
+  const MdHom& e = p.e;
+  if (p.m.id("SMX") < 0 || p.m.id("WRP") < 0) return out;
+  for (int64_t ti : {4, 8, 16, 32, 64, 128}) {
+    if (e.sizes[0] % ti || e.sizes[1] % 16 || e.sizes[2] % 128) continue;
+    std::vector<LayerParts> lp = {{"SMX", {e.sizes[0] / ti, e.sizes[1] / 16, e.sizes[2] / 128}}, {"DM", {ti, 1, 1}},
+                                  {"WRP", {1, 8, 1}}, {"CC", {1, 1, 32}}, {"SM", {1, 1, 1}}, {"RM", {1, 2, 4}}};
+    out.push_back(make_config(p, lp, {{e.in[0].name, "SM"}}, "RM"));
+  }
+  return out;
+}
+}  // namespace mdhb

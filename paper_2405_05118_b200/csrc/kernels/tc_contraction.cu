@@ -1,0 +1,510 @@
+// Tensor-core instance of the contraction template (MATH_TF32):
+// TMA -> 128B-swizzled shared memory -> tcgen05.mma.kind::tf32 -> TMEM ->
+// tcgen05.ld epilogue -> C through the additive offset tables.
+//
+// Each operand is described as a TMA box over its own buffer (no im2col,
+// no transposes): every buffer rank's index function is an affine sum of
+// md_hom dims, so a tile origin maps to per-rank coordinates
+//   coord[r] = c0_r + sum_{d in row dims} c_rd * origin_d + sum_{d in K} c_rd * k_d
+// which the planner tabulates per row tile and per k-tile.  A K-major
+// operand needs a K dim with unit coefficient in its innermost rank (32
+// elements = one 128-byte swizzle row per k-tile); an MN-major operand needs
+// a row dim there (32-element slabs) and the K dim in another rank.  MCC
+// over NHWC is therefore a plain 4-D box {32 c, 8 q, 8 p, 2 n} of the input
+// (the implicit GEMM needs no gather), and MatMul's B[k][n] is MN-major.
+//
+// CTA = 6 warps: warp 0 issues TMA, warp 1 owns TMEM and issues the MMAs
+// (one elected thread), warps 2-5 drain TMEM (lane quarter = warp % 4).
+// Pipelines: STAGES smem slots (full/empty mbarriers), one accumulator
+// (BM = 128 lanes x BN fp32 columns of TMEM).
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <sstream>
+
+#include "contraction_common.hpp"
+#include "tc_gemm.cuh"
+
+namespace mdhb {
+namespace ctr {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BKE = 32;  // k elements per tile = one 128-byte swizzle row of fp32
+constexpr int MAXR = 5;  // TMA rank limit
+
+struct TcArgs {
+  float* C;
+  const int32_t *tCm, *tCn, *cm, *cn;
+  const int32_t *a_mc, *a_kc, *b_nc, *b_kc;  // [tiles][MAXR] / [nk][MAXR], TMA order (innermost first)
+  int a_rank, b_rank;
+  int nk, tilesM, tilesN;
+  int cvec;
+};
+
+template <int BN, int STAGES, bool B_MN>
+__global__ void __launch_bounds__(192, 1)
+    tc_gemm_tf32(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, TcArgs g) {
+  constexpr uint32_t A_BYTES = BM * BKE * 4;
+  constexpr uint32_t B_BYTES = BN * BKE * 4;
+  constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // grouped raster over (tilesM x tilesN) for L2 reuse
+  constexpr int GROUP_M = 8;
+  const int x = blockIdx.x;
+  const int per_group = GROUP_M * g.tilesN;
+  const int first_m = (x / per_group) * GROUP_M;
+  const int gsz = min(g.tilesM - first_m, GROUP_M);
+  const int tm = first_m + (x % per_group) % gsz;
+  const int tn = (x % per_group) / gsz;
+
+  if (threadIdx.x == 0) {
+    tc::tma_prefetch(&tma_a);
+    tc::tma_prefetch(&tma_b);
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(tmem_full, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, TMEM_COLS);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer
+    for (int kt = 0; kt < g.nk; ++kt) {
+      const int s = kt % STAGES, it = kt / STAGES;
+      if (kt >= STAGES) tc::mbar_wait(&empty[s], (it - 1) & 1);
+      tc::mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+      uint8_t* sa = smem + s * STAGE_BYTES;
+      uint8_t* sb = sa + A_BYTES;
+      int c[MAXR];
+#pragma unroll
+      for (int r = 0; r < MAXR; ++r) c[r] = g.a_mc[tm * MAXR + r] + g.a_kc[kt * MAXR + r];
+      tc::tma_load(sa, &tma_a, &full[s], g.a_rank, c);
+#pragma unroll
+      for (int r = 0; r < MAXR; ++r) c[r] = g.b_nc[tn * MAXR + r] + g.b_kc[kt * MAXR + r];
+      if (B_MN) {
+        for (int j = 0; j < BN / 32; ++j) {
+          int cj[MAXR];
+#pragma unroll
+          for (int r = 0; r < MAXR; ++r) cj[r] = c[r];
+          cj[0] += 32 * j;
+          tc::tma_load(sb + j * (BKE * 128), &tma_b, &full[s], g.b_rank, cj);
+        }
+      } else {
+        tc::tma_load(sb, &tma_b, &full[s], g.b_rank, c);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer
+    constexpr uint32_t idesc = tc::instr_desc(2, 0, B_MN ? 1 : 0, BM, BN);
+    for (int kt = 0; kt < g.nk; ++kt) {
+      const int s = kt % STAGES, it = kt / STAGES;
+      tc::mbar_wait(&full[s], it & 1);
+      tc::tc_fence_after();
+      const uint32_t sa = tc::smem_u32(smem + s * STAGE_BYTES);
+      const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+      for (int k = 0; k < BKE / 8; ++k) {
+        const uint64_t da = tc::sw128_desc(sa + k * 32, 16, 1024);
+        // MN-major fp32 operands live in the 32-byte-atom 128B swizzle (layout 1):
+        // LBO = stride of 32-element MN slabs, SBO = stride of 4-row K atoms
+        const uint64_t db = B_MN ? tc::umma_desc(sb + k * 1024, BKE * 128, 512, 1) : tc::sw128_desc(sb + k * 32, 16, 1024);
+        tc::mma<true>(tmem, da, db, idesc, (kt | k) != 0 ? 1u : 0u);
+      }
+      tc::mma_commit(&empty[s]);  // frees the slot once these MMAs have read it
+    }
+    tc::mma_commit(tmem_full);
+  } else if (warp >= 2) {
+    // ---------------- epilogue: TMEM -> registers -> C
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = q * 32 + lane;
+    tc::mbar_wait(tmem_full, 0);
+    tc::tc_fence_after();
+    float* crow = g.C + g.tCm[tm] + g.cm[row] + g.tCn[tn];
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      uint32_t r[32];
+      tc::tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c0), r);
+      if (g.cvec) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(crow + g.cn[c0 + j]) =
+              make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) crow[g.cn[c0 + j]] = __uint_as_float(r[j]);
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, TMEM_COLS);
+}
+
+// ---------------------------------------------------------------- host
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encoder() {
+  static EncodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiled>(p);
+  });
+  if (!fn) fail("CudaError", "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// TMA description of one operand.
+struct View {
+  int buf = 0;
+  int rank = 0;                       // TMA rank (= buffer rank)
+  cuuint64_t dims[MAXR], strides[MAXR];  // innermost first; strides in bytes (strides[0] unused)
+  cuuint32_t box[MAXR];
+  std::vector<int> row_dims;          // smem row order (outer -> inner)
+  std::vector<int64_t> row_box;
+  bool mn = false;                    // MN-major (slabs of 32 along the inner row dim)
+  int kin = -1;                       // the K dim stepped by 32 per k-tile
+  std::vector<std::vector<int64_t>> coef;  // [TMA rank][dim]
+  std::vector<int64_t> c0;            // [TMA rank]
+};
+
+// Describes operand `b` (buffer) as a TMA view. `rows` = its row dims
+// (M for A, N for B), `K` = the contraction dims, `row_target` = BM or BN.
+bool describe_view(const Problem& p, int b, const std::vector<int>& rows, const std::vector<int>& K,
+                   int64_t row_target, bool allow_mn, View& v, std::string* why) {
+  const MdHom& e = p.e;
+  const Buf& buf = e.in[static_cast<size_t>(b)];
+  const int R = buf.rank, D = e.D();
+  if (R > MAXR) return *why = "rank > 5", false;
+  v.buf = b;
+  v.rank = R;
+  v.coef.assign(static_cast<size_t>(R), std::vector<int64_t>(static_cast<size_t>(D), 0));
+  v.c0.assign(static_cast<size_t>(R), 0);
+  int64_t stride = 4;
+  for (int t = 0; t < R; ++t) {  // t = TMA dim (innermost first), rank index R-1-t
+    const Affine& f = buf.acc[0].idx[static_cast<size_t>(R - 1 - t)];
+    v.dims[t] = static_cast<cuuint64_t>(p.in_ext[static_cast<size_t>(b)][static_cast<size_t>(R - 1 - t)]);
+    v.strides[t] = static_cast<cuuint64_t>(stride);
+    if (t > 0 && stride % 16) return *why = "TMA stride not a multiple of 16 bytes", false;
+    stride *= static_cast<int64_t>(v.dims[t]);
+    v.c0[static_cast<size_t>(t)] = f.c0;
+    for (int d = 0; d < D; ++d) v.coef[static_cast<size_t>(t)][static_cast<size_t>(d)] = f.coeff[static_cast<size_t>(d)];
+  }
+  auto is_row = [&](int d) { return std::find(rows.begin(), rows.end(), d) != rows.end(); };
+  auto is_k = [&](int d) { return std::find(K.begin(), K.end(), d) != K.end(); };
+  // the inner TMA dim decides the majorness
+  std::vector<int> inner;
+  for (int d = 0; d < D; ++d)
+    if (v.coef[0][static_cast<size_t>(d)] != 0) inner.push_back(d);
+  if (inner.size() != 1 || v.coef[0][static_cast<size_t>(inner[0])] != 1) return *why = "inner rank is not a single unit-stride dim", false;
+  int di = inner[0];
+  // row dims per rank (at most one, coefficient 1)
+  std::vector<int> rank_row(static_cast<size_t>(R), -1);
+  for (int t = 0; t < R; ++t)
+    for (int d = 0; d < D; ++d) {
+      int64_t c = v.coef[static_cast<size_t>(t)][static_cast<size_t>(d)];
+      if (c == 0) continue;
+      if (is_row(d)) {
+        if (c != 1 || rank_row[static_cast<size_t>(t)] >= 0) return *why = "row dim with non-unit coefficient or shared rank", false;
+        rank_row[static_cast<size_t>(t)] = d;
+      } else if (!is_k(d)) {
+        return *why = "operand depends on a dim outside its row / K groups", false;
+      }
+    }
+  for (int d : rows) {
+    int cnt = 0;
+    for (int t = 0; t < R; ++t) cnt += rank_row[static_cast<size_t>(t)] == d;
+    if (cnt != 1) return *why = "row dim not in exactly one rank", false;
+  }
+  for (int t = 0; t < R; ++t) v.box[t] = 1;
+  if (is_k(di)) {
+    // K-major: box 32 along the inner K dim, row boxes (outer -> inner by rank)
+    if (e.sizes[static_cast<size_t>(di)] % BKE) return *why = "inner K extent not a multiple of 32", false;
+    v.mn = false;
+    v.kin = di;
+    v.box[0] = BKE;
+    // factor the row target over the row ranks, innermost rank first
+    int64_t rem = row_target;
+    for (int t = 1; t < R; ++t) {
+      int d = rank_row[static_cast<size_t>(t)];
+      if (d < 0) continue;
+      int64_t gcd = std::gcd(e.sizes[static_cast<size_t>(d)], rem);
+      if (gcd > 256) gcd = 256;
+      v.box[t] = static_cast<cuuint32_t>(gcd);
+      rem /= gcd;
+    }
+    if (rem != 1) return *why = "row tile cannot be formed as a TMA box", false;
+    for (int t = R - 1; t >= 1; --t)
+      if (rank_row[static_cast<size_t>(t)] >= 0) {
+        v.row_dims.push_back(rank_row[static_cast<size_t>(t)]);
+        v.row_box.push_back(v.box[t]);
+      }
+  } else {
+    // MN-major: inner rank = a row dim, 32-element slabs; K dim in another rank
+    if (!allow_mn) return *why = "MN-major operand not supported here", false;
+    if (rows.size() != 1 || rank_row[0] != di) return *why = "MN-major operand needs a single row dim", false;
+    if (e.sizes[static_cast<size_t>(di)] % row_target || row_target % 32) return *why = "row tile does not split into slabs", false;
+    int tk = -1;
+    for (int t = 1; t < R; ++t)
+      for (int d : K)
+        if (v.coef[static_cast<size_t>(t)][static_cast<size_t>(d)] == 1 && e.sizes[static_cast<size_t>(d)] % BKE == 0) tk = t;
+    if (tk < 0) return *why = "no K rank with unit coefficient", false;
+    int kd = -1;
+    for (int d : K)
+      if (v.coef[static_cast<size_t>(tk)][static_cast<size_t>(d)] == 1) kd = d;
+    v.mn = true;
+    v.kin = kd;
+    v.box[0] = 32;
+    v.box[tk] = BKE;
+    v.row_dims = {di};
+    v.row_box = {row_target};
+  }
+  return true;
+}
+
+// coordinates (TMA order) of an origin given per-dim values
+std::vector<int32_t> coords(const View& v, const std::vector<int64_t>& origin, bool with_c0) {
+  std::vector<int32_t> c(MAXR, 0);
+  for (int t = 0; t < v.rank; ++t) {
+    int64_t x = with_c0 ? v.c0[static_cast<size_t>(t)] : 0;
+    for (size_t d = 0; d < origin.size(); ++d) x += v.coef[static_cast<size_t>(t)][d] * origin[d];
+    c[static_cast<size_t>(t)] = static_cast<int32_t>(x);
+  }
+  return c;
+}
+
+class TcRoutine final : public Routine {
+ public:
+  TcRoutine(const Problem& p, const Groups& g) : p_(p), g_(g) {}
+  ~TcRoutine() override {
+    if (blob_) cudaFree(blob_);
+  }
+  const char* family() const override { return "contraction"; }
+  const char* bound() const override { return "tensor"; }
+  int launches() const override { return 1; }
+  double flops() const override { return 2.0 * static_cast<double>(M_) * static_cast<double>(N_) * static_cast<double>(K_); }
+  double bytes() const override { return static_cast<double>(p_.in_bytes + p_.out_bytes); }
+  std::string describe() const override {
+    std::ostringstream os;
+    os << "{\"kernel\": \"tc_gemm_tf32<" << BN_ << "," << stages_ << "," << (va_.mn ? "A_MN" : "A_K") << ","
+       << (vb_.mn ? "B_MN" : "B_K") << ">\", \"math\": \"tf32\", \"M\": " << M_ << ", \"N\": " << N_ << ", \"K\": " << K_
+       << ", \"BM\": " << BM << ", \"BN\": " << BN_ << ", \"BK\": " << BKE << ", \"stages\": " << stages_
+       << ", \"umma\": \"tcgen05.mma.cta_group::1.kind::tf32 M128xN" << BN_ << "xK8\", \"tiles\": "
+       << static_cast<int64_t>(tilesM_) * tilesN_ << ", \"tmem_cols\": " << BN_ << "}";
+    return os.str();
+  }
+
+  bool setup(int BN, std::string* why) {
+    const MdHom& e = p_.e;
+    M_ = prod_sizes(e, g_.Md);
+    N_ = prod_sizes(e, g_.Nd);
+    K_ = prod_sizes(e, g_.Kd);
+    if (!describe_view(p_, g_.a_buf, g_.Md, g_.Kd, BM, false, va_, why)) return false;
+    if (!describe_view(p_, g_.b_buf, g_.Nd, g_.Kd, BN, true, vb_, why)) return false;
+    if (va_.kin != vb_.kin) return *why = "operands step different K dims", false;
+    BN_ = BN;
+    stages_ = BN >= 256 ? 4 : (BN >= 128 ? 6 : 8);
+    // row tiles: boxes over the row dims in the views' smem order
+    auto tiles = [&](const View& v, std::vector<std::vector<int64_t>>& origins) {
+      std::vector<int64_t> gext;
+      for (size_t q = 0; q < v.row_dims.size(); ++q) {
+        int64_t n = e.sizes[static_cast<size_t>(v.row_dims[q])];
+        if (n % v.row_box[q]) return false;
+        gext.push_back(n / v.row_box[q]);
+      }
+      int64_t cnt = 1;
+      for (auto x : gext) cnt *= x;
+      std::vector<int64_t> l(gext.size(), 0);
+      for (int64_t t = 0; t < cnt; ++t) {
+        std::vector<int64_t> o(static_cast<size_t>(e.D()), 0);
+        for (size_t q = 0; q < l.size(); ++q) o[static_cast<size_t>(v.row_dims[q])] = l[q] * v.row_box[q];
+        origins.push_back(o);
+        for (int q = static_cast<int>(l.size()) - 1; q >= 0; --q) {
+          if (++l[static_cast<size_t>(q)] < gext[static_cast<size_t>(q)]) break;
+          l[static_cast<size_t>(q)] = 0;
+        }
+      }
+      return true;
+    };
+    std::vector<std::vector<int64_t>> om, on;
+    if (!tiles(va_, om) || !tiles(vb_, on)) return *why = "row tiles do not divide", false;
+    tilesM_ = static_cast<int>(om.size());
+    tilesN_ = static_cast<int>(on.size());
+    // k-tiles: the K dims (kin stepped by 32, the rest by 1), kin innermost
+    std::vector<int> kd;
+    std::vector<int64_t> kext, kstep;
+    for (int d : g_.Kd)
+      if (d != va_.kin) {
+        kd.push_back(d);
+        kext.push_back(e.sizes[static_cast<size_t>(d)]);
+        kstep.push_back(1);
+      }
+    kd.push_back(va_.kin);
+    kext.push_back(e.sizes[static_cast<size_t>(va_.kin)] / BKE);
+    kstep.push_back(BKE);
+    nk_ = static_cast<int>(K_ / BKE);
+    std::vector<std::vector<int64_t>> ok;
+    {
+      std::vector<int64_t> l(kd.size(), 0);
+      for (int t = 0; t < nk_; ++t) {
+        std::vector<int64_t> o(static_cast<size_t>(e.D()), 0);
+        for (size_t q = 0; q < kd.size(); ++q) o[static_cast<size_t>(kd[q])] = l[q] * kstep[q];
+        ok.push_back(o);
+        for (int q = static_cast<int>(l.size()) - 1; q >= 0; --q) {
+          if (++l[static_cast<size_t>(q)] < kext[static_cast<size_t>(q)]) break;
+          l[static_cast<size_t>(q)] = 0;
+        }
+      }
+    }
+    // epilogue tables in the smem row orders of A (TMEM lanes) and B (columns)
+    std::vector<int64_t> tCm, tCn, cm, cn;
+    for (auto& o : om) {
+      int64_t x = g_.lc.c0;
+      for (int d = 0; d < e.D(); ++d) x += g_.lc.cj[static_cast<size_t>(d)] * o[static_cast<size_t>(d)];
+      tCm.push_back(x);
+    }
+    for (auto& o : on) {
+      int64_t x = 0;
+      for (int d = 0; d < e.D(); ++d) x += g_.lc.cj[static_cast<size_t>(d)] * o[static_cast<size_t>(d)];
+      tCn.push_back(x);
+    }
+    std::vector<int64_t> ones_m(va_.row_dims.size(), 1), ones_n(vb_.row_dims.size(), 1);
+    cm = box_offsets(va_.row_dims, va_.row_box, g_.lc.cj, ones_m);
+    cn = box_offsets(vb_.row_dims, vb_.row_box, g_.lc.cj, ones_n);
+    auto mod4 = [](const std::vector<int64_t>& v) {
+      for (auto x : v)
+        if (x % 4) return false;
+      return true;
+    };
+    bool grp = cn.size() % 4 == 0;
+    for (size_t t = 0; grp && t < cn.size(); t += 4)
+      for (size_t j = 1; j < 4; ++j) grp = grp && cn[t + j] == cn[t] + static_cast<int64_t>(j);
+    cvec_ = grp && mod4(cn) && mod4(cm) && mod4(tCm) && mod4(tCn);
+    // coordinate tables
+    std::vector<int64_t> amc, akc, bnc, bkc;
+    for (auto& o : om) for (auto c : coords(va_, o, true)) amc.push_back(c);
+    for (auto& o : ok) for (auto c : coords(va_, o, false)) akc.push_back(c);
+    for (auto& o : on) for (auto c : coords(vb_, o, true)) bnc.push_back(c);
+    for (auto& o : ok) for (auto c : coords(vb_, o, false)) bkc.push_back(c);
+    const std::vector<int64_t>* ts[8] = {&tCm, &tCn, &cm, &cn, &amc, &akc, &bnc, &bkc};
+    size_t total = 0;
+    for (auto* t : ts) total += (t->size() + 64) / 64 * 64;
+    std::vector<int32_t> host(total, 0);
+    size_t cur = 0, offs[8];
+    for (int q = 0; q < 8; ++q) {
+      offs[q] = cur;
+      for (int64_t x : *ts[q]) {
+        if (x > INT32_MAX || x < INT32_MIN) return *why = "offsets exceed int32", false;
+        host[cur++] = static_cast<int32_t>(x);
+      }
+      cur = (cur + 64) / 64 * 64;
+    }
+    MDHB_CUDA(cudaSetDevice(p_.opt.device));
+    MDHB_CUDA(cudaMalloc(&blob_, std::max<size_t>(cur, 64) * 4));
+    MDHB_CUDA(cudaMemcpy(blob_, host.data(), cur * 4, cudaMemcpyHostToDevice));
+    const int32_t* base = static_cast<const int32_t*>(blob_);
+    args_.tCm = base + offs[0];
+    args_.tCn = base + offs[1];
+    args_.cm = base + offs[2];
+    args_.cn = base + offs[3];
+    args_.a_mc = base + offs[4];
+    args_.a_kc = base + offs[5];
+    args_.b_nc = base + offs[6];
+    args_.b_kc = base + offs[7];
+    args_.a_rank = va_.rank;
+    args_.b_rank = vb_.rank;
+    args_.nk = nk_;
+    args_.tilesM = tilesM_;
+    args_.tilesN = tilesN_;
+    args_.cvec = cvec_;
+    smem_ = static_cast<size_t>(stages_) * (BM + BN) * BKE * 4 + 1024 + 256;
+    return true;
+  }
+
+  void launch(const void* const* d_in, void* const* d_out, cudaStream_t s) override {
+    const void* A = d_in[va_.buf];
+    const void* B = d_in[vb_.buf];
+    if (A != last_a_) encode(va_, A, &ma_), last_a_ = A;
+    if (B != last_b_) encode(vb_, B, &mb_), last_b_ = B;
+    TcArgs a = args_;
+    a.C = static_cast<float*>(d_out[0]);
+    dim3 grid(static_cast<unsigned>(tilesM_ * tilesN_));
+#define MDHB_TC(BNV, ST, MN)                                                                              \
+  if (BN_ == BNV && vb_.mn == MN) {                                                                      \
+    auto k = tc_gemm_tf32<BNV, ST, MN>;                                                                  \
+    MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_))); \
+    k<<<grid, 192, smem_, s>>>(ma_, mb_, a);                                                             \
+    MDHB_CUDA(cudaGetLastError());                                                                       \
+    return;                                                                                              \
+  }
+    MDHB_TC(256, 4, true) MDHB_TC(256, 4, false) MDHB_TC(128, 6, true) MDHB_TC(128, 6, false)
+    MDHB_TC(64, 8, true) MDHB_TC(64, 8, false)
+#undef MDHB_TC
+    fail("Unsupported", "no tensor-core instance for this tile");
+  }
+
+ private:
+  void encode(const View& v, const void* ptr, CUtensorMap* m) {
+    cuuint32_t estr[MAXR] = {1, 1, 1, 1, 1};
+    CUresult r = encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, static_cast<cuuint32_t>(v.rank), const_cast<void*>(ptr),
+                           v.dims, v.strides + 1, v.box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           v.mn ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail("CudaError", "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+  }
+
+  const Problem& p_;
+  Groups g_;
+  View va_, vb_;
+  int64_t M_ = 0, N_ = 0, K_ = 0;
+  int BN_ = 0, stages_ = 0, nk_ = 0, tilesM_ = 0, tilesN_ = 0;
+  bool cvec_ = false;
+  size_t smem_ = 0;
+  void* blob_ = nullptr;
+  TcArgs args_{};
+  CUtensorMap ma_{}, mb_{};
+  const void* last_a_ = nullptr;
+  const void* last_b_ = nullptr;
+};
+
+}  // namespace
+
+std::unique_ptr<Routine> make_tc_contraction(const Problem& p, const Groups& g, const Config* cfg, Config* cfg_out,
+                                             std::string* why) {
+  for (int bn : {256, 128, 64}) {
+    auto r = std::make_unique<TcRoutine>(p, g);
+    std::string w;
+    if (r->setup(bn, &w)) {
+      if (cfg_out) *cfg_out = cfg ? *cfg : baseline_config(p.e, p.m);
+      return r;
+    }
+    *why = w;
+  }
+  return nullptr;
+}
+
+}  // namespace ctr
+}  // namespace mdhb

@@ -45,7 +45,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch(const void* tmap) {
-  asm volatile("prefetch.tensor.global.tensormap [%0];" ::"l"(tmap) : "memory");
+  asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }
 __device__ __forceinline__ void tma_load(void* dst, const void* tmap, uint64_t* bar, int rank, const int* c) {
   uint32_t d = smem_u32(dst), b = smem_u32(bar);
@@ -121,9 +121,15 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 // Shared-memory matrix descriptor (SM100 UMMA): start>>4 [0,14), LBO>>4
 // [16,30), SBO>>4 [32,46), version 1 [46,48), layout type [61,64)
 // (2 = 128-byte swizzle).  Tile bases are 1024-byte aligned (base_offset 0).
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+// layout 2 = SWIZZLE_128B (16-byte atoms; K-major operands), layout 1 =
+// SWIZZLE_128B_BASE32B (32-byte atoms; the only layout for MN-major 32-bit
+// operands -- TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, K atom of 4 rows).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes, uint32_t layout) {
   return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFF) << 16) |
-         (static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
+         (static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32) | (1ull << 46) | (static_cast<uint64_t>(layout) << 61);
+}
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  return umma_desc(saddr, lbo_bytes, sbo_bytes, 2);
 }
 
 // Instruction descriptor: F32 accumulate; A/B format (2 = TF32, 1 = BF16);

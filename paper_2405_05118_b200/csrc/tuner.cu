@@ -1,0 +1,230 @@
+// On-device auto-tuner: the reference's search (autotuner.cpp:245-305 --
+// 3/10 of the budget random, then first-improving hill climbing, ties broken
+// by the lowest config hash, history of exactly `budget` rows) over the part
+// of the Table-1 space the selected kernel template can instantiate, with
+// compiled_time_objective replaced by CUDA-event timing on the B200.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <random>
+#include <sstream>
+
+#include "../../include/mdh_b200.h"
+#include "plan.hpp"
+
+namespace mdhb {
+namespace {
+
+uint64_t fnv1a(const std::string& s) {  // config_hash (autotuner.cpp:39-47)
+  uint64_t h = 14695981039346656037ULL;
+  for (unsigned char c : s) {
+    h ^= c;
+    h *= 1099511628211ULL;
+  }
+  return h;
+}
+
+__global__ void fill_uniform(float* p, int64_t n, uint32_t seed) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint32_t x = static_cast<uint32_t>(i) * 2654435761u ^ seed;
+    x ^= x >> 13;
+    x *= 0x5bd1e995u;
+    x ^= x >> 15;
+    p[i] = (x & 0xFFFFFF) / 8388608.0f - 1.0f;
+  }
+}
+__global__ void fill_small_int(void* p, int64_t n, int is64, uint32_t seed) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint32_t x = static_cast<uint32_t>(i) * 2246822519u ^ seed;
+    x ^= x >> 16;
+    int v = static_cast<int>(x % 3u);
+    if (is64) static_cast<int64_t*>(p)[i] = v; else static_cast<int32_t*>(p)[i] = v;
+  }
+}
+
+// two configurations are neighbours when one prime factor moved between two
+// layers of one dimension (default_neighborhood, autotuner.cpp:131-212)
+bool neighbours(const Config& a, const Config& b) {
+  if (a.parts.size() != b.parts.size()) return false;
+  int diffs = 0;
+  for (size_t d = 0; d < a.parts[0].size(); ++d) {
+    std::vector<size_t> ls;
+    for (size_t l = 0; l < a.parts.size(); ++l)
+      if (a.parts[l][d] != b.parts[l][d]) ls.push_back(l);
+    if (ls.empty()) continue;
+    if (ls.size() != 2) return false;
+    ++diffs;
+    int64_t x = a.parts[ls[0]][d], y = b.parts[ls[0]][d];
+    int64_t r = x > y ? x / y : y / x;
+    if ((x > y ? x % y : y % x) != 0 || r < 2) return false;
+    for (int64_t q = 2; q * q <= r; ++q)
+      if (r % q == 0) return false;  // must be a prime factor
+  }
+  return diffs == 1;
+}
+
+}  // namespace
+
+// per-family candidate spaces live next to each template
+std::vector<Config> stencil_space(const Problem& p);
+std::vector<Config> contraction_space(const Problem& p);
+std::vector<Config> prl_space(const Problem& p);
+
+std::vector<Config> family_space(const Problem& p, const std::string& family) {
+  if (family == "stencil") return stencil_space(p);
+  if (family == "contraction") return contraction_space(p);
+  if (family == "prl") return prl_space(p);
+  return {baseline_config(p.e, p.m)};
+}
+
+}  // namespace mdhb
+
+extern "C" int mdh_b200_tune(const char* comp_json, const char* asm_model, const mdh_b200_options* o, int budget,
+                             uint64_t seed, char* best_config, int64_t best_cap, char* history_csv, int64_t hist_cap,
+                             double* best_seconds) {
+  using namespace mdhb;
+  mdh_b200_plan* probe = nullptr;
+  if (mdh_b200_plan_create(comp_json, asm_model, nullptr, o, &probe)) return 1;
+  std::string family;
+  {
+    int64_t need = 0;
+    mdh_b200_describe(probe, nullptr, 0, &need);
+    std::string d(static_cast<size_t>(need), '\0');
+    mdh_b200_describe(probe, d.data(), need, &need);
+    auto at = d.find("\"family\": \"");
+    family = d.substr(at + 11, d.find('"', at + 11) - at - 11);
+  }
+  // inputs / outputs on the device, synthetic
+  std::vector<void*> din, dout;
+  int nin = 0, nout = 0;
+  mdh_b200_buffer_count(probe, 0, &nin);
+  mdh_b200_buffer_count(probe, 1, &nout);
+  auto alloc = [&](int side, int b, std::vector<void*>& v) {
+    int64_t dims[16], bytes = 0;
+    int rank = 0, dt = 0;
+    mdh_b200_buffer_info(probe, side, b, dims, &rank, &dt, &bytes);
+    void* ptr = nullptr;
+    if (cudaMalloc(&ptr, static_cast<size_t>(std::max<int64_t>(bytes, 16))) != cudaSuccess) return false;
+    if (side == 0) {
+      int64_t n = bytes / (dt == MDH_B200_F32 || dt == MDH_B200_I32 ? 4 : 8);
+      if (dt == MDH_B200_F32) fill_uniform<<<256, 256>>>(static_cast<float*>(ptr), n, 17u + b);
+      else if (dt == MDH_B200_I32 || dt == MDH_B200_I64) fill_small_int<<<256, 256>>>(ptr, n, dt == MDH_B200_I64, 5u + b);
+      else cudaMemset(ptr, 0, static_cast<size_t>(bytes));
+    }
+    v.push_back(ptr);
+    return true;
+  };
+  bool ok = true;
+  for (int b = 0; b < nin; ++b) ok = ok && alloc(0, b, din);
+  for (int b = 0; b < nout; ++b) ok = ok && alloc(1, b, dout);
+  // W of a PRL spec: small positive weights
+  int rc = 0;
+  try {
+    if (!ok) fail("CudaError", "tuner buffer allocation failed");
+    if (budget < 1) fail("InvalidConfig", "tuning budget must be at least 1, got " + std::to_string(budget));
+    Problem prob;
+    prob.e = parse_md_hom(comp_json);
+    prob.m = resolve_asm(asm_model ? asm_model : "B200");
+    prob.in_ext = infer_extents(prob.e.in, prob.e.sizes);
+    prob.out_ext = infer_extents(prob.e.out, prob.e.collapsed());
+    if (o) {
+      prob.opt.fstore = static_cast<Store>(o->float_storage);
+      prob.opt.istore = static_cast<Store>(o->int_storage);
+      prob.opt.math = static_cast<Math>(o->math);
+      prob.opt.device = o->device;
+    }
+    for (auto& b : prob.e.in) prob.in_store.push_back(prob.store_of(b.type));
+    for (auto& b : prob.e.out) prob.out_store.push_back(prob.store_of(b.type));
+    std::vector<Config> space = family_space(prob, family);
+    if (space.empty()) space.push_back(baseline_config(prob.e, prob.m));
+    std::vector<std::string> texts;
+    for (auto& c : space) texts.push_back(config_json(c, prob.e, prob.m));
+
+    std::mt19937_64 rng(seed);
+    struct Ev {
+      int idx;
+      uint64_t hash;
+      double obj;
+      bool valid;
+    };
+    std::vector<Ev> hist;
+    std::vector<double> memo(space.size(), -1.0);
+    double best = std::numeric_limits<double>::infinity();
+    int best_i = -1;
+    auto evaluate = [&](int i) {
+      double obj = std::numeric_limits<double>::infinity();
+      bool valid = true;
+      if (memo[static_cast<size_t>(i)] >= 0) {
+        obj = memo[static_cast<size_t>(i)];
+      } else {
+        mdh_b200_plan* pl = nullptr;
+        if (mdh_b200_plan_create(comp_json, asm_model, texts[static_cast<size_t>(i)].c_str(), o, &pl) == 0) {
+          double med = 0, ker = 0;
+          if (mdh_b200_time(pl, din.data(), dout.data(), 1, 3, 1, &med, &ker) == 0) obj = med;
+          else valid = false;
+          mdh_b200_plan_destroy(pl);
+        } else {
+          valid = false;
+        }
+        memo[static_cast<size_t>(i)] = valid ? obj : std::numeric_limits<double>::infinity();
+      }
+      uint64_t h = fnv1a(texts[static_cast<size_t>(i)]);
+      hist.push_back({static_cast<int>(hist.size()), h, obj, valid && std::isfinite(obj)});
+      if (valid && (obj < best || (obj == best && best_i >= 0 && h < fnv1a(texts[static_cast<size_t>(best_i)])))) {
+        best = obj;
+        best_i = i;
+      }
+      return obj;
+    };
+    const int n = static_cast<int>(space.size());
+    int n_random = std::min(budget, std::max(1, budget * 3 / 10));
+    for (int k = 0; k < n_random; ++k) evaluate(static_cast<int>(rng() % static_cast<uint64_t>(n)));
+    while (static_cast<int>(hist.size()) < budget) {
+      bool improved = false;
+      if (best_i >= 0) {
+        std::vector<int> nb;
+        for (int j = 0; j < n; ++j)
+          if (j != best_i && neighbours(space[static_cast<size_t>(best_i)], space[static_cast<size_t>(j)])) nb.push_back(j);
+        std::shuffle(nb.begin(), nb.end(), rng);
+        for (int j : nb) {
+          if (static_cast<int>(hist.size()) >= budget) break;
+          double before = best;
+          evaluate(j);
+          if (best < before) {
+            improved = true;
+            break;
+          }
+        }
+      }
+      if (!improved && static_cast<int>(hist.size()) < budget) evaluate(static_cast<int>(rng() % static_cast<uint64_t>(n)));
+    }
+    if (best_i < 0) fail("NoValidConfigFound", "every evaluated configuration failed");
+    std::ostringstream csv;
+    csv << "eval_index,config_hash,objective,valid\n";
+    for (auto& e : hist) {
+      char buf[64];
+      std::snprintf(buf, sizeof buf, "%.17g", e.obj);
+      csv << e.idx << "," << e.hash << "," << buf << "," << (e.valid ? 1 : 0) << "\n";
+    }
+    auto put = [](const std::string& s, char* b, int64_t cap) {
+      if (!b || cap <= 0) return;
+      size_t k = std::min<size_t>(s.size(), static_cast<size_t>(cap - 1));
+      std::memcpy(b, s.data(), k);
+      b[k] = '\0';
+    };
+    put(texts[static_cast<size_t>(best_i)], best_config, best_cap);
+    put(csv.str(), history_csv, hist_cap);
+    if (best_seconds) *best_seconds = best;
+  } catch (const Error& e) {
+    rc = 1;
+    // surface through the ABI's last-error slot: re-run a failing call
+    mdh_b200_plan* dummy = nullptr;
+    mdh_b200_plan_create("{", asm_model, nullptr, o, &dummy);
+    (void)e;
+  }
+  for (void* d : din) cudaFree(d);
+  for (void* d : dout) cudaFree(d);
+  mdh_b200_plan_destroy(probe);
+  return rc;
+}

@@ -1,0 +1,90 @@
+"""Tensor-core (tcgen05 kind::tf32) instance of the contraction family.
+
+Exact mode (k/4 inputs, |k| <= 5) is representable in TF32 and every partial
+sum is exact in FP32, so results must be bit-identical to the oracle.  In
+U(-1,1) mode the bound is the stated TF32 one:
+    |d_ij| <= 2^-9 * sum_k |a_ik| |b_kj|   (operand truncation to 10 bits + FP32 accumulate)
+with sum|a||b| computed by the oracle itself on |A|, |B|."""
+import numpy as np
+import pytest
+
+from helpers import exact_inputs, run_device, spec, uniform_inputs
+from oracle import mdh_oracle as mo
+
+CASES = [
+    ("matmul_fp32", [128, 256, 64], "tc_gemm_tf32<256"),
+    ("matmul_fp32", [256, 512, 96], "tc_gemm_tf32<256"),
+    ("matmul_fp32", [128, 128, 32], "tc_gemm_tf32<128"),
+    ("mcc_nhwc", [2, 8, 8, 64, 3, 3, 64], "tc_gemm_tf32<64"),
+    ("mcc_nhwc", [4, 16, 8, 64, 3, 3, 32], "tc_gemm_tf32<64"),
+]
+
+
+def plan_tf32(j):
+    from paper_2405_05118_b200 import mdh
+    return mdh.Plan(j, math=mdh.MATH_TF32)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,sizes,kernel", CASES)
+def test_tf32_exact_mode_bit_identical(name, sizes, kernel):
+    j = spec(name, sizes)
+    comp = mo.Computation.from_json(j)
+    plan = plan_tf32(j)
+    d = plan.describe()
+    assert d["family"] == "contraction" and d["template"]["kernel"].startswith(kernel), d
+    ins = exact_inputs(comp, 4)
+    (got,) = run_device(plan, ins)
+    ((want, dfd),) = mo.execute(comp, ins)
+    assert np.array_equal(got.astype(np.float64)[dfd], want[dfd])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,sizes,kernel", CASES)
+def test_tf32_uniform_mode_bound(name, sizes, kernel):
+    j = spec(name, sizes)
+    comp = mo.Computation.from_json(j)
+    plan = plan_tf32(j)
+    ins = uniform_inputs(comp, 8)
+    (got,) = run_device(plan, ins)
+    ((want, dfd),) = mo.execute(comp, ins)
+    ((absw, _),) = mo.execute(comp, [np.abs(x) for x in ins])
+    err = np.abs(got.astype(np.float64) - want)
+    assert (err <= 2.0 ** -9 * absw + 1e-30)[dfd].all(), float((err / np.maximum(absw, 1e-30)).max())
+
+
+@pytest.mark.gpu
+def test_tf32_matmul_8192_exact_rows():
+    import torch
+    j = spec("matmul_fp32")
+    comp = mo.Computation.from_json(j)
+    plan = plan_tf32(j)
+    assert "tc_gemm_tf32" in plan.describe()["template"]["kernel"]
+    ins = exact_inputs(comp, 3)
+    d_in = plan.empty(0)
+    for t, x in zip(d_in, ins):
+        t.copy_(torch.from_numpy(x).to(t.dtype))
+    (out,) = plan.empty(1)
+    plan.run(d_in, [out])
+    torch.cuda.synchronize()
+    for lo in (0, 8191):
+        ((part, dfd),), sh = mo.execute_box(comp, ins, {0: (lo, lo + 1)})
+        assert np.array_equal(out[lo:lo + 1].cpu().numpy().astype(np.float64), part)
+
+
+@pytest.mark.gpu
+def test_tf32_mcc_full_image_exact():
+    import torch
+    j = spec("mcc_nhwc")
+    comp = mo.Computation.from_json(j)
+    plan = plan_tf32(j)
+    assert "tc_gemm_tf32" in plan.describe()["template"]["kernel"]
+    ins = exact_inputs(comp, 3)
+    d_in = plan.empty(0)
+    for t, x in zip(d_in, ins):
+        t.copy_(torch.from_numpy(x).to(t.dtype))
+    (out,) = plan.empty(1)
+    plan.run(d_in, [out])
+    torch.cuda.synchronize()
+    ((part, dfd),), sh = mo.execute_box(comp, ins, {0: (255, 256)})
+    assert np.array_equal(out[255:256].cpu().numpy().astype(np.float64), part)
