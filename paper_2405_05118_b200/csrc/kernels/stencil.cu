@@ -16,6 +16,7 @@
 // Algorithmic traffic per run: every input cell read once + every output cell
 // written once = 4 * (514^3 + 512^3) B for the BASELINE size.
 #include <array>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 
@@ -158,6 +159,153 @@ __global__ void __launch_bounds__(NTHREADS, 3) star7_kernel(StencilArgs a) {
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// v2: the same 2.5D scheme with the plane rows moved by the TMA engine
+// (cp.async.bulk, one 16-byte-aligned bulk copy per row, completion tracked
+// by an mbarrier per ring slot).  No load/store instructions are spent on
+// staging, and NSLOT-2 planes stay in flight per CTA, which is what keeps
+// enough bytes outstanding to run at copy bandwidth.  Rows whose global
+// offset is not 16-byte aligned are copied from the aligned address below
+// them; the per-row float shift (0 or 2 for the BASELINE extents) is
+// re-applied when the row is read from shared memory.
+constexpr int NSLOT = 6;                 // ring slots
+constexpr int PD = NSLOT - 1;            // planes in flight ahead of compute
+constexpr int BPITCH = TK + 12;          // floats per smem row: 128 + halo 2 + shift <= 3, 16B rounded
+
+__device__ __forceinline__ uint32_t s_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+template <int TJ>
+__global__ void __launch_bounds__(NTHREADS, 3) star7_bulk(StencilArgs a) {
+  constexpr int ROWS = TJ + 2;
+  constexpr int JPT = TJ / 8;
+  extern __shared__ __align__(128) float sring[];  // [NSLOT][ROWS][BPITCH]
+  __shared__ __align__(8) uint64_t full[NSLOT];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * TK;
+  const int64_t j0 = static_cast<int64_t>(blockIdx.y) * TJ;
+  const int64_t i0 = static_cast<int64_t>(blockIdx.z) * a.ti;
+  const int kl = lane * 4, jl = warp * JPT;
+  const int iend = static_cast<int>(a.n0 - i0 < a.ti ? a.n0 - i0 : a.ti);
+  const int nplanes = iend + 2;  // input planes i0 .. i0+iend+1
+
+  if (tid == 0) {
+    for (int s = 0; s < NSLOT; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_u32(&full[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // row r of input plane p -> slot p % NSLOT (warp 0 issues, lane r copies row r)
+  auto issue = [&](int p) {
+    if (warp != 0 || p >= nplanes) return;
+    const int s = p % NSLOT;
+    const int64_t ip = i0 + p;
+    if (lane == 0) {
+      uint32_t bytes = 0;
+      for (int r = 0; r < ROWS; ++r) {
+        int64_t off = (ip * a.e1 + j0 + r) * a.e2 + k0;
+        uint32_t sh = static_cast<uint32_t>(off & 3);
+        bytes += (sh * 4 + (TK + 2) * 4 + 15) & ~15u;
+      }
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(&full[s])), "r"(bytes) : "memory");
+    }
+    __syncwarp();
+    for (int r = lane; r < ROWS; r += 32) {
+      int64_t off = (ip * a.e1 + j0 + r) * a.e2 + k0;
+      uint32_t sh = static_cast<uint32_t>(off & 3);
+      uint32_t bytes = (sh * 4 + (TK + 2) * 4 + 15) & ~15u;
+      const float* src = a.v + (off - sh);
+      float* dst = sring + (static_cast<size_t>(s) * ROWS + r) * BPITCH;
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(s_u32(dst)), "l"(src), "r"(bytes), "r"(s_u32(&full[s])) : "memory");
+    }
+  };
+  auto wait_plane = [&](int p) {
+    const int s = p % NSLOT;
+    const uint32_t parity = static_cast<uint32_t>((p / NSLOT) & 1);
+    uint32_t done = 0;
+    for (uint32_t spin = 0; !done; ++spin) {
+      asm volatile("{\n\t.reg .pred q;\n\tmbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n\tselp.u32 %0, 1, 0, q;\n\t}"
+                   : "=r"(done) : "r"(s_u32(&full[s])), "r"(parity) : "memory");
+      if (spin > (1u << 26)) __trap();
+    }
+  };
+  // 6 floats of row r of plane p starting at local column c
+  auto row6 = [&](int p, int r, int c, float (&x)[6]) {
+    const int64_t off = ((i0 + p) * a.e1 + j0 + r) * a.e2 + k0;
+    const int sh = static_cast<int>(off & 3);
+    const float* row = sring + (static_cast<size_t>(p % NSLOT) * ROWS + r) * BPITCH + sh + c;
+    if ((sh & 1) == 0) {
+      float2 u = *reinterpret_cast<const float2*>(row), v = *reinterpret_cast<const float2*>(row + 2),
+             w = *reinterpret_cast<const float2*>(row + 4);
+      x[0] = u.x; x[1] = u.y; x[2] = v.x; x[3] = v.y; x[4] = w.x; x[5] = w.y;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 6; ++q) x[q] = row[q];
+    }
+  };
+
+  for (int p = 0; p < PD && p < nplanes; ++p) issue(p);
+  wait_plane(0);
+  wait_plane(1);
+  float cprev[JPT][4], ccur[JPT][6];
+#pragma unroll
+  for (int jj = 0; jj < JPT; ++jj) {
+    float x[6];
+    row6(0, jl + 1 + jj, kl, x);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) cprev[jj][c] = x[c + 1];
+    row6(1, jl + 1 + jj, kl, ccur[jj]);
+  }
+  for (int t = 0; t < iend; ++t) {
+    wait_plane(t + 2);
+    float nxt[JPT][6], jm[6], jp[6];
+#pragma unroll
+    for (int jj = 0; jj < JPT; ++jj) row6(t + 2, jl + 1 + jj, kl, nxt[jj]);
+    row6(t + 1, jl, kl, jm);
+    row6(t + 1, jl + JPT + 1, kl, jp);
+    const int64_t i = i0 + t;
+#pragma unroll
+    for (int jj = 0; jj < JPT; ++jj) {
+      const float* up = jj == 0 ? jm : ccur[jj - 1];
+      const float* dn = jj == JPT - 1 ? jp : ccur[jj + 1];
+      float o[4];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        float acc = a.wc * ccur[jj][kk + 1];
+        acc = fmaf(a.wim, cprev[jj][kk], acc);
+        acc = fmaf(a.wip, nxt[jj][kk + 1], acc);
+        acc = fmaf(a.wjm, up[kk + 1], acc);
+        acc = fmaf(a.wjp, dn[kk + 1], acc);
+        acc = fmaf(a.wkm, ccur[jj][kk], acc);
+        acc = fmaf(a.wkp, ccur[jj][kk + 2], acc);
+        o[kk] = acc;
+      }
+      const int64_t j = j0 + jl + jj, k = k0 + kl;
+      if (j < a.n1 && k < a.n2) {
+        float* dst = a.w + (i * a.n1 + j) * a.n2 + k;
+        if (k + 4 <= a.n2 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+          __stcs(reinterpret_cast<float4*>(dst), make_float4(o[0], o[1], o[2], o[3]));
+        } else {
+          for (int kk = 0; kk < 4 && k + kk < a.n2; ++kk) dst[kk] = o[kk];
+        }
+      }
+    }
+#pragma unroll
+    for (int jj = 0; jj < JPT; ++jj) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) cprev[jj][c] = ccur[jj][c + 1];
+#pragma unroll
+      for (int c = 0; c < 6; ++c) ccur[jj][c] = nxt[jj][c];
+    }
+    // every thread is done with plane t+1 (its last reader): the slot of plane
+    // t + PD (== slot of plane t + PD - NSLOT <= t - 2) may be refilled
+    __syncthreads();
+    issue(t + PD);
+  }
+}
+
 // ---------------------------------------------------------------- host
 // Recognises  sum_t lit_t * in(1, a_t)  (any association of + over terms,
 // literal on either side of *, a bare in(1,a) = weight 1).
@@ -183,12 +331,12 @@ bool linear_terms(const Expr& e, std::vector<std::pair<double, int>>& terms) {
 
 class StencilRoutine final : public Routine {
  public:
-  StencilRoutine(const Problem& p, StencilArgs a, int tj) : p_(p), a_(a), tj_(tj) {}
+  StencilRoutine(const Problem& p, StencilArgs a, int tj, bool bulk) : p_(p), a_(a), tj_(tj), bulk_(bulk) {}
   const char* family() const override { return "stencil"; }
   std::string describe() const override {
     std::ostringstream os;
-    os << "{\"kernel\": \"star7_kernel<" << tj_ << ">\", \"TK\": " << TK << ", \"TJ\": " << tj_ << ", \"TI\": " << a_.ti
-       << ", \"threads\": " << NTHREADS << ", \"smem_ring_slots\": 4, \"grid\": [" << grid().x << ", " << grid().y
+ os << "{\"kernel\": \"" << (bulk_ ? "star7_bulk<" : "star7_kernel<") << tj_ << ">\", \"TK\": " << TK << ", \"TJ\": " << tj_ << ", \"TI\": " << a_.ti
+       << ", \"threads\": " << NTHREADS << ", \"smem_ring_slots\": " << (bulk_ ? NSLOT : 4) << ", \"grid\": [" << grid().x << ", " << grid().y
        << ", " << grid().z << "]}";
     return os.str();
   }
@@ -203,7 +351,17 @@ class StencilRoutine final : public Routine {
     StencilArgs a = a_;
     a.v = static_cast<const float*>(d_in[0]);
     a.w = static_cast<float*>(d_out[0]);
-    star7_kernel<16><<<grid(), NTHREADS, 0, s>>>(a);
+    if (bulk_) {
+      const size_t smem = static_cast<size_t>(NSLOT) * 18 * BPITCH * sizeof(float);
+      static bool attr = false;
+      if (!attr) {
+        MDHB_CUDA(cudaFuncSetAttribute(star7_bulk<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        attr = true;
+      }
+      star7_bulk<16><<<grid(), NTHREADS, smem, s>>>(a);
+    } else {
+      star7_kernel<16><<<grid(), NTHREADS, 0, s>>>(a);
+    }
     MDHB_CUDA(cudaGetLastError());
   }
 
@@ -211,6 +369,7 @@ class StencilRoutine final : public Routine {
   const Problem& p_;
   StencilArgs a_;
   int tj_;
+  bool bulk_;
 };
 
 }  // namespace
@@ -303,7 +462,12 @@ std::unique_ptr<Routine> make_stencil(const Problem& p, const Config* cfg, Confi
         *cfg_out = make_config(p, lp, {{in.name, "SM"}}, "RM");
     }
   }
-  return std::make_unique<StencilRoutine>(p, a, TJ);
+  // TMA bulk row copies need every copied span inside the allocation: the
+  // buffer size must be 16-byte rounded (rows overrun at most to the next
+  // 16-byte boundary) and the k tiles must not reach past the row end.
+  const int64_t vbytes = p.in_ext[0][0] * a.e1 * a.e2 * 4;
+  const bool bulk = vbytes % 16 == 0 && a.n2 % TK == 0 && !std::getenv("MDHB_STENCIL_V1");
+  return std::make_unique<StencilRoutine>(p, a, TJ, bulk);
 }
 
 }  // namespace mdhb
