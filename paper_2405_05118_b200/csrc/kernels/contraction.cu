@@ -266,18 +266,74 @@ __global__ void __launch_bounds__(128) gemv_rows(GemvArgs g) {
   }
 }
 
+
+// Skinny contraction (small M, e.g. the ResNet-50 FC layer 16 x 1000 x 2048):
+// a 128-row tile would idle 7/8 of its rows, so K is split across CTAs
+// instead.  Thread t of CTA (nt, ks) owns column n = nt*256 + t for all M
+// rows (M accumulators in registers) over the k-slice ks; B rows stream
+// coalesced along n, the A slice is staged once in shared memory and read
+// as broadcasts.  Partial sums land in a [splits][M][N] scratch and a second
+// pass folds them in fixed split order (deterministic).
+struct SkinnyArgs {
+  const float* A;
+  const float* B;
+  float* part;
+  float* C;
+  const int32_t *am, *ak, *bk, *bn, *cm, *cn;
+  int M, N, K, ks;  // ks = k per split
+  int splits;
+};
+
+template <int MT>
+__global__ void __launch_bounds__(256) skinny_partial(SkinnyArgs g) {
+  extern __shared__ float sA[];  // [M][ks]
+  const int n = blockIdx.x * 256 + threadIdx.x;
+  const int k0 = blockIdx.y * g.ks;
+  for (int i = threadIdx.x; i < g.M * g.ks; i += 256) {
+    int m = i / g.ks, k = i - m * g.ks;
+    sA[i] = __ldg(g.A + g.am[m] + g.ak[k0 + k]);
+  }
+  __syncthreads();
+  if (n >= g.N) return;
+  float acc[MT];
+#pragma unroll
+  for (int m = 0; m < MT; ++m) acc[m] = 0.f;
+  const float* Bn = g.B + g.bn[n];
+#pragma unroll 4
+  for (int k = 0; k < g.ks; ++k) {
+    const float b = __ldcs(Bn + g.bk[k0 + k]);
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+      if (m < g.M) acc[m] = fmaf(sA[m * g.ks + k], b, acc[m]);
+  }
+  float* out = g.part + static_cast<int64_t>(blockIdx.y) * g.M * g.N;
+#pragma unroll
+  for (int m = 0; m < MT; ++m)
+    if (m < g.M) out[m * g.N + n] = acc[m];
+}
+
+__global__ void __launch_bounds__(256) skinny_fold(SkinnyArgs g) {
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  if (i >= g.M * g.N) return;
+  const int m = i / g.N, n = i - m * g.N;
+  float s = g.part[i];
+  for (int sp = 1; sp < g.splits; ++sp) s += g.part[static_cast<int64_t>(sp) * g.M * g.N + i];
+  g.C[g.cm[m] + g.cn[n]] = s;
+}
+
 // ---------------------------------------------------------------- host
 class GemmRoutine final : public Routine {
  public:
   GemmRoutine(const Problem& p, Groups g) : p_(p), g_(std::move(g)) {}
   ~GemmRoutine() override {
     if (blob_) cudaFree(blob_);
+    if (part_) cudaFree(part_);
   }
   const char* family() const override { return "contraction"; }
   double flops() const override { return 2.0 * static_cast<double>(M_) * static_cast<double>(N_) * static_cast<double>(K_); }
   double bytes() const override { return static_cast<double>(p_.in_bytes + p_.out_bytes); }
-  const char* bound() const override { return gemv_ ? "hbm" : "fp32"; }
-  int launches() const override { return 1; }
+  const char* bound() const override { return (gemv_ || skinny_) ? "hbm" : "fp32"; }
+  int launches() const override { return skinny_ ? 2 : 1; }
 
   // Builds tables; returns false when this template cannot realise the problem.
   bool setup(int BM, int BN, const std::vector<int64_t>& Tm_in, const std::vector<int64_t>& Tn_in) {
@@ -294,6 +350,31 @@ class GemmRoutine final : public Routine {
     const int64_t a0 = g_.la.c0, b0 = g_.lb.c0, c0 = g_.lc.c0;
     std::vector<int64_t> tAm, tCm, tBn, tCn, am, cm, bn, cn;
     gemv_ = g_.Nd.empty();
+    if (!gemv_ && M_ <= 32 && N_ >= 64 && K_ >= 256 && Tm_in.empty()) {
+      // skinny: split K so that ~2 waves of CTAs stream B
+      std::vector<int64_t> fullM, fullN;
+      for (int d : g_.Md) fullM.push_back(e.sizes[static_cast<size_t>(d)]);
+      for (int d : g_.Nd) fullN.push_back(e.sizes[static_cast<size_t>(d)]);
+      am = box_offsets(g_.Md, fullM, g_.la.cj, scale1(g_.Md.size()));
+      cm = box_offsets(g_.Md, fullM, g_.lc.cj, scale1(g_.Md.size()));
+      bn = box_offsets(g_.Nd, fullN, g_.lb.cj, scale1(g_.Nd.size()));
+      cn = box_offsets(g_.Nd, fullN, g_.lc.cj, scale1(g_.Nd.size()));
+      for (auto& v : am) v += a0;
+      for (auto& v : bn) v += b0;
+      for (auto& v : cm) v += c0;
+      int64_t ntiles = (N_ + 255) / 256;
+      int64_t want = std::max<int64_t>(1, 2 * sm_count(p_.opt.device) / ntiles);
+      int64_t ks = 64;
+      while (ks * 2 <= K_ / want && ks < 1024) ks *= 2;
+      while (K_ % ks) ks /= 2;
+      if (ks < 8) return false;
+      skinny_ = true;
+      ks_ = static_cast<int>(ks);
+      splits_ = static_cast<int>(K_ / ks);
+      MDHB_CUDA(cudaMalloc(&part_, static_cast<size_t>(splits_) * M_ * N_ * sizeof(float)));
+      tables(am, ak, bk, bn, cm, cn, {}, {}, {}, {});
+      return true;
+    }
     if (gemv_) {
       // rows must be contiguous in k, x contiguous too
       for (int64_t k = 0; k < K_; ++k)
@@ -381,6 +462,12 @@ class GemmRoutine final : public Routine {
   std::string describe() const override {
     std::ostringstream os;
     const char* mn[] = {"scalar", "k4", "mn4"};
+    if (skinny_) {
+      os << "{\"kernel\": \"skinny_partial<" << (M_ <= 16 ? 16 : 32) << ">+skinny_fold\", \"M\": " << M_
+         << ", \"N\": " << N_ << ", \"K\": " << K_ << ", \"k_per_split\": " << ks_ << ", \"splits\": " << splits_
+         << ", \"threads\": 256}";
+      return os.str();
+    }
     if (gemv_) {
       os << "{\"kernel\": \"gemv_rows<2>\", \"M\": " << M_ << ", \"K\": " << K_ << ", \"threads\": 128}";
       return os.str();
@@ -398,6 +485,19 @@ class GemmRoutine final : public Routine {
     const float* A = static_cast<const float*>(d_in[g_.a_buf]);
     const float* B = static_cast<const float*>(d_in[g_.b_buf]);
     float* C = static_cast<float*>(d_out[0]);
+    if (skinny_) {
+      SkinnyArgs a{A, B, part_, C, tab_[0], tab_[1], tab_[2], tab_[3], tab_[4], tab_[5], static_cast<int>(M_),
+                   static_cast<int>(N_), static_cast<int>(K_), ks_, splits_};
+      dim3 grid(static_cast<unsigned>((N_ + 255) / 256), static_cast<unsigned>(splits_));
+      size_t smem = static_cast<size_t>(M_) * ks_ * sizeof(float);
+      if (smem > 48 * 1024) MDHB_CUDA(cudaFuncSetAttribute(skinny_partial<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      if (M_ <= 16) skinny_partial<16><<<grid, 256, smem, s>>>(a);
+      else skinny_partial<32><<<grid, 256, smem, s>>>(a);
+      MDHB_CUDA(cudaGetLastError());
+      skinny_fold<<<static_cast<unsigned>((M_ * N_ + 255) / 256), 256, 0, s>>>(a);
+      MDHB_CUDA(cudaGetLastError());
+      return;
+    }
     if (gemv_) {
       GemvArgs a{A, B + g_.lb.c0, C, tab_[0], tab_[1], M_, static_cast<int>(K_)};
       constexpr int ROWS = 2;
@@ -467,7 +567,9 @@ class GemmRoutine final : public Routine {
   int BM_ = 0, BN_ = 0, tilesM_ = 0, tilesN_ = 0;
   std::vector<int64_t> Tm_, Tn_;
   int amode_ = 0, bmode_ = 0;
-  bool cvec_ = false, gemv_ = false;
+  bool cvec_ = false, gemv_ = false, skinny_ = false;
+  int ks_ = 0, splits_ = 0;
+  float* part_ = nullptr;
   void* blob_ = nullptr;
 
  public:
@@ -506,6 +608,9 @@ void place(const std::vector<int64_t>& T, const std::vector<std::pair<int, int64
 Config GemmRoutine::canonical(const Config* given) const {
   if (given) return *given;
   const MdHom& e = p_.e;
+  // the skinny split-K instance tiles N by 256 threads with a masked tail:
+  // not a uniform partition, reported as the baseline configuration
+  if (skinny_) return baseline_config(e, p_.m);
   if (p_.m.id("SMX") < 0 || p_.m.id("CC") < 0) return baseline_config(e, p_.m);
   const int D = e.D();
   // layers: 0 SMX, 1 DM, 2 WRP, 3 CC, 4 SM, 5 RM

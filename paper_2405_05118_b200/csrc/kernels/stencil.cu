@@ -306,6 +306,163 @@ __global__ void __launch_bounds__(NTHREADS, 3) star7_bulk(StencilArgs a) {
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// v3 (default): warp-specialised.  Warp 8 is the producer: it streams input
+// planes into the NSLOT ring with cp.async.bulk (one copy per row, tx-counted
+// on full[slot]) as soon as the 8 compute warps release a slot (empty[slot],
+// one arrival per warp).  Compute warps never meet a CTA-wide barrier; they
+// rotate three register row-sets (previous / current / next plane) with a
+// 3-way unrolled loop so no register copies are needed.
+constexpr int WS_THREADS = 288;  // 8 compute warps + 1 producer warp
+
+struct Rows {
+  float r[2][6];  // the thread's centre rows (j = jl+1, jl+2), cols kl .. kl+5
+};
+
+__device__ __forceinline__ void ld6(const float* row, int sh, float (&x)[6]) {
+  if ((sh & 1) == 0) {
+    float2 u = *reinterpret_cast<const float2*>(row), v = *reinterpret_cast<const float2*>(row + 2),
+           w = *reinterpret_cast<const float2*>(row + 4);
+    x[0] = u.x; x[1] = u.y; x[2] = v.x; x[3] = v.y; x[4] = w.x; x[5] = w.y;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 6; ++q) x[q] = row[q];
+  }
+}
+
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  for (uint32_t spin = 0; !done; ++spin) {
+    asm volatile("{\n\t.reg .pred q;\n\tmbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n\tselp.u32 %0, 1, 0, q;\n\t}"
+                 : "=r"(done) : "r"(s_u32(bar)), "r"(parity) : "memory");
+    if (spin > (1u << 26)) __trap();
+  }
+}
+
+__global__ void __launch_bounds__(WS_THREADS, 3) star7_ws(StencilArgs a) {
+  constexpr int TJ = 16, ROWS = TJ + 2;
+  extern __shared__ __align__(128) float sring[];  // [NSLOT][ROWS][BPITCH]
+  __shared__ __align__(8) uint64_t full[NSLOT], empty[NSLOT];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * TK;
+  const int64_t j0 = static_cast<int64_t>(blockIdx.y) * TJ;
+  const int64_t i0 = static_cast<int64_t>(blockIdx.z) * a.ti;
+  const int iend = static_cast<int>(a.n0 - i0 < a.ti ? a.n0 - i0 : a.ti);
+  const int nplanes = iend + 2;
+  // low two bits of flat offsets decide each row's 16-byte shift
+  const uint32_t pstride = static_cast<uint32_t>(a.e1 * a.e2);
+  const uint32_t base0 = static_cast<uint32_t>((i0 * a.e1 + j0) * a.e2 + k0);
+  const uint32_t rstride = static_cast<uint32_t>(a.e2);
+
+  if (tid == 0) {
+    for (int s = 0; s < NSLOT; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_u32(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(s_u32(&empty[s])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 8) {
+    // ---------------- producer
+    const float* vbase = a.v + ((i0 * a.e1 + j0) * a.e2 + k0);
+    for (int p = 0; p < nplanes; ++p) {
+      const int s = p % NSLOT;
+      if (p >= NSLOT) mbar_wait_parity(&empty[s], static_cast<uint32_t>((p / NSLOT - 1) & 1));
+      uint32_t bytes = 0, sh = 0;
+      if (lane < ROWS) {
+        sh = (base0 + static_cast<uint32_t>(p) * pstride + static_cast<uint32_t>(lane) * rstride) & 3u;
+        bytes = (sh * 4 + (TK + 2) * 4 + 15) & ~15u;
+      }
+      uint32_t total = bytes;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(&full[s])), "r"(total) : "memory");
+      __syncwarp();
+      if (lane < ROWS && i0 + p < a.e0) {
+        const float* src = vbase + static_cast<int64_t>(p) * (a.e1 * a.e2) + static_cast<int64_t>(lane) * a.e2 - sh;
+        float* dst = sring + (static_cast<size_t>(s) * ROWS + lane) * BPITCH;
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(s_u32(dst)), "l"(src), "r"(bytes), "r"(s_u32(&full[s])) : "memory");
+      }
+    }
+    return;
+  }
+
+  // ---------------- 8 compute warps: 4 (k) x 2 (j) outputs per thread
+  const int kl = lane * 4, jl = warp * 2;
+  auto rowptr = [&](int p, int r, int& sh) {
+    sh = static_cast<int>((base0 + static_cast<uint32_t>(p) * pstride + static_cast<uint32_t>(r) * rstride) & 3u);
+    return sring + (static_cast<size_t>(p % NSLOT) * ROWS + r) * BPITCH + sh + kl;
+  };
+  auto load_centre = [&](int p, Rows& R) {
+    int sh;
+    const float* q0 = rowptr(p, jl + 1, sh);
+    ld6(q0, sh, R.r[0]);
+    const float* q1 = rowptr(p, jl + 2, sh);
+    ld6(q1, sh, R.r[1]);
+  };
+  auto release = [&](int p) {
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(&empty[p % NSLOT])) : "memory");
+  };
+  float* wout = a.w + (i0 * a.n1 + j0 + jl) * a.n2 + k0 + kl;
+  const int64_t wplane = a.n1 * a.n2;
+  const bool kin = k0 + kl + 4 <= a.n2;
+
+  auto step = [&](int t, const Rows& P, const Rows& C, Rows& N) {
+    mbar_wait_parity(&full[(t + 2) % NSLOT], static_cast<uint32_t>(((t + 2) / NSLOT) & 1));
+    load_centre(t + 2, N);
+    float jm[6], jp[6];
+    int sh;
+    const float* qm = rowptr(t + 1, jl, sh);
+    ld6(qm, sh, jm);
+    const float* qp = rowptr(t + 1, jl + 3, sh);
+    ld6(qp, sh, jp);
+    release(t + 1);  // plane t+1 has no readers after this step
+#pragma unroll
+    for (int jj = 0; jj < 2; ++jj) {
+      const float* up = jj == 0 ? jm : C.r[0];
+      const float* dn = jj == 1 ? jp : C.r[1];
+      float o[4];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        float acc = a.wc * C.r[jj][kk + 1];
+        acc = fmaf(a.wim, P.r[jj][kk + 1], acc);
+        acc = fmaf(a.wip, N.r[jj][kk + 1], acc);
+        acc = fmaf(a.wjm, up[kk + 1], acc);
+        acc = fmaf(a.wjp, dn[kk + 1], acc);
+        acc = fmaf(a.wkm, C.r[jj][kk], acc);
+        acc = fmaf(a.wkp, C.r[jj][kk + 2], acc);
+        o[kk] = acc;
+      }
+      const int64_t j = j0 + jl + jj;
+      if (j < a.n1 && kin) {
+        __stcs(reinterpret_cast<float4*>(wout + t * wplane + jj * a.n2), make_float4(o[0], o[1], o[2], o[3]));
+      } else if (j < a.n1) {
+        for (int kk = 0; kk < 4 && k0 + kl + kk < a.n2; ++kk) wout[t * wplane + jj * a.n2 + kk] = o[kk];
+      }
+    }
+  };
+
+  Rows R0, R1, R2;
+  mbar_wait_parity(&full[0], 0);
+  mbar_wait_parity(&full[1], 0);
+  load_centre(0, R0);
+  load_centre(1, R1);
+  release(0);
+  int t = 0;
+  for (; t + 3 <= iend; t += 3) {
+    step(t, R0, R1, R2);
+    step(t + 1, R1, R2, R0);
+    step(t + 2, R2, R0, R1);
+  }
+  if (t < iend) step(t, R0, R1, R2), ++t;
+  if (t < iend) step(t, R1, R2, R0), ++t;
+}
+
 // ---------------------------------------------------------------- host
 // Recognises  sum_t lit_t * in(1, a_t)  (any association of + over terms,
 // literal on either side of *, a bare in(1,a) = weight 1).
@@ -331,12 +488,13 @@ bool linear_terms(const Expr& e, std::vector<std::pair<double, int>>& terms) {
 
 class StencilRoutine final : public Routine {
  public:
-  StencilRoutine(const Problem& p, StencilArgs a, int tj, bool bulk) : p_(p), a_(a), tj_(tj), bulk_(bulk) {}
+  StencilRoutine(const Problem& p, StencilArgs a, int tj, bool bulk)
+      : p_(p), a_(a), tj_(tj), bulk_(bulk), ws_(bulk && !std::getenv("MDHB_STENCIL_V2")) {}
   const char* family() const override { return "stencil"; }
   std::string describe() const override {
     std::ostringstream os;
- os << "{\"kernel\": \"" << (bulk_ ? "star7_bulk<" : "star7_kernel<") << tj_ << ">\", \"TK\": " << TK << ", \"TJ\": " << tj_ << ", \"TI\": " << a_.ti
-       << ", \"threads\": " << NTHREADS << ", \"smem_ring_slots\": " << (bulk_ ? NSLOT : 4) << ", \"grid\": [" << grid().x << ", " << grid().y
+ os << "{\"kernel\": \"" << (ws_ ? "star7_ws<" : bulk_ ? "star7_bulk<" : "star7_kernel<") << tj_ << ">\", \"TK\": " << TK << ", \"TJ\": " << tj_ << ", \"TI\": " << a_.ti
+       << ", \"threads\": " << (ws_ ? WS_THREADS : NTHREADS) << ", \"smem_ring_slots\": " << (bulk_ ? NSLOT : 4) << ", \"grid\": [" << grid().x << ", " << grid().y
        << ", " << grid().z << "]}";
     return os.str();
   }
@@ -351,13 +509,12 @@ class StencilRoutine final : public Routine {
     StencilArgs a = a_;
     a.v = static_cast<const float*>(d_in[0]);
     a.w = static_cast<float*>(d_out[0]);
-    if (bulk_) {
-      const size_t smem = static_cast<size_t>(NSLOT) * 18 * BPITCH * sizeof(float);
-      static bool attr = false;
-      if (!attr) {
-        MDHB_CUDA(cudaFuncSetAttribute(star7_bulk<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        attr = true;
-      }
+    const size_t smem = static_cast<size_t>(NSLOT) * 18 * BPITCH * sizeof(float);
+    if (ws_) {
+      MDHB_CUDA(cudaFuncSetAttribute(star7_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      star7_ws<<<grid(), WS_THREADS, smem, s>>>(a);
+    } else if (bulk_) {
+      MDHB_CUDA(cudaFuncSetAttribute(star7_bulk<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       star7_bulk<16><<<grid(), NTHREADS, smem, s>>>(a);
     } else {
       star7_kernel<16><<<grid(), NTHREADS, 0, s>>>(a);
@@ -370,6 +527,7 @@ class StencilRoutine final : public Routine {
   StencilArgs a_;
   int tj_;
   bool bulk_;
+  bool ws_;
 };
 
 }  // namespace
