@@ -124,11 +124,20 @@ def prl_weights(d_in):
     d_in[2].copy_(d_in[2].new_tensor([3, 5, 7, 9]))
 
 
-def make_plan(name, device):
+def make_plan(name, device, world=1, rank=0):
+    """Plan for routine `name` ("<spec>[:tf32]").  With world > 1 the rank's
+    shard of the weak-scaled global problem (dim 0 grown world-fold, split
+    into world ++-parts by the GPU layer, paper_2405_05118_b200/shard.py)."""
     from paper_2405_05118_b200 import mdh
+    from paper_2405_05118_b200.shard import shard_spec
     base, _, math = name.partition(":")
     m = {"": mdh.MATH_FFMA, "tf32": mdh.MATH_TF32, "bf16": mdh.MATH_BF16}[math]
-    return mdh.Plan(spec(base), math=m, int_storage=mdh.I32, device=device), base, math or "ffma"
+    j = spec(base)
+    if world > 1:
+        j["sizes"][0] *= world
+        j, _, _, op = shard_spec(j, 0, world, rank)
+        assert op is None, "dim 0 of the BASELINE specs is a ++ dimension"
+    return mdh.Plan(j, math=m, int_storage=mdh.I32, device=device), base, math or "ffma"
 
 
 def roofline_of(desc, kernel_s, pk, clock_mhz, traffic):
@@ -306,7 +315,7 @@ def main():
     pk = peaks()
 
     # ---- headline: device-resident steps
-    plan, base, math = make_plan(args.routine, device)
+    plan, base, math = make_plan(args.routine, device, world, rank)
     desc = plan.describe()
     d_in = fill(plan.empty(0), 1234 + rank)
     if base == "prl_max":
@@ -333,7 +342,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32" if base != "prl_max" else "i32",
             "data": "synthetic (uniform(-1,1) fp32, seeded per rank)",
-            "config": {"workload": f"{base} {spec(base)['sizes']} ({math})", "family": desc["family"],
+            "config": {"workload": f"{base} {spec(base)['sizes']} per GPU ({math})", "family": desc["family"],
                        "kernel": desc["template"]["kernel"],
                        "parallelism": f"++-sharded z-slabs x{world} (weak)" if world > 1 else "single GPU",
                        "l2": "L2 flushed between steps" if flush else f"inputs ({in_bytes >> 20} MB) larger than L2"},

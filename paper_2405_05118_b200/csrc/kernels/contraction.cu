@@ -59,7 +59,7 @@ struct GemvArgs {
 };
 
 template <int BM, int BN, int AMODE, int BMODE, bool CVEC>
-__global__ void __launch_bounds__((BM / 8) * (BN / 8)) sgemm_tiled(GemmArgs g) {
+__global__ void __launch_bounds__((BM / 8) * (BN / 8), 256 / ((BM / 8) * (BN / 8)) * 2) sgemm_tiled(GemmArgs g) {
   constexpr int NT = (BM / 8) * (BN / 8);
   constexpr int TXN = BN / 8;
   __shared__ __align__(16) float As[2][BK][BM + 4];

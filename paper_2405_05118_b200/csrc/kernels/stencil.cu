@@ -15,6 +15,7 @@
 //          plane row is read from shared memory once per use class.
 // Algorithmic traffic per run: every input cell read once + every output cell
 // written once = 4 * (514^3 + 512^3) B for the BASELINE size.
+#include <algorithm>
 #include <array>
 #include <cstdlib>
 #include <cstring>
@@ -463,6 +464,152 @@ __global__ void __launch_bounds__(WS_THREADS, 3) star7_ws(StencilArgs a) {
   if (t < iend) step(t, R1, R2, R0), ++t;
 }
 
+
+// ---------------------------------------------------------------------------
+// v4 (default): persistent + warp-specialised.  The (tile, i-plane) step
+// space (n2/TK * n1/TJ tiles x n0 planes) is cut into `gridDim.x` contiguous
+// equal ranges, one per resident CTA, so every SM streams the same number of
+// planes (no wave tail) and consecutive segments of a CTA reuse the ring: a
+// global plane sequence number q drives slot = q % NSLOT and mbarrier parity.
+template <int MINB>
+__global__ void __launch_bounds__(WS_THREADS, MINB) star7_pers(StencilArgs a, int64_t tiles_k, int64_t total) {
+  constexpr int TJ = 16, ROWS = TJ + 2;
+  extern __shared__ __align__(128) float sring[];
+  __shared__ __align__(8) uint64_t full[NSLOT], empty[NSLOT];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t g_begin = total * blockIdx.x / gridDim.x, g_end = total * (blockIdx.x + 1) / gridDim.x;
+  const uint32_t pstride = static_cast<uint32_t>(a.e1 * a.e2), rstride = static_cast<uint32_t>(a.e2);
+
+  if (tid == 0) {
+    for (int s = 0; s < NSLOT; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_u32(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(s_u32(&empty[s])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 8) {
+    // ---------------- producer: walk the same segments, one plane per q
+    uint32_t q = 0;
+    for (int64_t g = g_begin; g < g_end;) {
+      const int64_t tile = g / a.n0, ilo = g % a.n0;
+      const int64_t ihi = min(a.n0, ilo + (g_end - g));
+      const int64_t k0 = (tile % tiles_k) * TK, j0 = (tile / tiles_k) * TJ;
+      const uint32_t base0 = static_cast<uint32_t>((ilo * a.e1 + j0) * a.e2 + k0);
+      const float* vbase = a.v + ((ilo * a.e1 + j0) * a.e2 + k0);
+      const int np = static_cast<int>(ihi - ilo) + 2;
+      for (int p = 0; p < np; ++p, ++q) {
+        const int s = static_cast<int>(q % NSLOT);
+        if (q >= NSLOT) mbar_wait_parity(&empty[s], (q / NSLOT - 1) & 1);
+        uint32_t bytes = 0, sh = 0;
+        if (lane < ROWS) {
+          sh = (base0 + static_cast<uint32_t>(p) * pstride + static_cast<uint32_t>(lane) * rstride) & 3u;
+          bytes = (sh * 4 + (TK + 2) * 4 + 15) & ~15u;
+        }
+        uint32_t tot = bytes;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(&full[s])), "r"(tot) : "memory");
+        __syncwarp();
+        if (lane < ROWS) {
+          const float* src = vbase + static_cast<int64_t>(p) * (a.e1 * a.e2) + static_cast<int64_t>(lane) * a.e2 - sh;
+          float* dst = sring + (static_cast<size_t>(s) * ROWS + lane) * BPITCH;
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                       ::"r"(s_u32(dst)), "l"(src), "r"(bytes), "r"(s_u32(&full[s])) : "memory");
+        }
+      }
+      g = ihi == a.n0 ? (tile + 1) * a.n0 : g_end;
+    }
+    return;
+  }
+
+  // ---------------- compute warps
+  const int kl = lane * 4, jl = warp * 2;
+  uint32_t q = 0;
+  for (int64_t g = g_begin; g < g_end;) {
+    const int64_t tile = g / a.n0, ilo = g % a.n0;
+    const int64_t ihi = min(a.n0, ilo + (g_end - g));
+    const int64_t k0 = (tile % tiles_k) * TK, j0 = (tile / tiles_k) * TJ;
+    const uint32_t base0 = static_cast<uint32_t>((ilo * a.e1 + j0) * a.e2 + k0);
+    const int n = static_cast<int>(ihi - ilo);
+    const uint32_t q0 = q;
+    auto rowptr = [&](int p, int r, int& sh) {
+      sh = static_cast<int>((base0 + static_cast<uint32_t>(p) * pstride + static_cast<uint32_t>(r) * rstride) & 3u);
+      return sring + (static_cast<size_t>((q0 + p) % NSLOT) * ROWS + r) * BPITCH + sh + kl;
+    };
+    auto wait = [&](int p) { mbar_wait_parity(&full[(q0 + p) % NSLOT], ((q0 + p) / NSLOT) & 1); };
+    auto release = [&](int p) {
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(&empty[(q0 + p) % NSLOT])) : "memory");
+    };
+    auto load_centre = [&](int p, Rows& R) {
+      int sh;
+      const float* p0 = rowptr(p, jl + 1, sh);
+      ld6(p0, sh, R.r[0]);
+      const float* p1 = rowptr(p, jl + 2, sh);
+      ld6(p1, sh, R.r[1]);
+    };
+    float* wout = a.w + (ilo * a.n1 + j0 + jl) * a.n2 + k0 + kl;
+    const int64_t wplane = a.n1 * a.n2;
+    const bool kin = k0 + kl + 4 <= a.n2;
+    auto step = [&](int t, const Rows& P, const Rows& C, Rows& N) {
+      wait(t + 2);
+      load_centre(t + 2, N);
+      float jm[6], jp[6];
+      int sh;
+      const float* pm = rowptr(t + 1, jl, sh);
+      ld6(pm, sh, jm);
+      const float* pp = rowptr(t + 1, jl + 3, sh);
+      ld6(pp, sh, jp);
+      release(t + 1);
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) {
+        const float* up = jj == 0 ? jm : C.r[0];
+        const float* dn = jj == 1 ? jp : C.r[1];
+        float o[4];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          float acc = a.wc * C.r[jj][kk + 1];
+          acc = fmaf(a.wim, P.r[jj][kk + 1], acc);
+          acc = fmaf(a.wip, N.r[jj][kk + 1], acc);
+          acc = fmaf(a.wjm, up[kk + 1], acc);
+          acc = fmaf(a.wjp, dn[kk + 1], acc);
+          acc = fmaf(a.wkm, C.r[jj][kk], acc);
+          acc = fmaf(a.wkp, C.r[jj][kk + 2], acc);
+          o[kk] = acc;
+        }
+        if (j0 + jl + jj < a.n1) {
+          float* dst = wout + t * wplane + jj * a.n2;
+          if (kin) {
+            __stcs(reinterpret_cast<float4*>(dst), make_float4(o[0], o[1], o[2], o[3]));
+          } else {
+            for (int kk = 0; kk < 4 && k0 + kl + kk < a.n2; ++kk) dst[kk] = o[kk];
+          }
+        }
+      }
+    };
+    Rows R0, R1, R2;
+    wait(0);
+    wait(1);
+    load_centre(0, R0);
+    load_centre(1, R1);
+    release(0);
+    int t = 0;
+    for (; t + 3 <= n; t += 3) {
+      step(t, R0, R1, R2);
+      step(t + 1, R1, R2, R0);
+      step(t + 2, R2, R0, R1);
+    }
+    if (t < n) step(t, R0, R1, R2), ++t;
+    if (t < n) step(t, R1, R2, R0), ++t;
+    release(n + 1);  // the last plane was only read as "next"
+    q += static_cast<uint32_t>(n + 2);
+    g = ihi == a.n0 ? (tile + 1) * a.n0 : g_end;
+  }
+}
+
 // ---------------------------------------------------------------- host
 // Recognises  sum_t lit_t * in(1, a_t)  (any association of + over terms,
 // literal on either side of *, a bare in(1,a) = weight 1).
@@ -489,11 +636,12 @@ bool linear_terms(const Expr& e, std::vector<std::pair<double, int>>& terms) {
 class StencilRoutine final : public Routine {
  public:
   StencilRoutine(const Problem& p, StencilArgs a, int tj, bool bulk)
-      : p_(p), a_(a), tj_(tj), bulk_(bulk), ws_(bulk && !std::getenv("MDHB_STENCIL_V2")) {}
+      : p_(p), a_(a), tj_(tj), bulk_(bulk), ws_(bulk && !std::getenv("MDHB_STENCIL_V2")),
+        pers_(ws_ && std::getenv("MDHB_STENCIL_PERS") != nullptr) {}
   const char* family() const override { return "stencil"; }
   std::string describe() const override {
     std::ostringstream os;
- os << "{\"kernel\": \"" << (ws_ ? "star7_ws<" : bulk_ ? "star7_bulk<" : "star7_kernel<") << tj_ << ">\", \"TK\": " << TK << ", \"TJ\": " << tj_ << ", \"TI\": " << a_.ti
+ os << "{\"kernel\": \"" << (pers_ ? "star7_pers<" : ws_ ? "star7_ws<" : bulk_ ? "star7_bulk<" : "star7_kernel<") << tj_ << ">\", \"TK\": " << TK << ", \"TJ\": " << tj_ << ", \"TI\": " << a_.ti
        << ", \"threads\": " << (ws_ ? WS_THREADS : NTHREADS) << ", \"smem_ring_slots\": " << (bulk_ ? NSLOT : 4) << ", \"grid\": [" << grid().x << ", " << grid().y
        << ", " << grid().z << "]}";
     return os.str();
@@ -510,7 +658,19 @@ class StencilRoutine final : public Routine {
     a.v = static_cast<const float*>(d_in[0]);
     a.w = static_cast<float*>(d_out[0]);
     const size_t smem = static_cast<size_t>(NSLOT) * 18 * BPITCH * sizeof(float);
-    if (ws_) {
+    if (pers_) {
+      auto kern = minb_ == 2 ? star7_pers<2> : star7_pers<3>;
+      MDHB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      if (!ctas_) {
+        int occ = 0;
+        MDHB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WS_THREADS, smem));
+        ctas_ = std::max(1, occ) * sm_count(p_.opt.device);
+      }
+      const int64_t tiles_k = (a.n2 + TK - 1) / TK, tiles = tiles_k * ((a.n1 + 15) / 16);
+      const int64_t total = tiles * a.n0;
+      const int grid_p = static_cast<int>(std::min<int64_t>(ctas_, std::max<int64_t>(1, total / 4)));
+      kern<<<grid_p, WS_THREADS, smem, s>>>(a, tiles_k, total);
+    } else if (ws_) {
       MDHB_CUDA(cudaFuncSetAttribute(star7_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       star7_ws<<<grid(), WS_THREADS, smem, s>>>(a);
     } else if (bulk_) {
@@ -528,6 +688,9 @@ class StencilRoutine final : public Routine {
   int tj_;
   bool bulk_;
   bool ws_;
+  bool pers_;
+  int ctas_ = 0;
+  int minb_ = std::getenv("MDHB_STENCIL_MINB") ? std::atoi(std::getenv("MDHB_STENCIL_MINB")) : 2;
 };
 
 }  // namespace
