@@ -25,6 +25,7 @@
 // Re-composition of K happens entirely in registers (each output cell has a
 // single writer), so the store is a plain coalesced write of C.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <sstream>
@@ -321,6 +322,57 @@ __global__ void __launch_bounds__(256) skinny_fold(SkinnyArgs g) {
   g.C[g.cm[m] + g.cn[n]] = s;
 }
 
+
+// MatVec v2: a CTA of 8 warps owns 2 rows; warp w reduces K-slice w, every
+// lane issues all of its 2 x V 16-byte loads of M (and V of x) before the
+// first FMA, so a full 64 MiB matrix is in flight after one pass of CTAs.
+// Partial dot products meet in shared memory (WRP combine in SM, the
+// CUDA+WRP model rule) and one lane per row writes the result.
+template <int V>
+__global__ void __launch_bounds__(256) gemv_split(GemvArgs g) {
+  constexpr int ROWS = 2;
+  __shared__ float part[8][ROWS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * ROWS;
+  const int kq = g.K / 8;  // floats per warp slice
+  const float4* x4 = reinterpret_cast<const float4*>(g.x + warp * kq);
+  float4 av[ROWS][V], xv[V];
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) {
+    const int64_t m = m0 + r < g.M ? m0 + r : g.M - 1;
+    const float4* row = reinterpret_cast<const float4*>(g.A + g.am[m] + warp * kq);
+#pragma unroll
+    for (int u = 0; u < V; ++u) av[r][u] = __ldcs(row + lane + 32 * u);
+  }
+#pragma unroll
+  for (int u = 0; u < V; ++u) xv[u] = __ldg(x4 + lane + 32 * u);
+  float acc[ROWS];
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) {
+    acc[r] = 0.f;
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      acc[r] = fmaf(av[r][u].x, xv[u].x, acc[r]);
+      acc[r] = fmaf(av[r][u].y, xv[u].y, acc[r]);
+      acc[r] = fmaf(av[r][u].z, xv[u].z, acc[r]);
+      acc[r] = fmaf(av[r][u].w, xv[u].w, acc[r]);
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], s);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) part[warp][r] = acc[r];
+  }
+  __syncthreads();
+  if (threadIdx.x < ROWS && m0 + threadIdx.x < g.M) {
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s += part[w][threadIdx.x];
+    g.y[g.cm[m0 + threadIdx.x]] = s;
+  }
+}
+
 // ---------------------------------------------------------------- host
 class GemmRoutine final : public Routine {
  public:
@@ -469,7 +521,9 @@ class GemmRoutine final : public Routine {
       return os.str();
     }
     if (gemv_) {
-      os << "{\"kernel\": \"gemv_rows<2>\", \"M\": " << M_ << ", \"K\": " << K_ << ", \"threads\": 128}";
+      const bool split = K_ % 1024 == 0 && K_ / 1024 <= 8 && !std::getenv("MDHB_GEMV_V1");
+      os << "{\"kernel\": \"" << (split ? "gemv_split<" + std::to_string(K_ / 1024) + ">" : std::string("gemv_rows<2>"))
+         << "\", \"M\": " << M_ << ", \"K\": " << K_ << ", \"threads\": " << (split ? 256 : 128) << "}";
       return os.str();
     }
     os << "{\"kernel\": \"sgemm_tiled<" << BM_ << "," << BN_ << ">\", \"M\": " << M_ << ", \"N\": " << N_
@@ -500,6 +554,18 @@ class GemmRoutine final : public Routine {
     }
     if (gemv_) {
       GemvArgs a{A, B + g_.lb.c0, C, tab_[0], tab_[1], M_, static_cast<int>(K_)};
+      const int V = static_cast<int>(K_ / 1024);
+      if (K_ % 1024 == 0 && (V == 1 || V == 2 || V == 4 || V == 8) && !std::getenv("MDHB_GEMV_V1")) {
+        unsigned grid = static_cast<unsigned>((M_ + 1) / 2);
+        switch (V) {
+          case 1: gemv_split<1><<<grid, 256, 0, s>>>(a); break;
+          case 2: gemv_split<2><<<grid, 256, 0, s>>>(a); break;
+          case 4: gemv_split<4><<<grid, 256, 0, s>>>(a); break;
+          default: gemv_split<8><<<grid, 256, 0, s>>>(a); break;
+        }
+        MDHB_CUDA(cudaGetLastError());
+        return;
+      }
       constexpr int ROWS = 2;
       int64_t warps = (M_ + ROWS - 1) / ROWS;
       unsigned grid = static_cast<unsigned>((warps * 32 + 127) / 128);
