@@ -35,13 +35,22 @@ constexpr int BM = 128;
 constexpr int BKE = 32;  // k elements per tile = one 128-byte swizzle row of fp32
 constexpr int MAXR = 5;  // TMA rank limit
 
+constexpr int MAXKD = 6;  // K dims handled by the producer's odometer
+
 struct TcArgs {
   float* C;
   const int32_t *tCm, *tCn, *cm, *cn;
-  const int32_t *a_mc, *a_kc, *b_nc, *b_kc;  // [tiles][MAXR] / [nk][MAXR], TMA order (innermost first)
+  const int32_t *a_mc, *b_nc;  // [tiles][MAXR] TMA coordinates of the row-tile origins (innermost first)
   int a_rank, b_rank;
   int nk, tilesM, tilesN;
   int cvec;
+  // k-tile -> TMA coordinate offsets, as a mixed-radix odometer over the K
+  // dims (innermost = the dim stepped by 32): kext digits, kstep elements per
+  // digit, per-rank coefficients for A and B.  Computed in registers by the
+  // producer thread -- no table loads on the TMA issue path.
+  int nkd;
+  int kext[MAXKD], kstep[MAXKD];
+  int kca[MAXKD][MAXR], kcb[MAXKD][MAXR];
 };
 
 template <int BN, int STAGES, bool B_MN>
@@ -86,6 +95,16 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer
+    int am0[MAXR], bn0[MAXR], ka[MAXR], kb[MAXR], dig[MAXKD];
+#pragma unroll
+    for (int r = 0; r < MAXR; ++r) {
+      am0[r] = g.a_mc[tm * MAXR + r];
+      bn0[r] = g.b_nc[tn * MAXR + r];
+      ka[r] = 0;
+      kb[r] = 0;
+    }
+#pragma unroll
+    for (int q = 0; q < MAXKD; ++q) dig[q] = 0;
     for (int kt = 0; kt < g.nk; ++kt) {
       const int s = kt % STAGES, it = kt / STAGES;
       if (kt >= STAGES) tc::mbar_wait(&empty[s], (it - 1) & 1);
@@ -94,10 +113,10 @@ __global__ void __launch_bounds__(192, 1)
       uint8_t* sb = sa + A_BYTES;
       int c[MAXR];
 #pragma unroll
-      for (int r = 0; r < MAXR; ++r) c[r] = g.a_mc[tm * MAXR + r] + g.a_kc[kt * MAXR + r];
+      for (int r = 0; r < MAXR; ++r) c[r] = am0[r] + ka[r];
       tc::tma_load(sa, &tma_a, &full[s], g.a_rank, c);
 #pragma unroll
-      for (int r = 0; r < MAXR; ++r) c[r] = g.b_nc[tn * MAXR + r] + g.b_kc[kt * MAXR + r];
+      for (int r = 0; r < MAXR; ++r) c[r] = bn0[r] + kb[r];
       if (B_MN) {
         for (int j = 0; j < BN / 32; ++j) {
           int cj[MAXR];
@@ -108,6 +127,23 @@ __global__ void __launch_bounds__(192, 1)
         }
       } else {
         tc::tma_load(sb, &tma_b, &full[s], g.b_rank, c);
+      }
+      // advance the K odometer (innermost digit last)
+      for (int q = g.nkd - 1; q >= 0; --q) {
+        if (++dig[q] < g.kext[q]) {
+#pragma unroll
+          for (int r = 0; r < MAXR; ++r) {
+            ka[r] += g.kca[q][r] * g.kstep[q];
+            kb[r] += g.kcb[q][r] * g.kstep[q];
+          }
+          break;
+        }
+#pragma unroll
+        for (int r = 0; r < MAXR; ++r) {
+          ka[r] -= g.kca[q][r] * g.kstep[q] * (g.kext[q] - 1);
+          kb[r] -= g.kcb[q][r] * g.kstep[q] * (g.kext[q] - 1);
+        }
+        dig[q] = 0;
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -365,17 +401,14 @@ class TcRoutine final : public Routine {
     kext.push_back(e.sizes[static_cast<size_t>(va_.kin)] / BKE);
     kstep.push_back(BKE);
     nk_ = static_cast<int>(K_ / BKE);
-    std::vector<std::vector<int64_t>> ok;
-    {
-      std::vector<int64_t> l(kd.size(), 0);
-      for (int t = 0; t < nk_; ++t) {
-        std::vector<int64_t> o(static_cast<size_t>(e.D()), 0);
-        for (size_t q = 0; q < kd.size(); ++q) o[static_cast<size_t>(kd[q])] = l[q] * kstep[q];
-        ok.push_back(o);
-        for (int q = static_cast<int>(l.size()) - 1; q >= 0; --q) {
-          if (++l[static_cast<size_t>(q)] < kext[static_cast<size_t>(q)]) break;
-          l[static_cast<size_t>(q)] = 0;
-        }
+    if (kd.size() > static_cast<size_t>(MAXKD)) return *why = "more than 6 contraction dims", false;
+    args_.nkd = static_cast<int>(kd.size());
+    for (size_t q = 0; q < kd.size(); ++q) {
+      args_.kext[q] = static_cast<int>(kext[q]);
+      args_.kstep[q] = static_cast<int>(kstep[q]);
+      for (int t = 0; t < MAXR; ++t) {
+        args_.kca[q][t] = t < va_.rank ? static_cast<int>(va_.coef[static_cast<size_t>(t)][static_cast<size_t>(kd[q])]) : 0;
+        args_.kcb[q][t] = t < vb_.rank ? static_cast<int>(vb_.coef[static_cast<size_t>(t)][static_cast<size_t>(kd[q])]) : 0;
       }
     }
     // epilogue tables in the smem row orders of A (TMEM lanes) and B (columns)
@@ -403,17 +436,15 @@ class TcRoutine final : public Routine {
       for (size_t j = 1; j < 4; ++j) grp = grp && cn[t + j] == cn[t] + static_cast<int64_t>(j);
     cvec_ = grp && mod4(cn) && mod4(cm) && mod4(tCm) && mod4(tCn);
     // coordinate tables
-    std::vector<int64_t> amc, akc, bnc, bkc;
+    std::vector<int64_t> amc, bnc;
     for (auto& o : om) for (auto c : coords(va_, o, true)) amc.push_back(c);
-    for (auto& o : ok) for (auto c : coords(va_, o, false)) akc.push_back(c);
     for (auto& o : on) for (auto c : coords(vb_, o, true)) bnc.push_back(c);
-    for (auto& o : ok) for (auto c : coords(vb_, o, false)) bkc.push_back(c);
-    const std::vector<int64_t>* ts[8] = {&tCm, &tCn, &cm, &cn, &amc, &akc, &bnc, &bkc};
+    const std::vector<int64_t>* ts[6] = {&tCm, &tCn, &cm, &cn, &amc, &bnc};
     size_t total = 0;
     for (auto* t : ts) total += (t->size() + 64) / 64 * 64;
     std::vector<int32_t> host(total, 0);
-    size_t cur = 0, offs[8];
-    for (int q = 0; q < 8; ++q) {
+    size_t cur = 0, offs[6];
+    for (int q = 0; q < 6; ++q) {
       offs[q] = cur;
       for (int64_t x : *ts[q]) {
         if (x > INT32_MAX || x < INT32_MIN) return *why = "offsets exceed int32", false;
@@ -430,9 +461,7 @@ class TcRoutine final : public Routine {
     args_.cm = base + offs[2];
     args_.cn = base + offs[3];
     args_.a_mc = base + offs[4];
-    args_.a_kc = base + offs[5];
-    args_.b_nc = base + offs[6];
-    args_.b_kc = base + offs[7];
+    args_.b_nc = base + offs[5];
     args_.a_rank = va_.rank;
     args_.b_rank = vb_.rank;
     args_.nk = nk_;
