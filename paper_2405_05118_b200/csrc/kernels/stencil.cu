@@ -653,6 +653,68 @@ class StencilRoutine final : public Routine {
   int launches() const override { return 1; }
   double bytes() const override { return static_cast<double>(p_.in_bytes + p_.out_bytes); }
   double flops() const override { return 13.0 * static_cast<double>(a_.n0 * a_.n1 * a_.n2); }
+
+  // End-to-end on host buffers, pipelined along the ++ dimension i: chunk c's
+  // input planes go up on one copy engine while chunk c-1 computes and chunk
+  // c-2's output planes come down on the other (the homomorphic split again:
+  // every chunk is the same md_hom over a sub-range of i).
+  bool supports_chunked_host() const override { return true; }
+  void launch_host_chunked(const void* const* h_in, void* const* h_out, void* const* d_in, void* const* d_out,
+                           cudaStream_t s) override {
+    constexpr int kChunks = 16;
+    if (!h2d_) {
+      MDHB_CUDA(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
+      MDHB_CUDA(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
+      for (int c = 0; c < kChunks + 2; ++c) {
+        MDHB_CUDA(cudaEventCreateWithFlags(&ev_in_[c], cudaEventDisableTiming));
+        MDHB_CUDA(cudaEventCreateWithFlags(&ev_cmp_[c], cudaEventDisableTiming));
+      }
+    }
+    const int64_t pin = a_.e1 * a_.e2, pout = a_.n1 * a_.n2;
+    const int64_t ci = (a_.n0 + kChunks - 1) / kChunks;
+    const char* hi_in = static_cast<const char*>(h_in[0]);
+    char* hi_out = static_cast<char*>(h_out[0]);
+    char* dv = static_cast<char*>(d_in[0]);
+    char* dw = static_cast<char*>(d_out[0]);
+    MDHB_CUDA(cudaEventRecord(ev_in_[kChunks], s));  // respect work already queued on s
+    MDHB_CUDA(cudaStreamWaitEvent(h2d_, ev_in_[kChunks], 0));
+    int64_t copied = 0;
+    int c = 0;
+    for (int64_t lo = 0; lo < a_.n0; lo += ci, ++c) {
+      const int64_t hi = std::min(a_.n0, lo + ci);
+      const int64_t need = std::min(a_.e0, hi + 2);
+      MDHB_CUDA(cudaMemcpyAsync(dv + copied * pin * 4, hi_in + copied * pin * 4,
+                                static_cast<size_t>((need - copied) * pin * 4), cudaMemcpyHostToDevice, h2d_));
+      copied = need;
+      MDHB_CUDA(cudaEventRecord(ev_in_[c], h2d_));
+      MDHB_CUDA(cudaStreamWaitEvent(s, ev_in_[c], 0));
+      StencilArgs a = a_;
+      a.n0 = hi - lo;
+      a.e0 = a_.e0 - lo;
+      const void* din[1] = {dv + lo * pin * 4};
+      void* dout[1] = {dw + lo * pout * 4};
+      StencilArgs keep = a_;
+      a_ = a;
+      launch(din, dout, s);
+      a_ = keep;
+      MDHB_CUDA(cudaEventRecord(ev_cmp_[c], s));
+      MDHB_CUDA(cudaStreamWaitEvent(d2h_, ev_cmp_[c], 0));
+      MDHB_CUDA(cudaMemcpyAsync(hi_out + lo * pout * 4, dw + lo * pout * 4, static_cast<size_t>((hi - lo) * pout * 4),
+                                cudaMemcpyDeviceToHost, d2h_));
+    }
+    MDHB_CUDA(cudaEventRecord(ev_cmp_[kChunks], d2h_));
+    MDHB_CUDA(cudaStreamWaitEvent(s, ev_cmp_[kChunks], 0));
+  }
+  ~StencilRoutine() override {
+    if (h2d_) {
+      cudaStreamDestroy(h2d_);
+      cudaStreamDestroy(d2h_);
+      for (int c = 0; c < 18; ++c) {
+        cudaEventDestroy(ev_in_[c]);
+        cudaEventDestroy(ev_cmp_[c]);
+      }
+    }
+  }
   void launch(const void* const* d_in, void* const* d_out, cudaStream_t s) override {
     StencilArgs a = a_;
     a.v = static_cast<const float*>(d_in[0]);
@@ -690,6 +752,8 @@ class StencilRoutine final : public Routine {
   bool ws_;
   bool pers_;
   int ctas_ = 0;
+  cudaStream_t h2d_ = nullptr, d2h_ = nullptr;
+  cudaEvent_t ev_in_[18] = {}, ev_cmp_[18] = {};
   int minb_ = std::getenv("MDHB_STENCIL_MINB") ? std::atoi(std::getenv("MDHB_STENCIL_MINB")) : 2;
 };
 
