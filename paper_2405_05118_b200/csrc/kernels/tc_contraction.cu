@@ -20,6 +20,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <sstream>
@@ -193,6 +194,28 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, TMEM_COLS);
 }
 
+// De-composition layout pass (Table-1 D4, layout_de = [2,1]): an MN-major
+// operand B[k][n] is rewritten K-major as Bt[n][k] so the MMA reads both
+// operands K-major -- MN-major fp32 operands run the tensor pipe at half
+// rate on sm_100 (measured: 237 vs 464 TFLOP/s at 8192^3).
+__global__ void __launch_bounds__(256) transpose_kn(const float* __restrict__ src, int64_t sk, int64_t sn,
+                                                   float* __restrict__ dst, int K, int N) {
+  __shared__ float t[32][33];
+  const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows per pass
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {
+    int k = k0 + r, n = n0 + tx;
+    t[r][tx] = (k < K && n < N) ? __ldcs(src + k * sk + n * sn) : 0.f;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {
+    int n = n0 + r, k = k0 + tx;
+    if (n < N && k < K) dst[static_cast<int64_t>(n) * K + k] = t[tx][r];
+  }
+}
+
 // ---------------------------------------------------------------- host
 using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -336,10 +359,11 @@ class TcRoutine final : public Routine {
   TcRoutine(const Problem& p, const Groups& g) : p_(p), g_(g) {}
   ~TcRoutine() override {
     if (blob_) cudaFree(blob_);
+    if (bt_) cudaFree(bt_);
   }
   const char* family() const override { return "contraction"; }
   const char* bound() const override { return "tensor"; }
-  int launches() const override { return 1; }
+  int launches() const override { return transposeB_ ? 2 : 1; }
   double flops() const override { return 2.0 * static_cast<double>(M_) * static_cast<double>(N_) * static_cast<double>(K_); }
   double bytes() const override { return static_cast<double>(p_.in_bytes + p_.out_bytes); }
   std::string describe() const override {
@@ -348,7 +372,9 @@ class TcRoutine final : public Routine {
        << (vb_.mn ? "B_MN" : "B_K") << ">\", \"math\": \"tf32\", \"M\": " << M_ << ", \"N\": " << N_ << ", \"K\": " << K_
        << ", \"BM\": " << BM << ", \"BN\": " << BN_ << ", \"BK\": " << BKE << ", \"stages\": " << stages_
        << ", \"umma\": \"tcgen05.mma.cta_group::1.kind::tf32 M128xN" << BN_ << "xK8\", \"tiles\": "
-       << static_cast<int64_t>(tilesM_) * tilesN_ << ", \"tmem_cols\": " << BN_ << "}";
+       << static_cast<int64_t>(tilesM_) * tilesN_ << ", \"tmem_cols\": " << BN_
+       << ", \"b_layout\": \"" << (transposeB_ ? "K-major copy (layout_de [2,1] pre-pass)" : (vb_.mn ? "MN-major" : "K-major"))
+       << "\"}";
     return os.str();
   }
 
@@ -359,6 +385,36 @@ class TcRoutine final : public Routine {
     K_ = prod_sizes(e, g_.Kd);
     if (!describe_view(p_, g_.a_buf, g_.Md, g_.Kd, BM, false, va_, why)) return false;
     if (!describe_view(p_, g_.b_buf, g_.Nd, g_.Kd, BN, true, vb_, why)) return false;
+    if (vb_.mn && g_.Nd.size() == 1 && g_.Kd.size() == 1 && !std::getenv("MDHB_TC_NO_TRANSPOSE")) {
+      // rewrite B K-major into scratch: Bt[n][k]
+      const int dn = g_.Nd[0], dk = g_.Kd[0];
+      const int64_t Nn = e.sizes[static_cast<size_t>(dn)], Kk = e.sizes[static_cast<size_t>(dk)];
+      if (Kk % BKE == 0 && Nn % BN == 0) {
+        View t;
+        t.buf = vb_.buf;
+        t.rank = 2;
+        t.dims[0] = static_cast<cuuint64_t>(Kk);
+        t.dims[1] = static_cast<cuuint64_t>(Nn);
+        t.strides[0] = 4;
+        t.strides[1] = static_cast<cuuint64_t>(Kk * 4);
+        t.box[0] = BKE;
+        t.box[1] = static_cast<cuuint32_t>(BN);
+        t.coef.assign(2, std::vector<int64_t>(static_cast<size_t>(e.D()), 0));
+        t.coef[0][static_cast<size_t>(dk)] = 1;
+        t.coef[1][static_cast<size_t>(dn)] = 1;
+        t.c0 = {0, 0};
+        t.mn = false;
+        t.kin = dk;
+        t.row_dims = {dn};
+        t.row_box = {BN};
+        if (BN > 256 || t.strides[1] % 16) return *why = "transposed view not TMA-able", false;
+        vb_ = t;
+        transposeB_ = true;
+        tK_ = Kk;
+        tN_ = Nn;
+        MDHB_CUDA(cudaMalloc(&bt_, static_cast<size_t>(Kk * Nn) * 4));
+      }
+    }
     if (va_.kin != vb_.kin) return *why = "operands step different K dims", false;
     BN_ = BN;
     stages_ = BN >= 256 ? 4 : (BN >= 128 ? 6 : 8);
@@ -475,6 +531,14 @@ class TcRoutine final : public Routine {
   void launch(const void* const* d_in, void* const* d_out, cudaStream_t s) override {
     const void* A = d_in[va_.buf];
     const void* B = d_in[vb_.buf];
+    if (transposeB_) {
+      const float* src = static_cast<const float*>(B) + g_.lb.c0;
+      dim3 tg(static_cast<unsigned>((tN_ + 31) / 32), static_cast<unsigned>((tK_ + 31) / 32));
+      transpose_kn<<<tg, 256, 0, s>>>(src, g_.lb.cj[static_cast<size_t>(g_.Kd[0])], g_.lb.cj[static_cast<size_t>(g_.Nd[0])],
+                                      static_cast<float*>(bt_), static_cast<int>(tK_), static_cast<int>(tN_));
+      MDHB_CUDA(cudaGetLastError());
+      B = bt_;
+    }
     if (A != last_a_) encode(va_, A, &ma_), last_a_ = A;
     if (B != last_b_) encode(vb_, B, &mb_), last_b_ = B;
     TcArgs a = args_;
@@ -517,13 +581,18 @@ class TcRoutine final : public Routine {
   CUtensorMap ma_{}, mb_{};
   const void* last_a_ = nullptr;
   const void* last_b_ = nullptr;
+  bool transposeB_ = false;
+  int64_t tK_ = 0, tN_ = 0;
+  void* bt_ = nullptr;
 };
 
 }  // namespace
 
 std::unique_ptr<Routine> make_tc_contraction(const Problem& p, const Groups& g, const Config* cfg, Config* cfg_out,
                                              std::string* why) {
-  for (int bn : {256, 128, 64}) {
+  std::vector<int> menu = {256, 128, 64};
+  if (const char* f = std::getenv("MDHB_TC_BN")) menu = {std::atoi(f)};
+  for (int bn : menu) {
     auto r = std::make_unique<TcRoutine>(p, g);
     std::string w;
     if (r->setup(bn, &w)) {
