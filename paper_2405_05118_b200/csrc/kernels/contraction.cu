@@ -373,6 +373,129 @@ __global__ void __launch_bounds__(256) gemv_split(GemvArgs g) {
   }
 }
 
+
+// FFMA template v2 (vector operand modes): global -> shared with cp.async
+// (16-byte LDGSTS, no register staging, no spills), a 4-stage ring, one
+// barrier per k-tile.  A in K4 mode is kept [m][k] in shared memory and
+// read as one 16-byte vector per row per 4 k; MN4 operands are [k][rows].
+// The register tile and epilogue are those of sgemm_tiled.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <bool AK4, bool CVEC, int TN>
+__global__ void __launch_bounds__(256, TN == 8 ? 2 : 1) sgemm_async(GemmArgs g) {
+  constexpr int BM = 128, BN = 16 * TN, ST = 4, NQ = TN / 4;  // NQ column quads per thread
+  __shared__ __align__(16) float As[ST][BM * BK];
+  __shared__ __align__(16) float Bs[ST][BK * BN];
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  constexpr int GROUP_M = 8;
+  const int x = blockIdx.x;
+  const int per_group = GROUP_M * g.tilesN;
+  const int first_m = (x / per_group) * GROUP_M;
+  const int gsz = min(g.tilesM - first_m, GROUP_M);
+  const int tm = first_m + (x % per_group) % gsz;
+  const int tn = (x % per_group) / gsz;
+  const float* __restrict__ A = g.A + g.tAm[tm];
+  const float* __restrict__ B = g.B + g.tBn[tn];
+  int a_r, a_k, a_dst;
+  if (AK4) { a_r = tid >> 1; a_k = (tid & 1) * 4; a_dst = a_r * BK + a_k; }
+  else { a_k = tid >> 5; a_r = (tid & 31) * 4; a_dst = a_k * BM + a_r; }
+  constexpr int BCH = BK * BN / 4 / 256;  // 16-byte B chunks per thread
+  int b_k[BCH], b_dst[BCH];
+  const float* b_src[BCH];
+#pragma unroll
+  for (int c = 0; c < BCH; ++c) {
+    const int ch = tid + c * 256;
+    b_k[c] = ch / (BN / 4);
+    const int col = (ch % (BN / 4)) * 4;
+    b_dst[c] = b_k[c] * BN + col;
+    b_src[c] = B + g.bn[col];
+  }
+  const float* a_src = A + g.am[a_r];
+  const int nk = g.K / BK;
+  auto issue = [&](int kt) {
+    const int s = kt % ST, k0 = kt * BK;
+    cp_async16(&As[s][a_dst], a_src + g.ak[k0 + a_k]);
+#pragma unroll
+    for (int c = 0; c < BCH; ++c) cp_async16(&Bs[s][b_dst[c]], b_src[c] + g.bk[k0 + b_k[c]]);
+  };
+#pragma unroll
+  for (int p = 0; p < ST - 1; ++p) {
+    if (p < nk) issue(p);
+    cp_async_commit();
+  }
+  float acc[8][TN];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<ST - 2>();
+    __syncthreads();
+    if (kt + ST - 1 < nk) issue(kt + ST - 1);
+    cp_async_commit();
+    const float* as = As[kt % ST];
+    const float* bs = Bs[kt % ST];
+#pragma unroll
+    for (int kq = 0; kq < BK; kq += 4) {
+      float a4[8][4];
+      if (AK4) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = i < 4 ? ty * 4 + i : BM / 2 + ty * 4 + (i - 4);
+          float4 v = *reinterpret_cast<const float4*>(as + r * BK + kq);
+          a4[i][0] = v.x; a4[i][1] = v.y; a4[i][2] = v.z; a4[i][3] = v.w;
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        float a[8];
+        if (AK4) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) a[i] = a4[i][kk];
+        } else {
+          float4 a0 = *reinterpret_cast<const float4*>(as + (kq + kk) * BM + ty * 4);
+          float4 a1 = *reinterpret_cast<const float4*>(as + (kq + kk) * BM + BM / 2 + ty * 4);
+          a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w; a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
+        }
+        float b[TN];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          float4 v = *reinterpret_cast<const float4*>(bs + (kq + kk) * BN + q * (BN / NQ) + tx * 4);
+          b[4 * q] = v.x; b[4 * q + 1] = v.y; b[4 * q + 2] = v.z; b[4 * q + 3] = v.w;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+      }
+    }
+  }
+  cp_async_wait<0>();
+  float* __restrict__ C = g.C + g.tCm[tm] + g.tCn[tn];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = i < 4 ? ty * 4 + i : BM / 2 + ty * 4 + (i - 4);
+    float* crow = C + g.cm[r];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int c = q * (BN / NQ) + tx * 4;
+      if (CVEC) {
+        *reinterpret_cast<float4*>(crow + g.cn[c]) =
+            make_float4(acc[i][q * 4 + 0], acc[i][q * 4 + 1], acc[i][q * 4 + 2], acc[i][q * 4 + 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) crow[g.cn[c + j]] = acc[i][q * 4 + j];
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- host
 class GemmRoutine final : public Routine {
  public:
@@ -526,8 +649,8 @@ class GemmRoutine final : public Routine {
          << "\", \"M\": " << M_ << ", \"K\": " << K_ << ", \"threads\": " << (split ? 256 : 128) << "}";
       return os.str();
     }
-    os << "{\"kernel\": \"sgemm_tiled<" << BM_ << "," << BN_ << ">\", \"M\": " << M_ << ", \"N\": " << N_
-       << ", \"K\": " << K_ << ", \"BK\": " << BK << ", \"threads\": " << (BM_ / 8) * (BN_ / 8) << ", \"a_load\": \""
+    os << "{\"kernel\": \"" << (async_ok() ? "sgemm_async<" : "sgemm_tiled<") << BM_ << "," << BN_ << ">\", \"M\": " << M_ << ", \"N\": " << N_
+       << ", \"K\": " << K_ << ", \"BK\": " << BK << ", \"threads\": " << (async_ok() ? 256 : (BM_ / 8) * (BN_ / 8)) << ", \"a_load\": \""
        << mn[amode_] << "\", \"b_load\": \"" << mn[bmode_] << "\", \"c_store\": \"" << (cvec_ ? "v4" : "scalar")
        << "\", \"tiles\": " << static_cast<int64_t>(tilesM_) * tilesN_;
     if (!note_.empty()) os << ", \"tc_declined\": \"" << note_ << "\"";
@@ -581,6 +704,7 @@ class GemmRoutine final : public Routine {
 
   Config canonical(const Config* given) const;
   bool is_gemv() const { return gemv_; }
+  bool uses_async() const { return async_ok(); }
 
  private:
   void tables(const std::vector<int64_t>& t0, const std::vector<int64_t>& t1, const std::vector<int64_t>& t2,
@@ -620,7 +744,21 @@ class GemmRoutine final : public Routine {
 #undef MDHB_G2
 #undef MDHB_G
   }
+  bool async_ok() const {
+    return BM_ == 128 && (BN_ == 128 || BN_ == 256) && bmode_ == LD_MN4 && amode_ != LD_SCALAR &&
+           !std::getenv("MDHB_SGEMM_V1");
+  }
+  template <int TN>
+  void dispatch_async(const GemmArgs& a, cudaStream_t s) {
+    dim3 grid(static_cast<unsigned>(tilesM_ * tilesN_));
+    if (amode_ == LD_K4) {
+      if (cvec_) sgemm_async<true, true, TN><<<grid, 256, 0, s>>>(a); else sgemm_async<true, false, TN><<<grid, 256, 0, s>>>(a);
+    } else {
+      if (cvec_) sgemm_async<false, true, TN><<<grid, 256, 0, s>>>(a); else sgemm_async<false, false, TN><<<grid, 256, 0, s>>>(a);
+    }
+  }
   void dispatch(const GemmArgs& a, cudaStream_t s) {
+    if (async_ok()) return BN_ == 256 ? dispatch_async<16>(a, s) : dispatch_async<8>(a, s);
     if (BM_ == 128 && BN_ == 128) return dispatch2<128, 128>(a, s);
     if (BM_ == 128 && BN_ == 64) return dispatch2<128, 64>(a, s);
     if (BM_ == 64 && BN_ == 128) return dispatch2<64, 128>(a, s);
@@ -796,7 +934,10 @@ bool analyze_contraction(const Problem& p, Groups& g) {
   auto by = [&](const std::vector<int64_t>& cj) {
     return [&cj](int x, int y) { return std::llabs(cj[static_cast<size_t>(x)]) > std::llabs(cj[static_cast<size_t>(y)]); };
   };
-  std::stable_sort(g.Md.begin(), g.Md.end(), by(g.lc.cj));
+  // M dims: A-contiguous dim innermost (16-byte loads of A along m when A is
+  // M-major, e.g. CCSD(T)'s A[g][d][a][b]); N dims: C-contiguous innermost
+  // (vector stores of the big output); K dims: unit-stride operand innermost.
+  std::stable_sort(g.Md.begin(), g.Md.end(), by(g.la.cj));
   std::stable_sort(g.Nd.begin(), g.Nd.end(), by(g.lc.cj));
   {
     // K innermost = the dim where A (else B) has unit stride
@@ -850,9 +991,14 @@ std::unique_ptr<Routine> make_contraction(const Problem& p, const Config* cfg, C
       fail("Unsupported", "contraction template instantiates BM, BN in {64, 128} with K % 8 == 0");
     }
   } else {
-    const int menu[4][2] = {{128, 128}, {128, 64}, {64, 128}, {64, 64}};
-    for (auto& t : menu)
-      if ((ok = r->setup(t[0], t[1], {}, {}))) break;
+    const bool wide = std::getenv("MDHB_SGEMM_NARROW") == nullptr;
+    const int menu[5][2] = {{128, wide ? 256 : 128}, {128, 128}, {128, 64}, {64, 128}, {64, 64}};
+    for (auto& t : menu) {
+      if ((ok = r->setup(t[0], t[1], {}, {}))) {
+        if (t[1] == 256 && !r->uses_async()) { r = std::make_unique<GemmRoutine>(p, g); ok = false; continue; }
+        break;
+      }
+    }
   }
   if (!ok) return nullptr;
   if (cfg_out) *cfg_out = r->canonical(cfg);

@@ -471,13 +471,41 @@ __global__ void __launch_bounds__(WS_THREADS, 3) star7_ws(StencilArgs a) {
 // equal ranges, one per resident CTA, so every SM streams the same number of
 // planes (no wave tail) and consecutive segments of a CTA reuse the ring: a
 // global plane sequence number q drives slot = q % NSLOT and mbarrier parity.
+// Work units: mode 0 = one contiguous range of (tile, plane) steps per CTA;
+// mode 1 = grid-stride over (tile, TI-plane chunk) items in launch-grid order,
+// so concurrently running CTAs hold neighbouring tiles (halo rows hit L2)
+// while each CTA's ring pipeline stays warm from one item to the next.
+struct Work {
+  int64_t tile, ilo, ihi;
+};
+__device__ __forceinline__ bool next_work(int mode, const StencilArgs& a, int64_t tiles, int64_t total, int64_t& cursor,
+                                          Work& w) {
+  if (mode == 0) {
+    const int64_t g_end = total * (blockIdx.x + 1) / gridDim.x;
+    if (cursor >= g_end) return false;
+    w.tile = cursor / a.n0;
+    w.ilo = cursor % a.n0;
+    w.ihi = min(a.n0, w.ilo + (g_end - cursor));
+    cursor = w.ihi == a.n0 ? (w.tile + 1) * a.n0 : g_end;
+    return true;
+  }
+  const int64_t chunks = (a.n0 + a.ti - 1) / a.ti;
+  if (cursor >= tiles * chunks) return false;
+  w.tile = cursor % tiles;
+  w.ilo = (cursor / tiles) * a.ti;
+  w.ihi = min(a.n0, w.ilo + a.ti);
+  cursor += gridDim.x;
+  return true;
+}
+
 template <int MINB>
-__global__ void __launch_bounds__(WS_THREADS, MINB) star7_pers(StencilArgs a, int64_t tiles_k, int64_t total) {
+__global__ void __launch_bounds__(WS_THREADS, MINB) star7_pers(StencilArgs a, int64_t tiles_k, int64_t total, int mode) {
   constexpr int TJ = 16, ROWS = TJ + 2;
   extern __shared__ __align__(128) float sring[];
   __shared__ __align__(8) uint64_t full[NSLOT], empty[NSLOT];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t g_begin = total * blockIdx.x / gridDim.x, g_end = total * (blockIdx.x + 1) / gridDim.x;
+  const int64_t tiles = total / a.n0;
+  const int64_t cursor0 = mode == 0 ? total * blockIdx.x / gridDim.x : blockIdx.x;
   const uint32_t pstride = static_cast<uint32_t>(a.e1 * a.e2), rstride = static_cast<uint32_t>(a.e2);
 
   if (tid == 0) {
@@ -492,9 +520,10 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) star7_pers(StencilArgs a, in
   if (warp == 8) {
     // ---------------- producer: walk the same segments, one plane per q
     uint32_t q = 0;
-    for (int64_t g = g_begin; g < g_end;) {
-      const int64_t tile = g / a.n0, ilo = g % a.n0;
-      const int64_t ihi = min(a.n0, ilo + (g_end - g));
+    int64_t cursor = cursor0;
+    Work wk;
+    while (next_work(mode, a, tiles, total, cursor, wk)) {
+      const int64_t tile = wk.tile, ilo = wk.ilo, ihi = wk.ihi;
       const int64_t k0 = (tile % tiles_k) * TK, j0 = (tile / tiles_k) * TJ;
       const uint32_t base0 = static_cast<uint32_t>((ilo * a.e1 + j0) * a.e2 + k0);
       const float* vbase = a.v + ((ilo * a.e1 + j0) * a.e2 + k0);
@@ -520,7 +549,6 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) star7_pers(StencilArgs a, in
                        ::"r"(s_u32(dst)), "l"(src), "r"(bytes), "r"(s_u32(&full[s])) : "memory");
         }
       }
-      g = ihi == a.n0 ? (tile + 1) * a.n0 : g_end;
     }
     return;
   }
@@ -528,9 +556,10 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) star7_pers(StencilArgs a, in
   // ---------------- compute warps
   const int kl = lane * 4, jl = warp * 2;
   uint32_t q = 0;
-  for (int64_t g = g_begin; g < g_end;) {
-    const int64_t tile = g / a.n0, ilo = g % a.n0;
-    const int64_t ihi = min(a.n0, ilo + (g_end - g));
+  int64_t cursor = cursor0;
+  Work wk;
+  while (next_work(mode, a, tiles, total, cursor, wk)) {
+    const int64_t tile = wk.tile, ilo = wk.ilo, ihi = wk.ihi;
     const int64_t k0 = (tile % tiles_k) * TK, j0 = (tile / tiles_k) * TJ;
     const uint32_t base0 = static_cast<uint32_t>((ilo * a.e1 + j0) * a.e2 + k0);
     const int n = static_cast<int>(ihi - ilo);
@@ -606,7 +635,6 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) star7_pers(StencilArgs a, in
     if (t < n) step(t, R1, R2, R0), ++t;
     release(n + 1);  // the last plane was only read as "next"
     q += static_cast<uint32_t>(n + 2);
-    g = ihi == a.n0 ? (tile + 1) * a.n0 : g_end;
   }
 }
 
@@ -730,8 +758,10 @@ class StencilRoutine final : public Routine {
       }
       const int64_t tiles_k = (a.n2 + TK - 1) / TK, tiles = tiles_k * ((a.n1 + 15) / 16);
       const int64_t total = tiles * a.n0;
-      const int grid_p = static_cast<int>(std::min<int64_t>(ctas_, std::max<int64_t>(1, total / 4)));
-      kern<<<grid_p, WS_THREADS, smem, s>>>(a, tiles_k, total);
+      const int mode = std::getenv("MDHB_STENCIL_RANGES") ? 0 : 1;
+      const int64_t items = tiles * ((a.n0 + a.ti - 1) / a.ti);
+      const int grid_p = static_cast<int>(std::min<int64_t>(ctas_, mode ? items : std::max<int64_t>(1, total / 4)));
+      kern<<<grid_p, WS_THREADS, smem, s>>>(a, tiles_k, total, mode);
     } else if (ws_) {
       MDHB_CUDA(cudaFuncSetAttribute(star7_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       star7_ws<<<grid(), WS_THREADS, smem, s>>>(a);
@@ -832,6 +862,7 @@ std::unique_ptr<Routine> make_stencil(const Problem& p, const Config* cfg, Confi
     ti = static_cast<int>(a.n0 / grid_i);
     if (ti < 1 || a.n0 % grid_i != 0) fail("Unsupported", "stencil template needs uniform i-chunks");
   }
+  if (const char* f = std::getenv("MDHB_STENCIL_TI")) ti = std::max(1, std::atoi(f));
   a.ti = ti;
   if (cfg_out) {
     int64_t gi = (a.n0 + ti - 1) / ti;
