@@ -216,6 +216,194 @@ __global__ void __launch_bounds__(256) transpose_kn(const float* __restrict__ sr
   }
 }
 
+
+// Persistent variant: one CTA per SM walks the tile list; two TMEM
+// accumulators (2 x BN columns) let the epilogue warps drain tile i while
+// the MMA warp already accumulates tile i+1.  With RB (resident B) the whole
+// K extent of B for the single N tile is loaded once per CTA and stays in
+// shared memory -- MCC's 147 KB filter -- so only A streams from HBM.
+template <int BN, int STAGES, bool B_MN, bool RB>
+__global__ void __launch_bounds__(192, 1)
+    tc_gemm_pers(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, TcArgs g) {
+  constexpr uint32_t A_BYTES = BM * BKE * 4;
+  constexpr uint32_t B_BYTES = BN * BKE * 4;
+  constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  const uint32_t b_slots = RB ? static_cast<uint32_t>(g.nk) : STAGES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + b_slots * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* bfull = empty + STAGES;
+  uint64_t* tfull = bfull + 1;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = g.tilesM * g.tilesN;
+  constexpr int GROUP_M = 8;
+  auto tile_mn = [&](int x, int& tm, int& tn) {
+    const int per_group = GROUP_M * g.tilesN;
+    const int first_m = (x / per_group) * GROUP_M;
+    const int gsz = min(g.tilesM - first_m, GROUP_M);
+    tm = first_m + (x % per_group) % gsz;
+    tn = (x % per_group) / gsz;
+  };
+  if (threadIdx.x == 0) {
+    tc::tma_prefetch(&tma_a);
+    tc::tma_prefetch(&tma_b);
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(bfull, 1);
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 4);  // one arrival per epilogue warp
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, TMEM_COLS);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  auto kstep = [&](int (&dig)[MAXKD], int (&ka)[MAXR], int (&kb)[MAXR]) {
+    for (int q = g.nkd - 1; q >= 0; --q) {
+      if (++dig[q] < g.kext[q]) {
+#pragma unroll
+        for (int r = 0; r < MAXR; ++r) {
+          ka[r] += g.kca[q][r] * g.kstep[q];
+          kb[r] += g.kcb[q][r] * g.kstep[q];
+        }
+        return;
+      }
+#pragma unroll
+      for (int r = 0; r < MAXR; ++r) {
+        ka[r] -= g.kca[q][r] * g.kstep[q] * (g.kext[q] - 1);
+        kb[r] -= g.kcb[q][r] * g.kstep[q] * (g.kext[q] - 1);
+      }
+      dig[q] = 0;
+    }
+  };
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer
+    if (RB) {  // all of B for the (single) N tile, once
+      int dig[MAXKD] = {0, 0, 0, 0, 0, 0}, ka[MAXR] = {0, 0, 0, 0, 0}, kb[MAXR] = {0, 0, 0, 0, 0};
+      tc::mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(g.nk) * B_BYTES);
+      for (int kt = 0; kt < g.nk; ++kt) {
+        int c[MAXR];
+#pragma unroll
+        for (int r = 0; r < MAXR; ++r) c[r] = g.b_nc[r] + kb[r];
+        tc::tma_load(sB + kt * B_BYTES, &tma_b, bfull, g.b_rank, c);
+        kstep(dig, ka, kb);
+      }
+    }
+    uint32_t it = 0;
+    for (int x = blockIdx.x; x < ntiles; x += gridDim.x) {
+      int tm, tn;
+      tile_mn(x, tm, tn);
+      int am0[MAXR], bn0[MAXR], ka[MAXR], kb[MAXR], dig[MAXKD];
+#pragma unroll
+      for (int r = 0; r < MAXR; ++r) {
+        am0[r] = g.a_mc[tm * MAXR + r];
+        bn0[r] = g.b_nc[tn * MAXR + r];
+        ka[r] = 0;
+        kb[r] = 0;
+      }
+#pragma unroll
+      for (int q = 0; q < MAXKD; ++q) dig[q] = 0;
+      for (int kt = 0; kt < g.nk; ++kt, ++it) {
+        const uint32_t s = it % STAGES;
+        if (it >= STAGES) tc::mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+        tc::mbar_arrive_expect_tx(&full[s], A_BYTES + (RB ? 0u : B_BYTES));
+        int c[MAXR];
+#pragma unroll
+        for (int r = 0; r < MAXR; ++r) c[r] = am0[r] + ka[r];
+        tc::tma_load(sA + s * A_BYTES, &tma_a, &full[s], g.a_rank, c);
+        if (!RB) {
+#pragma unroll
+          for (int r = 0; r < MAXR; ++r) c[r] = bn0[r] + kb[r];
+          if (B_MN) {
+            for (int j = 0; j < BN / 32; ++j) {
+              int cj[MAXR];
+#pragma unroll
+              for (int r = 0; r < MAXR; ++r) cj[r] = c[r];
+              cj[0] += 32 * j;
+              tc::tma_load(sB + s * B_BYTES + j * (BKE * 128), &tma_b, &full[s], g.b_rank, cj);
+            }
+          } else {
+            tc::tma_load(sB + s * B_BYTES, &tma_b, &full[s], g.b_rank, c);
+          }
+        }
+        kstep(dig, ka, kb);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer
+    constexpr uint32_t idesc = tc::instr_desc(2, 0, B_MN ? 1 : 0, BM, BN);
+    if (RB) tc::mbar_wait(bfull, 0);
+    uint32_t it = 0, tl = 0;
+    for (int x = blockIdx.x; x < ntiles; x += gridDim.x, ++tl) {
+      const uint32_t acc = tl & 1;
+      if (tl >= 2) tc::mbar_wait(&tempty[acc], ((tl / 2) - 1) & 1);
+      tc::tc_fence_after();
+      const uint32_t dtm = tmem + acc * BN;
+      for (int kt = 0; kt < g.nk; ++kt, ++it) {
+        const uint32_t s = it % STAGES;
+        tc::mbar_wait(&full[s], (it / STAGES) & 1);
+        tc::tc_fence_after();
+        const uint32_t sa = tc::smem_u32(sA + s * A_BYTES);
+        const uint32_t sb = tc::smem_u32(sB + (RB ? static_cast<uint32_t>(kt) : s) * B_BYTES);
+#pragma unroll
+        for (int k = 0; k < BKE / 8; ++k) {
+          const uint64_t da = tc::sw128_desc(sa + k * 32, 16, 1024);
+          const uint64_t db = B_MN ? tc::umma_desc(sb + k * 1024, BKE * 128, 512, 1) : tc::sw128_desc(sb + k * 32, 16, 1024);
+          tc::mma<true>(dtm, da, db, idesc, (kt | k) != 0 ? 1u : 0u);
+        }
+        tc::mma_commit(&empty[s]);
+      }
+      tc::mma_commit(&tfull[acc]);
+    }
+  } else if (warp >= 2) {
+    // ---------------- epilogue warps
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    uint32_t tl = 0;
+    for (int x = blockIdx.x; x < ntiles; x += gridDim.x, ++tl) {
+      int tm, tn;
+      tile_mn(x, tm, tn);
+      const uint32_t acc = tl & 1;
+      tc::mbar_wait(&tfull[acc], (tl / 2) & 1);
+      tc::tc_fence_after();
+      float* crow = g.C + g.tCm[tm] + g.cm[row] + g.tCn[tn];
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        tc::tmem_ld32(tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c0), r);
+        if (g.cvec) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            __stcs(reinterpret_cast<float4*>(crow + g.cn[c0 + j]),
+                   make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                               __uint_as_float(r[j + 3])));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) crow[g.cn[c0 + j]] = __uint_as_float(r[j]);
+        }
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, TMEM_COLS);
+}
+
 // ---------------------------------------------------------------- host
 using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -368,8 +556,9 @@ class TcRoutine final : public Routine {
   double bytes() const override { return static_cast<double>(p_.in_bytes + p_.out_bytes); }
   std::string describe() const override {
     std::ostringstream os;
-    os << "{\"kernel\": \"tc_gemm_tf32<" << BN_ << "," << stages_ << "," << (va_.mn ? "A_MN" : "A_K") << ","
-       << (vb_.mn ? "B_MN" : "B_K") << ">\", \"math\": \"tf32\", \"M\": " << M_ << ", \"N\": " << N_ << ", \"K\": " << K_
+ os << "{\"kernel\": \"" << (pers_ ? "tc_gemm_pers<" : "tc_gemm_tf32<") << BN_ << "," << (pers_ ? pstages_ : stages_) << ","
+       << (va_.mn ? "A_MN" : "A_K") << "," << (vb_.mn ? "B_MN" : "B_K") << (rb_ && pers_ ? ",B_RESIDENT" : "")
+       << ">\", \"math\": \"tf32\", \"M\": " << M_ << ", \"N\": " << N_ << ", \"K\": " << K_
        << ", \"BM\": " << BM << ", \"BN\": " << BN_ << ", \"BK\": " << BKE << ", \"stages\": " << stages_
        << ", \"umma\": \"tcgen05.mma.cta_group::1.kind::tf32 M128xN" << BN_ << "xK8\", \"tiles\": "
        << static_cast<int64_t>(tilesM_) * tilesN_ << ", \"tmem_cols\": " << BN_
@@ -525,6 +714,12 @@ class TcRoutine final : public Routine {
     args_.tilesN = tilesN_;
     args_.cvec = cvec_;
     smem_ = static_cast<size_t>(stages_) * (BM + BN) * BKE * 4 + 1024 + 256;
+    // persistent instance: resident B when the single N tile's K extent fits
+    const size_t rb_bytes = static_cast<size_t>(nk_) * BN * BKE * 4 + 4 * BM * BKE * 4 + 1024 + 256;
+    rb_ = tilesN_ == 1 && !vb_.mn && (BN == 64 || BN == 128) && rb_bytes <= 227 * 1024;
+    pstages_ = rb_ ? 4 : stages_;
+    psmem_ = rb_ ? rb_bytes : smem_;
+    pers_ = !std::getenv("MDHB_TC_NONPERSISTENT");
     return true;
   }
 
@@ -543,6 +738,22 @@ class TcRoutine final : public Routine {
     if (B != last_b_) encode(vb_, B, &mb_), last_b_ = B;
     TcArgs a = args_;
     a.C = static_cast<float*>(d_out[0]);
+    if (pers_) {
+      const int sms = sm_count(p_.opt.device);
+      dim3 pgrid(static_cast<unsigned>(std::min(sms, tilesM_ * tilesN_)));
+#define MDHB_TCP(BNV, ST, MN, RBV)                                                                           \
+  if (BN_ == BNV && vb_.mn == MN && rb_ == RBV) {                                                           \
+    auto k = tc_gemm_pers<BNV, ST, MN, RBV>;                                                                \
+    MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(psmem_))); \
+    k<<<pgrid, 192, psmem_, s>>>(ma_, mb_, a);                                                              \
+    MDHB_CUDA(cudaGetLastError());                                                                          \
+    return;                                                                                                 \
+  }
+      MDHB_TCP(256, 4, false, false) MDHB_TCP(256, 4, true, false) MDHB_TCP(128, 6, false, false)
+      MDHB_TCP(128, 6, true, false) MDHB_TCP(64, 8, false, false) MDHB_TCP(64, 4, false, true)
+      MDHB_TCP(128, 4, false, true)
+#undef MDHB_TCP
+    }
     dim3 grid(static_cast<unsigned>(tilesM_ * tilesN_));
 #define MDHB_TC(BNV, ST, MN)                                                                              \
   if (BN_ == BNV && vb_.mn == MN) {                                                                      \
@@ -584,6 +795,9 @@ class TcRoutine final : public Routine {
   bool transposeB_ = false;
   int64_t tK_ = 0, tN_ = 0;
   void* bt_ = nullptr;
+  bool pers_ = false, rb_ = false;
+  int pstages_ = 0;
+  size_t psmem_ = 0;
 };
 
 }  // namespace
