@@ -167,44 +167,51 @@ def roofline_of(desc, kernel_s, pk, clock_mhz, traffic):
             "frac": round(tflops / peak, 4), "traffic": traffic, "peak_note": "148 SM x 128 FMA x 2 x SM clock"}
 
 
-def traffic_of(kernel):
+def traffic_of(routine, kernel):
+    """dram read+write bytes of this routine's dominant kernel from the
+    committed ncu --set full capture (profiles/traffic.json), or None when the
+    capture is of a different kernel than the one running now."""
     p = os.path.join(REPO, "profiles", "traffic.json")
     if os.path.exists(p):
-        j = json.load(open(p))
-        for k, v in j.items():
-            if k in kernel:
-                return v
+        v = json.load(open(p)).get(routine)
+        if isinstance(v, dict) and kernel.split("<")[0] in v["kernel"]:
+            return v["bytes"]
     return None
 
 
-def time_device(plan, d_in, d_out, steps, warmup, flush):
-    """Device time of `steps` runs bracketed by events on the launching stream
-    (+ optional L2 flush outside the events); returns (total_s, per_run list)."""
+def time_device(plan, d_in, d_out, steps, warmup, rotate):
+    """Device time of `steps` back-to-back runs of the hot path, replayed from
+    one CUDA graph (so host launch overhead never enters the GPU timeline) and
+    bracketed by events on the replay stream.  With `rotate` (inputs that fit
+    in L2) the runs cycle over R input copies with R * bytes >= 3x L2, so every
+    run reads its inputs from HBM, not from L2.  Returns (total_s, copies)."""
     import torch
-    stream = torch.cuda.current_stream()
-    for _ in range(warmup):
-        plan.run(d_in, d_out)
+    copies = [d_in]
+    if rotate:
+        in_bytes = sum(t.numel() * t.element_size() for t in d_in)
+        R = max(2, (3 * L2_BYTES) // max(in_bytes, 1) + 1)
+        for _ in range(R - 1):
+            copies.append([t.clone() for t in d_in])
+    for i in range(max(warmup, len(copies))):
+        plan.run(copies[i % len(copies)], d_out)
     torch.cuda.synchronize()
-    flush_buf = torch.empty(3 * L2_BYTES // 4, dtype=torch.float32, device=d_in[0].device) if flush else None
-    per = []
-    if flush:
-        for _ in range(steps):
-            flush_buf.fill_(1.0)
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            plan.run(d_in, d_out)
-            b.record(stream)
-            b.synchronize()
-            per.append(a.elapsed_time(b) / 1e3)
-        return sum(per), per
+    g = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    with torch.cuda.graph(g, stream=cs):
+        for i in range(steps):
+            plan.run(copies[i % len(copies)], d_out)
+    for _ in range(max(1, warmup // steps)):
+        g.replay()  # warm replay (graph upload, clocks)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(stream)
-    for _ in range(steps):
-        plan.run(d_in, d_out)
+    g.replay()
     b.record(stream)
     b.synchronize()
     tot = a.elapsed_time(b) / 1e3
-    return tot, [tot / steps] * steps
+    del g
+    return tot, len(copies)
 
 
 # ------------------------------------------------------------------ CPU baseline
@@ -322,18 +329,18 @@ def main():
         prl_weights(d_in)
     d_out = plan.empty(1)
     in_bytes = sum(t.numel() * t.element_size() for t in d_in)
-    flush = in_bytes < 2 * L2_BYTES
+    rotate = in_bytes < 2 * L2_BYTES
     sync_all(world)
     with ClockSampler(device) as clk:
-        tot, per = time_device(plan, d_in, d_out, args.steps, args.warmup, flush)
+        tot, copies = time_device(plan, d_in, d_out, args.steps, args.warmup, rotate)
     tot = max_over_ranks(tot, world)
     ms = tot / args.steps * 1e3
     value = desc["bytes"] * world / (tot / args.steps) / 1e9 if desc["bound"] == "hbm" else \
         desc["flops"] * world / (tot / args.steps) / 1e9
     unit = "GB/s" if desc["bound"] == "hbm" else "GFLOP/s"
-    kernel_s = statistics.median(per)
+    kernel_s = tot / args.steps
     clocks = clk.summary()
-    roof = roofline_of(desc, kernel_s, pk, clocks["sm_mhz"], traffic_of(desc["template"]["kernel"]))
+    roof = roofline_of(desc, kernel_s, pk, clocks["sm_mhz"], traffic_of(args.routine, desc["template"]["kernel"]))
 
     # ---- e2e through the C ABI with pinned host buffers
     e2e = e2e_measure(plan, d_in, max(3, min(args.steps, 10)), world)
@@ -345,7 +352,9 @@ def main():
             "config": {"workload": f"{base} {spec(base)['sizes']} per GPU ({math})", "family": desc["family"],
                        "kernel": desc["template"]["kernel"],
                        "parallelism": f"++-sharded z-slabs x{world} (weak)" if world > 1 else "single GPU",
-                       "l2": "L2 flushed between steps" if flush else f"inputs ({in_bytes >> 20} MB) larger than L2"},
+                       "l2": f"inputs rotated over {copies} copies (> 3x L2)" if rotate else
+                       f"inputs ({in_bytes >> 20} MB) larger than L2",
+                       "timing": "K runs replayed from one CUDA graph, CUDA events on the replay stream"},
             "roofline": roof, "clocks": clocks, "e2e": e2e,
             "gpu_launches": plan.launches * args.steps}
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -432,13 +441,14 @@ def routines_table(device, pk, world, exclude):
         d_out = plan.empty(1)
         in_bytes = sum(t.numel() * t.element_size() for t in d_in)
         heavy = desc["flops"] > 1e11 or base == "prl_max"
-        steps = 3 if heavy else 20
-        tot, per = time_device(plan, d_in, d_out, steps, 2, in_bytes < 2 * L2_BYTES)
-        k = statistics.median(per)
-        roof = roofline_of(desc, k, pk, None, traffic_of(desc["template"]["kernel"]))
+        steps = 3 if heavy else 50
+        tot, copies = time_device(plan, d_in, d_out, steps, 3, in_bytes < 2 * L2_BYTES)
+        k = tot / steps
+        roof = roofline_of(desc, k, pk, None, traffic_of(name, desc["template"]["kernel"]))
         ent = {"routine": name, "family": desc["family"], "kernel": desc["template"]["kernel"],
                "ms": round(k * 1e3, 4), "GB/s": round(desc["bytes"] / k / 1e9, 1),
-               "GFLOP/s": round(desc["flops"] / k / 1e9, 1), "roofline": roof, "launches": plan.launches * (steps + 2)}
+               "GFLOP/s": round(desc["flops"] / k / 1e9, 1), "roofline": roof, "launches": plan.launches * steps,
+               "input_copies": copies}
         if base == "prl_max":
             ent["pairs_per_s"] = desc["template"]["pairs"] / k
         out.append(ent)

@@ -283,6 +283,7 @@ struct SkinnyArgs {
   const int32_t *am, *ak, *bk, *bn, *cm, *cn;
   int M, N, K, ks;  // ks = k per split
   int splits;
+  int64_t sak, sbk;  // affine k strides of A and B (skinny_cluster)
 };
 
 template <int MT>
@@ -320,6 +321,138 @@ __global__ void __launch_bounds__(256) skinny_fold(SkinnyArgs g) {
   float s = g.part[i];
   for (int sp = 1; sp < g.splits; ++sp) s += g.part[static_cast<int64_t>(sp) * g.M * g.N + i];
   g.C[g.cm[m] + g.cn[n]] = s;
+}
+
+
+// Skinny contraction v2 (vector operands): K is split across the CS CTAs of a
+// thread-block cluster and re-composed in distributed shared memory, so no
+// partial sums ever reach global memory and there is one launch per run.
+//   SMX : blockIdx.x = a strip of NW = 32 columns of N; blockIdx.y = one of
+//         CS k-slices (the cluster), KS = K / CS rows of B per CTA
+//   SM  : the CTA's whole B slice [KS][32] and A slice [MT][KS] land in shared
+//         memory through 16-byte cp.async in 4 commit groups (stages), so
+//         compute on stage s overlaps the flight of stages s+1..3
+//   CC  : 256 threads = 4 k-quarters x 8 m-groups x 8 column quads
+//   RM  : MT/8 rows x 4 columns per thread, 4 k per step (float4 A reads)
+// Re-composition of K: k-quarters meet in shared memory (WRP -> SM), the CS
+// slices meet over DSMEM (SM -> cluster), each CTA folding 1/CS of the
+// outputs in fixed slice order -- deterministic, single writer per C cell.
+template <int MT, int KS>
+__global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g) {
+  constexpr int NW = 32, NSTG = 4, R = MT / 8, SL = KS / NSTG, KQ = SL / 4, AKQ = SL / 4, AP = KS + 4;
+  static_assert(KQ % 4 == 0, "k per thread per stage must be a multiple of 4");
+  extern __shared__ __align__(16) float sm[];
+  float* Bs = sm;                 // [KS][NW]
+  float* As = Bs + KS * NW;       // [MT][KS + 4]
+  float* red = As + MT * AP;      // [4][MT][NW]   k-quarter partials
+  float* inbox = red + 4 * MT * NW;  // [CS][MT*NW/CS]  slices pushed by the cluster's CTAs
+  const int tid = threadIdx.x;
+  const int kq = tid >> 6, mg = (tid >> 3) & 7, cq = tid & 7;
+  const int n0 = blockIdx.x * NW;
+  const int kbase = blockIdx.y * KS;
+  // every CTA of the cluster must be running before anyone writes into its
+  // shared memory: arrive now, wait just before the DSMEM pushes
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  // ---- issue every stage's copies up front (NSTG commit groups).  k offsets
+  // are affine (g.sak == 1, g.sbk per k), so one table read per row / column
+  // precedes the copies and nothing serialises the issue on load latency.
+  const int bq = tid % (NW / 4), bk0 = tid / (NW / 4);
+  const bool bok = n0 + bq * 4 < g.N;
+  const float* bsrc = g.B + (bok ? g.bn[n0 + bq * 4] + static_cast<int64_t>(kbase) * g.sbk : 0);
+  constexpr int ACH = (MT * AKQ + 255) / 256;
+  const float* asrc[ACH];
+  int adst[ACH];
+  bool aok[ACH];
+#pragma unroll
+  for (int i = 0; i < ACH; ++i) {
+    const int c = tid + 256 * i, m = c / AKQ;
+    aok[i] = c < MT * AKQ && m < g.M;
+    adst[i] = m * AP + (c % AKQ) * 4;
+    asrc[i] = g.A + (aok[i] ? g.am[m] + kbase + (c % AKQ) * 4 : 0);
+  }
+#pragma unroll
+  for (int s = 0; s < NSTG; ++s) {
+#pragma unroll
+    for (int i = 0; i < ACH; ++i)
+      if (tid + 256 * i < MT * AKQ)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(As + adst[i] + s * SL))),
+                     "l"(asrc[i] + s * SL), "r"(aok[i] ? 16 : 0));
+#pragma unroll
+    for (int k = s * SL + bk0; k < (s + 1) * SL; k += 256 / (NW / 4))
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(Bs + k * NW + bq * 4))),
+                   "l"(bsrc + static_cast<int64_t>(k) * g.sbk), "r"(bok ? 16 : 0));
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  float acc[R][4];
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  auto stage = [&](int s) {
+    const int k0 = s * SL + kq * KQ;
+#pragma unroll
+    for (int k = k0; k < k0 + KQ; k += 4) {
+      float a[R][4];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const float4 v = *reinterpret_cast<const float4*>(As + (mg * R + i) * AP + k);
+        a[i][0] = v.x; a[i][1] = v.y; a[i][2] = v.z; a[i][3] = v.w;
+      }
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const float4 b = *reinterpret_cast<const float4*>(Bs + (k + kk) * NW + cq * 4);
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          acc[i][0] = fmaf(a[i][kk], b.x, acc[i][0]);
+          acc[i][1] = fmaf(a[i][kk], b.y, acc[i][1]);
+          acc[i][2] = fmaf(a[i][kk], b.z, acc[i][2]);
+          acc[i][3] = fmaf(a[i][kk], b.w, acc[i][3]);
+        }
+      }
+    }
+  };
+  asm volatile("cp.async.wait_group 3;" ::: "memory");
+  __syncthreads();
+  stage(0);
+  asm volatile("cp.async.wait_group 2;" ::: "memory");
+  __syncthreads();
+  stage(1);
+  asm volatile("cp.async.wait_group 1;" ::: "memory");
+  __syncthreads();
+  stage(2);
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  stage(3);
+  // ---- k-quarters meet in shared memory (fixed order)
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+    *reinterpret_cast<float4*>(red + (kq * MT + mg * R + i) * NW + cq * 4) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+  __syncthreads();
+  // ---- k-slices meet over DSMEM: output o belongs to CTA o / per of the
+  // cluster; every CTA pushes its partial of o into slot [my rank] of the
+  // owner's inbox (remote stores, no round trips), one cluster barrier, then
+  // each owner folds its inbox in rank order -- deterministic.
+  uint32_t rank, cs;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(cs));
+  const int per = MT * NW / static_cast<int>(cs);
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+  for (int o = tid; o < MT * NW; o += 256) {
+    const float v = ((red[o] + red[MT * NW + o]) + red[2 * MT * NW + o]) + red[3 * MT * NW + o];
+    const uint32_t owner = static_cast<uint32_t>(o / per);
+    const uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(inbox + rank * per + o % per));
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(owner));
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote), "f"(v) : "memory");
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  for (int t = tid; t < per; t += 256) {
+    float s = 0.f;
+    for (uint32_t c = 0; c < cs; ++c) s += inbox[c * per + t];
+    const int o = static_cast<int>(rank) * per + t;
+    const int m = o / NW, n = n0 + o % NW;
+    if (m < g.M && n < g.N) g.C[g.cm[m] + g.cn[n]] = s;
+  }
 }
 
 
@@ -497,6 +630,23 @@ __global__ void __launch_bounds__(256, TN == 8 ? 2 : 1) sgemm_async(GemmArgs g) 
 }
 
 // ---------------------------------------------------------------- host
+// every offset 16-byte aligned (in floats)
+bool all_mod4(const std::vector<int64_t>& v) {
+  for (int64_t x : v)
+    if (x % 4) return false;
+  return true;
+}
+// offsets come in aligned runs of 4 consecutive floats (one 16-byte vector)
+bool groups4(const std::vector<int64_t>& v) {
+  if (v.size() % 4) return false;
+  for (size_t t = 0; t < v.size(); t += 4) {
+    if (v[t] % 4) return false;
+    for (size_t j = 1; j < 4; ++j)
+      if (v[t + j] != v[t] + static_cast<int64_t>(j)) return false;
+  }
+  return true;
+}
+
 class GemmRoutine final : public Routine {
  public:
   GemmRoutine(const Problem& p, Groups g) : p_(p), g_(std::move(g)) {}
@@ -508,7 +658,7 @@ class GemmRoutine final : public Routine {
   double flops() const override { return 2.0 * static_cast<double>(M_) * static_cast<double>(N_) * static_cast<double>(K_); }
   double bytes() const override { return static_cast<double>(p_.in_bytes + p_.out_bytes); }
   const char* bound() const override { return (gemv_ || skinny_) ? "hbm" : "fp32"; }
-  int launches() const override { return skinny_ ? 2 : 1; }
+  int launches() const override { return skinny_ && !cluster_ ? 2 : 1; }
 
   // Builds tables; returns false when this template cannot realise the problem.
   bool setup(int BM, int BN, const std::vector<int64_t>& Tm_in, const std::vector<int64_t>& Tn_in) {
@@ -525,7 +675,7 @@ class GemmRoutine final : public Routine {
     const int64_t a0 = g_.la.c0, b0 = g_.lb.c0, c0 = g_.lc.c0;
     std::vector<int64_t> tAm, tCm, tBn, tCn, am, cm, bn, cn;
     gemv_ = g_.Nd.empty();
-    if (!gemv_ && M_ <= 32 && N_ >= 64 && K_ >= 256 && Tm_in.empty()) {
+    if (!gemv_ && M_ <= 32 && ((N_ >= 64 && K_ >= 256) || K_ >= 128) && Tm_in.empty()) {
       // skinny: split K so that ~2 waves of CTAs stream B
       std::vector<int64_t> fullM, fullN;
       for (int d : g_.Md) fullM.push_back(e.sizes[static_cast<size_t>(d)]);
@@ -537,6 +687,30 @@ class GemmRoutine final : public Routine {
       for (auto& v : am) v += a0;
       for (auto& v : bn) v += b0;
       for (auto& v : cm) v += c0;
+      // v2 (cluster, DSMEM re-composition): 16-byte operand groups along k
+      // for A and along n for B, N % 4 == 0, K split 8 (else 4, 2) ways into
+      // slices that are multiples of 64 and fit shared memory
+      auto affine = [](const std::vector<int64_t>& v) {
+        for (size_t k = 1; k < v.size(); ++k)
+          if (v[k] - v[k - 1] != v[1] - v[0]) return false;
+        return v.size() > 1;
+      };
+      if (groups4(bn) && all_mod4(bk) && groups4(ak) && all_mod4(am) && N_ % 4 == 0 && affine(ak) && affine(bk) &&
+          ak[0] == 0 && bk[0] == 0 && ak[1] == 1 && !std::getenv("MDHB_SKINNY_V1")) {
+        sak_ = ak[1];
+        sbk_ = bk[1];
+        for (int cs : {8, 4, 2}) {
+          const int64_t ks = K_ / cs;
+          const int64_t mt = M_ <= 16 ? 16 : 32;
+          if (K_ % (cs * 64) || ks > 1024 || (ks & (ks - 1))) continue;
+          if ((ks * 32 + mt * (ks + 4) + 5 * mt * 32) * 4 > 200 * 1024) continue;
+          skinny_ = cluster_ = true;
+          ks_ = static_cast<int>(ks);
+          splits_ = cs;
+          tables(am, ak, bk, bn, cm, cn, {}, {}, {}, {});
+          return true;
+        }
+      }
       int64_t ntiles = (N_ + 255) / 256;
       int64_t want = std::max<int64_t>(1, 2 * sm_count(p_.opt.device) / ntiles);
       int64_t ks = 64;
@@ -609,20 +783,6 @@ class GemmRoutine final : public Routine {
     tilesM_ = static_cast<int>(tAm.size());
     tilesN_ = static_cast<int>(tBn.size());
     // vector load / store directions
-    auto all_mod4 = [](const std::vector<int64_t>& v) {
-      for (int64_t x : v)
-        if (x % 4) return false;
-      return true;
-    };
-    auto groups4 = [](const std::vector<int64_t>& v) {
-      if (v.size() % 4) return false;
-      for (size_t t = 0; t < v.size(); t += 4) {
-        if (v[t] % 4) return false;
-        for (size_t j = 1; j < 4; ++j)
-          if (v[t + j] != v[t] + static_cast<int64_t>(j)) return false;
-      }
-      return true;
-    };
     if (groups4(ak) && all_mod4(am) && all_mod4(tAm)) amode_ = LD_K4;
     else if (groups4(am) && all_mod4(ak) && all_mod4(tAm)) amode_ = LD_MN4;
     else amode_ = LD_SCALAR;
@@ -637,6 +797,12 @@ class GemmRoutine final : public Routine {
   std::string describe() const override {
     std::ostringstream os;
     const char* mn[] = {"scalar", "k4", "mn4"};
+    if (cluster_) {
+      os << "{\"kernel\": \"skinny_cluster<" << (M_ <= 16 ? 16 : 32) << ">\", \"M\": " << M_ << ", \"N\": " << N_
+         << ", \"K\": " << K_ << ", \"k_per_cta\": " << ks_ << ", \"cluster\": " << splits_
+         << ", \"ctas\": " << (N_ + 31) / 32 * splits_ << ", \"threads\": 256}";
+      return os.str();
+    }
     if (skinny_) {
       os << "{\"kernel\": \"skinny_partial<" << (M_ <= 16 ? 16 : 32) << ">+skinny_fold\", \"M\": " << M_
          << ", \"N\": " << N_ << ", \"K\": " << K_ << ", \"k_per_split\": " << ks_ << ", \"splits\": " << splits_
@@ -662,9 +828,35 @@ class GemmRoutine final : public Routine {
     const float* A = static_cast<const float*>(d_in[g_.a_buf]);
     const float* B = static_cast<const float*>(d_in[g_.b_buf]);
     float* C = static_cast<float*>(d_out[0]);
+    if (cluster_) {
+      SkinnyArgs a{A, B, nullptr, C, tab_[0], tab_[1], tab_[2], tab_[3], tab_[4], tab_[5], static_cast<int>(M_),
+                   static_cast<int>(N_), static_cast<int>(K_), ks_, splits_, sak_, sbk_};
+      const int mt = M_ <= 16 ? 16 : 32;
+      const size_t smem = (static_cast<size_t>(ks_) * 32 + static_cast<size_t>(mt) * (ks_ + 4) + 5 * mt * 32) * sizeof(float);
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3(static_cast<unsigned>((N_ + 31) / 32), static_cast<unsigned>(splits_));
+      lc.blockDim = dim3(256);
+      lc.dynamicSmemBytes = smem;
+      lc.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 1;
+      at[0].val.clusterDim.y = static_cast<unsigned>(splits_);
+      at[0].val.clusterDim.z = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      void (*kern)(SkinnyArgs) = nullptr;
+#define MDHB_SK(KS) \
+  if (ks_ == KS) kern = mt == 16 ? skinny_cluster<16, KS> : skinny_cluster<32, KS>;
+      MDHB_SK(64) MDHB_SK(128) MDHB_SK(256) MDHB_SK(512) MDHB_SK(1024)
+#undef MDHB_SK
+      if (smem > 48 * 1024) MDHB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      MDHB_CUDA(cudaLaunchKernelEx(&lc, kern, a));
+      return;
+    }
     if (skinny_) {
       SkinnyArgs a{A, B, part_, C, tab_[0], tab_[1], tab_[2], tab_[3], tab_[4], tab_[5], static_cast<int>(M_),
-                   static_cast<int>(N_), static_cast<int>(K_), ks_, splits_};
+                   static_cast<int>(N_), static_cast<int>(K_), ks_, splits_, 0, 0};
       dim3 grid(static_cast<unsigned>((N_ + 255) / 256), static_cast<unsigned>(splits_));
       size_t smem = static_cast<size_t>(M_) * ks_ * sizeof(float);
       if (smem > 48 * 1024) MDHB_CUDA(cudaFuncSetAttribute(skinny_partial<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -771,8 +963,9 @@ class GemmRoutine final : public Routine {
   int BM_ = 0, BN_ = 0, tilesM_ = 0, tilesN_ = 0;
   std::vector<int64_t> Tm_, Tn_;
   int amode_ = 0, bmode_ = 0;
-  bool cvec_ = false, gemv_ = false, skinny_ = false;
+  bool cvec_ = false, gemv_ = false, skinny_ = false, cluster_ = false;
   int ks_ = 0, splits_ = 0;
+  int64_t sak_ = 0, sbk_ = 0;
   float* part_ = nullptr;
   void* blob_ = nullptr;
 
@@ -994,7 +1187,8 @@ std::unique_ptr<Routine> make_contraction(const Problem& p, const Config* cfg, C
     const bool wide = std::getenv("MDHB_SGEMM_NARROW") == nullptr;
     const int menu[5][2] = {{128, wide ? 256 : 128}, {128, 128}, {128, 64}, {64, 128}, {64, 64}};
     for (auto& t : menu) {
-      if ((ok = r->setup(t[0], t[1], {}, {}))) {
+      ok = r->setup(t[0], t[1], {}, {});
+      if (ok) {
         if (t[1] == 256 && !r->uses_async()) { r = std::make_unique<GemmRoutine>(p, g); ok = false; continue; }
         break;
       }

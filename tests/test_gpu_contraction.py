@@ -17,7 +17,12 @@ SMALL = [
     ("mcc_nhwc", [4, 8, 16, 64, 3, 3, 16], "sgemm"),
     ("ccsdt_abcdef_gdab_efgc", [4, 4, 4, 4, 4, 4, 8], "sgemm"),
     ("ccsdt_abcdef_gdab_efgc", [8, 4, 4, 4, 8, 4, 16], "sgemm"),
-    ("matmul_resnet_fc", [16, 1000, 2048], None),
+    ("matmul_resnet_fc", [16, 1000, 2048], "skinny_cluster<16>"),
+    ("matmul_resnet_fc", [1, 1000, 2048], "skinny_cluster<16>"),    # inference shape (M = 1)
+    ("matmul_resnet_fc", [5, 36, 512], "skinny_cluster<16>"),       # ragged N strip, cluster of 8
+    ("matmul_resnet_fc", [24, 100, 256], "skinny_cluster<32>"),     # 17..32 rows, cluster of 4
+    ("matmul_resnet_fc", [32, 64, 128], "skinny_cluster<32>"),      # cluster of 2
+    ("matmul_resnet_fc", [16, 100, 328], "skinny_partial"),         # K not a multiple of 128: v1
 ]
 
 

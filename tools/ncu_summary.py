@@ -19,10 +19,20 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 
 
 def summary(path):
+    """Summary of the longest launch in the report (the routine's dominant kernel)."""
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
-    d = {"kernel": vals[hdr.index("Kernel Name")] if "Kernel Name" in hdr else None}
+    hdr, units = rows[0], rows[1]
+    ti = hdr.index("gpu__time_duration.sum")
+
+    def dur(r):
+        try:
+            return float(r[ti].replace(",", ""))
+        except ValueError:
+            return -1.0
+    vals = max(rows[2:], key=dur)
+    d = {"kernel": vals[hdr.index("Kernel Name")] if "Kernel Name" in hdr else None,
+         "launches_in_report": len(rows) - 2}
     for k in KEYS:
         if k in hdr:
             d[k] = vals[hdr.index(k)] + (" " + units[hdr.index(k)] if units[hdr.index(k)] else "")
@@ -34,6 +44,38 @@ def summary(path):
     return d
 
 
+def dram_bytes(d):
+    """dram read + write of the summarised launch, in bytes."""
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tot = 0.0
+    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        v, u = d[k].split()
+        tot += float(v.replace(",", "")) * scale[u]
+    return int(tot)
+
+
 if __name__ == "__main__":
-    for p in sys.argv[1:]:
-        print(json.dumps(summary(p), indent=1))
+    # tools/ncu_summary.py report.ncu-rep ...            -> print
+    # tools/ncu_summary.py --by-routine DIR TAG          -> DIR/prof_<routine>.ncu-rep into
+    #                                                       profiles/<TAG>_ncu_<routine>.json + traffic.json
+    if sys.argv[1] == "--by-routine":
+        import glob
+        import os
+        src, tag = sys.argv[2], sys.argv[3]
+        repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        tp = os.path.join(repo, "profiles", "traffic.json")
+        traffic = json.load(open(tp)) if os.path.exists(tp) else {}
+        traffic = {k: v for k, v in traffic.items() if isinstance(v, dict)}
+        for rep in sorted(glob.glob(os.path.join(src, "prof_*.ncu-rep"))):
+            routine = os.path.basename(rep)[5:-8].replace("__", ":")
+            d = summary(rep)
+            d["routine"] = routine
+            with open(os.path.join(repo, "profiles", f"{tag}_ncu_{routine.replace(':', '_')}.json"), "w") as f:
+                json.dump(d, f, indent=1)
+            traffic[routine] = {"kernel": d["kernel"], "bytes": dram_bytes(d)}
+            print(routine, d["kernel"], d["gpu__time_duration.sum"], traffic[routine]["bytes"])
+        with open(tp, "w") as f:
+            json.dump(traffic, f, indent=1)
+    else:
+        for p in sys.argv[1:]:
+            print(json.dumps(summary(p), indent=1))
