@@ -48,6 +48,7 @@ struct GemmArgs {
   const int32_t *am, *cm, *bn, *cn;      // per local row / column of a tile
   const int32_t *ak, *bk;                // per k
   int K, tilesM, tilesN;
+  int sak, sbk;  // per-k strides inside one k-tile (sgemm_pipe: ak[k0 + j] = ak[k0] + j * sak)
 };
 
 struct GemvArgs {
@@ -629,6 +630,151 @@ __global__ void __launch_bounds__(256, TN == 8 ? 2 : 1) sgemm_async(GemmArgs g) 
   }
 }
 
+// FFMA template v3: 128 x 128 CTA tile, 8 x 8 register tile per thread
+// (two 4-row x two 4-column quads, conflict-free 16-byte shared reads),
+// <= 128 registers so two CTAs (16 warps) share an SM, and a 4-stage
+// cp.async ring of BKT-deep k-tiles in MN-major shared layout [k][m] /
+// [k][n].  Operands whose MN dim is 16-byte contiguous land with 16-byte
+// copies (V16); any other view -- K-contiguous A (MatMul), permuted tensors
+// (CCSD(T)), the filter of MCC -- lands element-wise with 4-byte copies that
+// are coalesced along k and transpose on the fly (no pre-pass, no registers).
+// Fragments of step k+1 are read from shared memory while step k's 64 FFMAs
+// issue (register double buffering).
+//   SMX : one 128 x 128 tile of (M, N) per CTA (grouped raster)
+//   DM  : the K / BKT k-tiles;  SM : the 4-slot ring;  CC : 16 x 16 threads
+//   RM  : 8 x 8 accumulators per thread
+template <int BM, int BN, int BKT>
+struct PipeSmem {
+  static constexpr int PA = BM + 4, PB = BN + 4;  // row pitch (floats): breaks k-stride bank aliasing of the 4-byte fills
+  static constexpr int STAGES = BKT >= 32 ? 3 : 4;
+  static constexpr int FLOATS = STAGES * BKT * (PA + PB);
+};
+
+template <int BM, int BN, bool AV, bool BV, bool CVEC, int BKT>
+__global__ void __launch_bounds__(256, 2) sgemm_pipe(GemmArgs g) {
+  using SM = PipeSmem<BM, BN, BKT>;
+  constexpr int PA = SM::PA, PB = SM::PB, ST = SM::STAGES, TX = BN / 8;
+  static_assert((BM / 8) * (BN / 8) == 256, "8 x 8 register tiles over 256 threads");
+  extern __shared__ __align__(16) float psm[];
+  float* As = psm;                   // [ST][BKT][PA]
+  float* Bs = psm + ST * BKT * PA;   // [ST][BKT][PB]
+  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+  constexpr int GROUP_M = 8;
+  const int x = blockIdx.x;
+  const int per_group = GROUP_M * g.tilesN;
+  const int first_m = (x / per_group) * GROUP_M;
+  const int gsz = min(g.tilesM - first_m, GROUP_M);
+  const int tm = first_m + (x % per_group) % gsz;
+  const int tn = (x % per_group) / gsz;
+  const float* __restrict__ A = g.A + g.tAm[tm];
+  const float* __restrict__ B = g.B + g.tBn[tn];
+
+  // ---- fill slots, fixed across k-tiles.  Inside a k-tile the k offsets
+  // are affine (host-checked), so a slot's source is  base(k-tile) + off[p]
+  // with one uniform table read per k-tile and one IMAD.WIDE per copy.
+  // V16: 16-byte chunk c = tid + 256 p -> k = c / (X/4), mn = (c % (X/4)) * 4
+  // S4 : element e = tid + 256 p      -> k = e % BKT,    mn = e / BKT
+  constexpr int TA = AV ? BM * BKT / 4 : BM * BKT, TB = BV ? BN * BKT / 4 : BN * BKT;  // fills per k-tile
+  constexpr int NA = (TA + 255) / 256, NB = (TB + 255) / 256;
+  int a_off[NA], b_off[NB];
+#pragma unroll
+  for (int p = 0; p < NA; ++p) {
+    const int c = tid + 256 * p;
+    const int k = AV ? c / (BM / 4) : c % BKT, m = AV ? (c % (BM / 4)) * 4 : c / BKT;
+    a_off[p] = c < TA ? g.am[m] + k * g.sak : 0;
+  }
+#pragma unroll
+  for (int p = 0; p < NB; ++p) {
+    const int c = tid + 256 * p;
+    const int k = BV ? c / (BN / 4) : c % BKT, n = BV ? (c % (BN / 4)) * 4 : c / BKT;
+    b_off[p] = c < TB ? g.bn[n] + k * g.sbk : 0;
+  }
+  // shared destinations: slot p sits at a fixed offset from slot 0
+  const int a_dst0 = AV ? (tid / (BM / 4)) * PA + (tid % (BM / 4)) * 4 : (tid % BKT) * PA + tid / BKT;
+  const int b_dst0 = BV ? (tid / (BN / 4)) * PB + (tid % (BN / 4)) * 4 : (tid % BKT) * PB + tid / BKT;
+  constexpr int A_STEP = AV ? (256 / (BM / 4)) * PA : 256 / BKT;  // floats between slots p and p+1
+  constexpr int B_STEP = BV ? (256 / (BN / 4)) * PB : 256 / BKT;
+  const int nk = g.K / BKT;
+  auto issue = [&](int kt) {
+    const int s = kt % ST, k0 = kt * BKT;
+    const float* abase = A + __ldg(g.ak + k0);
+    const float* bbase = B + __ldg(g.bk + k0);
+    const uint32_t as = static_cast<uint32_t>(__cvta_generic_to_shared(As + s * BKT * PA + a_dst0));
+    const uint32_t bs = static_cast<uint32_t>(__cvta_generic_to_shared(Bs + s * BKT * PB + b_dst0));
+#pragma unroll
+    for (int p = 0; p < NA; ++p) {
+      if (TA % 256 && tid + 256 * p >= TA) continue;
+      if (AV) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(as + p * A_STEP * 4), "l"(abase + a_off[p]));
+      else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(as + p * A_STEP * 4), "l"(abase + a_off[p]));
+    }
+#pragma unroll
+    for (int p = 0; p < NB; ++p) {
+      if (TB % 256 && tid + 256 * p >= TB) continue;
+      if (BV) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(bs + p * B_STEP * 4), "l"(bbase + b_off[p]));
+      else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(bs + p * B_STEP * 4), "l"(bbase + b_off[p]));
+    }
+  };
+#pragma unroll
+  for (int p = 0; p < ST - 1; ++p) {
+    if (p < nk) issue(p);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+  for (int kt = 0; kt < nk; ++kt) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(ST - 2) : "memory");
+    __syncthreads();
+    if (kt + ST - 1 < nk) issue(kt + ST - 1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const float* as = As + (kt % ST) * BKT * PA + ty * 4;
+    const float* bs = Bs + (kt % ST) * BKT * PB + tx * 4;
+    float4 fa[2][2], fb[2][2];
+    fa[0][0] = *reinterpret_cast<const float4*>(as);
+    fa[0][1] = *reinterpret_cast<const float4*>(as + BM / 2);
+    fb[0][0] = *reinterpret_cast<const float4*>(bs);
+    fb[0][1] = *reinterpret_cast<const float4*>(bs + BN / 2);
+#pragma unroll
+    for (int k = 0; k < BKT; ++k) {
+      const int cur = k & 1, nxt = cur ^ 1;
+      if (k + 1 < BKT) {
+        fa[nxt][0] = *reinterpret_cast<const float4*>(as + (k + 1) * PA);
+        fa[nxt][1] = *reinterpret_cast<const float4*>(as + (k + 1) * PA + BM / 2);
+        fb[nxt][0] = *reinterpret_cast<const float4*>(bs + (k + 1) * PB);
+        fb[nxt][1] = *reinterpret_cast<const float4*>(bs + (k + 1) * PB + BN / 2);
+      }
+      const float a[8] = {fa[cur][0].x, fa[cur][0].y, fa[cur][0].z, fa[cur][0].w,
+                          fa[cur][1].x, fa[cur][1].y, fa[cur][1].z, fa[cur][1].w};
+      const float b[8] = {fb[cur][0].x, fb[cur][0].y, fb[cur][0].z, fb[cur][0].w,
+                          fb[cur][1].x, fb[cur][1].y, fb[cur][1].z, fb[cur][1].w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  float* __restrict__ C = g.C + g.tCm[tm] + g.tCn[tn];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = i < 4 ? ty * 4 + i : BM / 2 + ty * 4 + (i - 4);
+    float* crow = C + g.cm[r];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = h * (BN / 2) + tx * 4;
+      if (CVEC) {
+        *reinterpret_cast<float4*>(crow + g.cn[c]) =
+            make_float4(acc[i][h * 4 + 0], acc[i][h * 4 + 1], acc[i][h * 4 + 2], acc[i][h * 4 + 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) crow[g.cn[c + j]] = acc[i][h * 4 + j];
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- host
 // every offset 16-byte aligned (in floats)
 bool all_mod4(const std::vector<int64_t>& v) {
@@ -790,6 +936,28 @@ class GemmRoutine final : public Routine {
     else if (groups4(bk) && all_mod4(bn) && all_mod4(tBn)) bmode_ = LD_K4;
     else bmode_ = LD_SCALAR;
     cvec_ = groups4(cn) && all_mod4(cm) && all_mod4(tCm) && all_mod4(tCn);
+    {
+      // k offsets affine inside every k-tile of the pipe template: the
+      // deepest k-tile (32 for 128 x 128 tiles, else 16, else 8) that keeps
+      // both operands affine and divides K
+      auto tile_aff = [&](const std::vector<int64_t>& v, int64_t bkt, int& stride) {
+        if (v.size() < 2 || K_ % bkt) return false;
+        const int64_t sd = v[1] - v[0];
+        for (size_t k = 0; k < v.size(); ++k)
+          if (v[k] != v[k / bkt * bkt] + static_cast<int64_t>(k % bkt) * sd) return false;
+        stride = static_cast<int>(sd);
+        return true;
+      };
+      pbk_ = 0;
+      for (int bkt : {32, 16, 8}) {
+        if (bkt == 32 && !(BM == 128 && BN == 128)) continue;
+        if (tile_aff(ak, bkt, psak_) && tile_aff(bk, bkt, psbk_)) {
+          pbk_ = bkt;
+          break;
+        }
+      }
+      tile_affine_ = pbk_ > 0;
+    }
     tables(tAm, tCm, tBn, tCn, am, cm, bn, cn, ak, bk);
     return true;
   }
@@ -815,8 +983,13 @@ class GemmRoutine final : public Routine {
          << "\", \"M\": " << M_ << ", \"K\": " << K_ << ", \"threads\": " << (split ? 256 : 128) << "}";
       return os.str();
     }
-    os << "{\"kernel\": \"" << (async_ok() ? "sgemm_async<" : "sgemm_tiled<") << BM_ << "," << BN_ << ">\", \"M\": " << M_ << ", \"N\": " << N_
-       << ", \"K\": " << K_ << ", \"BK\": " << BK << ", \"threads\": " << (async_ok() ? 256 : (BM_ / 8) * (BN_ / 8)) << ", \"a_load\": \""
+    const std::string kname = pipe_ok() ? "sgemm_pipe<" + std::to_string(BM_) + "x" + std::to_string(BN_) + "," +
+                                              std::string(pipe_av() ? "V16" : "S4") + "," +
+                                              (pipe_bv() ? "V16" : "S4") + ",BK" + std::to_string(pipe_bk()) + ">"
+                              : (async_ok() ? "sgemm_async<" : "sgemm_tiled<") + std::to_string(BM_) + "," +
+                                    std::to_string(BN_) + ">";
+    os << "{\"kernel\": \"" << kname << "\", \"M\": " << M_ << ", \"N\": " << N_
+       << ", \"K\": " << K_ << ", \"BK\": " << (pipe_ok() ? pipe_bk() : BK) << ", \"threads\": " << (async_ok() || pipe_ok() ? 256 : (BM_ / 8) * (BN_ / 8)) << ", \"a_load\": \""
        << mn[amode_] << "\", \"b_load\": \"" << mn[bmode_] << "\", \"c_store\": \"" << (cvec_ ? "v4" : "scalar")
        << "\", \"tiles\": " << static_cast<int64_t>(tilesM_) * tilesN_;
     if (!note_.empty()) os << ", \"tc_declined\": \"" << note_ << "\"";
@@ -889,7 +1062,7 @@ class GemmRoutine final : public Routine {
       return;
     }
     GemmArgs a{A, B, C, tab_[0], tab_[1], tab_[2], tab_[3], tab_[4], tab_[5], tab_[6], tab_[7], tab_[8], tab_[9],
-               static_cast<int>(K_), tilesM_, tilesN_};
+               static_cast<int>(K_), tilesM_, tilesN_, psak_, psbk_};
     dispatch(a, s);
     MDHB_CUDA(cudaGetLastError());
   }
@@ -897,6 +1070,7 @@ class GemmRoutine final : public Routine {
   Config canonical(const Config* given) const;
   bool is_gemv() const { return gemv_; }
   bool uses_async() const { return async_ok(); }
+  bool uses_pipe() const { return pipe_ok(); }
 
  private:
   void tables(const std::vector<int64_t>& t0, const std::vector<int64_t>& t1, const std::vector<int64_t>& t2,
@@ -949,7 +1123,34 @@ class GemmRoutine final : public Routine {
       if (cvec_) sgemm_async<false, true, TN><<<grid, 256, 0, s>>>(a); else sgemm_async<false, false, TN><<<grid, 256, 0, s>>>(a);
     }
   }
+  // v3 (sgemm_pipe): 128 x 128 tiles, any operand view (V16 where the MN dim
+  // is 16-byte contiguous, else 4-byte fills), K a multiple of the k-tile
+  bool pipe_ok() const {
+    return ((BM_ == 128 && BN_ == 128) || (BM_ == 256 && BN_ == 64)) && K_ % 8 == 0 && tile_affine_ &&
+           !std::getenv("MDHB_SGEMM_V2");
+  }
+  int pipe_bk() const { return pbk_; }
+  bool pipe_av() const { return amode_ == LD_MN4; }
+  bool pipe_bv() const { return bmode_ == LD_MN4; }
+  template <int PBM, int PBN, int BKT>
+  void dispatch_pipe(const GemmArgs& a, cudaStream_t s) {
+    dim3 grid(static_cast<unsigned>(tilesM_ * tilesN_));
+    const size_t smem = PipeSmem<PBM, PBN, BKT>::FLOATS * sizeof(float);
+    void (*k)(GemmArgs) = nullptr;
+#define MDHB_P(AV, BV, CV) \
+  if (pipe_av() == AV && pipe_bv() == BV && cvec_ == CV) k = sgemm_pipe<PBM, PBN, AV, BV, CV, BKT>;
+    MDHB_P(true, true, true) MDHB_P(true, true, false) MDHB_P(true, false, true) MDHB_P(true, false, false)
+    MDHB_P(false, true, true) MDHB_P(false, true, false) MDHB_P(false, false, true) MDHB_P(false, false, false)
+#undef MDHB_P
+    MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    k<<<grid, 256, smem, s>>>(a);
+  }
   void dispatch(const GemmArgs& a, cudaStream_t s) {
+    if (pipe_ok()) {
+      if (BM_ == 256) return pipe_bk() == 16 ? dispatch_pipe<256, 64, 16>(a, s) : dispatch_pipe<256, 64, 8>(a, s);
+      if (pipe_bk() == 32) return dispatch_pipe<128, 128, 32>(a, s);
+      return pipe_bk() == 16 ? dispatch_pipe<128, 128, 16>(a, s) : dispatch_pipe<128, 128, 8>(a, s);
+    }
     if (async_ok()) return BN_ == 256 ? dispatch_async<16>(a, s) : dispatch_async<8>(a, s);
     if (BM_ == 128 && BN_ == 128) return dispatch2<128, 128>(a, s);
     if (BM_ == 128 && BN_ == 64) return dispatch2<128, 64>(a, s);
@@ -966,6 +1167,8 @@ class GemmRoutine final : public Routine {
   bool cvec_ = false, gemv_ = false, skinny_ = false, cluster_ = false;
   int ks_ = 0, splits_ = 0;
   int64_t sak_ = 0, sbk_ = 0;
+  bool tile_affine_ = false;
+  int psak_ = 0, psbk_ = 0, pbk_ = 0;
   float* part_ = nullptr;
   void* blob_ = nullptr;
 
@@ -1184,12 +1387,16 @@ std::unique_ptr<Routine> make_contraction(const Problem& p, const Config* cfg, C
       fail("Unsupported", "contraction template instantiates BM, BN in {64, 128} with K % 8 == 0");
     }
   } else {
-    const bool wide = std::getenv("MDHB_SGEMM_NARROW") == nullptr;
-    const int menu[5][2] = {{128, wide ? 256 : 128}, {128, 128}, {128, 64}, {64, 128}, {64, 64}};
+    const bool wide = std::getenv("MDHB_SGEMM_WIDE") != nullptr;
+    const int menu[6][2] = {{128, wide ? 256 : 128}, {128, 128}, {256, 64}, {128, 64}, {64, 128}, {64, 64}};
     for (auto& t : menu) {
       ok = r->setup(t[0], t[1], {}, {});
       if (ok) {
-        if (t[1] == 256 && !r->uses_async()) { r = std::make_unique<GemmRoutine>(p, g); ok = false; continue; }
+        if ((t[1] == 256 && !r->uses_async()) || (t[0] == 256 && !r->uses_pipe())) {
+          r = std::make_unique<GemmRoutine>(p, g);
+          ok = false;
+          continue;
+        }
         break;
       }
     }
