@@ -20,6 +20,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -217,6 +218,30 @@ __global__ void __launch_bounds__(256) transpose_kn(const float* __restrict__ sr
 }
 
 
+// Operand packing pass (Table-1 D4 layout_de for views no TMA box can
+// describe, e.g. CCSD(T)'s A[g][d][a][b] with the contraction index outermost
+// and 24-wide M dims): the operand is gathered through the contraction
+// template's additive offset tables into a K-major [tile][row][Kp] scratch
+// (K zero-padded to a multiple of 32), i.e. exactly the order in which the
+// MMA tiles consume it.  Consecutive threads walk k, so the writes coalesce.
+__global__ void __launch_bounds__(256) pack_kmajor(const float* __restrict__ src, float* __restrict__ dst,
+                                                   const int32_t* __restrict__ tile_off, const int32_t* __restrict__ row_off,
+                                                   const int32_t* __restrict__ k_off, int rows, int K, int Kp, int64_t total) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x; i < total; i += static_cast<int64_t>(gridDim.x) * 256) {
+    const int k = static_cast<int>(i % Kp);
+    const int64_t rr = i / Kp;
+    const int r = static_cast<int>(rr % rows);
+    const int64_t t = rr / rows;
+    dst[i] = k < K ? __ldg(src + tile_off[t] + row_off[r] + k_off[k]) : 0.f;
+  }
+}
+
+// shared-memory layout of tc_gemm_pers: A ring | B ring (or resident B) |
+// barriers (256 B) | epilogue staging (4 warps x 32 x 33 floats)
+#define EPI_OFF(ST, BNV, BSLOTS) \
+  (static_cast<size_t>(ST) * BM * BKE * 4 + static_cast<size_t>(BSLOTS) * (BNV) * BKE * 4 + 256)
+constexpr size_t EPI_BYTES = 4 * 32 * 33 * 4;
+
 // Persistent variant: one CTA per SM walks the tile list; two TMEM
 // accumulators (2 x BN columns) let the epilogue warps drain tile i while
 // the MMA warp already accumulates tile i+1.  With RB (resident B) the whole
@@ -227,7 +252,7 @@ __global__ void __launch_bounds__(192, 1)
     tc_gemm_pers(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, TcArgs g) {
   constexpr uint32_t A_BYTES = BM * BKE * 4;
   constexpr uint32_t B_BYTES = BN * BKE * 4;
-  constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -239,6 +264,8 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* tfull = bfull + 1;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  // per epilogue warp: a 32 x 33 staging square (row-major in, column-major out)
+  float* stage_base = reinterpret_cast<float*>(smem + EPI_OFF(STAGES, BN, b_slots));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = g.tilesM * g.tilesN;
   constexpr int GROUP_M = 8;
@@ -368,31 +395,37 @@ __global__ void __launch_bounds__(192, 1)
       tc::mma_commit(&tfull[acc]);
     }
   } else if (warp >= 2) {
-    // ---------------- epilogue warps
+    // ---------------- epilogue warps: TMEM -> registers -> 32x32 smem
+    // transpose -> C.  After the transpose lane j holds column c0 + j of 32
+    // consecutive rows, so each store instruction writes one row's 32
+    // columns: 128 contiguous bytes whenever the tile's columns are
+    // contiguous in C (MatMul, MCC, CCSD(T) with a full (e, f) block) --
+    // instead of 32 scattered 16-byte pieces, one per TMEM lane / C row.
     const int q = warp & 3;
-    const int row = q * 32 + lane;
+    float* stg = stage_base + (warp - 2) * 32 * 33;
     uint32_t tl = 0;
     for (int x = blockIdx.x; x < ntiles; x += gridDim.x, ++tl) {
       int tm, tn;
       tile_mn(x, tm, tn);
       const uint32_t acc = tl & 1;
+      // lane r holds the C row offset of TMEM lane q*32 + r
+      const int64_t rowoff = static_cast<int64_t>(g.tCm[tm]) + g.cm[q * 32 + lane] + g.tCn[tn];
       tc::mbar_wait(&tfull[acc], (tl / 2) & 1);
       tc::tc_fence_after();
-      float* crow = g.C + g.tCm[tm] + g.cm[row] + g.tCn[tn];
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t r[32];
         tc::tmem_ld32(tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c0), r);
-        if (g.cvec) {
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            __stcs(reinterpret_cast<float4*>(crow + g.cn[c0 + j]),
-                   make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
-                               __uint_as_float(r[j + 3])));
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) crow[g.cn[c0 + j]] = __uint_as_float(r[j]);
+        for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = __uint_as_float(r[j]);
+        __syncwarp();
+        const int64_t coff = g.cn[c0 + lane];
+#pragma unroll 8
+        for (int rr = 0; rr < 32; ++rr) {
+          const int64_t ro = __shfl_sync(0xffffffffu, rowoff, rr);
+          __stcs(g.C + ro + coff, stg[rr * 33 + lane]);
         }
+        __syncwarp();
       }
       tc::tc_fence_before();
       __syncwarp();
@@ -548,10 +581,12 @@ class TcRoutine final : public Routine {
   ~TcRoutine() override {
     if (blob_) cudaFree(blob_);
     if (bt_) cudaFree(bt_);
+    if (pa_) cudaFree(pa_);
+    if (pb_) cudaFree(pb_);
   }
   const char* family() const override { return "contraction"; }
   const char* bound() const override { return "tensor"; }
-  int launches() const override { return transposeB_ ? 2 : 1; }
+  int launches() const override { return packed_ ? 3 : (transposeB_ ? 2 : 1); }
   double flops() const override { return 2.0 * static_cast<double>(M_) * static_cast<double>(N_) * static_cast<double>(K_); }
   double bytes() const override { return static_cast<double>(p_.in_bytes + p_.out_bytes); }
   std::string describe() const override {
@@ -562,8 +597,10 @@ class TcRoutine final : public Routine {
        << ", \"BM\": " << BM << ", \"BN\": " << BN_ << ", \"BK\": " << BKE << ", \"stages\": " << stages_
        << ", \"umma\": \"tcgen05.mma.cta_group::1.kind::tf32 M128xN" << BN_ << "xK8\", \"tiles\": "
        << static_cast<int64_t>(tilesM_) * tilesN_ << ", \"tmem_cols\": " << BN_
-       << ", \"b_layout\": \"" << (transposeB_ ? "K-major copy (layout_de [2,1] pre-pass)" : (vb_.mn ? "MN-major" : "K-major"))
-       << "\"}";
+       << ", \"b_layout\": \"" << (packed_ ? "packed K-major (pack_kmajor pre-pass, both operands)" : transposeB_ ? "K-major copy (layout_de [2,1] pre-pass)" : (vb_.mn ? "MN-major" : "K-major"))
+       << "\"";
+    if (packed_) os << ", \"K_padded\": " << Kp_;
+    os << "}";
     return os.str();
   }
 
@@ -572,8 +609,13 @@ class TcRoutine final : public Routine {
     M_ = prod_sizes(e, g_.Md);
     N_ = prod_sizes(e, g_.Nd);
     K_ = prod_sizes(e, g_.Kd);
-    if (!describe_view(p_, g_.a_buf, g_.Md, g_.Kd, BM, false, va_, why)) return false;
-    if (!describe_view(p_, g_.b_buf, g_.Nd, g_.Kd, BN, true, vb_, why)) return false;
+    std::string w;
+    if (!describe_view(p_, g_.a_buf, g_.Md, g_.Kd, BM, false, va_, &w) ||
+        !describe_view(p_, g_.b_buf, g_.Nd, g_.Kd, BN, true, vb_, &w) || va_.kin != vb_.kin) {
+      if (setup_packed(BN, why)) return true;
+      *why = w + "; packed: " + *why;
+      return false;
+    }
     if (vb_.mn && g_.Nd.size() == 1 && g_.Kd.size() == 1 && !std::getenv("MDHB_TC_NO_TRANSPOSE")) {
       // rewrite B K-major into scratch: Bt[n][k]
       const int dn = g_.Nd[0], dk = g_.Kd[0];
@@ -680,6 +722,7 @@ class TcRoutine final : public Routine {
     for (size_t t = 0; grp && t < cn.size(); t += 4)
       for (size_t j = 1; j < 4; ++j) grp = grp && cn[t + j] == cn[t] + static_cast<int64_t>(j);
     cvec_ = grp && mod4(cn) && mod4(cm) && mod4(tCm) && mod4(tCn);
+    c_run_ = run_of(cn);
     // coordinate tables
     std::vector<int64_t> amc, bnc;
     for (auto& o : om) for (auto c : coords(va_, o, true)) amc.push_back(c);
@@ -715,17 +758,145 @@ class TcRoutine final : public Routine {
     args_.cvec = cvec_;
     smem_ = static_cast<size_t>(stages_) * (BM + BN) * BKE * 4 + 1024 + 256;
     // persistent instance: resident B when the single N tile's K extent fits
-    const size_t rb_bytes = static_cast<size_t>(nk_) * BN * BKE * 4 + 4 * BM * BKE * 4 + 1024 + 256;
+    auto rb_need = [&](int st) { return static_cast<size_t>(nk_) * BN * BKE * 4 + st * BM * BKE * 4 + 1024 + 256 + EPI_BYTES; };
+    const int rb_st = rb_need(4) <= 227 * 1024 ? 4 : 3;
+    const size_t rb_bytes = rb_need(rb_st);
     rb_ = tilesN_ == 1 && !vb_.mn && (BN == 64 || BN == 128) && rb_bytes <= 227 * 1024;
-    pstages_ = rb_ ? 4 : stages_;
-    psmem_ = rb_ ? rb_bytes : smem_;
+    pstages_ = rb_ ? rb_st : pers_stages(BN);
+    psmem_ = rb_ ? rb_bytes : static_cast<size_t>(pstages_) * (BM + BN) * BKE * 4 + 1024 + 256 + EPI_BYTES;
     pers_ = !std::getenv("MDHB_TC_NONPERSISTENT");
     return true;
   }
 
+  // Packed-operand instance: both operands gathered K-major into scratch in
+  // tile order (pack_kmajor), so any view the contraction family accepts
+  // reaches the tensor cores; C is written through the FFMA template's tables.
+  bool setup_packed(int BN, std::string* why) {
+    const MdHom& e = p_.e;
+    std::vector<int64_t> Tm = factor_box(e, g_.Md, BM), Tn = factor_box(e, g_.Nd, BN);
+    if (Tm.empty() || Tn.empty()) return *why = "row tiles cannot be formed", false;
+    Kp_ = (K_ + BKE - 1) / BKE * BKE;
+    if ((M_ + N_) * Kp_ * 4 > (int64_t(1) << 30)) return *why = "packed operands exceed 1 GiB", false;
+    auto ones = [](size_t n) { return std::vector<int64_t>(n, 1); };
+    auto grid_of = [&](const std::vector<int>& dims, const std::vector<int64_t>& T, std::vector<int64_t>& gext) {
+      for (size_t q = 0; q < dims.size(); ++q) gext.push_back(e.sizes[static_cast<size_t>(dims[q])] / T[q]);
+    };
+    std::vector<int64_t> gm, gn, fullK;
+    grid_of(g_.Md, Tm, gm);
+    grid_of(g_.Nd, Tn, gn);
+    for (int d : g_.Kd) fullK.push_back(e.sizes[static_cast<size_t>(d)]);
+    std::vector<int64_t> tAm = box_offsets(g_.Md, gm, g_.la.cj, Tm), tBn = box_offsets(g_.Nd, gn, g_.lb.cj, Tn);
+    std::vector<int64_t> tCm = box_offsets(g_.Md, gm, g_.lc.cj, Tm), tCn = box_offsets(g_.Nd, gn, g_.lc.cj, Tn);
+    std::vector<int64_t> am = box_offsets(g_.Md, Tm, g_.la.cj, ones(Tm.size())), bn = box_offsets(g_.Nd, Tn, g_.lb.cj, ones(Tn.size()));
+    std::vector<int64_t> cm = box_offsets(g_.Md, Tm, g_.lc.cj, ones(Tm.size())), cn = box_offsets(g_.Nd, Tn, g_.lc.cj, ones(Tn.size()));
+    std::vector<int64_t> ak = box_offsets(g_.Kd, fullK, g_.la.cj, ones(fullK.size())), bk = box_offsets(g_.Kd, fullK, g_.lb.cj, ones(fullK.size()));
+    for (auto& v : tAm) v += g_.la.c0;
+    for (auto& v : tBn) v += g_.lb.c0;
+    for (auto& v : tCm) v += g_.lc.c0;
+    tilesM_ = static_cast<int>(tAm.size());
+    tilesN_ = static_cast<int>(tBn.size());
+    BN_ = BN;
+    stages_ = BN >= 256 ? 4 : (BN >= 128 ? 6 : 8);
+    nk_ = static_cast<int>(Kp_ / BKE);
+    auto view2 = [&](int buf, int64_t rows_total, int box_rows) {
+      View v;
+      v.buf = buf;
+      v.rank = 2;
+      v.dims[0] = static_cast<cuuint64_t>(Kp_);
+      v.dims[1] = static_cast<cuuint64_t>(rows_total);
+      v.strides[0] = 4;
+      v.strides[1] = static_cast<cuuint64_t>(Kp_ * 4);
+      v.box[0] = BKE;
+      v.box[1] = static_cast<cuuint32_t>(box_rows);
+      v.mn = false;
+      return v;
+    };
+    va_ = view2(g_.a_buf, M_, BM);
+    vb_ = view2(g_.b_buf, N_, BN);
+    args_.nkd = 1;
+    args_.kext[0] = nk_;
+    args_.kstep[0] = BKE;
+    for (int t = 0; t < MAXR; ++t) args_.kca[0][t] = args_.kcb[0][t] = t == 0 ? 1 : 0;
+    std::vector<int64_t> amc, bnc;
+    for (int t = 0; t < tilesM_; ++t) for (int r = 0; r < MAXR; ++r) amc.push_back(r == 1 ? int64_t(t) * BM : 0);
+    for (int t = 0; t < tilesN_; ++t) for (int r = 0; r < MAXR; ++r) bnc.push_back(r == 1 ? int64_t(t) * BN : 0);
+    bool grp = cn.size() % 4 == 0;
+    for (size_t t = 0; grp && t < cn.size(); t += 4)
+      for (size_t j = 1; j < 4; ++j) grp = grp && cn[t + j] == cn[t] + static_cast<int64_t>(j);
+    auto mod4 = [](const std::vector<int64_t>& v) {
+      for (auto x : v)
+        if (x % 4) return false;
+      return true;
+    };
+    cvec_ = grp && mod4(cn) && mod4(cm) && mod4(tCm) && mod4(tCn);
+    c_run_ = run_of(cn);
+    const std::vector<int64_t>* ts[12] = {&tCm, &tCn, &cm, &cn, &amc, &bnc, &tAm, &am, &ak, &tBn, &bn, &bk};
+    size_t cur = 0, offs[12];
+    std::vector<int32_t> host;
+    for (int q = 0; q < 12; ++q) {
+      offs[q] = cur;
+      for (int64_t x : *ts[q]) {
+        if (x > INT32_MAX || x < INT32_MIN) return *why = "offsets exceed int32", false;
+        host.push_back(static_cast<int32_t>(x));
+        ++cur;
+      }
+      while (cur % 64) host.push_back(0), ++cur;
+    }
+    MDHB_CUDA(cudaSetDevice(p_.opt.device));
+    MDHB_CUDA(cudaMalloc(&blob_, std::max<size_t>(cur, 64) * 4));
+    MDHB_CUDA(cudaMemcpy(blob_, host.data(), cur * 4, cudaMemcpyHostToDevice));
+    const int32_t* base = static_cast<const int32_t*>(blob_);
+    args_.tCm = base + offs[0];
+    args_.tCn = base + offs[1];
+    args_.cm = base + offs[2];
+    args_.cn = base + offs[3];
+    args_.a_mc = base + offs[4];
+    args_.b_nc = base + offs[5];
+    pk_ = {base + offs[6], base + offs[7], base + offs[8], base + offs[9], base + offs[10], base + offs[11]};
+    args_.a_rank = 2;
+    args_.b_rank = 2;
+    args_.nk = nk_;
+    args_.tilesM = tilesM_;
+    args_.tilesN = tilesN_;
+    args_.cvec = cvec_;
+    MDHB_CUDA(cudaMalloc(&pa_, static_cast<size_t>(M_ * Kp_) * 4));
+    MDHB_CUDA(cudaMalloc(&pb_, static_cast<size_t>(N_ * Kp_) * 4));
+    packed_ = true;
+    smem_ = static_cast<size_t>(stages_) * (BM + BN) * BKE * 4 + 1024 + 256;
+    rb_ = false;
+    pstages_ = pers_stages(BN);
+    psmem_ = static_cast<size_t>(pstages_) * (BM + BN) * BKE * 4 + 1024 + 256 + EPI_BYTES;
+    pers_ = !std::getenv("MDHB_TC_NONPERSISTENT");
+    return true;
+  }
+
+  bool packed() const { return packed_; }
+  int64_t c_run() const { return c_run_; }
+  static int64_t run_of(const std::vector<int64_t>& cn) {
+    int64_t n = 1;
+    while (n < static_cast<int64_t>(cn.size()) && cn[static_cast<size_t>(n)] == cn[0] + n) ++n;
+    return n;
+  }
+  // ring depth of the persistent kernel (fits 227 KB with the epilogue staging)
+  static int pers_stages(int BN) { return BN >= 192 ? 4 : (BN >= 128 ? 6 : 8); }
+
   void launch(const void* const* d_in, void* const* d_out, cudaStream_t s) override {
     const void* A = d_in[va_.buf];
     const void* B = d_in[vb_.buf];
+    if (packed_) {
+      const int sms = sm_count(p_.opt.device);
+      const int64_t ta = M_ * Kp_, tb = N_ * Kp_;
+      pack_kmajor<<<static_cast<unsigned>(std::min<int64_t>(8 * sms, (ta + 255) / 256)), 256, 0, s>>>(
+          static_cast<const float*>(A), static_cast<float*>(pa_), pk_[0], pk_[1], pk_[2], BM, static_cast<int>(K_),
+          static_cast<int>(Kp_), ta);
+      MDHB_CUDA(cudaGetLastError());
+      pack_kmajor<<<static_cast<unsigned>(std::min<int64_t>(8 * sms, (tb + 255) / 256)), 256, 0, s>>>(
+          static_cast<const float*>(B), static_cast<float*>(pb_), pk_[3], pk_[4], pk_[5], BN_, static_cast<int>(K_),
+          static_cast<int>(Kp_), tb);
+      MDHB_CUDA(cudaGetLastError());
+      A = pa_;
+      B = pb_;
+    }
     if (transposeB_) {
       const float* src = static_cast<const float*>(B) + g_.lb.c0;
       dim3 tg(static_cast<unsigned>((tN_ + 31) / 32), static_cast<unsigned>((tK_ + 31) / 32));
@@ -742,16 +913,17 @@ class TcRoutine final : public Routine {
       const int sms = sm_count(p_.opt.device);
       dim3 pgrid(static_cast<unsigned>(std::min(sms, tilesM_ * tilesN_)));
 #define MDHB_TCP(BNV, ST, MN, RBV)                                                                           \
-  if (BN_ == BNV && vb_.mn == MN && rb_ == RBV) {                                                           \
+  if (BN_ == BNV && vb_.mn == MN && rb_ == RBV && pstages_ == ST) {                                         \
     auto k = tc_gemm_pers<BNV, ST, MN, RBV>;                                                                \
     MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(psmem_))); \
     k<<<pgrid, 192, psmem_, s>>>(ma_, mb_, a);                                                              \
     MDHB_CUDA(cudaGetLastError());                                                                          \
     return;                                                                                                 \
   }
-      MDHB_TCP(256, 4, false, false) MDHB_TCP(256, 4, true, false) MDHB_TCP(128, 6, false, false)
-      MDHB_TCP(128, 6, true, false) MDHB_TCP(64, 8, false, false) MDHB_TCP(64, 4, false, true)
-      MDHB_TCP(128, 4, false, true)
+      MDHB_TCP(256, 4, false, false) MDHB_TCP(256, 4, true, false) MDHB_TCP(192, 4, false, false)
+      MDHB_TCP(128, 6, false, false) MDHB_TCP(128, 6, true, false) MDHB_TCP(64, 8, false, false)
+      MDHB_TCP(64, 4, false, true) MDHB_TCP(64, 3, false, true) MDHB_TCP(128, 4, false, true)
+      MDHB_TCP(128, 3, false, true)
 #undef MDHB_TCP
     }
     dim3 grid(static_cast<unsigned>(tilesM_ * tilesN_));
@@ -798,24 +970,35 @@ class TcRoutine final : public Routine {
   bool pers_ = false, rb_ = false;
   int pstages_ = 0;
   size_t psmem_ = 0;
+  bool packed_ = false;
+  int64_t Kp_ = 0, c_run_ = 1;
+  void *pa_ = nullptr, *pb_ = nullptr;
+  std::array<const int32_t*, 6> pk_{};  // packing tables: tAm, am, ak, tBn, bn, bk
 };
 
 }  // namespace
 
 std::unique_ptr<Routine> make_tc_contraction(const Problem& p, const Groups& g, const Config* cfg, Config* cfg_out,
                                              std::string* why) {
-  std::vector<int> menu = {256, 128, 64};
+  // N-tile menu; among the instances that set up, prefer a direct TMA view
+  // over packed operands, then the longest contiguous run of C per tile row
+  // (the epilogue's store width), then the wider tile.
+  std::vector<int> menu = {256, 192, 128, 64};
   if (const char* f = std::getenv("MDHB_TC_BN")) menu = {std::atoi(f)};
+  std::unique_ptr<TcRoutine> best;
+  int64_t best_score = -1;
   for (int bn : menu) {
     auto r = std::make_unique<TcRoutine>(p, g);
     std::string w;
-    if (r->setup(bn, &w)) {
-      if (cfg_out) *cfg_out = cfg ? *cfg : baseline_config(p.e, p.m);
-      return r;
+    if (!r->setup(bn, &w)) {
+      *why = w;
+      continue;
     }
-    *why = w;
+    const int64_t score = (r->packed() ? 0 : 1000000) + r->c_run() * 1000 + bn;
+    if (score > best_score) best_score = score, best = std::move(r);
   }
-  return nullptr;
+  if (best && cfg_out) *cfg_out = cfg ? *cfg : baseline_config(p.e, p.m);
+  return best;
 }
 
 }  // namespace ctr

@@ -17,6 +17,9 @@ CASES = [
     ("matmul_fp32", [128, 128, 32], "tc_gemm_tf32<128"),
     ("mcc_nhwc", [2, 8, 8, 64, 3, 3, 64], "tc_gemm_tf32<64"),
     ("mcc_nhwc", [4, 16, 8, 64, 3, 3, 32], "tc_gemm_tf32<64"),
+    # packed K-major operands (views no TMA box describes; K padded to 32)
+    ("ccsdt_abcdef_gdab_efgc", [4, 4, 8, 8, 8, 4, 72], "tc_gemm_tf32<256"),
+    ("ccsdt_abcdef_gdab_efgc", [8, 4, 4, 4, 8, 4, 40], "tc_gemm_tf32<128"),
 ]
 
 
@@ -102,3 +105,25 @@ def test_tf32_variants_agree(env, monkeypatch):
     monkeypatch.setenv(env, "1")
     (var,) = run_device(plan_tf32(j), ins)
     assert np.array_equal(base, var)
+
+
+@pytest.mark.gpu
+def test_tf32_ccsdt_full_slices_exact():
+    """Full CCSD(T) size on the tensor cores (packed operands) vs ++-slices."""
+    import torch
+    j = spec("ccsdt_abcdef_gdab_efgc")
+    comp = mo.Computation.from_json(j)
+    plan = plan_tf32(j)
+    d = plan.describe()["template"]
+    assert "tc_gemm" in d["kernel"] and "packed" in d["b_layout"], d
+    ins = exact_inputs(comp, 3)
+    d_in = plan.empty(0)
+    for t, x in zip(d_in, ins):
+        t.copy_(torch.from_numpy(x).to(t.dtype))
+    (out,) = plan.empty(1)
+    plan.run(d_in, [out])
+    torch.cuda.synchronize()
+    for box in ({0: (0, 1), 1: (0, 2)}, {0: (23, 24), 3: (22, 24)}):
+        ((part, dfd),), shifts = mo.execute_box(comp, ins, box)
+        sl = tuple(slice(s, s + n) for s, n in zip(shifts[0], part.shape))
+        assert np.array_equal(out[sl].cpu().numpy().astype(np.float64)[dfd], part[dfd]), box

@@ -66,9 +66,9 @@ if __name__ == "__main__":
         tp = os.path.join(repo, "profiles", "traffic.json")
         traffic = json.load(open(tp)) if os.path.exists(tp) else {}
         traffic = {k: v for k, v in traffic.items() if isinstance(v, dict)}
-        for rep in sorted(glob.glob(os.path.join(src, "prof_*.ncu-rep"))):
-            routine = os.path.basename(rep)[5:-8].replace("__", ":")
-            d = summary(rep)
+        for rep in sorted(glob.glob(os.path.join(src, "prof_*.json"))):
+            routine = os.path.basename(rep)[5:-5].replace("__", ":")
+            d = json.load(open(rep))
             d["routine"] = routine
             with open(os.path.join(repo, "profiles", f"{tag}_ncu_{routine.replace(':', '_')}.json"), "w") as f:
                 json.dump(d, f, indent=1)
