@@ -240,7 +240,11 @@ __global__ void __launch_bounds__(256) pack_kmajor(const float* __restrict__ src
 // barriers (256 B) | epilogue staging (4 warps x 32 x 33 floats)
 #define EPI_OFF(ST, BNV, BSLOTS) \
   (static_cast<size_t>(ST) * BM * BKE * 4 + static_cast<size_t>(BSLOTS) * (BNV) * BKE * 4 + 256)
-constexpr size_t EPI_BYTES = 4 * 32 * 33 * 4;
+// epilogue warps: 2 per TMEM lane quarter (splitting the tile's columns), or
+// 1 per quarter when a resident B
+// (resident B) or a 256-wide tile's 4-stage ring leaves no room for 8 squares
+__host__ __device__ constexpr int epi_warps(bool rb, int bn) { return rb || bn >= 256 ? 4 : 8; }
+__host__ __device__ constexpr size_t epi_bytes(bool rb, int bn) { return epi_warps(rb, bn) * (32 * 33 * 4 + 32 * 8); }
 
 // Persistent variant: one CTA per SM walks the tile list; two TMEM
 // accumulators (2 x BN columns) let the epilogue warps drain tile i while
@@ -248,7 +252,7 @@ constexpr size_t EPI_BYTES = 4 * 32 * 33 * 4;
 // K extent of B for the single N tile is loaded once per CTA and stays in
 // shared memory -- MCC's 147 KB filter -- so only A streams from HBM.
 template <int BN, int STAGES, bool B_MN, bool RB>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(64 + 32 * epi_warps(RB, BN), 1)
     tc_gemm_pers(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, TcArgs g) {
   constexpr uint32_t A_BYTES = BM * BKE * 4;
   constexpr uint32_t B_BYTES = BN * BKE * 4;
@@ -286,7 +290,7 @@ __global__ void __launch_bounds__(192, 1)
     tc::mbar_init(bfull, 1);
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
-      tc::mbar_init(&tempty[a], 4);  // one arrival per epilogue warp
+      tc::mbar_init(&tempty[a], epi_warps(RB, BN));  // one arrival per epilogue warp
     }
     tc::fence_barrier_init();
   }
@@ -401,29 +405,41 @@ __global__ void __launch_bounds__(192, 1)
     // columns: 128 contiguous bytes whenever the tile's columns are
     // contiguous in C (MatMul, MCC, CCSD(T) with a full (e, f) block) --
     // instead of 32 scattered 16-byte pieces, one per TMEM lane / C row.
-    const int q = warp & 3;
-    float* stg = stage_base + (warp - 2) * 32 * 33;
+    constexpr int NH = epi_warps(RB, BN) / 4;  // column parts per lane quarter
+    const int q = warp & 3, half = (warp - 2) >> 2;  // lane quarter, column part
+    const int ew = warp - 2;
+    // shared (.shared window) addresses of this warp's staging square and row table
+    const uint32_t stg = tc::smem_u32(stage_base) + static_cast<uint32_t>(ew) * (32 * 33 * 4 + 32 * 8);
+    const uint32_t rtab = stg + 32 * 33 * 4;
+    constexpr int CH = (BN / 32 + NH - 1) / NH;  // 32-column chunks per column part
     uint32_t tl = 0;
     for (int x = blockIdx.x; x < ntiles; x += gridDim.x, ++tl) {
       int tm, tn;
       tile_mn(x, tm, tn);
       const uint32_t acc = tl & 1;
-      // lane r holds the C row offset of TMEM lane q*32 + r
+      // row table: C offset of TMEM lane q*32 + r (tile origin folded in)
       const int64_t rowoff = static_cast<int64_t>(g.tCm[tm]) + g.cm[q * 32 + lane] + g.tCn[tn];
+      asm volatile("st.shared.s64 [%0], %1;" ::"r"(rtab + lane * 8), "l"(rowoff) : "memory");
       tc::mbar_wait(&tfull[acc], (tl / 2) & 1);
       tc::tc_fence_after();
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int ch = 0; ch < CH; ++ch) {
+        const int c0 = (half * CH + ch) * 32;
+        if (c0 >= BN) break;
         uint32_t r[32];
         tc::tmem_ld32(tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c0), r);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = __uint_as_float(r[j]);
+        for (int j = 0; j < 32; ++j)
+          asm volatile("st.shared.b32 [%0], %1;" ::"r"(stg + (lane * 33 + j) * 4), "r"(r[j]) : "memory");
         __syncwarp();
-        const int64_t coff = g.cn[c0 + lane];
-#pragma unroll 8
+        float* cc = g.C + g.cn[c0 + lane];
+#pragma unroll
         for (int rr = 0; rr < 32; ++rr) {
-          const int64_t ro = __shfl_sync(0xffffffffu, rowoff, rr);
-          __stcs(g.C + ro + coff, stg[rr * 33 + lane]);
+          int64_t ro;
+          float v;
+          asm volatile("ld.shared.s64 %0, [%1];" : "=l"(ro) : "r"(rtab + rr * 8) : "memory");
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(stg + (rr * 33 + lane) * 4) : "memory");
+          __stcs(cc + ro, v);
         }
         __syncwarp();
       }
@@ -758,12 +774,12 @@ class TcRoutine final : public Routine {
     args_.cvec = cvec_;
     smem_ = static_cast<size_t>(stages_) * (BM + BN) * BKE * 4 + 1024 + 256;
     // persistent instance: resident B when the single N tile's K extent fits
-    auto rb_need = [&](int st) { return static_cast<size_t>(nk_) * BN * BKE * 4 + st * BM * BKE * 4 + 1024 + 256 + EPI_BYTES; };
+    auto rb_need = [&](int st) { return static_cast<size_t>(nk_) * BN * BKE * 4 + st * BM * BKE * 4 + 1024 + 256 + epi_bytes(true, BN); };
     const int rb_st = rb_need(4) <= 227 * 1024 ? 4 : 3;
     const size_t rb_bytes = rb_need(rb_st);
     rb_ = tilesN_ == 1 && !vb_.mn && (BN == 64 || BN == 128) && rb_bytes <= 227 * 1024;
     pstages_ = rb_ ? rb_st : pers_stages(BN);
-    psmem_ = rb_ ? rb_bytes : static_cast<size_t>(pstages_) * (BM + BN) * BKE * 4 + 1024 + 256 + EPI_BYTES;
+    psmem_ = rb_ ? rb_bytes : static_cast<size_t>(pstages_) * (BM + BN) * BKE * 4 + 1024 + 256 + epi_bytes(false, BN);
     pers_ = !std::getenv("MDHB_TC_NONPERSISTENT");
     return true;
   }
@@ -865,7 +881,7 @@ class TcRoutine final : public Routine {
     smem_ = static_cast<size_t>(stages_) * (BM + BN) * BKE * 4 + 1024 + 256;
     rb_ = false;
     pstages_ = pers_stages(BN);
-    psmem_ = static_cast<size_t>(pstages_) * (BM + BN) * BKE * 4 + 1024 + 256 + EPI_BYTES;
+    psmem_ = static_cast<size_t>(pstages_) * (BM + BN) * BKE * 4 + 1024 + 256 + epi_bytes(false, BN);
     pers_ = !std::getenv("MDHB_TC_NONPERSISTENT");
     return true;
   }
@@ -878,7 +894,7 @@ class TcRoutine final : public Routine {
     return n;
   }
   // ring depth of the persistent kernel (fits 227 KB with the epilogue staging)
-  static int pers_stages(int BN) { return BN >= 192 ? 4 : (BN >= 128 ? 6 : 8); }
+  static int pers_stages(int BN) { return BN >= 192 ? 4 : (BN >= 128 ? 5 : 6); }
 
   void launch(const void* const* d_in, void* const* d_out, cudaStream_t s) override {
     const void* A = d_in[va_.buf];
@@ -916,12 +932,13 @@ class TcRoutine final : public Routine {
   if (BN_ == BNV && vb_.mn == MN && rb_ == RBV && pstages_ == ST) {                                         \
     auto k = tc_gemm_pers<BNV, ST, MN, RBV>;                                                                \
     MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(psmem_))); \
-    k<<<pgrid, 192, psmem_, s>>>(ma_, mb_, a);                                                              \
+    k<<<pgrid, 64 + 32 * epi_warps(RBV, BNV), psmem_, s>>>(ma_, mb_, a);                                              \
     MDHB_CUDA(cudaGetLastError());                                                                          \
     return;                                                                                                 \
   }
+      if (psmem_ > 227 * 1024) fail("Unsupported", "tensor-core instance exceeds 227 KB of shared memory");
       MDHB_TCP(256, 4, false, false) MDHB_TCP(256, 4, true, false) MDHB_TCP(192, 4, false, false)
-      MDHB_TCP(128, 6, false, false) MDHB_TCP(128, 6, true, false) MDHB_TCP(64, 8, false, false)
+      MDHB_TCP(128, 5, false, false) MDHB_TCP(128, 5, true, false) MDHB_TCP(64, 6, false, false)
       MDHB_TCP(64, 4, false, true) MDHB_TCP(64, 3, false, true) MDHB_TCP(128, 4, false, true)
       MDHB_TCP(128, 3, false, true)
 #undef MDHB_TCP
