@@ -141,11 +141,23 @@ def make_plan(name, device, world=1, rank=0):
 
 
 def roofline_of(desc, kernel_s, pk, clock_mhz, traffic):
+    """Roofline of the dominant kernel: achieved vs the peak of the resource
+    that binds it.  For contractions both the compute time (FFMA or tensor
+    peak) and the HBM time of the algorithmic bytes are computed and the
+    larger one names the bound (CCSD(T) on the tensor cores is bound by its
+    764 MB output write, not by its 27.5 GFLOP)."""
     bound = desc["bound"]
-    if bound == "hbm":
+    hbm_s = desc["bytes"] / (pk["hbm"] * 1e9)
+
+    def hbm_line(note=None):
         ach = desc["bytes"] / kernel_s / 1e9
-        return {"bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm"], "unit": "GB/s",
-                "frac": round(ach / pk["hbm"], 4), "traffic": traffic, "peak_source": pk["source"]}
+        d = {"bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm"], "unit": "GB/s",
+             "frac": round(ach / pk["hbm"], 4), "traffic": traffic, "peak_source": pk["source"]}
+        if note:
+            d["note"] = note
+        return d
+    if bound == "hbm":
+        return hbm_line()
     if bound == "int":
         # integer issue roofline: 4 schedulers x 32 lanes per SM per clock
         pairs = desc["template"]["pairs"]
@@ -155,14 +167,19 @@ def roofline_of(desc, kernel_s, pk, clock_mhz, traffic):
         return {"bound": "int-issue", "achieved": round(ach, 2), "peak": round(peak, 2), "unit": "Tops/s",
                 "frac": round(ach / peak, 4), "traffic": traffic, "pairs_per_s": pairs / kernel_s}
     if bound == "tensor":
+        tf32 = desc["template"].get("math") == "tf32"
+        peak = pk["bf16"] / 2.0 if tf32 else pk["bf16"]
+        if hbm_s > desc["flops"] / (peak * 1e12):
+            return hbm_line(f"tensor time {desc['flops'] / peak / 1e6:.1f} us < HBM time {hbm_s * 1e6:.1f} us: memory-bound")
         tflops = desc["flops"] / kernel_s / 1e12
-        peak = pk["bf16"] / 2.0 if desc["template"].get("math") == "tf32" else pk["bf16"]
         return {"bound": "tensor", "achieved": round(tflops, 1), "peak": round(peak, 1), "unit": "TFLOP/s",
                 "frac": round(tflops / peak, 4), "traffic": traffic,
-                "peak_note": "TF32 dense = 1/2 of the measured BF16 cuBLAS peak" if desc["template"].get("math") == "tf32" else "measured BF16"}
+                "peak_note": "TF32 dense = 1/2 of the measured BF16 cuBLAS peak" if tf32 else "measured BF16"}
     # fp32 FFMA: 148 SMs x 128 lanes x 2 flop x clock
-    tflops = desc["flops"] / kernel_s / 1e12
     peak = 148 * 128 * 2 * (clock_mhz or pk["sm_max_mhz"]) * 1e6 / 1e12
+    if hbm_s > desc["flops"] / (peak * 1e12):
+        return hbm_line(f"FFMA time {desc['flops'] / peak / 1e6:.1f} us < HBM time {hbm_s * 1e6:.1f} us: memory-bound")
+    tflops = desc["flops"] / kernel_s / 1e12
     return {"bound": "fp32-ffma", "achieved": round(tflops, 2), "peak": round(peak, 2), "unit": "TFLOP/s",
             "frac": round(tflops / peak, 4), "traffic": traffic, "peak_note": "148 SM x 128 FMA x 2 x SM clock"}
 
