@@ -64,5 +64,10 @@ inline std::vector<int64_t> factor_box(const MdHom& e, const std::vector<int>& d
 std::unique_ptr<Routine> make_tc_contraction(const Problem& p, const Groups& g, const Config* cfg, Config* cfg_out,
                                              std::string* why);
 
+// Tensor-core instance for NHWC convolutions (MCC): one input patch per
+// 32-channel chunk, all R*S taps issued from it through shifted descriptors
+// (kernels/tc_conv.cu).  nullptr when the md_hom is not such a convolution.
+std::unique_ptr<Routine> make_tc_conv(const Problem& p, const Groups& g, std::string* why);
+
 }  // namespace ctr
 }  // namespace mdhb

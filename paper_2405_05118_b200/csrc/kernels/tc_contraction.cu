@@ -1000,6 +1000,13 @@ std::unique_ptr<Routine> make_tc_contraction(const Problem& p, const Groups& g, 
   // N-tile menu; among the instances that set up, prefer a direct TMA view
   // over packed operands, then the longest contiguous run of C per tile row
   // (the epilogue's store width), then the wider tile.
+  {
+    std::string w;
+    if (auto conv = make_tc_conv(p, g, &w)) {
+      if (cfg_out) *cfg_out = cfg ? *cfg : baseline_config(p.e, p.m);
+      return conv;
+    }
+  }
   std::vector<int> menu = {256, 192, 128, 64};
   if (const char* f = std::getenv("MDHB_TC_BN")) menu = {std::atoi(f)};
   std::unique_ptr<TcRoutine> best;

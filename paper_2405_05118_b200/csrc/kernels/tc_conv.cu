@@ -1,0 +1,376 @@
+// Tensor-core (tcgen05 kind::tf32) instance for the multi-channel convolution
+// md_hom over NHWC (MCC, BASELINE config 4; the reference's mcc.json with
+// NHWC/KRSC/NPQK views):
+//
+//   O[n][p][q][k] = sum_{r,s,c}  I[n][p+r][q+s][c] * F[k][r][s][c]
+//
+// The generic tensor-core contraction re-reads the input once per filter tap
+// (r,s) -- 9 TMA boxes per output tile.  Here the input patch a tile needs is
+// loaded ONCE per 32-channel chunk and all R*S taps are issued from it by
+// shifting the UMMA shared-memory descriptor:
+//
+//   * tile = 16 output rows (p) x 8 output columns (q) of one image = 128 MMA
+//     rows (M), all K output channels as N (64);  P is padded to 16 (rows past
+//     P are computed on TMA zero-fill and never stored)
+//   * patch = (16+R-1) x (8+S-1) input pixels x 32 channels, landed by one 5-D
+//     TMA box {4 c, 8+S-1 q, 16+R-1 p, 8 c-groups, 1 n} without swizzle, i.e.
+//     [c-group][p'][q'][4 c]: every 16-byte core-matrix row is one pixel's 4
+//     channels, 8 consecutive q' are 128 contiguous bytes
+//   * tap (r,s), k-step j: A descriptor start = patch + 2j*plane + (r*Wq+s)*16,
+//     M-direction core stride 16*Wq bytes (next p), K-direction core stride
+//     plane bytes (next 4 channels) -- the K-major no-swizzle canonical layout
+//   * the filter (K x R*S*C, K-major) stays resident in shared memory, 128B
+//     swizzled, loaded once per CTA
+//
+// Warp roles as tc_gemm_pers: warp 0 TMA, warp 1 TMEM + MMA issue (one
+// thread), warps 2-5 drain the double-buffered TMEM accumulator through a
+// 32x32 smem transpose into coalesced 256-byte C rows.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <mutex>
+#include <sstream>
+
+#include "contraction_common.hpp"
+#include "tc_gemm.cuh"
+
+namespace mdhb {
+namespace ctr {
+namespace {
+
+constexpr int CV_BM = 128, CV_TP = 16, CV_TQ = 8, CV_BKE = 32;
+
+struct ConvArgs {
+  float* O;
+  int N, P, Q, K;          // output extents (K = output channels = BN)
+  int R, S, C;             // taps and input channels
+  int HP, WQ;              // patch extents (CV_TP + R - 1, CV_TQ + S - 1)
+  int pblocks, qblocks;    // tiles per image
+  int64_t on, op, oq;      // output strides (elements)
+  uint32_t plane;          // bytes of one 4-channel plane of the patch (HP * WQ * 16)
+  uint32_t lbo, sbo;       // descriptor core-matrix strides (K direction, M direction)
+};
+
+__device__ __forceinline__ uint64_t nosw_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return tc::umma_desc(saddr, lbo, sbo, 0);
+}
+
+template <int BN>
+__global__ void __launch_bounds__(192, 1)
+    tc_conv_tf32(const __grid_constant__ CUtensorMap tma_i, const __grid_constant__ CUtensorMap tma_f, ConvArgs g) {
+  constexpr int PSTAGES = 2;
+  constexpr uint32_t B_BYTES = BN * CV_BKE * 4;      // one 32-channel k-tile of the filter
+  constexpr uint32_t TMEM_COLS = 2 * BN <= 128 ? 128 : 256;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int ktiles = g.R * g.S * (g.C / CV_BKE);
+  const int chunks = g.C / CV_BKE;
+  const uint32_t patch_bytes = 8 * g.plane;           // 8 planes of 4 channels = 32 channels
+  const uint32_t patch_slot = (patch_bytes + 1023) & ~1023u;
+  uint8_t* sB = smem;                                 // resident filter [ktiles][BN][32] (128B swizzle)
+  uint8_t* sP = smem + static_cast<size_t>(ktiles) * B_BYTES;  // patch ring
+  uint64_t* full = reinterpret_cast<uint64_t*>(sP + PSTAGES * patch_slot);
+  uint64_t* empty = full + PSTAGES;
+  uint64_t* bfull = empty + PSTAGES;
+  uint64_t* tfull = bfull + 1;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* stage_base = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 256);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int per_img = g.pblocks * g.qblocks;
+  const int ntiles = g.N * per_img;
+
+  if (threadIdx.x == 0) {
+    tc::tma_prefetch(&tma_i);
+    tc::tma_prefetch(&tma_f);
+    for (int s = 0; s < PSTAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(bfull, 1);
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 4);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, TMEM_COLS);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer: the filter once, then one patch per (tile, chunk)
+    tc::mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(ktiles) * B_BYTES);
+    for (int kt = 0; kt < ktiles; ++kt) {
+      int c[5] = {kt * CV_BKE, 0, 0, 0, 0};
+      tc::tma_load(sB + static_cast<size_t>(kt) * B_BYTES, &tma_f, bfull, 2, c);
+    }
+    uint32_t it = 0;
+    for (int x = blockIdx.x; x < ntiles; x += gridDim.x) {
+      const int n = x / per_img, rem = x % per_img, pb = rem / g.qblocks, qb = rem % g.qblocks;
+      for (int cc = 0; cc < chunks; ++cc, ++it) {
+        const uint32_t s = it % PSTAGES;
+        if (it >= PSTAGES) tc::mbar_wait(&empty[s], ((it / PSTAGES) - 1) & 1);
+        tc::mbar_arrive_expect_tx(&full[s], patch_bytes);
+        int c[5] = {0, qb * CV_TQ, pb * CV_TP, cc * 8, n};
+        tc::tma_load(sP + s * patch_slot, &tma_i, &full[s], 5, c);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer
+    constexpr uint32_t idesc = tc::instr_desc(2, 0, 0, CV_BM, BN);
+    tc::mbar_wait(bfull, 0);
+    uint32_t it = 0, tl = 0;
+    for (int x = blockIdx.x; x < ntiles; x += gridDim.x, ++tl) {
+      const uint32_t acc = tl & 1;
+      if (tl >= 2) tc::mbar_wait(&tempty[acc], ((tl / 2) - 1) & 1);
+      tc::tc_fence_after();
+      const uint32_t dtm = tmem + acc * BN;
+      bool first = true;
+      for (int cc = 0; cc < chunks; ++cc, ++it) {
+        const uint32_t s = it % PSTAGES;
+        tc::mbar_wait(&full[s], (it / PSTAGES) & 1);
+        tc::tc_fence_after();
+        const uint32_t sp = tc::smem_u32(sP + s * patch_slot);
+        for (int r = 0; r < g.R; ++r)
+          for (int ss = 0; ss < g.S; ++ss) {
+            const uint32_t tap = sp + static_cast<uint32_t>(r * g.WQ + ss) * 16;
+            const uint32_t sb = tc::smem_u32(sB + static_cast<size_t>((r * g.S + ss) * chunks + cc) * B_BYTES);
+#pragma unroll
+            for (int j = 0; j < CV_BKE / 8; ++j) {
+              const uint64_t da = nosw_desc(tap + 2 * j * g.plane, g.lbo, g.sbo);
+              const uint64_t db = tc::sw128_desc(sb + j * 32, 16, 1024);
+              tc::mma<true>(dtm, da, db, idesc, first ? 0u : 1u);
+              first = false;
+            }
+          }
+        tc::mma_commit(&empty[s]);
+      }
+      tc::mma_commit(&tfull[acc]);
+    }
+  } else if (warp >= 2) {
+    // ---------------- epilogue: TMEM -> 32x32 smem transpose -> C rows
+    const int q = warp & 3;
+    const uint32_t stg = tc::smem_u32(stage_base) + static_cast<uint32_t>(warp - 2) * (32 * 33 * 4 + 32 * 8);
+    const uint32_t rtab = stg + 32 * 33 * 4;
+    uint32_t tl = 0;
+    for (int x = blockIdx.x; x < ntiles; x += gridDim.x, ++tl) {
+      const int n = x / per_img, rem = x % per_img, pb = rem / g.qblocks, qb = rem % g.qblocks;
+      const uint32_t acc = tl & 1;
+      // TMEM lane m = pp * 8 + qq  ->  output pixel (n, pb*16 + pp, qb*8 + qq); -1 = padding row
+      const int m = q * 32 + lane, p = pb * CV_TP + m / CV_TQ, qq = qb * CV_TQ + m % CV_TQ;
+      const int64_t rowoff = p < g.P ? n * g.on + p * g.op + qq * g.oq : -1;
+      asm volatile("st.shared.s64 [%0], %1;" ::"r"(rtab + lane * 8), "l"(rowoff) : "memory");
+      tc::mbar_wait(&tfull[acc], (tl / 2) & 1);
+      tc::tc_fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t rv[32];
+        tc::tmem_ld32(tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c0), rv);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          asm volatile("st.shared.b32 [%0], %1;" ::"r"(stg + (lane * 33 + j) * 4), "r"(rv[j]) : "memory");
+        __syncwarp();
+        float* cc = g.O + c0 + lane;
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) {
+          int64_t ro;
+          float v;
+          asm volatile("ld.shared.s64 %0, [%1];" : "=l"(ro) : "r"(rtab + rr * 8) : "memory");
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(stg + (rr * 33 + lane) * 4) : "memory");
+          if (ro >= 0) __stcs(cc + ro, v);
+        }
+        __syncwarp();
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, TMEM_COLS);
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn conv_encoder() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  if (!fn) fail("CudaError", "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// single-dim affine index function: coefficient 1 on `d` only, no offset
+bool is_dim(const Affine& f, int d) {
+  if (f.c0 != 0) return false;
+  for (size_t x = 0; x < f.coeff.size(); ++x)
+    if (f.coeff[x] != (static_cast<int>(x) == d ? 1 : 0)) return false;
+  return true;
+}
+// two-dim sum i_a + i_b
+bool is_sum(const Affine& f, int a, int b) {
+  if (f.c0 != 0) return false;
+  for (size_t x = 0; x < f.coeff.size(); ++x)
+    if (f.coeff[x] != ((static_cast<int>(x) == a || static_cast<int>(x) == b) ? 1 : 0)) return false;
+  return true;
+}
+int only_dim(const Affine& f) {
+  int d = -1;
+  for (size_t x = 0; x < f.coeff.size(); ++x)
+    if (f.coeff[x] != 0) {
+      if (d >= 0 || f.coeff[x] != 1) return -1;
+      d = static_cast<int>(x);
+    }
+  return f.c0 == 0 ? d : -1;
+}
+
+class ConvRoutine final : public Routine {
+ public:
+  ConvRoutine(const Problem& p, int ib, int fb) : p_(p), ib_(ib), fb_(fb) {}
+  const char* family() const override { return "contraction"; }
+  const char* bound() const override { return "tensor"; }
+  int launches() const override { return 1; }
+  double flops() const override {
+    return 2.0 * a_.N * a_.P * a_.Q * static_cast<double>(a_.K) * a_.R * a_.S * a_.C;
+  }
+  double bytes() const override { return static_cast<double>(p_.in_bytes + p_.out_bytes); }
+  std::string describe() const override {
+    std::ostringstream os;
+    os << "{\"kernel\": \"tc_conv_tf32<" << a_.K << ">\", \"math\": \"tf32\", \"M\": "
+       << static_cast<int64_t>(a_.N) * a_.P * a_.Q << ", \"N\": " << a_.K << ", \"K\": " << a_.R * a_.S * a_.C
+       << ", \"tile\": \"16 p x 8 q x " << a_.K << " k\", \"patch\": [" << a_.HP << ", " << a_.WQ << ", 32]"
+       << ", \"taps_per_patch\": " << a_.R * a_.S << ", \"tiles\": " << static_cast<int64_t>(a_.N) * a_.pblocks * a_.qblocks
+       << ", \"umma\": \"tcgen05.mma.cta_group::1.kind::tf32 M128xN" << a_.K
+       << "xK8, A no-swizzle shifted descriptors, B resident 128B-swizzled\", \"smem\": " << smem_ << "}";
+    return os.str();
+  }
+
+  bool setup(std::string* why) {
+    const MdHom& e = p_.e;
+    const Buf& I = e.in[static_cast<size_t>(ib_)];
+    const Buf& F = e.in[static_cast<size_t>(fb_)];
+    const Buf& O = e.out[0];
+    // dims: n p q k (cc), r s c (pw), read off the views
+    const int dn = only_dim(O.acc[0].idx[0]), dp = only_dim(O.acc[0].idx[1]), dq = only_dim(O.acc[0].idx[2]),
+              dk = only_dim(O.acc[0].idx[3]);
+    const int dr = only_dim(F.acc[0].idx[1]), ds = only_dim(F.acc[0].idx[2]), dc = only_dim(F.acc[0].idx[3]);
+    if (dn < 0 || dp < 0 || dq < 0 || dk < 0 || dr < 0 || ds < 0 || dc < 0) return *why = "not an NHWC convolution", false;
+    if (!is_dim(F.acc[0].idx[0], dk) || !is_dim(I.acc[0].idx[0], dn) || !is_sum(I.acc[0].idx[1], dp, dr) ||
+        !is_sum(I.acc[0].idx[2], dq, ds) || !is_dim(I.acc[0].idx[3], dc))
+      return *why = "not an NHWC convolution", false;
+    auto sz = [&](int d) { return static_cast<int>(e.sizes[static_cast<size_t>(d)]); };
+    a_.N = sz(dn), a_.P = sz(dp), a_.Q = sz(dq), a_.K = sz(dk), a_.R = sz(dr), a_.S = sz(ds), a_.C = sz(dc);
+    const auto& ie = p_.in_ext[static_cast<size_t>(ib_)];  // [N][H][W][C]
+    const auto& oe = p_.out_ext[0];                      // [N][P][Q][K]
+    if (a_.K != 64) return *why = "conv instance: 64 output channels", false;
+    if (a_.C % CV_BKE || a_.Q % CV_TQ) return *why = "conv instance: C % 32, Q % 8", false;
+    if (ie[3] != a_.C) return *why = "conv instance: input channel extent", false;
+    a_.HP = CV_TP + a_.R - 1;
+    a_.WQ = CV_TQ + a_.S - 1;
+    a_.pblocks = (a_.P + CV_TP - 1) / CV_TP;
+    a_.qblocks = a_.Q / CV_TQ;
+    a_.on = oe[1] * oe[2] * oe[3];
+    a_.op = oe[2] * oe[3];
+    a_.oq = oe[3];
+    a_.plane = static_cast<uint32_t>(a_.HP * a_.WQ * 16);
+    const char* swap = std::getenv("MDHB_CONV_SWAP_LBO");
+    a_.lbo = swap ? static_cast<uint32_t>(16 * a_.WQ) : a_.plane;
+    a_.sbo = swap ? a_.plane : static_cast<uint32_t>(16 * a_.WQ);
+    const int ktiles = a_.R * a_.S * (a_.C / CV_BKE);
+    const size_t patch_slot = (8 * static_cast<size_t>(a_.plane) + 1023) / 1024 * 1024;
+    smem_ = static_cast<size_t>(ktiles) * a_.K * CV_BKE * 4 + 2 * patch_slot + 256 + 4 * (32 * 33 * 4 + 32 * 8) + 1024;
+    if (smem_ > 227 * 1024) return *why = "conv instance: filter + patches exceed shared memory", false;
+    if (a_.plane / 16 >= (1u << 14)) return *why = "conv instance: patch plane too large for a descriptor", false;
+    // input and filter extents for the tensor maps
+    H_ = ie[1];
+    W_ = ie[2];
+    FK_ = static_cast<int64_t>(a_.R) * a_.S * a_.C;
+    if (p_.in_ext[static_cast<size_t>(fb_)][1] != a_.R || p_.in_ext[static_cast<size_t>(fb_)][2] != a_.S ||
+        p_.in_ext[static_cast<size_t>(fb_)][3] != a_.C)
+      return *why = "conv instance: filter extents", false;
+    return true;
+  }
+
+  void launch(const void* const* d_in, void* const* d_out, cudaStream_t s) override {
+    const void* I = d_in[ib_];
+    const void* F = d_in[fb_];
+    if (I != last_i_) {
+      // 5-D view of I: {4 c, W, H, C/4 c-groups, N}; the c-group stride (16 B)
+      // is smaller than the pixel stride -- TMA strides need not be ordered
+      cuuint64_t dims[5] = {4, static_cast<cuuint64_t>(W_), static_cast<cuuint64_t>(H_),
+                            static_cast<cuuint64_t>(a_.C / 4), static_cast<cuuint64_t>(a_.N)};
+      cuuint64_t strides[4] = {static_cast<cuuint64_t>(a_.C) * 4, static_cast<cuuint64_t>(W_ * a_.C) * 4, 16,
+                               static_cast<cuuint64_t>(H_ * W_ * a_.C) * 4};
+      cuuint32_t box[5] = {4, static_cast<cuuint32_t>(a_.WQ), static_cast<cuuint32_t>(a_.HP), 8, 1};
+      cuuint32_t es[5] = {1, 1, 1, 1, 1};
+      CUresult r = conv_encoder()(&mi_, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<void*>(I), dims, strides, box, es,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) fail("CudaError", "cuTensorMapEncodeTiled (conv input) failed (" + std::to_string(static_cast<int>(r)) + ")");
+      last_i_ = I;
+    }
+    if (F != last_f_) {
+      cuuint64_t dims[2] = {static_cast<cuuint64_t>(FK_), static_cast<cuuint64_t>(a_.K)};
+      cuuint64_t strides[1] = {static_cast<cuuint64_t>(FK_) * 4};
+      cuuint32_t box[2] = {CV_BKE, static_cast<cuuint32_t>(a_.K)};
+      cuuint32_t es[2] = {1, 1};
+      CUresult r = conv_encoder()(&mf_, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(F), dims, strides, box, es,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) fail("CudaError", "cuTensorMapEncodeTiled (conv filter) failed (" + std::to_string(static_cast<int>(r)) + ")");
+      last_f_ = F;
+    }
+    ConvArgs a = a_;
+    a.O = static_cast<float*>(d_out[0]);
+    const int sms = sm_count(p_.opt.device);
+    const int64_t tiles = static_cast<int64_t>(a_.N) * a_.pblocks * a_.qblocks;
+    auto k = tc_conv_tf32<64>;
+    MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_)));
+    k<<<static_cast<unsigned>(std::min<int64_t>(sms, tiles)), 192, smem_, s>>>(mi_, mf_, a);
+    MDHB_CUDA(cudaGetLastError());
+  }
+
+ private:
+  const Problem& p_;
+  int ib_, fb_;
+  ConvArgs a_{};
+  int64_t H_ = 0, W_ = 0, FK_ = 0;
+  size_t smem_ = 0;
+  CUtensorMap mi_{}, mf_{};
+  const void* last_i_ = nullptr;
+  const void* last_f_ = nullptr;
+};
+
+}  // namespace
+
+std::unique_ptr<Routine> make_tc_conv(const Problem& p, const Groups& g, std::string* why) {
+  if (std::getenv("MDHB_TC_NO_CONV")) return nullptr;
+  const MdHom& e = p.e;
+  if (e.D() != 7 || e.in.size() != 2 || e.out.size() != 1) return nullptr;
+  // the input is the operand with a 2-dim index function; the filter the other
+  for (int ib : {g.a_buf, g.b_buf}) {
+    const int fb = ib == g.a_buf ? g.b_buf : g.a_buf;
+    if (e.in[static_cast<size_t>(ib)].rank != 4 || e.in[static_cast<size_t>(fb)].rank != 4 || e.out[0].rank != 4) continue;
+    auto r = std::make_unique<ConvRoutine>(p, ib, fb);
+    std::string w;
+    if (r->setup(&w)) return r;
+    *why = w;
+  }
+  return nullptr;
+}
+
+}  // namespace ctr
+}  // namespace mdhb

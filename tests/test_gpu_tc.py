@@ -15,8 +15,10 @@ CASES = [
     ("matmul_fp32", [128, 256, 64], "tc_gemm_tf32<256"),
     ("matmul_fp32", [256, 512, 96], "tc_gemm_tf32<256"),
     ("matmul_fp32", [128, 128, 32], "tc_gemm_tf32<128"),
-    ("mcc_nhwc", [2, 8, 8, 64, 3, 3, 64], "tc_gemm_tf32<64"),
-    ("mcc_nhwc", [4, 16, 8, 64, 3, 3, 32], "tc_gemm_tf32<64"),
+    ("mcc_nhwc", [2, 8, 8, 64, 3, 3, 64], "tc_conv_tf32<64"),      # P padded 8 -> 16
+    ("mcc_nhwc", [4, 16, 8, 64, 3, 3, 32], "tc_conv_tf32<64"),
+    ("mcc_nhwc", [3, 20, 16, 64, 3, 3, 64], "tc_conv_tf32<64"),     # 2 p-blocks, ragged
+    ("mcc_nhwc", [2, 16, 16, 64, 1, 1, 32], "tc_conv_tf32<64"),     # 1x1 taps
     # packed K-major operands (views no TMA box describes; K padded to 32)
     ("ccsdt_abcdef_gdab_efgc", [4, 4, 8, 8, 8, 4, 72], "tc_gemm_tf32<256"),
     ("ccsdt_abcdef_gdab_efgc", [8, 4, 4, 4, 8, 4, 40], "tc_gemm_tf32<128"),
@@ -37,6 +39,7 @@ def test_tf32_exact_mode_bit_identical(name, sizes, kernel):
     d = plan.describe()
     kern = d["template"]["kernel"]
     assert d["family"] == "contraction" and (kern.startswith(kernel) or kern.startswith(kernel.replace("tc_gemm_tf32", "tc_gemm_pers"))), d
+    assert d["family"] == "contraction" and d["template"].get("math") == "tf32", d
     ins = exact_inputs(comp, 4)
     (got,) = run_device(plan, ins)
     ((want, dfd),) = mo.execute(comp, ins)
@@ -82,7 +85,7 @@ def test_tf32_mcc_full_image_exact():
     j = spec("mcc_nhwc")
     comp = mo.Computation.from_json(j)
     plan = plan_tf32(j)
-    assert "tc_gemm" in plan.describe()["template"]["kernel"]
+    assert "tc_conv" in plan.describe()["template"]["kernel"]
     ins = exact_inputs(comp, 3)
     d_in = plan.empty(0)
     for t, x in zip(d_in, ins):
@@ -92,6 +95,23 @@ def test_tf32_mcc_full_image_exact():
     torch.cuda.synchronize()
     ((part, dfd),), sh = mo.execute_box(comp, ins, {0: (255, 256)})
     assert np.array_equal(out[255:256].cpu().numpy().astype(np.float64), part)
+
+
+@pytest.mark.gpu
+def test_tf32_conv_matches_generic_tc_instance(monkeypatch):
+    """The shifted-descriptor conv instance and the generic TMA-box instance
+    (one box per tap) give the same bits on exact inputs."""
+    j = spec("mcc_nhwc", [2, 16, 16, 64, 3, 3, 64])
+    comp = mo.Computation.from_json(j)
+    ins = exact_inputs(comp, 11)
+    p1 = plan_tf32(j)
+    assert p1.describe()["template"]["kernel"].startswith("tc_conv"), p1.describe()
+    (a,) = run_device(p1, ins)
+    monkeypatch.setenv("MDHB_TC_NO_CONV", "1")
+    p2 = plan_tf32(j)
+    assert p2.describe()["template"]["kernel"].startswith("tc_gemm"), p2.describe()
+    (b,) = run_device(p2, ins)
+    assert np.array_equal(a, b)
 
 
 @pytest.mark.gpu
