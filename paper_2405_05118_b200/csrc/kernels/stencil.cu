@@ -170,7 +170,13 @@ __global__ void __launch_bounds__(NTHREADS, 3) star7_kernel(StencilArgs a) {
 // offset is not 16-byte aligned are copied from the aligned address below
 // them; the per-row float shift (0 or 2 for the BASELINE extents) is
 // re-applied when the row is read from shared memory.
-constexpr int NSLOT = 6;                 // ring slots
+#ifndef MDHB_STENCIL_NSLOT
+#define MDHB_STENCIL_NSLOT 6
+#endif
+#ifndef MDHB_STENCIL_WS_MINB
+#define MDHB_STENCIL_WS_MINB 3
+#endif
+constexpr int NSLOT = MDHB_STENCIL_NSLOT;  // ring slots
 constexpr int PD = NSLOT - 1;            // planes in flight ahead of compute
 constexpr int BPITCH = TK + 12;          // floats per smem row: 128 + halo 2 + shift <= 3, 16B rounded
 
@@ -341,7 +347,7 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
   }
 }
 
-__global__ void __launch_bounds__(WS_THREADS, 3) star7_ws(StencilArgs a) {
+__global__ void __launch_bounds__(WS_THREADS, MDHB_STENCIL_WS_MINB) star7_ws(StencilArgs a) {
   constexpr int TJ = 16, ROWS = TJ + 2;
   extern __shared__ __align__(128) float sring[];  // [NSLOT][ROWS][BPITCH]
   __shared__ __align__(8) uint64_t full[NSLOT], empty[NSLOT];
@@ -464,6 +470,157 @@ __global__ void __launch_bounds__(WS_THREADS, 3) star7_ws(StencilArgs a) {
   if (t < iend) step(t, R1, R2, R0), ++t;
 }
 
+
+// ---------------------------------------------------------------------------
+// v3b (lean registers): star7_ws with only the 4 centre columns of each
+// plane's two rows kept in registers across steps; the centre plane's k-1 /
+// k+4 halo values are re-read from shared memory in the step that uses them
+// (the plane is still resident until that step releases it).  24 instead of
+// 36 carried floats -> <= 56 registers -> 4 CTAs per SM, i.e. one more
+// producer warp and ring per SM keeping HBM reads in flight.
+struct Rows4 {
+  float r[2][4];
+};
+__device__ __forceinline__ void ld4c(const float* row, int sh, float (&x)[4]) {
+  // columns 1..4 of the 6-wide window at `row` (sh even: float2-aligned at row)
+  if ((sh & 1) == 0) {
+    float2 u = *reinterpret_cast<const float2*>(row), v = *reinterpret_cast<const float2*>(row + 2),
+           w = *reinterpret_cast<const float2*>(row + 4);
+    x[0] = u.y; x[1] = v.x; x[2] = v.y; x[3] = w.x;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) x[q] = row[q + 1];
+  }
+}
+
+template <int NS, int MINB>
+__global__ void __launch_bounds__(WS_THREADS, MINB) star7_lean(StencilArgs a) {
+  constexpr int TJ = 16, ROWS = TJ + 2;
+  extern __shared__ __align__(128) float sring[];  // [NS][ROWS][BPITCH]
+  __shared__ __align__(8) uint64_t full[NS], empty[NS];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * TK;
+  const int64_t j0 = static_cast<int64_t>(blockIdx.y) * TJ;
+  const int64_t i0 = static_cast<int64_t>(blockIdx.z) * a.ti;
+  const int iend = static_cast<int>(a.n0 - i0 < a.ti ? a.n0 - i0 : a.ti);
+  const int nplanes = iend + 2;
+  const uint32_t pstride = static_cast<uint32_t>(a.e1 * a.e2);
+  const uint32_t base0 = static_cast<uint32_t>((i0 * a.e1 + j0) * a.e2 + k0);
+  const uint32_t rstride = static_cast<uint32_t>(a.e2);
+
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_u32(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(s_u32(&empty[s])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 8) {
+    const float* vbase = a.v + ((i0 * a.e1 + j0) * a.e2 + k0);
+    for (int p = 0; p < nplanes; ++p) {
+      const int s = p % NS;
+      if (p >= NS) mbar_wait_parity(&empty[s], static_cast<uint32_t>((p / NS - 1) & 1));
+      uint32_t bytes = 0, sh = 0;
+      if (lane < ROWS) {
+        sh = (base0 + static_cast<uint32_t>(p) * pstride + static_cast<uint32_t>(lane) * rstride) & 3u;
+        bytes = (sh * 4 + (TK + 2) * 4 + 15) & ~15u;
+      }
+      uint32_t total = bytes;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(&full[s])), "r"(total) : "memory");
+      __syncwarp();
+      if (lane < ROWS && i0 + p < a.e0) {
+        const float* src = vbase + static_cast<int64_t>(p) * (a.e1 * a.e2) + static_cast<int64_t>(lane) * a.e2 - sh;
+        float* dst = sring + (static_cast<size_t>(s) * ROWS + lane) * BPITCH;
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(s_u32(dst)), "l"(src), "r"(bytes), "r"(s_u32(&full[s])) : "memory");
+      }
+    }
+    return;
+  }
+
+  const int kl = lane * 4, jl = warp * 2;
+  auto rowptr = [&](int p, int r, int& sh) {
+    sh = static_cast<int>((base0 + static_cast<uint32_t>(p) * pstride + static_cast<uint32_t>(r) * rstride) & 3u);
+    return sring + (static_cast<size_t>(p % NS) * ROWS + r) * BPITCH + sh + kl;
+  };
+  auto load_centre = [&](int p, Rows4& R) {
+    int sh;
+    const float* q0 = rowptr(p, jl + 1, sh);
+    ld4c(q0, sh, R.r[0]);
+    const float* q1 = rowptr(p, jl + 2, sh);
+    ld4c(q1, sh, R.r[1]);
+  };
+  auto release = [&](int p) {
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(&empty[p % NS])) : "memory");
+  };
+  float* wout = a.w + (i0 * a.n1 + j0 + jl) * a.n2 + k0 + kl;
+  const int64_t wplane = a.n1 * a.n2;
+  const bool kin = k0 + kl + 4 <= a.n2;
+
+  auto step = [&](int t, const Rows4& P, const Rows4& C, Rows4& N) {
+    mbar_wait_parity(&full[(t + 2) % NS], static_cast<uint32_t>(((t + 2) / NS) & 1));
+    load_centre(t + 2, N);
+    float jm[4], jp[4], hl[2], hr[2];
+    int sh;
+    ld4c(rowptr(t + 1, jl, sh), sh, jm);
+    ld4c(rowptr(t + 1, jl + 3, sh), sh, jp);
+    {
+      const float* c0 = rowptr(t + 1, jl + 1, sh);
+      hl[0] = c0[0];
+      hr[0] = c0[5];
+      const float* c1 = rowptr(t + 1, jl + 2, sh);
+      hl[1] = c1[0];
+      hr[1] = c1[5];
+    }
+    release(t + 1);
+#pragma unroll
+    for (int jj = 0; jj < 2; ++jj) {
+      const float* up = jj == 0 ? jm : C.r[0];
+      const float* dn = jj == 1 ? jp : C.r[1];
+      float o[4];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const float km = kk == 0 ? hl[jj] : C.r[jj][kk - 1];
+        const float kp = kk == 3 ? hr[jj] : C.r[jj][kk + 1];
+        float acc = a.wc * C.r[jj][kk];
+        acc = fmaf(a.wim, P.r[jj][kk], acc);
+        acc = fmaf(a.wip, N.r[jj][kk], acc);
+        acc = fmaf(a.wjm, up[kk], acc);
+        acc = fmaf(a.wjp, dn[kk], acc);
+        acc = fmaf(a.wkm, km, acc);
+        acc = fmaf(a.wkp, kp, acc);
+        o[kk] = acc;
+      }
+      const int64_t j = j0 + jl + jj;
+      if (j < a.n1 && kin) {
+        __stcs(reinterpret_cast<float4*>(wout + t * wplane + jj * a.n2), make_float4(o[0], o[1], o[2], o[3]));
+      } else if (j < a.n1) {
+        for (int kk = 0; kk < 4 && k0 + kl + kk < a.n2; ++kk) wout[t * wplane + jj * a.n2 + kk] = o[kk];
+      }
+    }
+  };
+
+  Rows4 R0, R1, R2;
+  mbar_wait_parity(&full[0], 0);
+  mbar_wait_parity(&full[1], 0);
+  load_centre(0, R0);
+  load_centre(1, R1);
+  release(0);
+  int t = 0;
+  for (; t + 3 <= iend; t += 3) {
+    step(t, R0, R1, R2);
+    step(t + 1, R1, R2, R0);
+    step(t + 2, R2, R0, R1);
+  }
+  if (t < iend) step(t, R0, R1, R2), ++t;
+  if (t < iend) step(t, R1, R2, R0), ++t;
+}
 
 // ---------------------------------------------------------------------------
 // v4 (default): persistent + warp-specialised.  The (tile, i-plane) step
@@ -665,12 +822,18 @@ class StencilRoutine final : public Routine {
  public:
   StencilRoutine(const Problem& p, StencilArgs a, int tj, bool bulk)
       : p_(p), a_(a), tj_(tj), bulk_(bulk), ws_(bulk && !std::getenv("MDHB_STENCIL_V2")),
-        pers_(ws_ && std::getenv("MDHB_STENCIL_PERS") != nullptr) {}
+        pers_(ws_ && std::getenv("MDHB_STENCIL_PERS") != nullptr) {
+    if (!ws_ || pers_) lean_ = 0;
+  }
   const char* family() const override { return "stencil"; }
   std::string describe() const override {
     std::ostringstream os;
- os << "{\"kernel\": \"" << (pers_ ? "star7_pers<" : ws_ ? "star7_ws<" : bulk_ ? "star7_bulk<" : "star7_kernel<") << tj_ << ">\", \"TK\": " << TK << ", \"TJ\": " << tj_ << ", \"TI\": " << a_.ti
-       << ", \"threads\": " << (ws_ ? WS_THREADS : NTHREADS) << ", \"smem_ring_slots\": " << (bulk_ ? NSLOT : 4) << ", \"grid\": [" << grid().x << ", " << grid().y
+    const std::string kname = lean_ ? "star7_lean<" + std::to_string(lean_ / 10) + "," + std::to_string(lean_ % 10) + ">"
+                                    : std::string(pers_ ? "star7_pers<" : ws_ ? "star7_ws<" : bulk_ ? "star7_bulk<" : "star7_kernel<") +
+                                          std::to_string(tj_) + ">";
+    os << "{\"kernel\": \"" << kname << "\", \"TK\": " << TK << ", \"TJ\": " << tj_ << ", \"TI\": " << a_.ti
+       << ", \"threads\": " << (ws_ ? WS_THREADS : NTHREADS) << ", \"smem_ring_slots\": " << (lean_ ? lean_ / 10 : bulk_ ? NSLOT : 4)
+       << ", \"ctas_per_sm\": " << (lean_ ? lean_ % 10 : 3) << ", \"grid\": [" << grid().x << ", " << grid().y
        << ", " << grid().z << "]}";
     return os.str();
   }
@@ -762,6 +925,16 @@ class StencilRoutine final : public Routine {
       const int64_t items = tiles * ((a.n0 + a.ti - 1) / a.ti);
       const int grid_p = static_cast<int>(std::min<int64_t>(ctas_, mode ? items : std::max<int64_t>(1, total / 4)));
       kern<<<grid_p, WS_THREADS, smem, s>>>(a, tiles_k, total, mode);
+    } else if (lean_) {
+      void (*k)(StencilArgs) = nullptr;
+      if (lean_ == 53) k = star7_lean<5, 3>;
+      else if (lean_ == 54) k = star7_lean<5, 4>;
+      else if (lean_ == 44) k = star7_lean<4, 4>;
+      else if (lean_ == 45) k = star7_lean<4, 5>;
+      else k = star7_lean<6, 3>;
+      const size_t lsmem = static_cast<size_t>(lean_ / 10) * 18 * BPITCH * sizeof(float);
+      MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lsmem)));
+      k<<<grid(), WS_THREADS, lsmem, s>>>(a);
     } else if (ws_) {
       MDHB_CUDA(cudaFuncSetAttribute(star7_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       star7_ws<<<grid(), WS_THREADS, smem, s>>>(a);
@@ -785,6 +958,8 @@ class StencilRoutine final : public Routine {
   cudaStream_t h2d_ = nullptr, d2h_ = nullptr;
   cudaEvent_t ev_in_[18] = {}, ev_cmp_[18] = {};
   int minb_ = std::getenv("MDHB_STENCIL_MINB") ? std::atoi(std::getenv("MDHB_STENCIL_MINB")) : 2;
+  // lean-register variant (default): 5 ring slots, 4 CTAs per SM (NS*10+MINB; 0 = star7_ws)
+  int lean_ = std::getenv("MDHB_STENCIL_LEAN") ? std::atoi(std::getenv("MDHB_STENCIL_LEAN")) : 54;
 };
 
 }  // namespace

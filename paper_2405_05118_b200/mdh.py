@@ -26,7 +26,7 @@ from typing import Any, List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmdh_b200.so")
+LIB_PATH = os.environ.get("MDHB_LIB") or os.path.join(_HERE, "libmdh_b200.so")  # MDHB_LIB: variant builds (dev aid)
 
 F32, F64, I32, I64 = 0, 1, 2, 3
 MATH_FFMA, MATH_TF32, MATH_BF16 = 0, 1, 2

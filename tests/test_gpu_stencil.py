@@ -66,3 +66,20 @@ def test_jacobi3d_host_pipeline_equals_device_run(sizes):
     wh = torch.empty(w.shape, dtype=w.dtype).pin_memory()
     plan.run_host([vh.numpy()], [wh.numpy()])
     assert torch.equal(wh, w.cpu())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env", ["0", "63", "44"])
+def test_jacobi3d_variants_bit_identical(env, monkeypatch):
+    """Every stencil kernel variant (star7_ws, lean-register rings) computes
+    the same bits: same FMA order per output cell."""
+    from paper_2405_05118_b200 import mdh
+    j = spec("jacobi3d_fp32", [40, 48, 384])
+    comp = mo.Computation.from_json(j)
+    ins = uniform_inputs(comp, 5)
+    (base,) = run_device(mdh.Plan(j), ins)
+    monkeypatch.setenv("MDHB_STENCIL_LEAN", env)
+    plan = mdh.Plan(j)
+    assert plan.describe()["template"]["kernel"].startswith("star7_ws" if env == "0" else "star7_lean"), plan.describe()
+    (var,) = run_device(plan, ins)
+    assert np.array_equal(base, var)
