@@ -95,7 +95,7 @@ std::unique_ptr<mdhb::Routine> select_routine(const mdhb::Problem& prob, const m
                                               std::string* note) {
   if (prob.opt.force_generic) return mdhb::make_generic(prob, cfg, out);
   using Factory = std::unique_ptr<mdhb::Routine> (*)(const mdhb::Problem&, const mdhb::Config*, mdhb::Config*);
-  const Factory fams[] = {mdhb::make_prl, mdhb::make_stencil, mdhb::make_contraction};
+  const Factory fams[] = {mdhb::make_prl, mdhb::make_stencil, mdhb::make_contraction, mdhb::make_scan};
   for (Factory f : fams) {
     try {
       auto r = f(prob, cfg, out);

@@ -371,6 +371,12 @@ __global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g) {
     adst[i] = m * AP + (c % AKQ) * 4;
     asrc[i] = g.A + (aok[i] ? g.am[m] + kbase + (c % AKQ) * 4 : 0);
   }
+  // programmatic dependent launch: everything above touches only plan-owned
+  // tables; the operands may be produced by the previous kernel in the
+  // stream, so wait for it here (no-op without the PDL launch attribute) and
+  // let the next kernel's prologue start.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
 #pragma unroll
   for (int s = 0; s < NSTG; ++s) {
 #pragma unroll
@@ -471,10 +477,14 @@ __global__ void __launch_bounds__(256) gemv_split(GemvArgs g) {
   const int kq = g.K / 8;  // floats per warp slice
   const float4* x4 = reinterpret_cast<const float4*>(g.x + warp * kq);
   float4 av[ROWS][V], xv[V];
+  int32_t amr[ROWS];
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) amr[r] = g.am[m0 + r < g.M ? m0 + r : g.M - 1];  // plan-owned table
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // operands may come from the previous kernel (PDL)
+  asm volatile("griddepcontrol.launch_dependents;");
 #pragma unroll
   for (int r = 0; r < ROWS; ++r) {
-    const int64_t m = m0 + r < g.M ? m0 + r : g.M - 1;
-    const float4* row = reinterpret_cast<const float4*>(g.A + g.am[m] + warp * kq);
+    const float4* row = reinterpret_cast<const float4*>(g.A + amr[r] + warp * kq);
 #pragma unroll
     for (int u = 0; u < V; ++u) av[r][u] = __ldcs(row + lane + 32 * u);
   }
@@ -776,6 +786,12 @@ __global__ void __launch_bounds__(256, 2) sgemm_pipe(GemmArgs g) {
 }
 
 // ---------------------------------------------------------------- host
+// Programmatic dependent launch for the latency-bound kernels (MDHB_NO_PDL=1 off)
+bool pdl_enabled() {
+  static const bool on = std::getenv("MDHB_NO_PDL") == nullptr;
+  return on;
+}
+
 // every offset 16-byte aligned (in floats)
 bool all_mod4(const std::vector<int64_t>& v) {
   for (int64_t x : v)
@@ -1011,13 +1027,15 @@ class GemmRoutine final : public Routine {
       lc.blockDim = dim3(256);
       lc.dynamicSmemBytes = smem;
       lc.stream = s;
-      cudaLaunchAttribute at[1];
+      cudaLaunchAttribute at[2];
       at[0].id = cudaLaunchAttributeClusterDimension;
       at[0].val.clusterDim.x = 1;
       at[0].val.clusterDim.y = static_cast<unsigned>(splits_);
       at[0].val.clusterDim.z = 1;
+      at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
       lc.attrs = at;
-      lc.numAttrs = 1;
+      lc.numAttrs = 2;
       void (*kern)(SkinnyArgs) = nullptr;
 #define MDHB_SK(KS) \
   if (ks_ == KS) kern = mt == 16 ? skinny_cluster<16, KS> : skinny_cluster<32, KS>;
@@ -1044,13 +1062,17 @@ class GemmRoutine final : public Routine {
       GemvArgs a{A, B + g_.lb.c0, C, tab_[0], tab_[1], M_, static_cast<int>(K_)};
       const int V = static_cast<int>(K_ / 1024);
       if (K_ % 1024 == 0 && (V == 1 || V == 2 || V == 4 || V == 8) && !std::getenv("MDHB_GEMV_V1")) {
-        unsigned grid = static_cast<unsigned>((M_ + 1) / 2);
-        switch (V) {
-          case 1: gemv_split<1><<<grid, 256, 0, s>>>(a); break;
-          case 2: gemv_split<2><<<grid, 256, 0, s>>>(a); break;
-          case 4: gemv_split<4><<<grid, 256, 0, s>>>(a); break;
-          default: gemv_split<8><<<grid, 256, 0, s>>>(a); break;
-        }
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(static_cast<unsigned>((M_ + 1) / 2));
+        lc.blockDim = dim3(256);
+        lc.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        void (*k)(GemvArgs) = V == 1 ? gemv_split<1> : V == 2 ? gemv_split<2> : V == 4 ? gemv_split<4> : gemv_split<8>;
+        MDHB_CUDA(cudaLaunchKernelEx(&lc, k, a));
         MDHB_CUDA(cudaGetLastError());
         return;
       }
