@@ -34,8 +34,11 @@
 namespace mdhb {
 namespace {
 
-constexpr int SC_THREADS = 256, SC_ROUNDS = 4, SC_VEC = 4;
-constexpr int SC_TILE = SC_THREADS * SC_ROUNDS * SC_VEC;  // 4096 elements
+#ifndef MDHB_SCAN_ROUNDS
+#define MDHB_SCAN_ROUNDS 8
+#endif
+constexpr int SC_THREADS = 256, SC_ROUNDS = MDHB_SCAN_ROUNDS, SC_VEC = 4;
+constexpr int SC_TILE = SC_THREADS * SC_ROUNDS * SC_VEC;  // 8192 elements
 constexpr int kScanMaxD = 15;
 
 struct ScanArgs {
@@ -135,23 +138,32 @@ __device__ __forceinline__ void publish(const ScanArgs& a, int64_t slot, unsigne
   if (sizeof(T) == 4) {
     atomicExch(a.status + slot, flag | to_bits(v));
   } else {
-    atomicExch(a.values + slot, to_bits(v));
+    // separate words for the aggregate and the inclusive prefix: a reader
+    // that saw F_AGG must not pick up the later inclusive value
+    atomicExch(a.values + 2 * slot + (flag == F_INC ? 1 : 0), to_bits(v));
     __threadfence();
     atomicExch(a.status + slot, flag);
   }
 }
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long w;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+  return w;
+}
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long w;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+  return w;
+}
+// Spins until tile `slot` has published; returns its flag and value.
 template <typename T>
 __device__ __forceinline__ unsigned long long observe(const ScanArgs& a, int64_t slot, T& v) {
   unsigned long long w;
   do {
-    w = atomicAdd(a.status + slot, 0ull);
+    w = sizeof(T) == 4 ? ld_relaxed(a.status + slot) : ld_acquire(a.status + slot);
   } while ((w & F_MASK) == 0);
-  if (sizeof(T) == 4) {
-    v = from_bits<T>(w & 0xffffffffull);
-  } else {
-    __threadfence();
-    v = from_bits<T>(atomicAdd(a.values + slot, 0ull));
-  }
+  if (sizeof(T) == 4) v = from_bits<T>(w & 0xffffffffull);
+  else v = from_bits<T>(ld_relaxed(a.values + 2 * slot + ((w & F_MASK) == F_INC ? 1 : 0)));
   return w & F_MASK;
 }
 
@@ -230,27 +242,41 @@ __global__ void __launch_bounds__(SC_THREADS) scan_tiles(ScanArgs a) {
   // ---- decoupled look-back for the tile's exclusive prefix
   const int64_t slot = id;  // tile ids are line-major
   if (warp == 0) {
-    T prefix = idn;
     if (tile == 0) {
-      if (lane == 0) publish<T>(a, slot, F_INC, aggregate);
+      if (lane == 0) {
+        publish<T>(a, slot, F_INC, aggregate);
+        tile_prefix = idn;
+      }
     } else {
       if (lane == 0) publish<T>(a, slot, F_AGG, aggregate);
-      // one lane walks back (tiles are claimed in order, so predecessors
-      // always make progress); stops at the first inclusive prefix
-      if (lane == 0) {
-        int64_t p = slot - 1;
-        for (;;) {
-          T pv;
-          const unsigned long long f = observe<T>(a, p, pv);
-          prefix = op_apply<T, OP>(pv, prefix);
-          if (f == F_INC) break;
-          --p;
+      // warp-parallel look-back: lane l observes tile p - l; the window is
+      // folded up to (and including) the newest inclusive prefix in it, else
+      // entirely, and the walk moves 32 tiles further back.  The first tile
+      // of the line is always inclusive, so the walk never leaves the line.
+      const int64_t first = slot - tile;
+      T prefix = idn;
+      for (int64_t p = slot - 1;; p -= 32) {
+        const int64_t q = p - lane;
+        T v = idn;
+        unsigned long long f = F_INC;
+        if (q >= first) f = observe<T>(a, q, v);
+        const unsigned inc = __ballot_sync(0xffffffffu, f == F_INC);
+        const int stop = inc ? __ffs(inc) - 1 : 31;  // lanes 0..stop contribute
+        if (lane > stop) v = idn;
+        // fold the window, older tiles (higher lanes) on the left
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const T y = __shfl_down_sync(0xffffffffu, v, o);
+          if (lane + o < 32) v = op_apply<T, OP>(y, v);
         }
+        prefix = op_apply<T, OP>(__shfl_sync(0xffffffffu, v, 0), prefix);
+        if (inc) break;
+      }
+      if (lane == 0) {
         publish<T>(a, slot, F_INC, op_apply<T, OP>(prefix, aggregate));
         tile_prefix = prefix;
       }
     }
-    if (tile == 0 && lane == 0) tile_prefix = idn;
   }
   __syncthreads();
   const T tp = tile_prefix;
@@ -371,7 +397,7 @@ class ScanRoutine final : public Routine {
       vec = vec && (a_.in0 * esz) % 16 == 0 && (a_.out0 * esz) % 16 == 0;
       a_.vec = vec ? 1 : 0;
       const int64_t nt = a_.lines * a_.tiles_per_line;
-      status_bytes_ = static_cast<size_t>(nt) * 8 * (esz == 8 ? 2 : 1) + 256;
+      status_bytes_ = static_cast<size_t>(nt) * 8 * (esz == 8 ? 3 : 1) + 256;
       MDHB_CUDA(cudaSetDevice(p_.opt.device));
       MDHB_CUDA(cudaMalloc(&scratch_, status_bytes_));
       a_.counter = static_cast<unsigned int*>(scratch_);

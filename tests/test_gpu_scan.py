@@ -25,7 +25,7 @@ def _check_exact(j, kernel, seed=3, **kw):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("sizes,kernel", [([16], "scan_lines"), ([5000], "scan_lines"), ([100000], "scan_tiles"),
+@pytest.mark.parametrize("sizes,kernel", [([16], "scan_lines"), ([3000], "scan_lines"), ([5000], "scan_tiles"), ([100000], "scan_tiles"),
                                           ([4096 * 7 + 3], "scan_tiles")])
 def test_scan_1d_exact(sizes, kernel):
     _check_exact(bundled("scan", sizes), kernel)
