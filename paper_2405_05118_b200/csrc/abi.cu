@@ -104,9 +104,16 @@ std::unique_ptr<mdhb::Routine> select_routine(const mdhb::Problem& prob, const m
       if (e.code != "Unsupported") throw;
       // A configuration outside the specialised template's instantiation
       // space still executes -- on the generic device kernel.
-      *note = std::string("specialised template declined: ") + e.what() + "; generic kernel used";
+      *note = std::string("specialised template declined: ") + e.what() + "; emitted kernel used";
       break;
     }
+  }
+  // catch-all: the md_hom compiled to its own kernel (NVRTC), else the
+  // device bytecode VM (prefix dims, or NVRTC unavailable / failing)
+  try {
+    if (auto r = mdhb::make_emitted(prob, cfg, out)) return r;
+  } catch (const mdhb::Error& e) {
+    *note += std::string(note->empty() ? "" : "; ") + "emitted kernel unavailable (" + e.what() + "); device VM used";
   }
   return mdhb::make_generic(prob, cfg, out);
 }

@@ -77,6 +77,7 @@ std::unique_ptr<Routine> make_stencil(const Problem& p, const Config* cfg, Confi
 std::unique_ptr<Routine> make_contraction(const Problem& p, const Config* cfg, Config* cfg_out);
 std::unique_ptr<Routine> make_generic(const Problem& p, const Config* cfg, Config* cfg_out);
 std::unique_ptr<Routine> make_scan(const Problem& p, const Config* cfg, Config* cfg_out);
+std::unique_ptr<Routine> make_emitted(const Problem& p, const Config* cfg, Config* cfg_out);
 
 // The candidate configurations a family can instantiate for this problem
 // (the tuner's search space), canonical Table-1 form.

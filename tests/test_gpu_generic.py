@@ -80,3 +80,74 @@ def test_run_host_end_to_end():
     text, comp, ins, want = load("matvec")
     got = mdh.execute(text, ins)
     assert np.array_equal(got[0].astype(np.float64)[want[0][1]], want[0][0][want[0][1]])
+
+
+PREFIX_FREE = [n for n in REFS if "ps:" not in open(os.path.join(REFDATA, "computations", n + ".json")).read()]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", PREFIX_FREE)
+def test_emitted_f64_matches_frozen_vectors_exactly(name):
+    """The NVRTC-emitted kernel in f64 storage: ascending
+    lexicographic fold, no FMA contraction -> bit-identical to the frozen
+    reference outputs."""
+    from paper_2405_05118_b200 import mdh
+    text, comp, ins, want = load(name)
+    plan = mdh.Plan(text, float_storage=mdh.F64, int_storage=mdh.I64)
+    d = plan.describe()
+    if d["family"] != "emitted":  # a specialised family claimed it (f64 storage keeps contraction/stencil off)
+        assert d["family"] in ("prl",), d
+        return
+    got = run_device(plan, ins)
+    for g, (w, dd) in zip(got, want):
+        assert np.array_equal(g[dd], w[dd]), name
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,sizes", [("conv2d", [37, 29, 5, 3]), ("bmatmul", [5, 33, 17, 9]), ("histo", [700, 9]),
+                                        ("double_reduce", [4097]), ("jacobi1d", [1000]), ("map", [123, 77])])
+def test_emitted_matches_vm_at_other_sizes(name, sizes):
+    """Emitted kernel vs the device VM (generic=True) on the same inputs."""
+    from paper_2405_05118_b200 import mdh
+    text = json.load(open(os.path.join(REFDATA, "computations", name + ".json")))
+    text["sizes"] = sizes
+    comp = mo.Computation.from_json(text)
+    ins = mo.make_inputs(comp, 5)
+    if name == "histo":
+        ins = [np.abs(x) % 9 for x in ins]
+    em = mdh.Plan(text, float_storage=mdh.F64)
+    assert em.describe()["family"] in ("emitted", "contraction", "stencil"), em.describe()
+    vm = mdh.Plan(text, float_storage=mdh.F64, generic=True)
+    for a, b in zip(run_device(em, ins), run_device(vm, ins)):
+        assert np.array_equal(a, b), name
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,sizes,f64", [("dot", [300000], False), ("reduce", [1 << 20], False),
+                                            ("double_reduce", [100003], False), ("histo", [200000, 16], False),
+                                            ("genhisto", [70000, 8], False), ("dot", [300000], True)])
+def test_emitted_split_fiber_reductions(name, sizes, f64):
+    """Few cells, long point-wise fibers: the split-fiber emitted kernels
+    (G CTAs per cell + ordered final fold).  Integer results are exact (the
+    fold is associative and commutative on integers); the f64-typed variant
+    runs in f32 storage and is checked with the FP32 bound."""
+    from helpers import assert_close
+    from paper_2405_05118_b200 import mdh
+    text = json.load(open(os.path.join(REFDATA, "computations", name + ".json")))
+    text["sizes"] = sizes
+    if f64:
+        for b in text["inputs"] + text["outputs"]:
+            b["type"] = "f64"
+    comp = mo.Computation.from_json(text)
+    ins = mo.make_inputs(comp, 7)
+    if name in ("histo", "genhisto"):
+        ins[0] = np.abs(ins[0]) % sizes[1]
+    plan = mdh.Plan(text)
+    d = plan.describe()
+    assert d["family"] == "emitted" and d["template"]["fiber_parts"] > 1, d
+    got = run_device(plan, ins)
+    for g, (w, dd) in zip(got, mo.execute(comp, ins)):
+        if f64:
+            assert_close(g, w, dd, sizes[0], name)
+        else:
+            assert np.array_equal(g[dd], w[dd]), name
