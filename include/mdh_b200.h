@@ -121,6 +121,11 @@ int mdh_b200_tune(const char* computation_json, const char* asm_model, const mdh
                   uint64_t seed, char* best_config, int64_t best_cap, char* history_csv, int64_t hist_cap,
                   double* best_seconds);
 
+/* CUDA C++ source of the kernel the plan compiled at plan time (the emitted
+ * family, NVRTC); "" for the precompiled template families.  The B200
+ * counterpart of mdh::emit (codegen.hpp:38-53, `mdh emit`). */
+int mdh_b200_kernel_source(const mdh_b200_plan* plan, char* buf, int64_t cap, int64_t* need);
+
 /* Number of kernel launches one mdh_b200_run issues. */
 int mdh_b200_launches_per_run(const mdh_b200_plan* plan, int* launches);
 

@@ -25,6 +25,19 @@ namespace {
 
 thread_local std::string g_err;
 
+std::string json_escape(const std::string& x) {
+  std::string o;
+  for (char c : x) {
+    if (c == '"' || c == '\\') o += '\\';
+    if (c == '\n') {
+      o += "\\n";
+      continue;
+    }
+    o += c;
+  }
+  return o;
+}
+
 template <class F>
 int guard(F&& f) {
   try {
@@ -291,10 +304,14 @@ int mdh_b200_describe(const mdh_b200_plan* p, char* buf, int64_t cap, int64_t* n
     os << "{\"family\": \"" << p->r->family() << "\", \"template\": " << p->r->describe()
        << ", \"launches\": " << p->r->launches() << ", \"bytes\": " << static_cast<int64_t>(p->r->bytes())
        << ", \"flops\": " << static_cast<int64_t>(p->r->flops()) << ", \"bound\": \"" << p->r->bound() << "\""
-       << ", \"note\": \"" << p->note << "\", \"asm\": \"" << p->prob.m.name << "\", \"config\": "
+       << ", \"note\": \"" << json_escape(p->note) << "\", \"asm\": \"" << p->prob.m.name << "\", \"config\": "
        << mdhb::config_json(p->cfg, p->prob.e, p->prob.m) << "}";
     put(os.str(), buf, cap, need);
   });
+}
+
+int mdh_b200_kernel_source(const mdh_b200_plan* p, char* buf, int64_t cap, int64_t* need) {
+  return guard([&] { put(p->r->source(), buf, cap, need); });
 }
 
 int mdh_b200_validate_config(const char* comp_json, const char* asm_model, const char* config_json, char* buf,

@@ -399,6 +399,7 @@ class EmittedRoutine final : public Routine {
   explicit EmittedRoutine(const Problem& p) : p_(p) {}
   const char* family() const override { return "emitted"; }
   int launches() const override { return G_ ? 2 : 1; }
+  std::string source() const override { return src_; }
   double bytes() const override { return static_cast<double>(p_.in_bytes + p_.out_bytes); }
   std::string describe() const override {
     std::ostringstream os;

@@ -58,6 +58,8 @@ class Routine {
   virtual double flops() const { return 0.0; }  // algorithmic, per run
   virtual double bytes() const = 0;             // algorithmic, per run
   virtual const char* bound() const { return "hbm"; }
+  // source of a kernel compiled at plan time (emitted family), else ""
+  virtual std::string source() const { return ""; }
   // Chunked host<->device execution along a concatenation dimension, when
   // the family can overlap copies with compute (nullptr = whole-buffer copy).
   virtual bool supports_chunked_host() const { return false; }

@@ -35,7 +35,7 @@ _NP = {F32: np.float32, F64: np.float64, I32: np.int32, I64: np.int64}
 EXPORTED = [
     "mdh_b200_default_options", "mdh_b200_plan_create", "mdh_b200_plan_destroy", "mdh_b200_buffer_count",
     "mdh_b200_buffer_info", "mdh_b200_run", "mdh_b200_run_host", "mdh_b200_time", "mdh_b200_describe",
-    "mdh_b200_validate_config", "mdh_b200_tune", "mdh_b200_launches_per_run", "mdh_b200_last_error",
+    "mdh_b200_validate_config", "mdh_b200_tune", "mdh_b200_launches_per_run", "mdh_b200_kernel_source", "mdh_b200_last_error",
     "mdh_b200_version",
 ]
 
@@ -133,6 +133,14 @@ class Plan:
         buf = ctypes.create_string_buffer(need.value)
         _check(lib().mdh_b200_describe(self._h, buf, need.value, ctypes.byref(need)))
         return json.loads(buf.value.decode())
+
+    def kernel_source(self) -> str:
+        """CUDA source of the NVRTC-compiled kernel (emitted family), else ""."""
+        need = ctypes.c_int64()
+        _check(lib().mdh_b200_kernel_source(self._h, None, 0, ctypes.byref(need)))
+        buf = ctypes.create_string_buffer(max(1, need.value))
+        _check(lib().mdh_b200_kernel_source(self._h, buf, need.value, ctypes.byref(need)))
+        return buf.value.decode()
 
     @property
     def launches(self) -> int:

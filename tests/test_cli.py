@@ -1,0 +1,109 @@
+"""The `mdh` driver (paper_2405_05118_b200/cli.py): subcommands,
+output lines and exit codes of proj/tools/mdh_main.cpp."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+REFDATA = os.path.join(GOLDEN, "reference_data")
+
+
+def run(args, capsys):
+    from paper_2405_05118_b200 import cli
+    rc = cli.main(args + (["--data", REFDATA] if args[0] != "examples" else ["--data", REFDATA]))
+    out = capsys.readouterr()
+    return rc, out.out, out.err
+
+
+def test_exit_codes_mirror_the_reference():
+    from paper_2405_05118_b200 import cli
+    assert cli.exit_code_for("ParseError") == 3
+    for c in ("InvalidConfig", "Mismatch", "NoValidConfigFound", "NonDivisible", "MixedIncompatibleOperators",
+              "UnknownPreset", "UnknownFixture"):
+        assert cli.exit_code_for(c) == 2
+    assert cli.exit_code_for("CudaError") == 1
+
+
+def test_missing_spec_is_a_parse_error(capsys):
+    rc, _, err = run(["verify", "--spec", "no_such_computation"], capsys)
+    assert rc == 3 and "ParseError" in err
+
+
+def test_unknown_fixture(capsys):
+    rc, _, err = run(["verify", "--fixture", "no_such_fixture"], capsys)
+    assert rc == 2 and "UnknownFixture" in err
+
+
+def test_bad_arguments_exit_3():
+    from paper_2405_05118_b200 import cli
+    assert cli.main(["frobnicate"]) == 3
+
+
+def test_examples_lists_bundled_computations(capsys):
+    rc, out, _ = run(["examples"], capsys)
+    assert rc == 0
+    assert "matvec: dims" in out and "fixture tvm_gpu: matmul_resnet on CUDA" in out
+
+
+def test_driver_inputs_follow_the_reference_rng():
+    """mdh_main.cpp:46-66: mt19937_64(seed ^ 0x9e3779b97f4a7c15), below(11) - 5."""
+    from paper_2405_05118_b200 import cli
+    g = cli._MT64(5489)
+    for _ in range(9999):
+        g.next()
+    assert g.next() == 9981545732273789042   # the C++ standard's check value
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("spec", ["matvec", "matmul", "mcc", "jacobi3d", "histo", "scan", "prl"])
+def test_verify_bundled(spec, capsys):
+    rc, out, _ = run(["verify", "--spec", spec], capsys)
+    assert rc == 0 and "1/1 configurations pass" in out, out
+
+
+@pytest.mark.gpu
+def test_verify_published_fixture(capsys):
+    """tvm_gpu: TVM's MatMul decomposition (the reference's AC4 fixture)."""
+    rc, out, _ = run(["verify", "--fixture", "tvm_gpu"], capsys)
+    assert rc == 0 and "config tvm_gpu: pass" in out, out
+
+
+@pytest.mark.gpu
+def test_verify_invalid_config_exit_2(tmp_path, capsys):
+    cfg = tmp_path / "bad.json"
+    cfg.write_text(json.dumps({"num_parts": [[3, 1]]}))
+    rc, out, err = run(["verify", "--spec", "matvec", "--config", str(cfg)], capsys)
+    assert rc in (2, 3), (out, err)
+
+
+@pytest.mark.gpu
+def test_emit_prints_the_nvrtc_kernel(capsys):
+    rc, out, _ = run(["emit", "--spec", "histo"], capsys)
+    assert rc == 0 and 'extern "C" __global__' in out and "mdh_emitted" in out
+
+
+@pytest.mark.gpu
+def test_tune_writes_history_with_reference_columns(tmp_path, capsys):
+    hist = tmp_path / "h.csv"
+    best = tmp_path / "best.json"
+    rc, out, _ = run(["tune", "--spec", "matvec", "--budget", "3", "--history", str(hist), "--out", str(best)], capsys)
+    assert rc == 0 and "evaluations: 3" in out
+    rows = hist.read_text().strip().splitlines()
+    assert rows[0] == "eval_index,config_hash,objective,valid" and len(rows) == 4
+    assert "num_parts" in json.loads(best.read_text())
+
+
+@pytest.mark.gpu
+def test_run_reproduces_a_frozen_reference_vector(tmp_path, capsys):
+    ref = os.path.join(REFDATA, "refs", "matmul.ref.json")
+    out_file = tmp_path / "o.json"
+    rc, _, _ = run(["run", "--spec", "matmul", "--inputs", ref, "--out", str(out_file)], capsys)
+    assert rc == 0
+    got = json.loads(out_file.read_text())["outputs"]
+    want = json.load(open(ref))["outputs"]
+    for name, g in want.items():
+        w = np.array([0 if x is None else x for x in g["data"]], dtype=np.float64)
+        assert np.array_equal(np.array(got[name]["data"], dtype=np.float64), w), name
