@@ -861,7 +861,9 @@ class GemmRoutine final : public Routine {
           ak[0] == 0 && bk[0] == 0 && ak[1] == 1 && !std::getenv("MDHB_SKINNY_V1")) {
         sak_ = ak[1];
         sbk_ = bk[1];
-        for (int cs : {8, 4, 2}) {
+        std::vector<int> css = {8, 4, 2};
+        if (const char* f = std::getenv("MDHB_SKINNY_CS")) css.insert(css.begin(), std::atoi(f));
+        for (int cs : css) {
           const int64_t ks = K_ / cs;
           const int64_t mt = M_ <= 16 ? 16 : 32;
           if (K_ % (cs * 64) || ks > 1024 || (ks & (ks - 1))) continue;
@@ -1040,6 +1042,7 @@ class GemmRoutine final : public Routine {
       MDHB_SK(64) MDHB_SK(128) MDHB_SK(256) MDHB_SK(512) MDHB_SK(1024)
 #undef MDHB_SK
       if (smem > 48 * 1024) MDHB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      if (splits_ > 8) MDHB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       MDHB_CUDA(cudaLaunchKernelEx(&lc, kern, a));
       return;
     }
