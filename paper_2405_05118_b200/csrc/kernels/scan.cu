@@ -14,9 +14,10 @@
 //
 // Two kernels, chosen by where the scan dimension lies in memory:
 //   * scan_tiles  -- the ps dim is unit-stride in input and output: a
-//     single-pass decoupled look-back scan.  Tiles of 4096 elements (256
-//     threads x 4 rounds x 4) are claimed in order from an atomic counter;
-//     each publishes its aggregate, then its inclusive prefix, in a per-tile
+//     single-pass decoupled look-back scan.  Tiles of 4096 elements (128
+//     threads x 8 rounds x 4, 8 CTAs per SM so the look-back of one CTA hides
+//     behind the loads of the others) are claimed in order from an atomic
+//     counter; each publishes its aggregate, then its inclusive prefix, in a per-tile
 //     status word (flag | value packed in 64 bits for 32-bit types, a flag
 //     word fenced after the value otherwise).  Per element: one read, one
 //     write -- the HBM roofline of a copy.
@@ -37,8 +38,14 @@ namespace {
 #ifndef MDHB_SCAN_ROUNDS
 #define MDHB_SCAN_ROUNDS 8
 #endif
-constexpr int SC_THREADS = 256, SC_ROUNDS = MDHB_SCAN_ROUNDS, SC_VEC = 4;
-constexpr int SC_TILE = SC_THREADS * SC_ROUNDS * SC_VEC;  // 8192 elements
+#ifndef MDHB_SCAN_THREADS
+#define MDHB_SCAN_THREADS 128
+#endif
+#ifndef MDHB_SCAN_MINB
+#define MDHB_SCAN_MINB 8
+#endif
+constexpr int SC_THREADS = MDHB_SCAN_THREADS, SC_ROUNDS = MDHB_SCAN_ROUNDS, SC_VEC = 4;
+constexpr int SC_TILE = SC_THREADS * SC_ROUNDS * SC_VEC;  // elements per tile
 constexpr int kScanMaxD = 15;
 
 struct ScanArgs {
@@ -159,16 +166,18 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 template <typename T>
 __device__ __forceinline__ unsigned long long observe(const ScanArgs& a, int64_t slot, T& v) {
   unsigned long long w;
-  do {
+  for (unsigned ns = 8;; ns = ns < 256 ? 2 * ns : ns) {
     w = sizeof(T) == 4 ? ld_relaxed(a.status + slot) : ld_acquire(a.status + slot);
-  } while ((w & F_MASK) == 0);
+    if (w & F_MASK) break;
+    __nanosleep(ns);
+  }
   if (sizeof(T) == 4) v = from_bits<T>(w & 0xffffffffull);
   else v = from_bits<T>(ld_relaxed(a.values + 2 * slot + ((w & F_MASK) == F_INC ? 1 : 0)));
   return w & F_MASK;
 }
 
 template <typename T, int OP>
-__global__ void __launch_bounds__(SC_THREADS) scan_tiles(ScanArgs a) {
+__global__ void __launch_bounds__(SC_THREADS, MDHB_SCAN_MINB) scan_tiles(ScanArgs a) {
   __shared__ T wsum[SC_ROUNDS][SC_THREADS / 32];
   __shared__ T tile_prefix;
   __shared__ unsigned int s_tile;
