@@ -19,6 +19,7 @@
 // When the data does not fit that encoding the same kernel takes an exact
 // 64-bit path (a device-side flag decides; no host round trip).
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 
@@ -45,8 +46,10 @@ struct PrlArgs {
   // pre-pass scratch
   uint32_t* qp;   // [nq]
   uint32_t* dp;   // [nr]
-  int* info;      // [0] fast-path flag, [1] packed weights, [2] S / 128
+  int* info;      // [0] fast-path flag, [1] packed weights, [2] S / 128,
+                  // [3] weights * 16 as unsigned bytes, [4] five-instruction path flag
   int qt;         // queries per thread
+  int allow5;     // five-instruction path permitted (MDHB_PRL_5=1)
   int rsplit;     // record splits (grid.y)
 };
 
@@ -116,12 +119,24 @@ __global__ void __launch_bounds__(512) prl_pack(PrlArgs a, const long long* part
       long long lo = wneg * a.S + (a.C - (a.nr - 1)), hi = wpos * a.S + a.C;
       ok = lo >= INT_MIN && hi <= INT_MAX;
     }
+    // five-instruction variant: weights in [0, 15] scaled by 16 into unsigned
+    // bytes, so DP4A yields 2^11 * wsum and its accumulator adds the
+    // tile-local reversed record index: key_local = wsum * 2^11 + (2047 - k)
+    bool ok5 = ok && a.S >= 2048 && a.allow5;
+    uint32_t wp16 = 0;
+    for (int t = 0; t < a.F; ++t) {
+      long long w = ld(a.W, a.w_is64, a.wf[t]);
+      ok5 = ok5 && w >= 0 && w <= 15;
+      wp16 |= (static_cast<uint32_t>(w * 16) & 0xFFu) << (8 * t);
+    }
     s_fast = ok ? 1 : 0;
     s_base = mn;
     if (blockIdx.x == 0) {
       a.info[0] = s_fast;
       a.info[1] = static_cast<int>(wp);
       a.info[2] = ok ? static_cast<int>(a.S / 128) : 0;
+      a.info[3] = static_cast<int>(wp16);
+      a.info[4] = ok5 ? 1 : 0;
     }
   }
   __syncthreads();
@@ -173,7 +188,53 @@ __global__ void __launch_bounds__(NT) prl_main(PrlArgs a) {
   const int64_t r_begin = static_cast<int64_t>(blockIdx.y) * per;
   const int64_t r_end = min(a.nr, r_begin + per);
   long long best64[QT];
-  if (a.info[0]) {
+  if (a.info[4]) {
+    // ---- five instructions per pair: LOP3 (xor & mask) + IADD + LOP3 (byte
+    // equality) + DP4A (2^11 * weighted count + reversed tile index) + IMNMX.
+    // The tile's best local key converts to the global key once per tile.
+    const uint32_t wp16 = static_cast<uint32_t>(a.info[3]);
+    uint32_t qp[QT];
+    int best[QT];
+#pragma unroll
+    for (int j = 0; j < QT; ++j) {
+      int64_t q = q0 + static_cast<int64_t>(j) * NT;
+      qp[j] = q < a.nq ? a.qp[q] : 0u;
+      best[j] = INT_MIN;
+    }
+    uint32_t* tile1 = reinterpret_cast<uint32_t*>(tile);
+    for (int64_t rt = r_begin; rt < r_end; rt += RT) {
+      const int n = static_cast<int>(r_end - rt < RT ? r_end - rt : RT);
+      __syncthreads();
+      for (int k = threadIdx.x; k < n; k += NT) tile1[k] = a.dp[rt + k];
+      __syncthreads();
+      int loc[QT];
+#pragma unroll
+      for (int j = 0; j < QT; ++j) loc[j] = -1;
+#pragma unroll 4
+      for (int k = 0; k < n; ++k) {
+        const uint32_t rec = tile1[k];
+        const uint32_t krev = static_cast<uint32_t>(RT - 1 - k);
+#pragma unroll
+        for (int j = 0; j < QT; ++j) {
+          const uint32_t x = qp[j] ^ rec;
+          const uint32_t t = (x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
+          const uint32_t eq = ~t & 0x80808080u;
+          int key;
+          asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(key) : "r"(eq), "r"(wp16), "r"(krev));
+          loc[j] = max(loc[j], key);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < QT; ++j) {
+        const int wsum = loc[j] >> 11;
+        const int64_t r = rt + (RT - 1 - (loc[j] & (RT - 1)));
+        const int g = static_cast<int>(static_cast<int64_t>(wsum) * a.S + (a.C - r));  // fits: host/pack checked
+        best[j] = max(best[j], g);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < QT; ++j) best64[j] = best[j];
+  } else if (a.info[0]) {
     // ---- packed fast path (32-bit keys, exact while info[0] holds)
     const uint32_t wp = static_cast<uint32_t>(a.info[1]);
     const int sdiv = a.info[2];
@@ -259,6 +320,10 @@ class PrlRoutine final : public Routine {
     size_t head = 256 + static_cast<size_t>(nparts_) * 16;
     MDHB_CUDA(cudaMalloc(&scratch_, static_cast<size_t>(a.nq + a.nr) * 4 + head));
     a_.info = static_cast<int*>(scratch_);
+    // the five-instruction path measured slower on B200 (8.24 vs 7.93 ms at
+    // 2^15 x 2^20: IDP.4A.U8.U8 + VIMNMX per pair vs the six-instruction mix);
+    // kept selectable (MDHB_PRL_5=1), bit-exact either way
+    a_.allow5 = std::getenv("MDHB_PRL_5") ? 1 : 0;
     part_ = reinterpret_cast<long long*>(static_cast<char*>(scratch_) + 256);
     a_.qp = reinterpret_cast<uint32_t*>(static_cast<char*>(scratch_) + head);
     a_.dp = a_.qp + a.nq;

@@ -74,3 +74,27 @@ def test_prl_full_size_sampled_queries():
         assert np.array_equal(got[lo:lo + 8], part)
     idx = np.random.default_rng(1).integers(0, 32768, 24)
     assert np.array_equal(got[idx], brute(Q[idx], D, W))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("five", [False, True])
+@pytest.mark.parametrize("W", [[3, 20, 7, 9], [3, -2, 7, 9], [0, 15, 1, 15]])
+def test_prl_weight_encodings_bit_exact(W, five, monkeypatch):
+    """Weights in [0, 15] take the five-instruction path (DP4A yields
+    2^11 * wsum + reversed tile index); byte-range weights outside it take the
+    six-instruction path; both are bit-exact.  Record counts straddle the
+    2048-record tiles and the record splits."""
+    from paper_2405_05118_b200 import mdh
+    j = spec("prl_max", [300, 2048 * 3 + 77])
+    comp = mo.Computation.from_json(j)
+    rng = np.random.default_rng(11)
+    Q = rng.integers(0, 3, (300, 4))
+    D = rng.integers(0, 3, (2048 * 3 + 77, 4))
+    W = np.array(W)
+    if five:
+        monkeypatch.setenv("MDHB_PRL_5", "1")
+    plan = mdh.Plan(j, int_storage=mdh.I32)
+    (got,) = run_device(plan, [Q, D, W])
+    ((want, _),) = mo.execute(comp, [Q, D, W])
+    assert np.array_equal(got.astype(np.int64), want)
+    assert np.array_equal(want, brute(Q, D, W))
