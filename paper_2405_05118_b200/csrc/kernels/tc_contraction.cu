@@ -453,6 +453,225 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps(RB, BN), 1)
   if (warp == 1) tc::tmem_dealloc(tmem, TMEM_COLS);
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant (tcgen05 cta_group::2): a cluster of two CTAs on one TPC
+// computes a 256 x BN tile with M = 256 MMAs issued by the leader.  Each CTA
+// lands its own 128 rows of A and HALF of the BN rows of B (the MMA reads
+// the peer's half at the same shared-memory offsets), so per SM the ring
+// moves A + B/2 per k-tile instead of A + B -- the single-CTA kernel is
+// shared-memory-bandwidth bound (TMA writes + MMA reads of 96 KB per k-tile
+// at BN = 256).  Both CTAs' TMA loads complete on the leader's full[s]
+// barrier; the leader's MMA commits multicast to both CTAs' empty[s] /
+// tfull[a]; both CTAs' epilogue warps release the accumulator on the
+// leader's tempty[a].  Each CTA drains its own 128 TMEM lanes x BN columns.
+__device__ __forceinline__ uint32_t peer_addr(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void tma_load_2sm(void* dst, const void* tmap, uint32_t mbar_cluster, int rank, const int* c) {
+  const uint32_t d = tc::smem_u32(dst);
+  switch (rank) {
+    case 2:
+      asm volatile("cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+                   ::"r"(d), "l"(tmap), "r"(mbar_cluster), "r"(c[0]), "r"(c[1]) : "memory");
+      break;
+    case 3:
+      asm volatile("cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+                   ::"r"(d), "l"(tmap), "r"(mbar_cluster), "r"(c[0]), "r"(c[1]), "r"(c[2]) : "memory");
+      break;
+    case 4:
+      asm volatile("cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];"
+                   ::"r"(d), "l"(tmap), "r"(mbar_cluster), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]) : "memory");
+      break;
+    default:
+      asm volatile("cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], [%2];"
+                   ::"r"(d), "l"(tmap), "r"(mbar_cluster), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]) : "memory");
+      break;
+  }
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(64 + 32 * 4, 1)
+    tc_gemm_2sm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, TcArgs g, int b_row_rank) {
+  constexpr int EPW = 4;
+  constexpr uint32_t A_BYTES = BM * BKE * 4;
+  constexpr uint32_t B_BYTES = (BN / 2) * BKE * 4;  // this CTA's half of the B tile
+  constexpr uint32_t TMEM_COLS = 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* stage_base = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 256);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const bool leader = rank == 0;
+  const int pair = static_cast<int>(blockIdx.x) >> 1, npairs = static_cast<int>(gridDim.x) >> 1;
+  const int tilesM2 = g.tilesM / 2;  // 256-row tiles
+  const int ntiles = tilesM2 * g.tilesN;
+  constexpr int GROUP_M = 8;
+  auto tile_mn = [&](int x, int& tm, int& tn) {
+    const int per_group = GROUP_M * g.tilesN;
+    const int first_m = (x / per_group) * GROUP_M;
+    const int gsz = min(tilesM2 - first_m, GROUP_M);
+    tm = first_m + (x % per_group) % gsz;
+    tn = (x % per_group) / gsz;
+  };
+  if (threadIdx.x == 0) {
+    tc::tma_prefetch(&tma_a);
+    tc::tma_prefetch(&tma_b);
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 2 * EPW);  // leader's copy: the epilogue warps of both CTAs
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc::tc_fence_before();
+  // both CTAs' barriers exist before anyone touches the peer's
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer (both CTAs): own A rows, own half of B
+    const uint32_t full_leader0 = peer_addr(tc::smem_u32(&full[0]), 0);
+    uint32_t it = 0;
+    for (int x = pair; x < ntiles; x += npairs) {
+      int tm, tn;
+      tile_mn(x, tm, tn);
+      const int ta = 2 * tm + static_cast<int>(rank);
+      int am0[MAXR], bn0[MAXR], ka[MAXR], kb[MAXR], dig[MAXKD];
+#pragma unroll
+      for (int r = 0; r < MAXR; ++r) {
+        am0[r] = g.a_mc[ta * MAXR + r];
+        bn0[r] = g.b_nc[tn * MAXR + r] + (r == b_row_rank ? static_cast<int>(rank) * (BN / 2) : 0);
+        ka[r] = 0;
+        kb[r] = 0;
+      }
+#pragma unroll
+      for (int q = 0; q < MAXKD; ++q) dig[q] = 0;
+      for (int kt = 0; kt < g.nk; ++kt, ++it) {
+        const uint32_t s = it % STAGES;
+        if (it >= STAGES) tc::mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+        if (leader) tc::mbar_arrive_expect_tx(&full[s], 2 * (A_BYTES + B_BYTES));
+        const uint32_t fb = full_leader0 + s * 8;
+        int c[MAXR];
+#pragma unroll
+        for (int r = 0; r < MAXR; ++r) c[r] = am0[r] + ka[r];
+        tma_load_2sm(sA + s * A_BYTES, &tma_a, fb, g.a_rank, c);
+#pragma unroll
+        for (int r = 0; r < MAXR; ++r) c[r] = bn0[r] + kb[r];
+        tma_load_2sm(sB + s * B_BYTES, &tma_b, fb, g.b_rank, c);
+        for (int q = g.nkd - 1; q >= 0; --q) {
+          if (++dig[q] < g.kext[q]) {
+#pragma unroll
+            for (int r = 0; r < MAXR; ++r) {
+              ka[r] += g.kca[q][r] * g.kstep[q];
+              kb[r] += g.kcb[q][r] * g.kstep[q];
+            }
+            break;
+          }
+#pragma unroll
+          for (int r = 0; r < MAXR; ++r) {
+            ka[r] -= g.kca[q][r] * g.kstep[q] * (g.kext[q] - 1);
+            kb[r] -= g.kcb[q][r] * g.kstep[q] * (g.kext[q] - 1);
+          }
+          dig[q] = 0;
+        }
+      }
+    }
+  } else if (warp == 1 && lane == 0 && leader) {
+    // ---------------- MMA issuer (leader only): M = 256 across the pair
+    constexpr uint32_t idesc = tc::instr_desc(2, 0, 0, 2 * BM, BN);
+    uint32_t it = 0, tl = 0;
+    for (int x = pair; x < ntiles; x += npairs, ++tl) {
+      const uint32_t acc = tl & 1;
+      if (tl >= 2) tc::mbar_wait(&tempty[acc], ((tl / 2) - 1) & 1);
+      tc::tc_fence_after();
+      const uint32_t dtm = tmem + acc * BN;
+      for (int kt = 0; kt < g.nk; ++kt, ++it) {
+        const uint32_t s = it % STAGES;
+        tc::mbar_wait(&full[s], (it / STAGES) & 1);
+        tc::tc_fence_after();
+        const uint32_t sa = tc::smem_u32(sA + s * A_BYTES);
+        const uint32_t sb = tc::smem_u32(sB + s * B_BYTES);
+#pragma unroll
+        for (int k = 0; k < BKE / 8; ++k) {
+          const uint64_t da = tc::sw128_desc(sa + k * 32, 16, 1024);
+          const uint64_t db = tc::sw128_desc(sb + k * 32, 16, 1024);
+          const uint32_t accum = (kt | k) != 0 ? 1u : 0u;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtm), "l"(da), "l"(db), "r"(idesc),
+              "r"(accum));
+        }
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                     ::"r"(tc::smem_u32(&empty[s])), "h"(static_cast<uint16_t>(3)) : "memory");
+      }
+      asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                   ::"r"(tc::smem_u32(&tfull[acc])), "h"(static_cast<uint16_t>(3)) : "memory");
+    }
+  } else if (warp >= 2) {
+    // ---------------- epilogue warps (both CTAs): own 128 TMEM lanes
+    const int q = warp & 3;
+    const uint32_t stg = tc::smem_u32(stage_base) + static_cast<uint32_t>(warp - 2) * (32 * 33 * 4 + 32 * 8);
+    const uint32_t rtab = stg + 32 * 33 * 4;
+    const uint32_t tempty_leader0 = peer_addr(tc::smem_u32(&tempty[0]), 0);
+    uint32_t tl = 0;
+    for (int x = pair; x < ntiles; x += npairs, ++tl) {
+      int tm, tn;
+      tile_mn(x, tm, tn);
+      const int ta = 2 * tm + static_cast<int>(rank);
+      const uint32_t acc = tl & 1;
+      const int64_t rowoff = static_cast<int64_t>(g.tCm[ta]) + g.cm[q * 32 + lane] + g.tCn[tn];
+      asm volatile("st.shared.s64 [%0], %1;" ::"r"(rtab + lane * 8), "l"(rowoff) : "memory");
+      tc::mbar_wait(&tfull[acc], (tl / 2) & 1);
+      tc::tc_fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t rv[32];
+        tc::tmem_ld32(tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c0), rv);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          asm volatile("st.shared.b32 [%0], %1;" ::"r"(stg + (lane * 33 + j) * 4), "r"(rv[j]) : "memory");
+        __syncwarp();
+        float* cc = g.C + g.cn[c0 + lane];
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) {
+          int64_t ro;
+          float v;
+          asm volatile("ld.shared.s64 %0, [%1];" : "=l"(ro) : "r"(rtab + rr * 8) : "memory");
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(stg + (rr * 33 + lane) * 4) : "memory");
+          __stcs(cc + ro, v);
+        }
+        __syncwarp();
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty_leader0 + acc * 8) : "memory");
+    }
+  }
+  tc::tc_fence_before();
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
 // ---------------------------------------------------------------- host
 using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -607,7 +826,8 @@ class TcRoutine final : public Routine {
   double bytes() const override { return static_cast<double>(p_.in_bytes + p_.out_bytes); }
   std::string describe() const override {
     std::ostringstream os;
- os << "{\"kernel\": \"" << (pers_ ? "tc_gemm_pers<" : "tc_gemm_tf32<") << BN_ << "," << (pers_ ? pstages_ : stages_) << ","
+ os << "{\"kernel\": \"" << (two_sm_ ? "tc_gemm_2sm<" : pers_ ? "tc_gemm_pers<" : "tc_gemm_tf32<") << BN_ << ","
+       << (two_sm_ ? st2_ : pers_ ? pstages_ : stages_) << ","
        << (va_.mn ? "A_MN" : "A_K") << "," << (vb_.mn ? "B_MN" : "B_K") << (rb_ && pers_ ? ",B_RESIDENT" : "")
        << ">\", \"math\": \"tf32\", \"M\": " << M_ << ", \"N\": " << N_ << ", \"K\": " << K_
        << ", \"BM\": " << BM << ", \"BN\": " << BN_ << ", \"BK\": " << BKE << ", \"stages\": " << stages_
@@ -616,6 +836,7 @@ class TcRoutine final : public Routine {
        << ", \"b_layout\": \"" << (packed_ ? "packed K-major (pack_kmajor pre-pass, both operands)" : transposeB_ ? "K-major copy (layout_de [2,1] pre-pass)" : (vb_.mn ? "MN-major" : "K-major"))
        << "\"";
     if (packed_) os << ", \"K_padded\": " << Kp_;
+    if (two_sm_) os << ", \"cta_pair\": \"tc_gemm_2sm<" << BN_ << "," << st2_ << ">: tcgen05.mma.cta_group::2 M256xN" << BN_ << "xK8\"";
     os << "}";
     return os.str();
   }
@@ -781,6 +1002,7 @@ class TcRoutine final : public Routine {
     pstages_ = rb_ ? rb_st : pers_stages(BN);
     psmem_ = rb_ ? rb_bytes : static_cast<size_t>(pstages_) * (BM + BN) * BKE * 4 + 1024 + 256 + epi_bytes(false, BN);
     pers_ = !std::getenv("MDHB_TC_NONPERSISTENT");
+    decide_2sm();
     return true;
   }
 
@@ -883,9 +1105,32 @@ class TcRoutine final : public Routine {
     pstages_ = pers_stages(BN);
     psmem_ = static_cast<size_t>(pstages_) * (BM + BN) * BKE * 4 + 1024 + 256 + epi_bytes(false, BN);
     pers_ = !std::getenv("MDHB_TC_NONPERSISTENT");
+    decide_2sm();
     return true;
   }
 
+  // CTA-pair instance: K-major B whose tile rows live in one TMA rank (the
+  // half-box split), an even number of 128-row tiles, BN 128 / 256
+  void decide_2sm() {
+    two_sm_ = false;
+    if (std::getenv("MDHB_TC_1SM") || !pers_ || rb_ || vb_.mn || (BN_ != 256 && BN_ != 128) || tilesM_ % 2) return;
+    int row_rank = -1;
+    for (int t = 1; t < vb_.rank; ++t) {
+      if (vb_.box[t] == static_cast<cuuint32_t>(BN_)) {
+        if (row_rank >= 0) return;
+        row_rank = t;
+      } else if (vb_.box[t] != 1) {
+        return;
+      }
+    }
+    if (row_rank < 0) return;
+    b_row_rank_ = row_rank;
+    vb2_ = vb_;
+    vb2_.box[row_rank] = static_cast<cuuint32_t>(BN_ / 2);
+    st2_ = BN_ == 256 ? 6 : 8;
+    smem2_ = static_cast<size_t>(st2_) * (BM + BN_ / 2) * BKE * 4 + 1024 + 256 + 4 * (32 * 33 * 4 + 32 * 8);
+    two_sm_ = smem2_ <= 227 * 1024;
+  }
   bool packed() const { return packed_; }
   int64_t c_run() const { return c_run_; }
   static int64_t run_of(const std::vector<int64_t>& cn) {
@@ -922,9 +1167,34 @@ class TcRoutine final : public Routine {
       B = bt_;
     }
     if (A != last_a_) encode(va_, A, &ma_), last_a_ = A;
-    if (B != last_b_) encode(vb_, B, &mb_), last_b_ = B;
+    if (B != last_b_) {
+      encode(vb_, B, &mb_);
+      if (two_sm_) encode(vb2_, B, &mb2_);
+      last_b_ = B;
+    }
     TcArgs a = args_;
     a.C = static_cast<float*>(d_out[0]);
+    if (two_sm_) {
+      const int sms = sm_count(p_.opt.device);
+      const int pairs = std::min(sms / 2, (tilesM_ / 2) * tilesN_);
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3(static_cast<unsigned>(2 * pairs));
+      lc.blockDim = dim3(64 + 32 * 4);
+      lc.dynamicSmemBytes = smem2_;
+      lc.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      void (*k)(const CUtensorMap, const CUtensorMap, TcArgs, int) =
+          BN_ == 256 ? tc_gemm_2sm<256, 6> : tc_gemm_2sm<128, 8>;
+      MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2_)));
+      MDHB_CUDA(cudaLaunchKernelEx(&lc, k, ma_, mb2_, a, b_row_rank_));
+      return;
+    }
     if (pers_) {
       const int sms = sm_count(p_.opt.device);
       dim3 pgrid(static_cast<unsigned>(std::min(sms, tilesM_ * tilesN_)));
@@ -989,6 +1259,11 @@ class TcRoutine final : public Routine {
   size_t psmem_ = 0;
   bool packed_ = false;
   int64_t Kp_ = 0, c_run_ = 1;
+  bool two_sm_ = false;
+  int b_row_rank_ = 1, st2_ = 0;
+  size_t smem2_ = 0;
+  View vb2_;
+  CUtensorMap mb2_{};
   void *pa_ = nullptr, *pb_ = nullptr;
   std::array<const int32_t*, 6> pk_{};  // packing tables: tAm, am, ak, tBn, bn, bk
 };

@@ -38,7 +38,8 @@ def test_tf32_exact_mode_bit_identical(name, sizes, kernel):
     plan = plan_tf32(j)
     d = plan.describe()
     kern = d["template"]["kernel"]
-    assert d["family"] == "contraction" and (kern.startswith(kernel) or kern.startswith(kernel.replace("tc_gemm_tf32", "tc_gemm_pers"))), d
+    assert d["family"] == "contraction" and any(kern.startswith(kernel.replace("tc_gemm_tf32", v))
+                                                for v in ("tc_gemm_tf32", "tc_gemm_pers", "tc_gemm_2sm")), d
     assert d["family"] == "contraction" and d["template"].get("math") == "tf32", d
     ins = exact_inputs(comp, 4)
     (got,) = run_device(plan, ins)
@@ -115,7 +116,7 @@ def test_tf32_conv_matches_generic_tc_instance(monkeypatch):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("env", ["MDHB_TC_NONPERSISTENT", "MDHB_TC_NO_TRANSPOSE"])
+@pytest.mark.parametrize("env", ["MDHB_TC_NONPERSISTENT", "MDHB_TC_NO_TRANSPOSE", "MDHB_TC_1SM"])
 def test_tf32_variants_agree(env, monkeypatch):
     """Non-persistent / MN-major instances give the same bits as the default."""
     j = spec("matmul_fp32", [256, 512, 96])
