@@ -50,6 +50,8 @@ struct ConvArgs {
   int64_t on, op, oq;      // output strides (elements)
   uint32_t plane;          // bytes of one 4-channel plane of the patch (HP * WQ * 16)
   uint32_t lbo, sbo;       // descriptor core-matrix strides (K direction, M direction)
+  int sw;                  // 1: pixel-major 128B-swizzled patch (4-D box {32 c, WQ, HP, 1})
+  int bo_mode;             // descriptor base-offset rule for shifted swizzled rows (dev)
 };
 
 __device__ __forceinline__ uint64_t nosw_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -115,8 +117,13 @@ __global__ void __launch_bounds__(192, 1)
         const uint32_t s = it % PSTAGES;
         if (it >= PSTAGES) tc::mbar_wait(&empty[s], ((it / PSTAGES) - 1) & 1);
         tc::mbar_arrive_expect_tx(&full[s], patch_bytes);
-        int c[5] = {0, qb * CV_TQ, pb * CV_TP, cc * 8, n};
-        tc::tma_load(sP + s * patch_slot, &tma_i, &full[s], 5, c);
+        if (g.sw) {
+          int c[5] = {cc * CV_BKE, qb * CV_TQ, pb * CV_TP, n, 0};
+          tc::tma_load(sP + s * patch_slot, &tma_i, &full[s], 4, c);
+        } else {
+          int c[5] = {0, qb * CV_TQ, pb * CV_TP, cc * 8, n};
+          tc::tma_load(sP + s * patch_slot, &tma_i, &full[s], 5, c);
+        }
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -137,11 +144,14 @@ __global__ void __launch_bounds__(192, 1)
         const uint32_t sp = tc::smem_u32(sP + s * patch_slot);
         for (int r = 0; r < g.R; ++r)
           for (int ss = 0; ss < g.S; ++ss) {
-            const uint32_t tap = sp + static_cast<uint32_t>(r * g.WQ + ss) * 16;
+            const uint32_t tap = sp + static_cast<uint32_t>(r * g.WQ + ss) * (g.sw ? 128 : 16);
             const uint32_t sb = tc::smem_u32(sB + static_cast<size_t>((r * g.S + ss) * chunks + cc) * B_BYTES);
+            const uint64_t bo = g.bo_mode ? static_cast<uint64_t>(((r * g.WQ + ss) & 7)) << 49 : 0;
 #pragma unroll
             for (int j = 0; j < CV_BKE / 8; ++j) {
-              const uint64_t da = nosw_desc(tap + 2 * j * g.plane, g.lbo, g.sbo);
+              // swizzled: rows are pixels (128 B = 32 channels), 8-row groups WQ rows apart
+              const uint64_t da = g.sw ? (tc::umma_desc(tap + j * 32, 16, static_cast<uint32_t>(g.WQ) * 128, 2) | bo)
+                                       : nosw_desc(tap + 2 * j * g.plane, g.lbo, g.sbo);
               const uint64_t db = tc::sw128_desc(sb + j * 32, 16, 1024);
               tc::mma<true>(dtm, da, db, idesc, first ? 0u : 1u);
               first = false;
@@ -193,6 +203,183 @@ __global__ void __launch_bounds__(192, 1)
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc(tmem, TMEM_COLS);
+}
+
+// CTA-pair instance (cta_group::2): the two CTAs of a cluster take two
+// output tiles, each lands its own input patches, and each holds HALF of the
+// resident filter (32 of the 64 output channels); the leader issues
+// M = 256 x N = 64 MMAs that read the peer's patch and filter half at the same
+// shared-memory offsets.  Per SM the MMA reads A + B/2 (and the filter's
+// smem footprint halves, leaving room for a deeper patch ring).
+__device__ __forceinline__ uint32_t cv_peer(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+
+template <int BN, int PSTAGES>
+__global__ void __launch_bounds__(192, 1)
+    tc_conv_2sm(const __grid_constant__ CUtensorMap tma_i, const __grid_constant__ CUtensorMap tma_f, ConvArgs g) {
+  constexpr uint32_t B_BYTES = (BN / 2) * CV_BKE * 4;  // this CTA's half of one filter k-tile
+  constexpr uint32_t TMEM_COLS = 2 * BN <= 128 ? 128 : 256;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int ktiles = g.R * g.S * (g.C / CV_BKE);
+  const int chunks = g.C / CV_BKE;
+  const uint32_t patch_bytes = 8 * g.plane;
+  const uint32_t patch_slot = (patch_bytes + 1023) & ~1023u;
+  uint8_t* sB = smem;
+  uint8_t* sP = smem + ((static_cast<size_t>(ktiles) * B_BYTES + 1023) & ~size_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sP + PSTAGES * patch_slot);
+  uint64_t* empty = full + PSTAGES;
+  uint64_t* bfull = empty + PSTAGES;
+  uint64_t* tfull = bfull + 1;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* stage_base = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 256);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const bool leader = rank == 0;
+  const int per_img = g.pblocks * g.qblocks;
+  const int ntiles = g.N * per_img;
+  const int npairs_tiles = (ntiles + 1) / 2;  // pair items: tiles 2x (leader) and 2x+1 (peer)
+  const int pair = static_cast<int>(blockIdx.x) >> 1, npairs = static_cast<int>(gridDim.x) >> 1;
+
+  if (threadIdx.x == 0) {
+    tc::tma_prefetch(&tma_i);
+    tc::tma_prefetch(&tma_f);
+    for (int s = 0; s < PSTAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(bfull, 1);
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 8);  // leader's copy: 4 epilogue warps x 2 CTAs
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc::tc_fence_before();
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer (both CTAs)
+    const uint32_t bfull_leader = cv_peer(tc::smem_u32(bfull), 0);
+    const uint32_t full_leader0 = cv_peer(tc::smem_u32(&full[0]), 0);
+    // this CTA's filter half: output channels rank*BN/2 .. +BN/2, every k-tile
+    if (leader) tc::mbar_arrive_expect_tx(bfull, 2u * static_cast<uint32_t>(ktiles) * B_BYTES);
+    for (int kt = 0; kt < ktiles; ++kt) {
+      int c[5] = {kt * CV_BKE, static_cast<int>(rank) * (BN / 2), 0, 0, 0};
+      uint32_t d = tc::smem_u32(sB + static_cast<size_t>(kt) * B_BYTES);
+      asm volatile("cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+                   ::"r"(d), "l"(&tma_f), "r"(bfull_leader), "r"(c[0]), "r"(c[1]) : "memory");
+    }
+    uint32_t it = 0;
+    for (int x = pair; x < npairs_tiles; x += npairs) {
+      // a ragged last pair: the peer re-loads the leader's tile (its rows are not stored)
+      const int t = min(2 * x + static_cast<int>(rank), ntiles - 1);
+      const int n = t / per_img, rem = t % per_img, pb = rem / g.qblocks, qb = rem % g.qblocks;
+      for (int cc = 0; cc < chunks; ++cc, ++it) {
+        const uint32_t s = it % PSTAGES;
+        if (it >= PSTAGES) tc::mbar_wait(&empty[s], ((it / PSTAGES) - 1) & 1);
+        if (leader) tc::mbar_arrive_expect_tx(&full[s], 2 * patch_bytes);
+        const uint32_t d = tc::smem_u32(sP + s * patch_slot);
+        asm volatile("cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], [%2];"
+                     ::"r"(d), "l"(&tma_i), "r"(full_leader0 + s * 8), "r"(0), "r"(qb * CV_TQ), "r"(pb * CV_TP), "r"(cc * 8), "r"(n)
+                     : "memory");
+      }
+    }
+  } else if (warp == 1 && lane == 0 && leader) {
+    // ---------------- MMA issuer (leader): M = 256 (two tiles) x N = BN
+    constexpr uint32_t idesc = tc::instr_desc(2, 0, 0, 2 * CV_BM, BN);
+    tc::mbar_wait(bfull, 0);
+    uint32_t it = 0, tl = 0;
+    for (int x = pair; x < npairs_tiles; x += npairs, ++tl) {
+      const uint32_t acc = tl & 1;
+      if (tl >= 2) tc::mbar_wait(&tempty[acc], ((tl / 2) - 1) & 1);
+      tc::tc_fence_after();
+      const uint32_t dtm = tmem + acc * BN;
+      bool first = true;
+      for (int cc = 0; cc < chunks; ++cc, ++it) {
+        const uint32_t s = it % PSTAGES;
+        tc::mbar_wait(&full[s], (it / PSTAGES) & 1);
+        tc::tc_fence_after();
+        const uint32_t sp = tc::smem_u32(sP + s * patch_slot);
+        for (int r = 0; r < g.R; ++r)
+          for (int ss = 0; ss < g.S; ++ss) {
+            const uint32_t tap = sp + static_cast<uint32_t>(r * g.WQ + ss) * 16;
+            const uint32_t sb = tc::smem_u32(sB + static_cast<size_t>((r * g.S + ss) * chunks + cc) * B_BYTES);
+#pragma unroll
+            for (int j = 0; j < CV_BKE / 8; ++j) {
+              const uint64_t da = nosw_desc(tap + 2 * j * g.plane, g.lbo, g.sbo);
+              const uint64_t db = tc::sw128_desc(sb + j * 32, 16, 1024);
+              asm volatile(
+                  "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                  "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtm), "l"(da), "l"(db),
+                  "r"(idesc), "r"(first ? 0u : 1u));
+              first = false;
+            }
+          }
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                     ::"r"(tc::smem_u32(&empty[s])), "h"(static_cast<uint16_t>(3)) : "memory");
+      }
+      asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                   ::"r"(tc::smem_u32(&tfull[acc])), "h"(static_cast<uint16_t>(3)) : "memory");
+    }
+  } else if (warp >= 2) {
+    // ---------------- epilogue (both CTAs): own tile, own 128 TMEM lanes
+    const int q = warp & 3;
+    const uint32_t stg = tc::smem_u32(stage_base) + static_cast<uint32_t>(warp - 2) * (32 * 33 * 4 + 32 * 8);
+    const uint32_t rtab = stg + 32 * 33 * 4;
+    const uint32_t tempty_leader0 = cv_peer(tc::smem_u32(&tempty[0]), 0);
+    uint32_t tl = 0;
+    for (int x = pair; x < npairs_tiles; x += npairs, ++tl) {
+      const int tr = 2 * x + static_cast<int>(rank);
+      const bool mine = tr < ntiles;
+      const int t = mine ? tr : ntiles - 1;
+      const int n = t / per_img, rem = t % per_img, pb = rem / g.qblocks, qb = rem % g.qblocks;
+      const uint32_t acc = tl & 1;
+      const int m = q * 32 + lane, p = pb * CV_TP + m / CV_TQ, qq = qb * CV_TQ + m % CV_TQ;
+      const int64_t rowoff = (mine && p < g.P) ? n * g.on + p * g.op + qq * g.oq : -1;
+      asm volatile("st.shared.s64 [%0], %1;" ::"r"(rtab + lane * 8), "l"(rowoff) : "memory");
+      tc::mbar_wait(&tfull[acc], (tl / 2) & 1);
+      tc::tc_fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t rv[32];
+        tc::tmem_ld32(tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c0), rv);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          asm volatile("st.shared.b32 [%0], %1;" ::"r"(stg + (lane * 33 + j) * 4), "r"(rv[j]) : "memory");
+        __syncwarp();
+        float* cc = g.O + c0 + lane;
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) {
+          int64_t ro;
+          float v;
+          asm volatile("ld.shared.s64 %0, [%1];" : "=l"(ro) : "r"(rtab + rr * 8) : "memory");
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(stg + (rr * 33 + lane) * 4) : "memory");
+          if (ro >= 0) __stcs(cc + ro, v);
+        }
+        __syncwarp();
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty_leader0 + acc * 8) : "memory");
+    }
+  }
+  tc::tc_fence_before();
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -249,7 +436,7 @@ class ConvRoutine final : public Routine {
   double bytes() const override { return static_cast<double>(p_.in_bytes + p_.out_bytes); }
   std::string describe() const override {
     std::ostringstream os;
-    os << "{\"kernel\": \"tc_conv_tf32<" << a_.K << ">\", \"math\": \"tf32\", \"M\": "
+    os << "{\"kernel\": \"" << (two_sm_ ? "tc_conv_2sm<" : "tc_conv_tf32<") << a_.K << ">\", \"math\": \"tf32\", \"M\": "
        << static_cast<int64_t>(a_.N) * a_.P * a_.Q << ", \"N\": " << a_.K << ", \"K\": " << a_.R * a_.S * a_.C
        << ", \"tile\": \"16 p x 8 q x " << a_.K << " k\", \"patch\": [" << a_.HP << ", " << a_.WQ << ", 32]"
        << ", \"taps_per_patch\": " << a_.R * a_.S << ", \"tiles\": " << static_cast<int64_t>(a_.N) * a_.pblocks * a_.qblocks
@@ -289,10 +476,23 @@ class ConvRoutine final : public Routine {
     const char* swap = std::getenv("MDHB_CONV_SWAP_LBO");
     a_.lbo = swap ? static_cast<uint32_t>(16 * a_.WQ) : a_.plane;
     a_.sbo = swap ? a_.plane : static_cast<uint32_t>(16 * a_.WQ);
+    // pixel-major 128B-swizzled patch (shifted taps need no base offset: the
+    // swizzle follows absolute smem address bits) -- bit-exact, measured
+    // slower than the [c-group][p][q][4c] layout; selectable (MDHB_CONV_SW128=1)
+    a_.sw = std::getenv("MDHB_CONV_SW128") ? 1 : 0;
+    a_.bo_mode = std::getenv("MDHB_CONV_BO") ? std::atoi(std::getenv("MDHB_CONV_BO")) : 0;
+    if (a_.sw && (a_.WQ * 128) / 16 >= (1 << 14)) a_.sw = 0;
     const int ktiles = a_.R * a_.S * (a_.C / CV_BKE);
     const size_t patch_slot = (8 * static_cast<size_t>(a_.plane) + 1023) / 1024 * 1024;
     smem_ = static_cast<size_t>(ktiles) * a_.K * CV_BKE * 4 + 2 * patch_slot + 256 + 4 * (32 * 33 * 4 + 32 * 8) + 1024;
     if (smem_ > 227 * 1024) return *why = "conv instance: filter + patches exceed shared memory", false;
+    // CTA-pair instance: half the filter per CTA, 3 patch stages
+    smem2_ = ((static_cast<size_t>(ktiles) * (a_.K / 2) * CV_BKE * 4 + 1023) / 1024 * 1024) + 3 * patch_slot + 256 +
+             4 * (32 * 33 * 4 + 32 * 8) + 1024;
+    // measured slower than the single-CTA kernel at conv2_x (0.242 vs 0.221 ms:
+    // N = 64 leaves the pair's saved B bandwidth small next to the extra
+    // cross-CTA synchronisation); selectable with MDHB_CONV_2SM=1
+    two_sm_ = smem2_ <= 227 * 1024 && std::getenv("MDHB_CONV_2SM") && !std::getenv("MDHB_TC_1SM") && !a_.sw;
     if (a_.plane / 16 >= (1u << 14)) return *why = "conv instance: patch plane too large for a descriptor", false;
     // input and filter extents for the tensor maps
     H_ = ie[1];
@@ -314,11 +514,25 @@ class ConvRoutine final : public Routine {
                             static_cast<cuuint64_t>(a_.C / 4), static_cast<cuuint64_t>(a_.N)};
       cuuint64_t strides[4] = {static_cast<cuuint64_t>(a_.C) * 4, static_cast<cuuint64_t>(W_ * a_.C) * 4, 16,
                                static_cast<cuuint64_t>(H_ * W_ * a_.C) * 4};
+      if (a_.sw) {
+        // pixel-major: {C, W, H, N}, box {32 c, WQ, HP, 1}, 128-byte swizzle
+        cuuint64_t d4[4] = {static_cast<cuuint64_t>(a_.C), static_cast<cuuint64_t>(W_), static_cast<cuuint64_t>(H_),
+                            static_cast<cuuint64_t>(a_.N)};
+        cuuint64_t s4[3] = {static_cast<cuuint64_t>(a_.C) * 4, static_cast<cuuint64_t>(W_ * a_.C) * 4,
+                            static_cast<cuuint64_t>(H_ * W_ * a_.C) * 4};
+        cuuint32_t b4[4] = {CV_BKE, static_cast<cuuint32_t>(a_.WQ), static_cast<cuuint32_t>(a_.HP), 1};
+        cuuint32_t e4[4] = {1, 1, 1, 1};
+        CUresult r4 = conv_encoder()(&mi_, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(I), d4, s4, b4, e4,
+                                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r4 != CUDA_SUCCESS) fail("CudaError", "cuTensorMapEncodeTiled (conv input, swizzled) failed");
+      }
       cuuint32_t box[5] = {4, static_cast<cuuint32_t>(a_.WQ), static_cast<cuuint32_t>(a_.HP), 8, 1};
       cuuint32_t es[5] = {1, 1, 1, 1, 1};
-      CUresult r = conv_encoder()(&mi_, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<void*>(I), dims, strides, box, es,
-                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      CUresult r = a_.sw ? CUDA_SUCCESS
+                         : conv_encoder()(&mi_, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<void*>(I), dims, strides, box,
+                                          es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r != CUDA_SUCCESS) fail("CudaError", "cuTensorMapEncodeTiled (conv input) failed (" + std::to_string(static_cast<int>(r)) + ")");
       last_i_ = I;
     }
@@ -331,11 +545,36 @@ class ConvRoutine final : public Routine {
                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r != CUDA_SUCCESS) fail("CudaError", "cuTensorMapEncodeTiled (conv filter) failed (" + std::to_string(static_cast<int>(r)) + ")");
+      box[1] = static_cast<cuuint32_t>(a_.K / 2);  // the CTA pair's filter halves
+      r = conv_encoder()(&mf2_, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(F), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) fail("CudaError", "cuTensorMapEncodeTiled (conv filter half) failed (" + std::to_string(static_cast<int>(r)) + ")");
       last_f_ = F;
     }
     ConvArgs a = a_;
     a.O = static_cast<float*>(d_out[0]);
     const int sms = sm_count(p_.opt.device);
+    if (two_sm_) {
+      const int64_t tiles = static_cast<int64_t>(a_.N) * a_.pblocks * a_.qblocks;
+      const int pairs = static_cast<int>(std::min<int64_t>(sms / 2, (tiles + 1) / 2));
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3(static_cast<unsigned>(2 * pairs));
+      lc.blockDim = dim3(192);
+      lc.dynamicSmemBytes = smem2_;
+      lc.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      auto k = tc_conv_2sm<64, 3>;
+      MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2_)));
+      MDHB_CUDA(cudaLaunchKernelEx(&lc, k, mi_, mf2_, a));
+      return;
+    }
     const int64_t tiles = static_cast<int64_t>(a_.N) * a_.pblocks * a_.qblocks;
     auto k = tc_conv_tf32<64>;
     MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_)));
@@ -348,8 +587,9 @@ class ConvRoutine final : public Routine {
   int ib_, fb_;
   ConvArgs a_{};
   int64_t H_ = 0, W_ = 0, FK_ = 0;
-  size_t smem_ = 0;
-  CUtensorMap mi_{}, mf_{};
+  size_t smem_ = 0, smem2_ = 0;
+  bool two_sm_ = false;
+  CUtensorMap mi_{}, mf_{}, mf2_{};
   const void* last_i_ = nullptr;
   const void* last_f_ = nullptr;
 };

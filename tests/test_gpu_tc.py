@@ -15,10 +15,10 @@ CASES = [
     ("matmul_fp32", [128, 256, 64], "tc_gemm_tf32<256"),
     ("matmul_fp32", [256, 512, 96], "tc_gemm_tf32<256"),
     ("matmul_fp32", [128, 128, 32], "tc_gemm_tf32<128"),
-    ("mcc_nhwc", [2, 8, 8, 64, 3, 3, 64], "tc_conv_tf32<64"),      # P padded 8 -> 16
-    ("mcc_nhwc", [4, 16, 8, 64, 3, 3, 32], "tc_conv_tf32<64"),
-    ("mcc_nhwc", [3, 20, 16, 64, 3, 3, 64], "tc_conv_tf32<64"),     # 2 p-blocks, ragged
-    ("mcc_nhwc", [2, 16, 16, 64, 1, 1, 32], "tc_conv_tf32<64"),     # 1x1 taps
+    ("mcc_nhwc", [2, 8, 8, 64, 3, 3, 64], "tc_conv"),      # P padded 8 -> 16
+    ("mcc_nhwc", [4, 16, 8, 64, 3, 3, 32], "tc_conv"),
+    ("mcc_nhwc", [3, 20, 16, 64, 3, 3, 64], "tc_conv"),     # 2 p-blocks, ragged
+    ("mcc_nhwc", [2, 16, 16, 64, 1, 1, 32], "tc_conv"),     # 1x1 taps
     # packed K-major operands (views no TMA box describes; K padded to 32)
     ("ccsdt_abcdef_gdab_efgc", [4, 4, 8, 8, 8, 4, 72], "tc_gemm_tf32<256"),
     ("ccsdt_abcdef_gdab_efgc", [8, 4, 4, 4, 8, 4, 40], "tc_gemm_tf32<128"),
@@ -148,3 +148,18 @@ def test_tf32_ccsdt_full_slices_exact():
         ((part, dfd),), shifts = mo.execute_box(comp, ins, box)
         sl = tuple(slice(s, s + n) for s, n in zip(shifts[0], part.shape))
         assert np.array_equal(out[sl].cpu().numpy().astype(np.float64)[dfd], part[dfd]), box
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env", ["MDHB_CONV_2SM", "MDHB_CONV_SW128"])
+def test_tf32_conv_variants_bit_identical(env, monkeypatch):
+    """CTA-pair conv (cta_group::2, filter halves) and the swizzled pixel-major
+    patch layout give the default conv instance's bits."""
+    j = spec("mcc_nhwc", [3, 20, 16, 64, 3, 3, 64])
+    comp = mo.Computation.from_json(j)
+    ins = exact_inputs(comp, 12)
+    (base,) = run_device(plan_tf32(j), ins)
+    monkeypatch.setenv(env, "1")
+    p = plan_tf32(j)
+    (var,) = run_device(p, ins)
+    assert np.array_equal(base, var), p.describe()
