@@ -332,9 +332,12 @@ def main():
     import torch
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
-    device = local
+        # MDHB_BENCH_BACKEND=gloo + fewer GPUs than ranks exercises the N>1
+        # path on one GPU (test aid); the real run is NCCL, one rank per GPU
+        backend = os.environ.get("MDHB_BENCH_BACKEND", "nccl")
+        torch.cuda.set_device(local % torch.cuda.device_count())
+        dist.init_process_group(backend)
+    device = local % torch.cuda.device_count()
     torch.cuda.set_device(device)
     pk = peaks()
 
@@ -412,7 +415,7 @@ def max_over_ranks(x, world):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
