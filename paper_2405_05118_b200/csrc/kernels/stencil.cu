@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(NTHREADS, 3) star7_kernel(StencilArgs a) {
 #endif
 constexpr int NSLOT = MDHB_STENCIL_NSLOT;  // ring slots
 constexpr int PD = NSLOT - 1;            // planes in flight ahead of compute
-constexpr int BPITCH = TK + 12;          // floats per smem row: 128 + halo 2 + shift <= 3, 16B rounded
+constexpr int BPITCH = TK + 8;           // floats per smem row: 128 + halo 2 + shift <= 3, 16B rounded
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
@@ -493,10 +493,14 @@ __device__ __forceinline__ void ld4c(const float* row, int sh, float (&x)[4]) {
   }
 }
 
-template <int NS, int MINB>
+// TS variant: every warp stages its two output rows of the plane in shared
+// memory and its lane 0 writes them with two 512-byte bulk copies
+// (cp.async.bulk.global.shared::cta), double-buffered per warp -- the store
+// traffic leaves the LSU / L1 path for the TMA engine.  Full tiles only.
+template <int NS, int MINB, bool TS>
 __global__ void __launch_bounds__(WS_THREADS, MINB) star7_lean(StencilArgs a) {
   constexpr int TJ = 16, ROWS = TJ + 2;
-  extern __shared__ __align__(128) float sring[];  // [NS][ROWS][BPITCH]
+  extern __shared__ __align__(128) float sring[];  // [NS][ROWS][BPITCH] (+ TS: [8 warps][2 bufs][2 rows][TK])
   __shared__ __align__(8) uint64_t full[NS], empty[NS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t k0 = static_cast<int64_t>(blockIdx.x) * TK;
@@ -563,7 +567,14 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) star7_lean(StencilArgs a) {
   const int64_t wplane = a.n1 * a.n2;
   const bool kin = k0 + kl + 4 <= a.n2;
 
+  // TS: this warp's output staging, 2 buffers x 2 rows x TK floats
+  float* sout = sring + static_cast<size_t>(NS) * ROWS * BPITCH + static_cast<size_t>(warp) * 4 * TK;
   auto step = [&](int t, const Rows4& P, const Rows4& C, Rows4& N) {
+    if (TS) {
+      // the bulk store issued two steps ago from this buffer must have read it
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      __syncwarp();
+    }
     mbar_wait_parity(&full[(t + 2) % NS], static_cast<uint32_t>(((t + 2) / NS) & 1));
     load_centre(t + 2, N);
     float jm[4], jp[4], hl[2], hr[2];
@@ -598,10 +609,25 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) star7_lean(StencilArgs a) {
         o[kk] = acc;
       }
       const int64_t j = j0 + jl + jj;
-      if (j < a.n1 && kin) {
+      if (TS) {
+        *reinterpret_cast<float4*>(sout + ((t & 1) * 2 + jj) * TK + kl) = make_float4(o[0], o[1], o[2], o[3]);
+      } else if (j < a.n1 && kin) {
         __stcs(reinterpret_cast<float4*>(wout + t * wplane + jj * a.n2), make_float4(o[0], o[1], o[2], o[3]));
       } else if (j < a.n1) {
         for (int kk = 0; kk < 4 && k0 + kl + kk < a.n2; ++kk) wout[t * wplane + jj * a.n2 + kk] = o[kk];
+      }
+    }
+    if (TS) {
+      // generic-proxy writes -> async proxy, then lane 0 ships both rows
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj)
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                       ::"l"(wout - kl + t * wplane + jj * a.n2), "r"(s_u32(sout + ((t & 1) * 2 + jj) * TK)),
+                       "r"(static_cast<uint32_t>(TK * 4)) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     }
   };
@@ -620,6 +646,7 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) star7_lean(StencilArgs a) {
   }
   if (t < iend) step(t, R0, R1, R2), ++t;
   if (t < iend) step(t, R1, R2, R0), ++t;
+  if (TS && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -828,7 +855,8 @@ class StencilRoutine final : public Routine {
   const char* family() const override { return "stencil"; }
   std::string describe() const override {
     std::ostringstream os;
-    const std::string kname = lean_ ? "star7_lean<" + std::to_string(lean_ / 10) + "," + std::to_string(lean_ % 10) + ">"
+    const std::string kname = lean_ && ts_ok() ? std::string("star7_lean<4,4,tma_store>")
+                              : lean_ ? "star7_lean<" + std::to_string(lean_ / 10) + "," + std::to_string(lean_ % 10) + ">"
                                     : std::string(pers_ ? "star7_pers<" : ws_ ? "star7_ws<" : bulk_ ? "star7_bulk<" : "star7_kernel<") +
                                           std::to_string(tj_) + ">";
     os << "{\"kernel\": \"" << kname << "\", \"TK\": " << TK << ", \"TJ\": " << tj_ << ", \"TI\": " << a_.ti
@@ -927,12 +955,15 @@ class StencilRoutine final : public Routine {
       kern<<<grid_p, WS_THREADS, smem, s>>>(a, tiles_k, total, mode);
     } else if (lean_) {
       void (*k)(StencilArgs) = nullptr;
-      if (lean_ == 53) k = star7_lean<5, 3>;
-      else if (lean_ == 54) k = star7_lean<5, 4>;
-      else if (lean_ == 44) k = star7_lean<4, 4>;
-      else if (lean_ == 45) k = star7_lean<4, 5>;
-      else k = star7_lean<6, 3>;
-      const size_t lsmem = static_cast<size_t>(lean_ / 10) * 18 * BPITCH * sizeof(float);
+      const bool ts = ts_ok();
+      if (ts) k = star7_lean<4, 4, true>;
+      else if (lean_ == 53) k = star7_lean<5, 3, false>;
+      else if (lean_ == 54) k = star7_lean<5, 4, false>;
+      else if (lean_ == 44) k = star7_lean<4, 4, false>;
+      else if (lean_ == 45) k = star7_lean<4, 5, false>;
+      else k = star7_lean<6, 3, false>;
+      const size_t lsmem = static_cast<size_t>(ts ? 4 : lean_ / 10) * 18 * BPITCH * sizeof(float) +
+                           (ts ? static_cast<size_t>(8) * 4 * TK * sizeof(float) : 0);
       MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lsmem)));
       k<<<grid(), WS_THREADS, lsmem, s>>>(a);
     } else if (ws_) {
@@ -960,6 +991,10 @@ class StencilRoutine final : public Routine {
   int minb_ = std::getenv("MDHB_STENCIL_MINB") ? std::atoi(std::getenv("MDHB_STENCIL_MINB")) : 2;
   // lean-register variant (default): 5 ring slots, 4 CTAs per SM (NS*10+MINB; 0 = star7_ws)
   int lean_ = std::getenv("MDHB_STENCIL_LEAN") ? std::atoi(std::getenv("MDHB_STENCIL_LEAN")) : 54;
+  // TMA-store variant: full tiles, 16-byte aligned output rows (MDHB_STENCIL_TS=1)
+  bool ts_ok() const {
+    return std::getenv("MDHB_STENCIL_TS") && a_.n2 % TK == 0 && a_.n1 % 16 == 0 && (a_.n2 * 4) % 16 == 0;
+  }
 };
 
 }  // namespace

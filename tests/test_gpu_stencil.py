@@ -69,7 +69,7 @@ def test_jacobi3d_host_pipeline_equals_device_run(sizes):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("env", ["0", "63", "44"])
+@pytest.mark.parametrize("env", ["0", "63", "44", "ts"])
 def test_jacobi3d_variants_bit_identical(env, monkeypatch):
     """Every stencil kernel variant (star7_ws, lean-register rings) computes
     the same bits: same FMA order per output cell."""
@@ -78,7 +78,10 @@ def test_jacobi3d_variants_bit_identical(env, monkeypatch):
     comp = mo.Computation.from_json(j)
     ins = uniform_inputs(comp, 5)
     (base,) = run_device(mdh.Plan(j), ins)
-    monkeypatch.setenv("MDHB_STENCIL_LEAN", env)
+    if env == "ts":
+        monkeypatch.setenv("MDHB_STENCIL_TS", "1")  # TMA bulk stores (full tiles: 48 x 384 qualify)
+    else:
+        monkeypatch.setenv("MDHB_STENCIL_LEAN", env)
     plan = mdh.Plan(j)
     assert plan.describe()["template"]["kernel"].startswith("star7_ws" if env == "0" else "star7_lean"), plan.describe()
     (var,) = run_device(plan, ins)
