@@ -1374,12 +1374,8 @@ std::unique_ptr<Routine> make_contraction(const Problem& p, const Config* cfg, C
   const MdHom& e = p.e;
   std::string tc_why;
   if (p.opt.math != Math::FFMA) {
-    if (p.opt.math == Math::TF32) {
-      auto tc = make_tc_contraction(p, g, cfg, cfg_out, &tc_why);
-      if (tc) return tc;
-    } else {
-      tc_why = "BF16 operands need a conversion pass (not instantiated)";
-    }
+    auto tc = make_tc_contraction(p, g, cfg, cfg_out, &tc_why);
+    if (tc) return tc;
   }
   auto r = std::make_unique<GemmRoutine>(p, g);
   r->note_ = tc_why;

@@ -18,6 +18,7 @@
 // Pipelines: STAGES smem slots (full/empty mbarriers), one accumulator
 // (BM = 128 lanes x BN fp32 columns of TMEM).
 #include <cuda.h>
+#include <cuda_bf16.h>
 
 #include <algorithm>
 #include <array>
@@ -246,12 +247,52 @@ __global__ void __launch_bounds__(256) pack_kmajor(const float* __restrict__ src
 __host__ __device__ constexpr int epi_warps(bool rb, int bn) { return rb || bn >= 256 ? 4 : 8; }
 __host__ __device__ constexpr size_t epi_bytes(bool rb, int bn) { return epi_warps(rb, bn) * (32 * 33 * 4 + 32 * 8); }
 
+// bf16 packing (MATH_BF16): the same gather, converting to bf16 (round to
+// nearest even).  k-fast: consecutive threads walk k (coalesced when k is the
+// operand's unit-stride direction).  row-fast: a 32 x 32 (row, k) block goes
+// through shared memory so that reads walk the rows (MatMul's B[k][n]) and
+// writes walk k.
+__global__ void __launch_bounds__(256) pack_kmajor_bf16(const float* __restrict__ src, uint16_t* __restrict__ dst,
+                                                        const int32_t* __restrict__ tile_off, const int32_t* __restrict__ row_off,
+                                                        const int32_t* __restrict__ k_off, int rows, int K, int Kp, int64_t total) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x; i < total; i += static_cast<int64_t>(gridDim.x) * 256) {
+    const int k = static_cast<int>(i % Kp);
+    const int64_t rr = i / Kp;
+    const int r = static_cast<int>(rr % rows);
+    const int64_t t = rr / rows;
+    const float v = k < K ? __ldg(src + tile_off[t] + row_off[r] + k_off[k]) : 0.f;
+    dst[i] = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+  }
+}
+__global__ void __launch_bounds__(256) pack_rows_bf16(const float* __restrict__ src, uint16_t* __restrict__ dst,
+                                                      const int32_t* __restrict__ tile_off, const int32_t* __restrict__ row_off,
+                                                      const int32_t* __restrict__ k_off, int rows, int K, int Kp, int64_t n_rows) {
+  __shared__ float t[32][33];
+  const int k0 = blockIdx.x * 32;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+  for (int kk = ty; kk < 32; kk += 8) {  // read: lanes along rows
+    const int64_t gr = r0 + tx;
+    const int k = k0 + kk;
+    float v = 0.f;
+    if (gr < n_rows && k < K) v = __ldg(src + tile_off[gr / rows] + row_off[gr % rows] + k_off[k]);
+    t[kk][tx] = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int rr = ty; rr < 32; rr += 8) {  // write: lanes along k
+    const int64_t gr = r0 + rr;
+    if (gr < n_rows) dst[gr * Kp + k0 + tx] = __bfloat16_as_ushort(__float2bfloat16_rn(t[tx][rr]));
+  }
+}
+
 // Persistent variant: one CTA per SM walks the tile list; two TMEM
 // accumulators (2 x BN columns) let the epilogue warps drain tile i while
 // the MMA warp already accumulates tile i+1.  With RB (resident B) the whole
 // K extent of B for the single N tile is loaded once per CTA and stays in
 // shared memory -- MCC's 147 KB filter -- so only A streams from HBM.
-template <int BN, int STAGES, bool B_MN, bool RB>
+template <int BN, int STAGES, bool B_MN, bool RB, bool BF16 = false>
 __global__ void __launch_bounds__(64 + 32 * epi_warps(RB, BN), 1)
     tc_gemm_pers(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, TcArgs g) {
   constexpr uint32_t A_BYTES = BM * BKE * 4;
@@ -374,7 +415,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps(RB, BN), 1)
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer
-    constexpr uint32_t idesc = tc::instr_desc(2, 0, B_MN ? 1 : 0, BM, BN);
+    constexpr uint32_t idesc = tc::instr_desc(BF16 ? 1 : 2, 0, B_MN ? 1 : 0, BM, BN);  // kind::f16 bf16 | kind::tf32
     if (RB) tc::mbar_wait(bfull, 0);
     uint32_t it = 0, tl = 0;
     for (int x = blockIdx.x; x < ntiles; x += gridDim.x, ++tl) {
@@ -392,7 +433,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps(RB, BN), 1)
         for (int k = 0; k < BKE / 8; ++k) {
           const uint64_t da = tc::sw128_desc(sa + k * 32, 16, 1024);
           const uint64_t db = B_MN ? tc::umma_desc(sb + k * 1024, BKE * 128, 512, 1) : tc::sw128_desc(sb + k * 32, 16, 1024);
-          tc::mma<true>(dtm, da, db, idesc, (kt | k) != 0 ? 1u : 0u);
+          tc::mma<!BF16>(dtm, da, db, idesc, (kt | k) != 0 ? 1u : 0u);
         }
         tc::mma_commit(&empty[s]);
       }
@@ -491,7 +532,7 @@ __device__ __forceinline__ void tma_load_2sm(void* dst, const void* tmap, uint32
   }
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool BF16 = false>
 __global__ void __launch_bounds__(64 + 32 * 4, 1)
     tc_gemm_2sm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, TcArgs g, int b_row_rank) {
   constexpr int EPW = 4;
@@ -597,7 +638,7 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
     }
   } else if (warp == 1 && lane == 0 && leader) {
     // ---------------- MMA issuer (leader only): M = 256 across the pair
-    constexpr uint32_t idesc = tc::instr_desc(2, 0, 0, 2 * BM, BN);
+    constexpr uint32_t idesc = tc::instr_desc(BF16 ? 1 : 2, 0, 0, 2 * BM, BN);
     uint32_t it = 0, tl = 0;
     for (int x = pair; x < ntiles; x += npairs, ++tl) {
       const uint32_t acc = tl & 1;
@@ -615,10 +656,16 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
           const uint64_t da = tc::sw128_desc(sa + k * 32, 16, 1024);
           const uint64_t db = tc::sw128_desc(sb + k * 32, 16, 1024);
           const uint32_t accum = (kt | k) != 0 ? 1u : 0u;
-          asm volatile(
-              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtm), "l"(da), "l"(db), "r"(idesc),
-              "r"(accum));
+          if (BF16)
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtm), "l"(da), "l"(db), "r"(idesc),
+                "r"(accum));
+          else
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtm), "l"(da), "l"(db), "r"(idesc),
+                "r"(accum));
         }
         asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
                      ::"r"(tc::smem_u32(&empty[s])), "h"(static_cast<uint16_t>(3)) : "memory");
@@ -700,6 +747,7 @@ struct View {
   std::vector<int> row_dims;          // smem row order (outer -> inner)
   std::vector<int64_t> row_box;
   bool mn = false;                    // MN-major (slabs of 32 along the inner row dim)
+  bool bf16 = false;                  // packed bf16 operand (64 elements per 128-byte row)
   int kin = -1;                       // the K dim stepped by 32 per k-tile
   std::vector<std::vector<int64_t>> coef;  // [TMA rank][dim]
   std::vector<int64_t> c0;            // [TMA rank]
@@ -829,14 +877,15 @@ class TcRoutine final : public Routine {
  os << "{\"kernel\": \"" << (two_sm_ ? "tc_gemm_2sm<" : pers_ ? "tc_gemm_pers<" : "tc_gemm_tf32<") << BN_ << ","
        << (two_sm_ ? st2_ : pers_ ? pstages_ : stages_) << ","
        << (va_.mn ? "A_MN" : "A_K") << "," << (vb_.mn ? "B_MN" : "B_K") << (rb_ && pers_ ? ",B_RESIDENT" : "")
-       << ">\", \"math\": \"tf32\", \"M\": " << M_ << ", \"N\": " << N_ << ", \"K\": " << K_
+       << ">\", \"math\": \"" << (bf16_ ? "bf16" : "tf32") << "\", \"M\": " << M_ << ", \"N\": " << N_ << ", \"K\": " << K_
        << ", \"BM\": " << BM << ", \"BN\": " << BN_ << ", \"BK\": " << BKE << ", \"stages\": " << stages_
-       << ", \"umma\": \"tcgen05.mma.cta_group::1.kind::tf32 M128xN" << BN_ << "xK8\", \"tiles\": "
+       << ", \"umma\": \"tcgen05.mma.cta_group::1.kind::" << (bf16_ ? "f16 (bf16) M128xN" : "tf32 M128xN") << BN_
+       << (bf16_ ? "xK16" : "xK8") << "\", \"tiles\": "
        << static_cast<int64_t>(tilesM_) * tilesN_ << ", \"tmem_cols\": " << BN_
        << ", \"b_layout\": \"" << (packed_ ? "packed K-major (pack_kmajor pre-pass, both operands)" : transposeB_ ? "K-major copy (layout_de [2,1] pre-pass)" : (vb_.mn ? "MN-major" : "K-major"))
        << "\"";
     if (packed_) os << ", \"K_padded\": " << Kp_;
-    if (two_sm_) os << ", \"cta_pair\": \"tc_gemm_2sm<" << BN_ << "," << st2_ << ">: tcgen05.mma.cta_group::2 M256xN" << BN_ << "xK8\"";
+    if (two_sm_) os << ", \"cta_pair\": \"tc_gemm_2sm<" << BN_ << "," << st2_ << ">: tcgen05.mma.cta_group::2 M256xN" << BN_ << (bf16_ ? "xK16 (bf16)" : "xK8") << "\"";
     os << "}";
     return os.str();
   }
@@ -847,6 +896,8 @@ class TcRoutine final : public Routine {
     N_ = prod_sizes(e, g_.Nd);
     K_ = prod_sizes(e, g_.Kd);
     std::string w;
+    bf16_ = p_.opt.math == Math::BF16;
+    if (bf16_) return setup_packed(BN, why);  // operands converted + packed (layout_de) for kind::f16
     if (!describe_view(p_, g_.a_buf, g_.Md, g_.Kd, BM, false, va_, &w) ||
         !describe_view(p_, g_.b_buf, g_.Nd, g_.Kd, BN, true, vb_, &w) || va_.kin != vb_.kin) {
       if (setup_packed(BN, why)) return true;
@@ -1013,8 +1064,10 @@ class TcRoutine final : public Routine {
     const MdHom& e = p_.e;
     std::vector<int64_t> Tm = factor_box(e, g_.Md, BM), Tn = factor_box(e, g_.Nd, BN);
     if (Tm.empty() || Tn.empty()) return *why = "row tiles cannot be formed", false;
-    Kp_ = (K_ + BKE - 1) / BKE * BKE;
-    if ((M_ + N_) * Kp_ * 4 > (int64_t(1) << 30)) return *why = "packed operands exceed 1 GiB", false;
+    const int ek = bf16_ ? 2 * BKE : BKE;  // elements per 128-byte k-tile row
+    const int esz = bf16_ ? 2 : 4;
+    Kp_ = (K_ + ek - 1) / ek * ek;
+    if ((M_ + N_) * Kp_ * esz > (int64_t(1) << 30)) return *why = "packed operands exceed 1 GiB", false;
     auto ones = [](size_t n) { return std::vector<int64_t>(n, 1); };
     auto grid_of = [&](const std::vector<int>& dims, const std::vector<int64_t>& T, std::vector<int64_t>& gext) {
       for (size_t q = 0; q < dims.size(); ++q) gext.push_back(e.sizes[static_cast<size_t>(dims[q])] / T[q]);
@@ -1035,7 +1088,7 @@ class TcRoutine final : public Routine {
     tilesN_ = static_cast<int>(tBn.size());
     BN_ = BN;
     stages_ = BN >= 256 ? 4 : (BN >= 128 ? 6 : 8);
-    nk_ = static_cast<int>(Kp_ / BKE);
+    nk_ = static_cast<int>(Kp_ / ek);
     auto view2 = [&](int buf, int64_t rows_total, int box_rows) {
       View v;
       v.buf = buf;
@@ -1043,8 +1096,9 @@ class TcRoutine final : public Routine {
       v.dims[0] = static_cast<cuuint64_t>(Kp_);
       v.dims[1] = static_cast<cuuint64_t>(rows_total);
       v.strides[0] = 4;
-      v.strides[1] = static_cast<cuuint64_t>(Kp_ * 4);
-      v.box[0] = BKE;
+      v.strides[1] = static_cast<cuuint64_t>(Kp_ * esz);
+      v.box[0] = static_cast<cuuint32_t>(ek);
+      v.bf16 = bf16_;
       v.box[1] = static_cast<cuuint32_t>(box_rows);
       v.mn = false;
       return v;
@@ -1053,7 +1107,7 @@ class TcRoutine final : public Routine {
     vb_ = view2(g_.b_buf, N_, BN);
     args_.nkd = 1;
     args_.kext[0] = nk_;
-    args_.kstep[0] = BKE;
+    args_.kstep[0] = ek;
     for (int t = 0; t < MAXR; ++t) args_.kca[0][t] = args_.kcb[0][t] = t == 0 ? 1 : 0;
     std::vector<int64_t> amc, bnc;
     for (int t = 0; t < tilesM_; ++t) for (int r = 0; r < MAXR; ++r) amc.push_back(r == 1 ? int64_t(t) * BM : 0);
@@ -1097,8 +1151,11 @@ class TcRoutine final : public Routine {
     args_.tilesM = tilesM_;
     args_.tilesN = tilesN_;
     args_.cvec = cvec_;
-    MDHB_CUDA(cudaMalloc(&pa_, static_cast<size_t>(M_ * Kp_) * 4));
-    MDHB_CUDA(cudaMalloc(&pb_, static_cast<size_t>(N_ * Kp_) * 4));
+    MDHB_CUDA(cudaMalloc(&pa_, static_cast<size_t>(M_ * Kp_) * esz));
+    MDHB_CUDA(cudaMalloc(&pb_, static_cast<size_t>(N_ * Kp_) * esz));
+    // bf16 packing reads along the operand's unit-stride direction
+    a_rowfast_ = bf16_ && am.size() > 1 && am[1] - am[0] == 1 && !(ak.size() > 1 && ak[1] - ak[0] == 1);
+    b_rowfast_ = bf16_ && bn.size() > 1 && bn[1] - bn[0] == 1 && !(bk.size() > 1 && bk[1] - bk[0] == 1);
     packed_ = true;
     smem_ = static_cast<size_t>(stages_) * (BM + BN) * BKE * 4 + 1024 + 256;
     rb_ = false;
@@ -1144,7 +1201,27 @@ class TcRoutine final : public Routine {
   void launch(const void* const* d_in, void* const* d_out, cudaStream_t s) override {
     const void* A = d_in[va_.buf];
     const void* B = d_in[vb_.buf];
-    if (packed_) {
+    if (packed_ && bf16_) {
+      const int sms = sm_count(p_.opt.device);
+      auto pack = [&](const void* src, void* dst, const int32_t* t, const int32_t* r, const int32_t* k, int rows, int64_t n_rows,
+                      bool rowfast) {
+        if (rowfast) {
+          dim3 g(static_cast<unsigned>(Kp_ / 32), static_cast<unsigned>((n_rows + 31) / 32));
+          pack_rows_bf16<<<g, 256, 0, s>>>(static_cast<const float*>(src), static_cast<uint16_t*>(dst), t, r, k, rows,
+                                            static_cast<int>(K_), static_cast<int>(Kp_), n_rows);
+        } else {
+          const int64_t tot = n_rows * Kp_;
+          pack_kmajor_bf16<<<static_cast<unsigned>(std::min<int64_t>(8 * sms, (tot + 255) / 256)), 256, 0, s>>>(
+              static_cast<const float*>(src), static_cast<uint16_t*>(dst), t, r, k, rows, static_cast<int>(K_),
+              static_cast<int>(Kp_), tot);
+        }
+        MDHB_CUDA(cudaGetLastError());
+      };
+      pack(A, pa_, pk_[0], pk_[1], pk_[2], BM, M_, a_rowfast_);
+      pack(B, pb_, pk_[3], pk_[4], pk_[5], BN_, N_, b_rowfast_);
+      A = pa_;
+      B = pb_;
+    } else if (packed_) {
       const int sms = sm_count(p_.opt.device);
       const int64_t ta = M_ * Kp_, tb = N_ * Kp_;
       pack_kmajor<<<static_cast<unsigned>(std::min<int64_t>(8 * sms, (ta + 255) / 256)), 256, 0, s>>>(
@@ -1190,7 +1267,8 @@ class TcRoutine final : public Routine {
       lc.attrs = at;
       lc.numAttrs = 1;
       void (*k)(const CUtensorMap, const CUtensorMap, TcArgs, int) =
-          BN_ == 256 ? tc_gemm_2sm<256, 6> : tc_gemm_2sm<128, 8>;
+          bf16_ ? (BN_ == 256 ? tc_gemm_2sm<256, 6, true> : tc_gemm_2sm<128, 8, true>)
+                : (BN_ == 256 ? tc_gemm_2sm<256, 6> : tc_gemm_2sm<128, 8>);
       MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2_)));
       MDHB_CUDA(cudaLaunchKernelEx(&lc, k, ma_, mb2_, a, b_row_rank_));
       return;
@@ -1200,7 +1278,7 @@ class TcRoutine final : public Routine {
       dim3 pgrid(static_cast<unsigned>(std::min(sms, tilesM_ * tilesN_)));
 #define MDHB_TCP(BNV, ST, MN, RBV)                                                                           \
   if (BN_ == BNV && vb_.mn == MN && rb_ == RBV && pstages_ == ST) {                                         \
-    auto k = tc_gemm_pers<BNV, ST, MN, RBV>;                                                                \
+    auto k = bf16_ ? tc_gemm_pers<BNV, ST, MN, RBV, true> : tc_gemm_pers<BNV, ST, MN, RBV, false>;          \
     MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(psmem_))); \
     k<<<pgrid, 64 + 32 * epi_warps(RBV, BNV), psmem_, s>>>(ma_, mb_, a);                                              \
     MDHB_CUDA(cudaGetLastError());                                                                          \
@@ -1231,7 +1309,8 @@ class TcRoutine final : public Routine {
  private:
   void encode(const View& v, const void* ptr, CUtensorMap* m) {
     cuuint32_t estr[MAXR] = {1, 1, 1, 1, 1};
-    CUresult r = encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, static_cast<cuuint32_t>(v.rank), const_cast<void*>(ptr),
+    CUresult r = encoder()(m, v.bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                           static_cast<cuuint32_t>(v.rank), const_cast<void*>(ptr),
                            v.dims, v.strides + 1, v.box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                            v.mn ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1260,6 +1339,7 @@ class TcRoutine final : public Routine {
   bool packed_ = false;
   int64_t Kp_ = 0, c_run_ = 1;
   bool two_sm_ = false;
+  bool bf16_ = false, a_rowfast_ = false, b_rowfast_ = false;
   int b_row_rank_ = 1, st2_ = 0;
   size_t smem2_ = 0;
   View vb2_;
@@ -1275,7 +1355,7 @@ std::unique_ptr<Routine> make_tc_contraction(const Problem& p, const Groups& g, 
   // N-tile menu; among the instances that set up, prefer a direct TMA view
   // over packed operands, then the longest contiguous run of C per tile row
   // (the epilogue's store width), then the wider tile.
-  {
+  if (p.opt.math == Math::TF32) {
     std::string w;
     if (auto conv = make_tc_conv(p, g, &w)) {
       if (cfg_out) *cfg_out = cfg ? *cfg : baseline_config(p.e, p.m);

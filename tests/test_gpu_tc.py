@@ -163,3 +163,66 @@ def test_tf32_conv_variants_bit_identical(env, monkeypatch):
     p = plan_tf32(j)
     (var,) = run_device(p, ins)
     assert np.array_equal(base, var), p.describe()
+
+
+BF16_CASES = [
+    ("matmul_fp32", [256, 512, 96]),
+    ("matmul_fp32", [512, 256, 200]),            # K padded to 256
+    ("ccsdt_abcdef_gdab_efgc", [4, 4, 8, 8, 8, 4, 72]),
+    ("mcc_nhwc", [2, 8, 8, 64, 3, 3, 64]),       # packed (im2col-free gather) operands
+]
+
+
+def plan_bf16(j):
+    from paper_2405_05118_b200 import mdh
+    return mdh.Plan(j, math=mdh.MATH_BF16)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,sizes", BF16_CASES)
+def test_bf16_exact_mode_bit_identical(name, sizes):
+    """k/4 inputs are exact in bf16 and every partial sum is exact in the FP32
+    accumulator: the BF16 tensor-core path is bit-identical to the oracle."""
+    j = spec(name, sizes)
+    comp = mo.Computation.from_json(j)
+    plan = plan_bf16(j)
+    d = plan.describe()
+    assert d["family"] == "contraction" and d["template"]["math"] == "bf16", d
+    ins = exact_inputs(comp, 4)
+    (got,) = run_device(plan, ins)
+    ((want, dfd),) = mo.execute(comp, ins)
+    assert np.array_equal(got.astype(np.float64)[dfd], want[dfd])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,sizes", BF16_CASES)
+def test_bf16_uniform_mode_bound(name, sizes):
+    """|d_ij| <= 2^-8 * sum_k |a_ik| |b_kj| (operands rounded to 8 significant
+    bits, FP32 accumulation) -- SURVEY 8(c)'s BF16 bound."""
+    j = spec(name, sizes)
+    comp = mo.Computation.from_json(j)
+    plan = plan_bf16(j)
+    ins = uniform_inputs(comp, 9)
+    (got,) = run_device(plan, ins)
+    ((want, dfd),) = mo.execute(comp, ins)
+    ((absw, _),) = mo.execute(comp, [np.abs(x) for x in ins])
+    err = np.abs(got.astype(np.float64) - want)
+    assert (err <= 2.0 ** -8 * absw + 1e-30)[dfd].all(), float((err / np.maximum(absw, 1e-30)).max())
+
+
+@pytest.mark.gpu
+def test_bf16_matmul_8192_rows_exact():
+    import torch
+    j = spec("matmul_fp32")
+    comp = mo.Computation.from_json(j)
+    plan = plan_bf16(j)
+    ins = exact_inputs(comp, 3)
+    d_in = plan.empty(0)
+    for t, x in zip(d_in, ins):
+        t.copy_(torch.from_numpy(x).to(t.dtype))
+    (out,) = plan.empty(1)
+    plan.run(d_in, [out])
+    torch.cuda.synchronize()
+    for lo in (0, 4097, 8191):
+        ((part, dfd),), sh = mo.execute_box(comp, ins, {0: (lo, lo + 1)})
+        assert np.array_equal(out[lo:lo + 1].cpu().numpy().astype(np.float64), part)
