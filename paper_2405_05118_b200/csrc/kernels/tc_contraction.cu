@@ -287,6 +287,74 @@ __global__ void __launch_bounds__(256) pack_rows_bf16(const float* __restrict__ 
   }
 }
 
+// Vectorised layout passes for plain 2-D operands (the MatMul case):
+//   transpose64<OutT>: dst[n][k] (pitch Kp, zero-padded past K) from src with
+//     n unit-stride and k stride sk -- 64 x 64 tiles, 16-byte reads along n,
+//     16-byte writes along k (4 fp32 or 8 bf16)
+//   convert_kvec_bf16: dst[r][k] (pitch Kp) from src rows of K contiguous
+//     floats (row stride sr) -- 8 k per thread, two 16-byte reads, one write
+template <typename OutT>
+__global__ void __launch_bounds__(256) transpose64(const float* __restrict__ src, int64_t sk, OutT* __restrict__ dst, int K,
+                                                   int N, int Kp) {
+  __shared__ float t[64][65];
+  const int k0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {  // 64 k-rows x 16 float4 along n
+    const int c = tid + 256 * i, kk = c >> 4, n4 = (c & 15) * 4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (k0 + kk < K && n0 + n4 + 3 < N) v = __ldcs(reinterpret_cast<const float4*>(src + (k0 + kk) * sk + n0 + n4));
+    t[kk][n4] = v.x;
+    t[kk][n4 + 1] = v.y;
+    t[kk][n4 + 2] = v.z;
+    t[kk][n4 + 3] = v.w;
+  }
+  __syncthreads();
+  constexpr int V = sizeof(OutT) == 4 ? 4 : 8;  // k per 16-byte store
+#pragma unroll
+  for (int i = 0; i < (64 * 64 / V) / 256; ++i) {
+    const int c = tid + 256 * i, nn = c / (64 / V), kq = (c % (64 / V)) * V;
+    if (n0 + nn >= N || k0 + kq >= Kp) continue;
+    OutT* d = dst + static_cast<int64_t>(n0 + nn) * Kp + k0 + kq;
+    if (sizeof(OutT) == 4) {
+      *reinterpret_cast<float4*>(d) = make_float4(t[kq][nn], t[kq + 1][nn], t[kq + 2][nn], t[kq + 3][nn]);
+    } else {
+      uint32_t w[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const __nv_bfloat162 b2 = __floats2bfloat162_rn(t[kq + 2 * h][nn], t[kq + 2 * h + 1][nn]);
+        w[h] = *reinterpret_cast<const uint32_t*>(&b2);
+      }
+      *reinterpret_cast<uint4*>(d) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+__global__ void __launch_bounds__(256) convert_kvec_bf16(const float* __restrict__ src, int64_t sr, uint16_t* __restrict__ dst,
+                                                         int K, int Kp, int64_t n_rows) {
+  const int per = Kp / 8;
+  const int64_t total = n_rows * per;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x; i < total; i += static_cast<int64_t>(gridDim.x) * 256) {
+    const int64_t r = i / per;
+    const int k = static_cast<int>(i - r * per) * 8;
+    float v[8];
+    if (k + 8 <= K) {
+      const float4 a = __ldcs(reinterpret_cast<const float4*>(src + r * sr + k));
+      const float4 b = __ldcs(reinterpret_cast<const float4*>(src + r * sr + k + 4));
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = k + j < K ? src[r * sr + k + j] : 0.f;
+    }
+    uint32_t w[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * h], v[2 * h + 1]);
+      w[h] = *reinterpret_cast<const uint32_t*>(&b2);
+    }
+    *reinterpret_cast<uint4*>(dst + r * Kp + k) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
 // Persistent variant: one CTA per SM walks the tile list; two TMEM
 // accumulators (2 x BN columns) let the epilogue warps drain tile i while
 // the MMA warp already accumulates tile i+1.  With RB (resident B) the whole
@@ -1156,6 +1224,33 @@ class TcRoutine final : public Routine {
     // bf16 packing reads along the operand's unit-stride direction
     a_rowfast_ = bf16_ && am.size() > 1 && am[1] - am[0] == 1 && !(ak.size() > 1 && ak[1] - ak[0] == 1);
     b_rowfast_ = bf16_ && bn.size() > 1 && bn[1] - bn[0] == 1 && !(bk.size() > 1 && bk[1] - bk[0] == 1);
+    // plain 2-D operands (global row r = t*rows + local at base + r*sr, k at k*sk):
+    // vectorised convert (sk == 1) or 64x64 transposing convert (sr == 1)
+    auto plain = [](const std::vector<int64_t>& toff, const std::vector<int64_t>& roff, const std::vector<int64_t>& koff,
+                    int64_t& base, int64_t& sr, int64_t& sk) {
+      if (roff.size() < 2 || koff.size() < 2) return false;
+      base = toff[0] + roff[0];
+      sr = roff[1] - roff[0];
+      sk = koff[1] - koff[0];
+      const int64_t rows = static_cast<int64_t>(roff.size());
+      for (size_t r = 0; r < roff.size(); ++r)
+        if (roff[r] != roff[0] + static_cast<int64_t>(r) * sr) return false;
+      for (size_t t = 0; t < toff.size(); ++t)
+        if (toff[t] + roff[0] != base + static_cast<int64_t>(t) * rows * sr) return false;
+      for (size_t k = 0; k < koff.size(); ++k)
+        if (koff[k] != static_cast<int64_t>(k) * sk) return false;
+      return true;
+    };
+    auto mode = [&](const std::vector<int64_t>& toff, const std::vector<int64_t>& roff, const std::vector<int64_t>& koff,
+                    PlainPack& pp) {
+      int64_t base, sr, sk;
+      pp.kind = 0;
+      if (!bf16_ || !plain(toff, roff, koff, base, sr, sk)) return;
+      if (sk == 1 && K_ % 8 == 0 && base % 4 == 0 && sr % 4 == 0) pp = {1, base, sr};
+      else if (sr == 1 && base % 4 == 0 && sk % 4 == 0) pp = {2, base, sk};
+    };
+    mode(tAm, am, ak, ppa_);
+    mode(tBn, bn, bk, ppb_);
     packed_ = true;
     smem_ = static_cast<size_t>(stages_) * (BM + BN) * BKE * 4 + 1024 + 256;
     rb_ = false;
@@ -1217,8 +1312,23 @@ class TcRoutine final : public Routine {
         }
         MDHB_CUDA(cudaGetLastError());
       };
-      pack(A, pa_, pk_[0], pk_[1], pk_[2], BM, M_, a_rowfast_);
-      pack(B, pb_, pk_[3], pk_[4], pk_[5], BN_, N_, b_rowfast_);
+      auto plain_pack = [&](const void* src, void* dst, const PlainPack& pp, int64_t n_rows) {
+        const float* base = static_cast<const float*>(src) + pp.base;
+        if (pp.kind == 1) {
+          const int64_t tot = n_rows * (Kp_ / 8);
+          convert_kvec_bf16<<<static_cast<unsigned>(std::min<int64_t>(8 * sms, (tot + 255) / 256)), 256, 0, s>>>(
+              base, pp.stride, static_cast<uint16_t*>(dst), static_cast<int>(K_), static_cast<int>(Kp_), n_rows);
+        } else {
+          dim3 g(static_cast<unsigned>((n_rows + 63) / 64), static_cast<unsigned>((Kp_ + 63) / 64));
+          transpose64<__nv_bfloat16><<<g, 256, 0, s>>>(base, pp.stride, static_cast<__nv_bfloat16*>(dst), static_cast<int>(K_),
+                                                       static_cast<int>(n_rows), static_cast<int>(Kp_));
+        }
+        MDHB_CUDA(cudaGetLastError());
+      };
+      if (ppa_.kind) plain_pack(A, pa_, ppa_, M_);
+      else pack(A, pa_, pk_[0], pk_[1], pk_[2], BM, M_, a_rowfast_);
+      if (ppb_.kind) plain_pack(B, pb_, ppb_, N_);
+      else pack(B, pb_, pk_[3], pk_[4], pk_[5], BN_, N_, b_rowfast_);
       A = pa_;
       B = pb_;
     } else if (packed_) {
@@ -1237,9 +1347,15 @@ class TcRoutine final : public Routine {
     }
     if (transposeB_) {
       const float* src = static_cast<const float*>(B) + g_.lb.c0;
-      dim3 tg(static_cast<unsigned>((tN_ + 31) / 32), static_cast<unsigned>((tK_ + 31) / 32));
-      transpose_kn<<<tg, 256, 0, s>>>(src, g_.lb.cj[static_cast<size_t>(g_.Kd[0])], g_.lb.cj[static_cast<size_t>(g_.Nd[0])],
-                                      static_cast<float*>(bt_), static_cast<int>(tK_), static_cast<int>(tN_));
+      const int64_t sk = g_.lb.cj[static_cast<size_t>(g_.Kd[0])], sn = g_.lb.cj[static_cast<size_t>(g_.Nd[0])];
+      if (sn == 1 && sk % 4 == 0 && g_.lb.c0 % 4 == 0 && tN_ % 4 == 0) {
+        dim3 tg(static_cast<unsigned>((tN_ + 63) / 64), static_cast<unsigned>((tK_ + 63) / 64));
+        transpose64<float><<<tg, 256, 0, s>>>(src, sk, static_cast<float*>(bt_), static_cast<int>(tK_), static_cast<int>(tN_),
+                                              static_cast<int>(tK_));
+      } else {
+        dim3 tg(static_cast<unsigned>((tN_ + 31) / 32), static_cast<unsigned>((tK_ + 31) / 32));
+        transpose_kn<<<tg, 256, 0, s>>>(src, sk, sn, static_cast<float*>(bt_), static_cast<int>(tK_), static_cast<int>(tN_));
+      }
       MDHB_CUDA(cudaGetLastError());
       B = bt_;
     }
@@ -1340,6 +1456,11 @@ class TcRoutine final : public Routine {
   int64_t Kp_ = 0, c_run_ = 1;
   bool two_sm_ = false;
   bool bf16_ = false, a_rowfast_ = false, b_rowfast_ = false;
+  struct PlainPack {
+    int kind = 0;  // 0 table gather, 1 vectorised convert (k unit-stride), 2 64x64 transpose (rows unit-stride)
+    int64_t base = 0, stride = 0;
+  };
+  PlainPack ppa_, ppb_;
   int b_row_rank_ = 1, st2_ = 0;
   size_t smem2_ = 0;
   View vb2_;
