@@ -40,7 +40,7 @@ sys.path.insert(0, REPO)
 METRIC = json.load(open(os.path.join(REPO, "BASELINE.json")))["metric"]
 HEADLINE = "jacobi3d_fp32"
 ROUTINES = ["matvec_fp32", "jacobi3d_fp32", "matmul_fp32", "matmul_fp32:tf32", "matmul_resnet_fc", "mcc_nhwc",
-            "mcc_nhwc:tf32", "ccsdt_abcdef_gdab_efgc", "ccsdt_abcdef_gdab_efgc:tf32", "matmul_fp32:bf16",
+            "mcc_nhwc:tf32", "ccsdt_abcdef_gdab_efgc", "ccsdt_abcdef_gdab_efgc:tf32", "matmul_fp32:bf16", "mcc_nhwc:bf16",
             "ccsdt_abcdef_gdab_efgc:bf16", "prl_max", "scan_i32"]
 L2_BYTES = 126 << 20
 

@@ -1476,7 +1476,7 @@ std::unique_ptr<Routine> make_tc_contraction(const Problem& p, const Groups& g, 
   // N-tile menu; among the instances that set up, prefer a direct TMA view
   // over packed operands, then the longest contiguous run of C per tile row
   // (the epilogue's store width), then the wider tile.
-  if (p.opt.math == Math::TF32) {
+  {
     std::string w;
     if (auto conv = make_tc_conv(p, g, &w)) {
       if (cfg_out) *cfg_out = cfg ? *cfg : baseline_config(p.e, p.m);

@@ -26,6 +26,7 @@
 // thread), warps 2-5 drain the double-buffered TMEM accumulator through a
 // 32x32 smem transpose into coalesced 256-byte C rows.
 #include <cuda.h>
+#include <cuda_bf16.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -50,6 +51,7 @@ struct ConvArgs {
   int64_t on, op, oq;      // output strides (elements)
   uint32_t plane;          // bytes of one 4-channel plane of the patch (HP * WQ * 16)
   uint32_t lbo, sbo;       // descriptor core-matrix strides (K direction, M direction)
+  int ek;                  // channels per k-tile row of 128 bytes (32 fp32 / 64 bf16)
   int sw;                  // 1: pixel-major 128B-swizzled patch (4-D box {32 c, WQ, HP, 1})
   int bo_mode;             // descriptor base-offset rule for shifted swizzled rows (dev)
 };
@@ -58,16 +60,15 @@ __device__ __forceinline__ uint64_t nosw_desc(uint32_t saddr, uint32_t lbo, uint
   return tc::umma_desc(saddr, lbo, sbo, 0);
 }
 
-template <int BN>
+template <int BN, bool BF16 = false, int PSTAGES = 2>
 __global__ void __launch_bounds__(192, 1)
     tc_conv_tf32(const __grid_constant__ CUtensorMap tma_i, const __grid_constant__ CUtensorMap tma_f, ConvArgs g) {
-  constexpr int PSTAGES = 2;
-  constexpr uint32_t B_BYTES = BN * CV_BKE * 4;      // one 32-channel k-tile of the filter
+  constexpr uint32_t B_BYTES = BN * CV_BKE * 4;      // one 128-byte-row k-tile of the filter (32 fp32 / 64 bf16)
   constexpr uint32_t TMEM_COLS = 2 * BN <= 128 ? 128 : 256;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int ktiles = g.R * g.S * (g.C / CV_BKE);
-  const int chunks = g.C / CV_BKE;
+  const int ktiles = g.R * g.S * (g.C / g.ek);
+  const int chunks = g.C / g.ek;
   const uint32_t patch_bytes = 8 * g.plane;           // 8 planes of 4 channels = 32 channels
   const uint32_t patch_slot = (patch_bytes + 1023) & ~1023u;
   uint8_t* sB = smem;                                 // resident filter [ktiles][BN][32] (128B swizzle)
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(192, 1)
     // ---------------- TMA producer: the filter once, then one patch per (tile, chunk)
     tc::mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(ktiles) * B_BYTES);
     for (int kt = 0; kt < ktiles; ++kt) {
-      int c[5] = {kt * CV_BKE, 0, 0, 0, 0};
+      int c[5] = {kt * g.ek, 0, 0, 0, 0};
       tc::tma_load(sB + static_cast<size_t>(kt) * B_BYTES, &tma_f, bfull, 2, c);
     }
     uint32_t it = 0;
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(192, 1)
         if (it >= PSTAGES) tc::mbar_wait(&empty[s], ((it / PSTAGES) - 1) & 1);
         tc::mbar_arrive_expect_tx(&full[s], patch_bytes);
         if (g.sw) {
-          int c[5] = {cc * CV_BKE, qb * CV_TQ, pb * CV_TP, n, 0};
+          int c[5] = {cc * g.ek, qb * CV_TQ, pb * CV_TP, n, 0};
           tc::tma_load(sP + s * patch_slot, &tma_i, &full[s], 4, c);
         } else {
           int c[5] = {0, qb * CV_TQ, pb * CV_TP, cc * 8, n};
@@ -128,7 +129,7 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer
-    constexpr uint32_t idesc = tc::instr_desc(2, 0, 0, CV_BM, BN);
+    constexpr uint32_t idesc = tc::instr_desc(BF16 ? 1 : 2, 0, 0, CV_BM, BN);
     tc::mbar_wait(bfull, 0);
     uint32_t it = 0, tl = 0;
     for (int x = blockIdx.x; x < ntiles; x += gridDim.x, ++tl) {
@@ -153,7 +154,7 @@ __global__ void __launch_bounds__(192, 1)
               const uint64_t da = g.sw ? (tc::umma_desc(tap + j * 32, 16, static_cast<uint32_t>(g.WQ) * 128, 2) | bo)
                                        : nosw_desc(tap + 2 * j * g.plane, g.lbo, g.sbo);
               const uint64_t db = tc::sw128_desc(sb + j * 32, 16, 1024);
-              tc::mma<true>(dtm, da, db, idesc, first ? 0u : 1u);
+              tc::mma<!BF16>(dtm, da, db, idesc, first ? 0u : 1u);
               first = false;
             }
           }
@@ -382,6 +383,21 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
+__global__ void __launch_bounds__(256) to_bf16(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, int64_t n8) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x; i < n8; i += static_cast<int64_t>(gridDim.x) * 256) {
+    const float4 a = __ldcs(reinterpret_cast<const float4*>(src) + 2 * i);
+    const float4 b = __ldcs(reinterpret_cast<const float4*>(src) + 2 * i + 1);
+    const __nv_bfloat162 h0 = __floats2bfloat162_rn(a.x, a.y), h1 = __floats2bfloat162_rn(a.z, a.w),
+                         h2 = __floats2bfloat162_rn(b.x, b.y), h3 = __floats2bfloat162_rn(b.z, b.w);
+    uint4 w;
+    w.x = *reinterpret_cast<const uint32_t*>(&h0);
+    w.y = *reinterpret_cast<const uint32_t*>(&h1);
+    w.z = *reinterpret_cast<const uint32_t*>(&h2);
+    w.w = *reinterpret_cast<const uint32_t*>(&h3);
+    reinterpret_cast<uint4*>(dst)[i] = w;
+  }
+}
+
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -429,19 +445,21 @@ class ConvRoutine final : public Routine {
   ConvRoutine(const Problem& p, int ib, int fb) : p_(p), ib_(ib), fb_(fb) {}
   const char* family() const override { return "contraction"; }
   const char* bound() const override { return "tensor"; }
-  int launches() const override { return 1; }
+  int launches() const override { return bf16_ ? 3 : 1; }
   double flops() const override {
     return 2.0 * a_.N * a_.P * a_.Q * static_cast<double>(a_.K) * a_.R * a_.S * a_.C;
   }
   double bytes() const override { return static_cast<double>(p_.in_bytes + p_.out_bytes); }
   std::string describe() const override {
     std::ostringstream os;
-    os << "{\"kernel\": \"" << (two_sm_ ? "tc_conv_2sm<" : "tc_conv_tf32<") << a_.K << ">\", \"math\": \"tf32\", \"M\": "
+    os << "{\"kernel\": \"" << (two_sm_ ? "tc_conv_2sm<" : bf16_ ? "tc_conv_bf16<" : "tc_conv_tf32<") << a_.K
+       << ">\", \"math\": \"" << (bf16_ ? "bf16" : "tf32") << "\", \"M\": "
        << static_cast<int64_t>(a_.N) * a_.P * a_.Q << ", \"N\": " << a_.K << ", \"K\": " << a_.R * a_.S * a_.C
        << ", \"tile\": \"16 p x 8 q x " << a_.K << " k\", \"patch\": [" << a_.HP << ", " << a_.WQ << ", 32]"
        << ", \"taps_per_patch\": " << a_.R * a_.S << ", \"tiles\": " << static_cast<int64_t>(a_.N) * a_.pblocks * a_.qblocks
-       << ", \"umma\": \"tcgen05.mma.cta_group::1.kind::tf32 M128xN" << a_.K
-       << "xK8, A no-swizzle shifted descriptors, B resident 128B-swizzled\", \"smem\": " << smem_ << "}";
+       << ", \"umma\": \"tcgen05.mma.cta_group::1.kind::" << (bf16_ ? "f16 (bf16) M128xN" : "tf32 M128xN") << a_.K
+       << (bf16_ ? "xK16" : "xK8") << ", A no-swizzle shifted descriptors, B resident 128B-swizzled\", \"smem\": " << smem_
+       << (bf16_ ? ", \"conversion\": \"to_bf16 of input and filter per run\"" : "") << "}";
     return os.str();
   }
 
@@ -463,7 +481,9 @@ class ConvRoutine final : public Routine {
     const auto& ie = p_.in_ext[static_cast<size_t>(ib_)];  // [N][H][W][C]
     const auto& oe = p_.out_ext[0];                      // [N][P][Q][K]
     if (a_.K != 64) return *why = "conv instance: 64 output channels", false;
-    if (a_.C % CV_BKE || a_.Q % CV_TQ) return *why = "conv instance: C % 32, Q % 8", false;
+    bf16_ = p_.opt.math == Math::BF16;
+    a_.ek = bf16_ ? 2 * CV_BKE : CV_BKE;
+    if (a_.C % a_.ek || a_.Q % CV_TQ) return *why = "conv instance: C % (32 fp32 | 64 bf16), Q % 8", false;
     if (ie[3] != a_.C) return *why = "conv instance: input channel extent", false;
     a_.HP = CV_TP + a_.R - 1;
     a_.WQ = CV_TQ + a_.S - 1;
@@ -479,12 +499,17 @@ class ConvRoutine final : public Routine {
     // pixel-major 128B-swizzled patch (shifted taps need no base offset: the
     // swizzle follows absolute smem address bits) -- bit-exact, measured
     // slower than the [c-group][p][q][4c] layout; selectable (MDHB_CONV_SW128=1)
-    a_.sw = std::getenv("MDHB_CONV_SW128") ? 1 : 0;
+    a_.sw = std::getenv("MDHB_CONV_SW128") && !bf16_ ? 1 : 0;
     a_.bo_mode = std::getenv("MDHB_CONV_BO") ? std::atoi(std::getenv("MDHB_CONV_BO")) : 0;
     if (a_.sw && (a_.WQ * 128) / 16 >= (1 << 14)) a_.sw = 0;
-    const int ktiles = a_.R * a_.S * (a_.C / CV_BKE);
+    const int ktiles = a_.R * a_.S * (a_.C / a_.ek);
     const size_t patch_slot = (8 * static_cast<size_t>(a_.plane) + 1023) / 1024 * 1024;
-    smem_ = static_cast<size_t>(ktiles) * a_.K * CV_BKE * 4 + 2 * patch_slot + 256 + 4 * (32 * 33 * 4 + 32 * 8) + 1024;
+    pst_ = bf16_ ? 4 : 2;  // the bf16 filter is half the bytes: room for a deeper patch ring
+    smem_ = static_cast<size_t>(ktiles) * a_.K * CV_BKE * 4 + pst_ * patch_slot + 256 + 4 * (32 * 33 * 4 + 32 * 8) + 1024;
+    if (bf16_ && smem_ > 227 * 1024) {
+      pst_ = 2;
+      smem_ = static_cast<size_t>(ktiles) * a_.K * CV_BKE * 4 + pst_ * patch_slot + 256 + 4 * (32 * 33 * 4 + 32 * 8) + 1024;
+    }
     if (smem_ > 227 * 1024) return *why = "conv instance: filter + patches exceed shared memory", false;
     // CTA-pair instance: half the filter per CTA, 3 patch stages
     smem2_ = ((static_cast<size_t>(ktiles) * (a_.K / 2) * CV_BKE * 4 + 1023) / 1024 * 1024) + 3 * patch_slot + 256 +
@@ -492,7 +517,7 @@ class ConvRoutine final : public Routine {
     // measured slower than the single-CTA kernel at conv2_x (0.242 vs 0.221 ms:
     // N = 64 leaves the pair's saved B bandwidth small next to the extra
     // cross-CTA synchronisation); selectable with MDHB_CONV_2SM=1
-    two_sm_ = smem2_ <= 227 * 1024 && std::getenv("MDHB_CONV_2SM") && !std::getenv("MDHB_TC_1SM") && !a_.sw;
+    two_sm_ = smem2_ <= 227 * 1024 && std::getenv("MDHB_CONV_2SM") && !std::getenv("MDHB_TC_1SM") && !a_.sw && !bf16_;
     if (a_.plane / 16 >= (1u << 14)) return *why = "conv instance: patch plane too large for a descriptor", false;
     // input and filter extents for the tensor maps
     H_ = ie[1];
@@ -507,6 +532,42 @@ class ConvRoutine final : public Routine {
   void launch(const void* const* d_in, void* const* d_out, cudaStream_t s) override {
     const void* I = d_in[ib_];
     const void* F = d_in[fb_];
+    const int sms0 = sm_count(p_.opt.device);
+    if (bf16_) {
+      // operand conversion (layout_de): fp32 views -> bf16 copies of the same layout
+      const int64_t ni = static_cast<int64_t>(a_.N) * H_ * W_ * a_.C, nf = FK_ * a_.K;
+      if (!ibf_) {
+        MDHB_CUDA(cudaMalloc(&ibf_, static_cast<size_t>(ni) * 2));
+        MDHB_CUDA(cudaMalloc(&fbf_, static_cast<size_t>(nf) * 2 + 16));
+      }
+      to_bf16<<<static_cast<unsigned>(std::min<int64_t>(8 * sms0, (ni / 8 + 255) / 256)), 256, 0, s>>>(
+          static_cast<const float*>(I), static_cast<__nv_bfloat16*>(ibf_), ni / 8);
+      to_bf16<<<static_cast<unsigned>(std::min<int64_t>(8 * sms0, (nf / 8 + 255) / 256)), 256, 0, s>>>(
+          static_cast<const float*>(F), static_cast<__nv_bfloat16*>(fbf_), nf / 8);
+      MDHB_CUDA(cudaGetLastError());
+      if (!bf_maps_) {
+        const int64_t C = a_.C;
+        cuuint64_t dims[5] = {8, static_cast<cuuint64_t>(W_), static_cast<cuuint64_t>(H_), static_cast<cuuint64_t>(C / 8),
+                              static_cast<cuuint64_t>(a_.N)};
+        cuuint64_t strides[4] = {static_cast<cuuint64_t>(C) * 2, static_cast<cuuint64_t>(W_ * C) * 2, 16,
+                                 static_cast<cuuint64_t>(H_ * W_ * C) * 2};
+        cuuint32_t box[5] = {8, static_cast<cuuint32_t>(a_.WQ), static_cast<cuuint32_t>(a_.HP), 8, 1};
+        cuuint32_t es[5] = {1, 1, 1, 1, 1};
+        CUresult r = conv_encoder()(&mi_, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, ibf_, dims, strides, box, es,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) fail("CudaError", "cuTensorMapEncodeTiled (bf16 conv input) failed");
+        cuuint64_t fd[2] = {static_cast<cuuint64_t>(FK_), static_cast<cuuint64_t>(a_.K)};
+        cuuint64_t fs[1] = {static_cast<cuuint64_t>(FK_) * 2};
+        cuuint32_t fbx[2] = {64, static_cast<cuuint32_t>(a_.K)};
+        r = conv_encoder()(&mf_, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, fbf_, fd, fs, fbx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) fail("CudaError", "cuTensorMapEncodeTiled (bf16 conv filter) failed");
+        bf_maps_ = true;
+      }
+      last_i_ = I;
+      last_f_ = F;
+    }
     if (I != last_i_) {
       // 5-D view of I: {4 c, W, H, C/4 c-groups, N}; the c-group stride (16 B)
       // is smaller than the pixel stride -- TMA strides need not be ordered
@@ -576,7 +637,7 @@ class ConvRoutine final : public Routine {
       return;
     }
     const int64_t tiles = static_cast<int64_t>(a_.N) * a_.pblocks * a_.qblocks;
-    auto k = tc_conv_tf32<64>;
+    auto k = bf16_ ? (pst_ == 4 ? tc_conv_tf32<64, true, 4> : tc_conv_tf32<64, true, 2>) : tc_conv_tf32<64>;
     MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_)));
     k<<<static_cast<unsigned>(std::min<int64_t>(sms, tiles)), 192, smem_, s>>>(mi_, mf_, a);
     MDHB_CUDA(cudaGetLastError());
@@ -589,6 +650,17 @@ class ConvRoutine final : public Routine {
   int64_t H_ = 0, W_ = 0, FK_ = 0;
   size_t smem_ = 0, smem2_ = 0;
   bool two_sm_ = false;
+  bool bf16_ = false, bf_maps_ = false;
+  int pst_ = 2;
+  void *ibf_ = nullptr, *fbf_ = nullptr;
+
+ public:
+  ~ConvRoutine() override {
+    if (ibf_) cudaFree(ibf_);
+    if (fbf_) cudaFree(fbf_);
+  }
+
+ private:
   CUtensorMap mi_{}, mf_{}, mf2_{};
   const void* last_i_ = nullptr;
   const void* last_f_ = nullptr;

@@ -169,7 +169,8 @@ BF16_CASES = [
     ("matmul_fp32", [256, 512, 96]),
     ("matmul_fp32", [512, 256, 200]),            # K padded to 256
     ("ccsdt_abcdef_gdab_efgc", [4, 4, 8, 8, 8, 4, 72]),
-    ("mcc_nhwc", [2, 8, 8, 64, 3, 3, 64]),       # packed (im2col-free gather) operands
+    ("mcc_nhwc", [2, 8, 8, 64, 3, 3, 64]),       # bf16 shifted-descriptor conv (tc_conv_bf16)
+    ("mcc_nhwc", [3, 20, 16, 64, 3, 3, 128]),    # two 64-channel chunks, ragged p-blocks
 ]
 
 
