@@ -661,10 +661,11 @@ struct PipeSmem {
 };
 
 template <int BM, int BN, bool AV, bool BV, bool CVEC, int BKT>
-__global__ void __launch_bounds__(256, 2) sgemm_pipe(GemmArgs g) {
+__global__ void __launch_bounds__((BM / 8) * (BN / 8), 512 / ((BM / 8) * (BN / 8))) sgemm_pipe(GemmArgs g) {
+  constexpr int NT = (BM / 8) * (BN / 8);  // threads: one 8 x 8 register tile each
   using SM = PipeSmem<BM, BN, BKT>;
   constexpr int PA = SM::PA, PB = SM::PB, ST = SM::STAGES, TX = BN / 8;
-  static_assert((BM / 8) * (BN / 8) == 256, "8 x 8 register tiles over 256 threads");
+  static_assert(NT == 256 || NT == 128, "8 x 8 register tiles over 128 or 256 threads");
   extern __shared__ __align__(16) float psm[];
   float* As = psm;                   // [ST][BKT][PA]
   float* Bs = psm + ST * BKT * PA;   // [ST][BKT][PB]
@@ -682,28 +683,28 @@ __global__ void __launch_bounds__(256, 2) sgemm_pipe(GemmArgs g) {
   // ---- fill slots, fixed across k-tiles.  Inside a k-tile the k offsets
   // are affine (host-checked), so a slot's source is  base(k-tile) + off[p]
   // with one uniform table read per k-tile and one IMAD.WIDE per copy.
-  // V16: 16-byte chunk c = tid + 256 p -> k = c / (X/4), mn = (c % (X/4)) * 4
-  // S4 : element e = tid + 256 p      -> k = e % BKT,    mn = e / BKT
+  // V16: 16-byte chunk c = tid + NT p -> k = c / (X/4), mn = (c % (X/4)) * 4
+  // S4 : element e = tid + NT p      -> k = e % BKT,    mn = e / BKT
   constexpr int TA = AV ? BM * BKT / 4 : BM * BKT, TB = BV ? BN * BKT / 4 : BN * BKT;  // fills per k-tile
-  constexpr int NA = (TA + 255) / 256, NB = (TB + 255) / 256;
+  constexpr int NA = (TA + NT - 1) / NT, NB = (TB + NT - 1) / NT;
   int a_off[NA], b_off[NB];
 #pragma unroll
   for (int p = 0; p < NA; ++p) {
-    const int c = tid + 256 * p;
+    const int c = tid + NT * p;
     const int k = AV ? c / (BM / 4) : c % BKT, m = AV ? (c % (BM / 4)) * 4 : c / BKT;
     a_off[p] = c < TA ? g.am[m] + k * g.sak : 0;
   }
 #pragma unroll
   for (int p = 0; p < NB; ++p) {
-    const int c = tid + 256 * p;
+    const int c = tid + NT * p;
     const int k = BV ? c / (BN / 4) : c % BKT, n = BV ? (c % (BN / 4)) * 4 : c / BKT;
     b_off[p] = c < TB ? g.bn[n] + k * g.sbk : 0;
   }
   // shared destinations: slot p sits at a fixed offset from slot 0
   const int a_dst0 = AV ? (tid / (BM / 4)) * PA + (tid % (BM / 4)) * 4 : (tid % BKT) * PA + tid / BKT;
   const int b_dst0 = BV ? (tid / (BN / 4)) * PB + (tid % (BN / 4)) * 4 : (tid % BKT) * PB + tid / BKT;
-  constexpr int A_STEP = AV ? (256 / (BM / 4)) * PA : 256 / BKT;  // floats between slots p and p+1
-  constexpr int B_STEP = BV ? (256 / (BN / 4)) * PB : 256 / BKT;
+  constexpr int A_STEP = AV ? (NT / (BM / 4)) * PA : NT / BKT;  // floats between slots p and p+1
+  constexpr int B_STEP = BV ? (NT / (BN / 4)) * PB : NT / BKT;
   const int nk = g.K / BKT;
   auto issue = [&](int kt) {
     const int s = kt % ST, k0 = kt * BKT;
@@ -713,13 +714,13 @@ __global__ void __launch_bounds__(256, 2) sgemm_pipe(GemmArgs g) {
     const uint32_t bs = static_cast<uint32_t>(__cvta_generic_to_shared(Bs + s * BKT * PB + b_dst0));
 #pragma unroll
     for (int p = 0; p < NA; ++p) {
-      if (TA % 256 && tid + 256 * p >= TA) continue;
+      if (TA % NT && tid + NT * p >= TA) continue;
       if (AV) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(as + p * A_STEP * 4), "l"(abase + a_off[p]));
       else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(as + p * A_STEP * 4), "l"(abase + a_off[p]));
     }
 #pragma unroll
     for (int p = 0; p < NB; ++p) {
-      if (TB % 256 && tid + 256 * p >= TB) continue;
+      if (TB % NT && tid + NT * p >= TB) continue;
       if (BV) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(bs + p * B_STEP * 4), "l"(bbase + b_off[p]));
       else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(bs + p * B_STEP * 4), "l"(bbase + b_off[p]));
     }
@@ -1149,8 +1150,8 @@ class GemmRoutine final : public Routine {
   // v3 (sgemm_pipe): 128 x 128 tiles, any operand view (V16 where the MN dim
   // is 16-byte contiguous, else 4-byte fills), K a multiple of the k-tile
   bool pipe_ok() const {
-    return ((BM_ == 128 && BN_ == 128) || (BM_ == 256 && BN_ == 64)) && K_ % 8 == 0 && tile_affine_ &&
-           !std::getenv("MDHB_SGEMM_V2");
+    return ((BM_ == 128 && BN_ == 128) || (BM_ == 256 && BN_ == 64) || (BM_ == 128 && BN_ == 64)) && K_ % 8 == 0 &&
+           tile_affine_ && !std::getenv("MDHB_SGEMM_V2");
   }
   int pipe_bk() const { return pbk_; }
   bool pipe_av() const { return amode_ == LD_MN4; }
@@ -1166,11 +1167,12 @@ class GemmRoutine final : public Routine {
     MDHB_P(false, true, true) MDHB_P(false, true, false) MDHB_P(false, false, true) MDHB_P(false, false, false)
 #undef MDHB_P
     MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    k<<<grid, 256, smem, s>>>(a);
+    k<<<grid, (PBM / 8) * (PBN / 8), smem, s>>>(a);
   }
   void dispatch(const GemmArgs& a, cudaStream_t s) {
     if (pipe_ok()) {
       if (BM_ == 256) return pipe_bk() == 16 ? dispatch_pipe<256, 64, 16>(a, s) : dispatch_pipe<256, 64, 8>(a, s);
+      if (BN_ == 64) return pipe_bk() == 16 ? dispatch_pipe<128, 64, 16>(a, s) : dispatch_pipe<128, 64, 8>(a, s);
       if (pipe_bk() == 32) return dispatch_pipe<128, 128, 32>(a, s);
       return pipe_bk() == 16 ? dispatch_pipe<128, 128, 16>(a, s) : dispatch_pipe<128, 128, 8>(a, s);
     }
@@ -1407,7 +1409,8 @@ std::unique_ptr<Routine> make_contraction(const Problem& p, const Config* cfg, C
     }
   } else {
     const bool wide = std::getenv("MDHB_SGEMM_WIDE") != nullptr;
-    const int menu[6][2] = {{128, wide ? 256 : 128}, {128, 128}, {256, 64}, {128, 64}, {64, 128}, {64, 64}};
+    const bool m64 = std::getenv("MDHB_PIPE_128x64") != nullptr;
+    const int menu[6][2] = {{128, wide ? 256 : 128}, {128, 128}, {m64 ? 128 : 256, 64}, {128, 64}, {64, 128}, {64, 64}};
     for (auto& t : menu) {
       ok = r->setup(t[0], t[1], {}, {});
       if (ok) {
