@@ -50,6 +50,7 @@ struct PrlArgs {
                   // [3] weights * 16 as unsigned bytes, [4] five-instruction path flag
   int qt;         // queries per thread
   int allow5;     // five-instruction path permitted (MDHB_PRL_5=1)
+  uint32_t one;   // 1 (keeps the byte-compare add an IMAD, see add7f_fma)
   int rsplit;     // record splits (grid.y)
 };
 
@@ -163,6 +164,16 @@ __global__ void __launch_bounds__(512) prl_pack(PrlArgs a, const long long* part
   }
 }
 
+// (x & 0x7F7F7F7F) + 0x7F7F7F7F as an integer multiply-add: the add runs on
+// the FMA pipe (IMAD) instead of the integer ALU pipe, which the byte
+// compares (LOP3) and the fold (VIMNMX) already saturate.  `one` is a kernel
+// argument equal to 1 so ptxas cannot fold the multiply back into an IADD3.
+__device__ __forceinline__ uint32_t add7f_fma(uint32_t xm, uint32_t one) {
+  uint32_t t;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(xm), "r"(one), "r"(0x7F7F7F7Fu));
+  return t;
+}
+
 template <int QT>
 __device__ __forceinline__ void commit_best(const PrlArgs& a, int64_t q0, const long long (&best)[QT]) {
 #pragma unroll
@@ -217,7 +228,7 @@ __global__ void __launch_bounds__(NT) prl_main(PrlArgs a) {
 #pragma unroll
         for (int j = 0; j < QT; ++j) {
           const uint32_t x = qp[j] ^ rec;
-          const uint32_t t = (x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
+          const uint32_t t = add7f_fma(x & 0x7F7F7F7Fu, a.one);
           const uint32_t eq = ~t & 0x80808080u;
           int key;
           asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(key) : "r"(eq), "r"(wp16), "r"(krev));
@@ -258,7 +269,7 @@ __global__ void __launch_bounds__(NT) prl_main(PrlArgs a) {
 #pragma unroll
         for (int j = 0; j < QT; ++j) {
           const uint32_t x = qp[j] ^ rec.x;
-          const uint32_t t = (x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;  // bit 7 set per non-zero byte
+          const uint32_t t = add7f_fma(x & 0x7F7F7F7Fu, a.one);  // bit 7 set per non-zero byte
           const uint32_t eq = ~t & 0x80808080u;                // codes < 128: x's bit 7 is 0
           int dot;
           asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(dot) : "r"(eq), "r"(wp), "r"(0));
@@ -324,6 +335,7 @@ class PrlRoutine final : public Routine {
     // 2^15 x 2^20: IDP.4A.U8.U8 + VIMNMX per pair vs the six-instruction mix);
     // kept selectable (MDHB_PRL_5=1), bit-exact either way
     a_.allow5 = std::getenv("MDHB_PRL_5") ? 1 : 0;
+    a_.one = 1;
     part_ = reinterpret_cast<long long*>(static_cast<char*>(scratch_) + 256);
     a_.qp = reinterpret_cast<uint32_t*>(static_cast<char*>(scratch_) + head);
     a_.dp = a_.qp + a.nq;
