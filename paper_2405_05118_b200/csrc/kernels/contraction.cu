@@ -786,6 +786,18 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 512 / ((BM / 8) * (BN / 8
   }
 }
 
+// B layout pass: Bp[k][t * BN + c] = B[tBn[t] + bn[c] + bk[k]] (n in N-tile
+// order; consecutive threads walk n).
+__global__ void __launch_bounds__(256) bpack(const float* __restrict__ B, float* __restrict__ Bp, const int32_t* __restrict__ tBn,
+                                             const int32_t* __restrict__ bn, const int32_t* __restrict__ bk, int bnl, int64_t ntot,
+                                             int64_t total) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x; i < total; i += static_cast<int64_t>(gridDim.x) * 256) {
+    const int64_t k = i / ntot, n = i - k * ntot;
+    const int t = static_cast<int>(n / bnl), c = static_cast<int>(n - static_cast<int64_t>(t) * bnl);
+    Bp[i] = __ldg(B + tBn[t] + bn[c] + bk[k]);
+  }
+}
+
 // ---------------------------------------------------------------- host
 // Programmatic dependent launch for the latency-bound kernels (MDHB_NO_PDL=1 off)
 bool pdl_enabled() {
@@ -816,12 +828,14 @@ class GemmRoutine final : public Routine {
   ~GemmRoutine() override {
     if (blob_) cudaFree(blob_);
     if (part_) cudaFree(part_);
+    if (bp_tab_) cudaFree(bp_tab_);
+    if (bp_) cudaFree(bp_);
   }
   const char* family() const override { return "contraction"; }
   double flops() const override { return 2.0 * static_cast<double>(M_) * static_cast<double>(N_) * static_cast<double>(K_); }
   double bytes() const override { return static_cast<double>(p_.in_bytes + p_.out_bytes); }
   const char* bound() const override { return (gemv_ || skinny_) ? "hbm" : "fp32"; }
-  int launches() const override { return skinny_ && !cluster_ ? 2 : 1; }
+  int launches() const override { return (skinny_ && !cluster_ ? 2 : 1) + (bpack_n_ ? 1 : 0); }
 
   // Builds tables; returns false when this template cannot realise the problem.
   bool setup(int BM, int BN, const std::vector<int64_t>& Tm_in, const std::vector<int64_t>& Tn_in) {
@@ -955,6 +969,22 @@ class GemmRoutine final : public Routine {
     else if (groups4(bk) && all_mod4(bn) && all_mod4(tBn)) bmode_ = LD_K4;
     else bmode_ = LD_SCALAR;
     cvec_ = groups4(cn) && all_mod4(cm) && all_mod4(tCm) && all_mod4(tCn);
+    // layout_de pass for a small B that no 16-byte fill can read (CCSD(T)'s
+    // B[e][f][g][c] against an (c, e, f) N tile): gather it once per run into
+    // Bp[k][n] with n in N-tile order, so the template reads B with 16-byte
+    // MN-major copies
+    if (bmode_ != LD_MN4 && N_ % 4 == 0 && BN % 4 == 0 && K_ * N_ * 4 <= (int64_t(64) << 20) &&
+        !std::getenv("MDHB_NO_BPACK")) {
+      bp_tBn_ = tBn;
+      bp_bn_ = bn;
+      bp_bk_ = bk;
+      const int64_t ntot = static_cast<int64_t>(tilesN_) * BN;
+      for (size_t t = 0; t < tBn.size(); ++t) tBn[t] = static_cast<int64_t>(t) * BN;
+      for (size_t c = 0; c < bn.size(); ++c) bn[c] = static_cast<int64_t>(c);
+      for (size_t k = 0; k < bk.size(); ++k) bk[k] = static_cast<int64_t>(k) * ntot;
+      bpack_n_ = ntot;
+      bmode_ = LD_MN4;
+    }
     {
       // k offsets affine inside every k-tile of the pipe template: the
       // deepest k-tile (32 for 128 x 128 tiles, else 16, else 8) that keeps
@@ -978,6 +1008,18 @@ class GemmRoutine final : public Routine {
       tile_affine_ = pbk_ > 0;
     }
     tables(tAm, tCm, tBn, tCn, am, cm, bn, cn, ak, bk);
+    if (bpack_n_) {
+      // gather tables (original B offsets) + the packed copy
+      std::vector<int32_t> h;
+      for (auto* v : {&bp_tBn_, &bp_bn_, &bp_bk_})
+        for (int64_t x : *v) {
+          if (x > INT32_MAX || x < INT32_MIN) fail("Unsupported", "B offsets exceed int32");
+          h.push_back(static_cast<int32_t>(x));
+        }
+      MDHB_CUDA(cudaMalloc(&bp_tab_, h.size() * sizeof(int32_t)));
+      MDHB_CUDA(cudaMemcpy(bp_tab_, h.data(), h.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+      MDHB_CUDA(cudaMalloc(&bp_, static_cast<size_t>(K_ * bpack_n_) * sizeof(float)));
+    }
     return true;
   }
 
@@ -1084,6 +1126,15 @@ class GemmRoutine final : public Routine {
       gemv_rows<ROWS><<<grid, 128, 0, s>>>(a);
       MDHB_CUDA(cudaGetLastError());
       return;
+    }
+    if (bpack_n_) {
+      const int32_t* tb = static_cast<const int32_t*>(bp_tab_);
+      const int nt = static_cast<int>(bp_tBn_.size()), bnl = static_cast<int>(bp_bn_.size());
+      const int64_t total = K_ * bpack_n_;
+      bpack<<<static_cast<unsigned>(std::min<int64_t>(8 * sm_count(p_.opt.device), (total + 255) / 256)), 256, 0, s>>>(
+          B, static_cast<float*>(bp_), tb, tb + nt, tb + nt + bnl, bnl, bpack_n_, total);
+      MDHB_CUDA(cudaGetLastError());
+      B = static_cast<const float*>(bp_);
     }
     GemmArgs a{A, B, C, tab_[0], tab_[1], tab_[2], tab_[3], tab_[4], tab_[5], tab_[6], tab_[7], tab_[8], tab_[9],
                static_cast<int>(K_), tilesM_, tilesN_, psak_, psbk_};
@@ -1193,6 +1244,11 @@ class GemmRoutine final : public Routine {
   int ks_ = 0, splits_ = 0;
   int64_t sak_ = 0, sbk_ = 0;
   bool tile_affine_ = false;
+  // B layout pass (bpack): original gather tables, packed copy, its row length
+  std::vector<int64_t> bp_tBn_, bp_bn_, bp_bk_;
+  void* bp_tab_ = nullptr;
+  void* bp_ = nullptr;
+  int64_t bpack_n_ = 0;
   int psak_ = 0, psbk_ = 0, pbk_ = 0;
   float* part_ = nullptr;
   void* blob_ = nullptr;
