@@ -54,6 +54,8 @@ struct ConvArgs {
   int ek;                  // channels per k-tile row of 128 bytes (32 fp32 / 64 bf16)
   int sw;                  // 1: pixel-major 128B-swizzled patch (4-D box {32 c, WQ, HP, 1})
   int bo_mode;             // descriptor base-offset rule for shifted swizzled rows (dev)
+  int dbg;                 // dev bisection (MDHB_CONV_DBG): 1 no MMA, 2 no patch TMA, 4 no stores
+  int tma_store;           // 1: output tiles leave through TMA tensor stores (NPQK view, clipped at P)
 };
 
 __device__ __forceinline__ uint64_t nosw_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -62,7 +64,8 @@ __device__ __forceinline__ uint64_t nosw_desc(uint32_t saddr, uint32_t lbo, uint
 
 template <int BN, bool BF16 = false, int PSTAGES = 2>
 __global__ void __launch_bounds__(192, 1)
-    tc_conv_tf32(const __grid_constant__ CUtensorMap tma_i, const __grid_constant__ CUtensorMap tma_f, ConvArgs g) {
+    tc_conv_tf32(const __grid_constant__ CUtensorMap tma_i, const __grid_constant__ CUtensorMap tma_f,
+                 const __grid_constant__ CUtensorMap tma_o, ConvArgs g) {
   constexpr uint32_t B_BYTES = BN * CV_BKE * 4;      // one 128-byte-row k-tile of the filter (32 fp32 / 64 bf16)
   constexpr uint32_t TMEM_COLS = 2 * BN <= 128 ? 128 : 256;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -80,7 +83,9 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* stage_base = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 256);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // TMA-store staging: 1024-aligned, 8 KB per epilogue warp (two 128B-swizzled 32-channel halves)
+  const uint32_t ostage = (tc::smem_u32(full) + 256 + 1023) & ~1023u;
+  const int warp = tc::warp_uniform(), lane = threadIdx.x & 31;
   const int per_img = g.pblocks * g.qblocks;
   const int ntiles = g.N * per_img;
 
@@ -117,6 +122,10 @@ __global__ void __launch_bounds__(192, 1)
       for (int cc = 0; cc < chunks; ++cc, ++it) {
         const uint32_t s = it % PSTAGES;
         if (it >= PSTAGES) tc::mbar_wait(&empty[s], ((it / PSTAGES) - 1) & 1);
+        if (g.dbg & 2) {
+          tc::mbar_arrive(&full[s]);
+          continue;
+        }
         tc::mbar_arrive_expect_tx(&full[s], patch_bytes);
         if (g.sw) {
           int c[5] = {cc * g.ek, qb * CV_TQ, pb * CV_TP, n, 0};
@@ -127,44 +136,89 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer
+  } else if (warp == 1) {
+    // ---------------- MMA issuer: the whole warp walks the loop with uniform
+    // operands, one elected lane issues.  Descriptors are built once and
+    // advanced by adding 16-byte units to the start-address field (shared
+    // addresses < 256 KB never carry out of its 14 bits).
     constexpr uint32_t idesc = tc::instr_desc(BF16 ? 1 : 2, 0, 0, CV_BM, BN);
-    tc::mbar_wait(bfull, 0);
+    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+    const uint64_t da0 = g.sw ? tc::umma_desc(tc::smem_u32(sP), 16, static_cast<uint32_t>(g.WQ) * 128, 2)
+                              : nosw_desc(tc::smem_u32(sP), g.lbo, g.sbo);
+    const uint64_t db0 = tc::sw128_desc(tc::smem_u32(sB), 16, 1024);
+    const uint32_t tap_u = g.sw ? 8 : 1;                         // one pixel, 16-byte units
+    const uint32_t j_u = g.sw ? 2 : (2 * g.plane) >> 4;          // next 8 (tf32) / 16 (bf16) channels
+    const uint32_t slot_u = patch_slot >> 4, btap_u = (static_cast<uint32_t>(chunks) * B_BYTES) >> 4;
+    tc::mbar_wait_warp(bfull, 0);
     uint32_t it = 0, tl = 0;
     for (int x = blockIdx.x; x < ntiles; x += gridDim.x, ++tl) {
       const uint32_t acc = tl & 1;
-      if (tl >= 2) tc::mbar_wait(&tempty[acc], ((tl / 2) - 1) & 1);
+      if (tl >= 2) tc::mbar_wait_warp(&tempty[acc], ((tl / 2) - 1) & 1);
       tc::tc_fence_after();
-      const uint32_t dtm = tmem + acc * BN;
-      bool first = true;
+      const uint32_t dtm = tm + acc * BN;
       for (int cc = 0; cc < chunks; ++cc, ++it) {
         const uint32_t s = it % PSTAGES;
-        tc::mbar_wait(&full[s], (it / PSTAGES) & 1);
+        tc::mbar_wait_warp(&full[s], (it / PSTAGES) & 1);
         tc::tc_fence_after();
-        const uint32_t sp = tc::smem_u32(sP + s * patch_slot);
+        const uint64_t dA = da0 + s * slot_u;
+        uint64_t dB = db0 + ((static_cast<uint32_t>(cc) * B_BYTES) >> 4);
+        uint32_t first = cc == 0 ? 1u : 0u;
         for (int r = 0; r < g.R; ++r)
-          for (int ss = 0; ss < g.S; ++ss) {
-            const uint32_t tap = sp + static_cast<uint32_t>(r * g.WQ + ss) * (g.sw ? 128 : 16);
-            const uint32_t sb = tc::smem_u32(sB + static_cast<size_t>((r * g.S + ss) * chunks + cc) * B_BYTES);
-            const uint64_t bo = g.bo_mode ? static_cast<uint64_t>(((r * g.WQ + ss) & 7)) << 49 : 0;
+          for (int ss = 0; ss < g.S; ++ss, dB += btap_u) {
+            const uint32_t t = static_cast<uint32_t>(r * g.WQ + ss);
+            const uint64_t a = dA + t * tap_u + (g.bo_mode ? static_cast<uint64_t>(t & 7) << 49 : 0);
 #pragma unroll
             for (int j = 0; j < CV_BKE / 8; ++j) {
-              // swizzled: rows are pixels (128 B = 32 channels), 8-row groups WQ rows apart
-              const uint64_t da = g.sw ? (tc::umma_desc(tap + j * 32, 16, static_cast<uint32_t>(g.WQ) * 128, 2) | bo)
-                                       : nosw_desc(tap + 2 * j * g.plane, g.lbo, g.sbo);
-              const uint64_t db = tc::sw128_desc(sb + j * 32, 16, 1024);
-              tc::mma<!BF16>(dtm, da, db, idesc, first ? 0u : 1u);
-              first = false;
+              if (!(g.dbg & 1)) tc::mma_warp<!BF16>(dtm, a + j * j_u, dB + 2 * j, idesc, first ? 0u : 1u);
+              first = 0;
             }
           }
-        tc::mma_commit(&empty[s]);
+        tc::mma_commit_warp(&empty[s]);
       }
-      tc::mma_commit(&tfull[acc]);
+      tc::mma_commit_warp(&tfull[acc]);
     }
   } else if (warp >= 2) {
     // ---------------- epilogue: TMEM -> 32x32 smem transpose -> C rows
     const int q = warp & 3;
+    if (g.tma_store) {
+      // TMEM lane = output pixel, columns = channels: each lane owns a 256-byte
+      // output row; lanes write their rows 128B-swizzled (conflict-free) and one
+      // lane stores the warp's 4 p x 8 q x 64 k box (rows past P are clipped)
+      const uint32_t stg = ostage + static_cast<uint32_t>(warp - 2) * 8192;
+      uint32_t tl = 0;
+      for (int x = blockIdx.x; x < ntiles; x += gridDim.x, ++tl) {
+        const int n = x / per_img, rem = x % per_img, pb = rem / g.qblocks, qb = rem % g.qblocks;
+        const uint32_t acc = tl & 1;
+        tc::mbar_wait(&tfull[acc], (tl / 2) & 1);
+        tc::tc_fence_after();
+        if (lane == 0) tc::bulk_wait_read0();
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < BN / 32; ++h) {
+          uint32_t rv[32];
+          tc::tmem_ld32(tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(h * 32), rv);
+          const uint32_t row = stg + static_cast<uint32_t>(h) * 4096 + static_cast<uint32_t>(lane) * 128;
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + ((c ^ (lane & 7)) << 4)), "r"(rv[4 * c]),
+                         "r"(rv[4 * c + 1]), "r"(rv[4 * c + 2]), "r"(rv[4 * c + 3])
+                         : "memory");
+        }
+        tc::tc_fence_before();
+        tc::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          tc::mbar_arrive(&tempty[acc]);
+          if (!(g.dbg & 4)) {
+#pragma unroll
+            for (int h = 0; h < BN / 32; ++h)
+              tc::tma_store4(&tma_o, stg + static_cast<uint32_t>(h) * 4096, h * 32, qb * CV_TQ, pb * CV_TP + q * 4, n);
+          }
+          tc::bulk_commit();
+        }
+      }
+      if (lane == 0) tc::bulk_wait0();
+    } else {
     const uint32_t stg = tc::smem_u32(stage_base) + static_cast<uint32_t>(warp - 2) * (32 * 33 * 4 + 32 * 8);
     const uint32_t rtab = stg + 32 * 33 * 4;
     uint32_t tl = 0;
@@ -192,13 +246,14 @@ __global__ void __launch_bounds__(192, 1)
           float v;
           asm volatile("ld.shared.s64 %0, [%1];" : "=l"(ro) : "r"(rtab + rr * 8) : "memory");
           asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(stg + (rr * 33 + lane) * 4) : "memory");
-          if (ro >= 0) __stcs(cc + ro, v);
+          if (ro >= 0 && !(g.dbg & 4)) __stcs(cc + ro, v);
         }
         __syncwarp();
       }
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+    }
     }
   }
   tc::tc_fence_before();
@@ -218,16 +273,17 @@ __device__ __forceinline__ uint32_t cv_peer(uint32_t local, uint32_t rank) {
   return r;
 }
 
-template <int BN, int PSTAGES>
+template <int BN, int PSTAGES, bool BF16 = false>
 __global__ void __launch_bounds__(192, 1)
-    tc_conv_2sm(const __grid_constant__ CUtensorMap tma_i, const __grid_constant__ CUtensorMap tma_f, ConvArgs g) {
-  constexpr uint32_t B_BYTES = (BN / 2) * CV_BKE * 4;  // this CTA's half of one filter k-tile
+    tc_conv_2sm(const __grid_constant__ CUtensorMap tma_i, const __grid_constant__ CUtensorMap tma_f,
+                const __grid_constant__ CUtensorMap tma_o, ConvArgs g) {
+  constexpr uint32_t B_BYTES = (BN / 2) * CV_BKE * 4;  // this CTA's half of one filter k-tile (128-byte rows)
   constexpr uint32_t TMEM_COLS = 2 * BN <= 128 ? 128 : 256;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int ktiles = g.R * g.S * (g.C / CV_BKE);
-  const int chunks = g.C / CV_BKE;
-  const uint32_t patch_bytes = 8 * g.plane;
+  const int chunks = g.C / g.ek;
+  const int ktiles = g.R * g.S * chunks;
+  const uint32_t patch_bytes = g.sw ? static_cast<uint32_t>(g.HP * g.WQ) * 128 : 8 * g.plane;
   const uint32_t patch_slot = (patch_bytes + 1023) & ~1023u;
   uint8_t* sB = smem;
   uint8_t* sP = smem + ((static_cast<size_t>(ktiles) * B_BYTES + 1023) & ~size_t(1023));
@@ -238,7 +294,8 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* stage_base = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 256);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t ostage = (tc::smem_u32(full) + 256 + 1023) & ~1023u;
+  const int warp = tc::warp_uniform(), lane = threadIdx.x & 31;
   uint32_t rank;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   const bool leader = rank == 0;
@@ -272,13 +329,13 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer (both CTAs)
+    // ---------------- TMA producer (both CTAs); everything completes on the leader's barriers
     const uint32_t bfull_leader = cv_peer(tc::smem_u32(bfull), 0);
     const uint32_t full_leader0 = cv_peer(tc::smem_u32(&full[0]), 0);
     // this CTA's filter half: output channels rank*BN/2 .. +BN/2, every k-tile
     if (leader) tc::mbar_arrive_expect_tx(bfull, 2u * static_cast<uint32_t>(ktiles) * B_BYTES);
     for (int kt = 0; kt < ktiles; ++kt) {
-      int c[5] = {kt * CV_BKE, static_cast<int>(rank) * (BN / 2), 0, 0, 0};
+      int c[2] = {kt * g.ek, static_cast<int>(rank) * (BN / 2)};
       uint32_t d = tc::smem_u32(sB + static_cast<size_t>(kt) * B_BYTES);
       asm volatile("cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
                    ::"r"(d), "l"(&tma_f), "r"(bfull_leader), "r"(c[0]), "r"(c[1]) : "memory");
@@ -293,89 +350,148 @@ __global__ void __launch_bounds__(192, 1)
         if (it >= PSTAGES) tc::mbar_wait(&empty[s], ((it / PSTAGES) - 1) & 1);
         if (leader) tc::mbar_arrive_expect_tx(&full[s], 2 * patch_bytes);
         const uint32_t d = tc::smem_u32(sP + s * patch_slot);
-        asm volatile("cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], [%2];"
-                     ::"r"(d), "l"(&tma_i), "r"(full_leader0 + s * 8), "r"(0), "r"(qb * CV_TQ), "r"(pb * CV_TP), "r"(cc * 8), "r"(n)
-                     : "memory");
+        if (g.sw)
+          asm volatile("cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];"
+                       ::"r"(d), "l"(&tma_i), "r"(full_leader0 + s * 8), "r"(cc * g.ek), "r"(qb * CV_TQ), "r"(pb * CV_TP), "r"(n)
+                       : "memory");
+        else
+          asm volatile("cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], [%2];"
+                       ::"r"(d), "l"(&tma_i), "r"(full_leader0 + s * 8), "r"(0), "r"(qb * CV_TQ), "r"(pb * CV_TP), "r"(cc * 8), "r"(n)
+                       : "memory");
       }
     }
-  } else if (warp == 1 && lane == 0 && leader) {
-    // ---------------- MMA issuer (leader): M = 256 (two tiles) x N = BN
-    constexpr uint32_t idesc = tc::instr_desc(2, 0, 0, 2 * CV_BM, BN);
-    tc::mbar_wait(bfull, 0);
+  } else if (warp == 1 && leader) {
+    // ---------------- MMA issuer (leader warp, one elected lane): M = 256 (two tiles) x N = BN;
+    // descriptors advanced by 16-byte units as in tc_conv_tf32
+    constexpr uint32_t idesc = tc::instr_desc(BF16 ? 1 : 2, 0, 0, 2 * CV_BM, BN);
+    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+    const uint64_t da0 = g.sw ? tc::umma_desc(tc::smem_u32(sP), 16, static_cast<uint32_t>(g.WQ) * 128, 2)
+                              : nosw_desc(tc::smem_u32(sP), g.lbo, g.sbo);
+    const uint64_t db0 = tc::sw128_desc(tc::smem_u32(sB), 16, 1024);
+    const uint32_t tap_u = g.sw ? 8 : 1;
+    const uint32_t j_u = g.sw ? 2 : (2 * g.plane) >> 4;
+    const uint32_t slot_u = patch_slot >> 4, btap_u = (static_cast<uint32_t>(chunks) * B_BYTES) >> 4;
+    tc::mbar_wait_warp(bfull, 0);
     uint32_t it = 0, tl = 0;
     for (int x = pair; x < npairs_tiles; x += npairs, ++tl) {
       const uint32_t acc = tl & 1;
-      if (tl >= 2) tc::mbar_wait(&tempty[acc], ((tl / 2) - 1) & 1);
+      if (tl >= 2) tc::mbar_wait_warp(&tempty[acc], ((tl / 2) - 1) & 1);
       tc::tc_fence_after();
-      const uint32_t dtm = tmem + acc * BN;
-      bool first = true;
+      const uint32_t dtm = tm + acc * BN;
       for (int cc = 0; cc < chunks; ++cc, ++it) {
         const uint32_t s = it % PSTAGES;
-        tc::mbar_wait(&full[s], (it / PSTAGES) & 1);
+        tc::mbar_wait_warp(&full[s], (it / PSTAGES) & 1);
         tc::tc_fence_after();
-        const uint32_t sp = tc::smem_u32(sP + s * patch_slot);
+        const uint64_t dA = da0 + s * slot_u;
+        uint64_t dB = db0 + ((static_cast<uint32_t>(cc) * B_BYTES) >> 4);
+        uint32_t first = cc == 0 ? 1u : 0u;
         for (int r = 0; r < g.R; ++r)
-          for (int ss = 0; ss < g.S; ++ss) {
-            const uint32_t tap = sp + static_cast<uint32_t>(r * g.WQ + ss) * 16;
-            const uint32_t sb = tc::smem_u32(sB + static_cast<size_t>((r * g.S + ss) * chunks + cc) * B_BYTES);
+          for (int ss = 0; ss < g.S; ++ss, dB += btap_u) {
+            const uint64_t a = dA + static_cast<uint32_t>(r * g.WQ + ss) * tap_u;
 #pragma unroll
             for (int j = 0; j < CV_BKE / 8; ++j) {
-              const uint64_t da = nosw_desc(tap + 2 * j * g.plane, g.lbo, g.sbo);
-              const uint64_t db = tc::sw128_desc(sb + j * 32, 16, 1024);
-              asm volatile(
-                  "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                  "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtm), "l"(da), "l"(db),
-                  "r"(idesc), "r"(first ? 0u : 1u));
-              first = false;
+              if (g.dbg & 1) {
+              } else if (BF16)
+                asm volatile(
+                    "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtm), "l"(a + j * j_u),
+                    "l"(dB + 2 * j), "r"(idesc), "r"(first ? 0u : 1u));
+              else
+                asm volatile(
+                    "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtm), "l"(a + j * j_u),
+                    "l"(dB + 2 * j), "r"(idesc), "r"(first ? 0u : 1u));
+              first = 0;
             }
           }
-        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
-                     ::"r"(tc::smem_u32(&empty[s])), "h"(static_cast<uint16_t>(3)) : "memory");
+        asm volatile(
+            "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+            "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
+            ::"r"(tc::smem_u32(&empty[s])), "h"(static_cast<uint16_t>(3)) : "memory");
       }
-      asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
-                   ::"r"(tc::smem_u32(&tfull[acc])), "h"(static_cast<uint16_t>(3)) : "memory");
+      asm volatile(
+          "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+          "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
+          ::"r"(tc::smem_u32(&tfull[acc])), "h"(static_cast<uint16_t>(3)) : "memory");
     }
   } else if (warp >= 2) {
     // ---------------- epilogue (both CTAs): own tile, own 128 TMEM lanes
     const int q = warp & 3;
-    const uint32_t stg = tc::smem_u32(stage_base) + static_cast<uint32_t>(warp - 2) * (32 * 33 * 4 + 32 * 8);
-    const uint32_t rtab = stg + 32 * 33 * 4;
     const uint32_t tempty_leader0 = cv_peer(tc::smem_u32(&tempty[0]), 0);
     uint32_t tl = 0;
-    for (int x = pair; x < npairs_tiles; x += npairs, ++tl) {
-      const int tr = 2 * x + static_cast<int>(rank);
-      const bool mine = tr < ntiles;
-      const int t = mine ? tr : ntiles - 1;
-      const int n = t / per_img, rem = t % per_img, pb = rem / g.qblocks, qb = rem % g.qblocks;
-      const uint32_t acc = tl & 1;
-      const int m = q * 32 + lane, p = pb * CV_TP + m / CV_TQ, qq = qb * CV_TQ + m % CV_TQ;
-      const int64_t rowoff = (mine && p < g.P) ? n * g.on + p * g.op + qq * g.oq : -1;
-      asm volatile("st.shared.s64 [%0], %1;" ::"r"(rtab + lane * 8), "l"(rowoff) : "memory");
-      tc::mbar_wait(&tfull[acc], (tl / 2) & 1);
-      tc::tc_fence_after();
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t rv[32];
-        tc::tmem_ld32(tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c0), rv);
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          asm volatile("st.shared.b32 [%0], %1;" ::"r"(stg + (lane * 33 + j) * 4), "r"(rv[j]) : "memory");
+    if (g.tma_store) {
+      const uint32_t stg = ostage + static_cast<uint32_t>(warp - 2) * 8192;
+      for (int x = pair; x < npairs_tiles; x += npairs, ++tl) {
+        const int t = 2 * x + static_cast<int>(rank);
+        const int n = t / per_img, rem = t % per_img, pb = rem / g.qblocks, qb = rem % g.qblocks;
+        const uint32_t acc = tl & 1;
+        tc::mbar_wait(&tfull[acc], (tl / 2) & 1);
+        tc::tc_fence_after();
+        if (lane == 0) tc::bulk_wait_read0();
         __syncwarp();
-        float* cc = g.O + c0 + lane;
 #pragma unroll
-        for (int rr = 0; rr < 32; ++rr) {
-          int64_t ro;
-          float v;
-          asm volatile("ld.shared.s64 %0, [%1];" : "=l"(ro) : "r"(rtab + rr * 8) : "memory");
-          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(stg + (rr * 33 + lane) * 4) : "memory");
-          if (ro >= 0) __stcs(cc + ro, v);
+        for (int h = 0; h < BN / 32; ++h) {
+          uint32_t rv[32];
+          tc::tmem_ld32(tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(h * 32), rv);
+          const uint32_t row = stg + static_cast<uint32_t>(h) * 4096 + static_cast<uint32_t>(lane) * 128;
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + ((c ^ (lane & 7)) << 4)), "r"(rv[4 * c]),
+                         "r"(rv[4 * c + 1]), "r"(rv[4 * c + 2]), "r"(rv[4 * c + 3])
+                         : "memory");
         }
+        tc::tc_fence_before();
+        tc::fence_proxy_async();
         __syncwarp();
+        if (lane == 0) {
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty_leader0 + acc * 8) : "memory");
+          if (t < ntiles && !(g.dbg & 4)) {
+#pragma unroll
+            for (int h = 0; h < BN / 32; ++h)
+              tc::tma_store4(&tma_o, stg + static_cast<uint32_t>(h) * 4096, h * 32, qb * CV_TQ, pb * CV_TP + q * 4, n);
+          }
+          tc::bulk_commit();
+        }
       }
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty_leader0 + acc * 8) : "memory");
+      if (lane == 0) tc::bulk_wait0();
+    } else {
+      const uint32_t stg = tc::smem_u32(stage_base) + static_cast<uint32_t>(warp - 2) * (32 * 33 * 4 + 32 * 8);
+      const uint32_t rtab = stg + 32 * 33 * 4;
+      for (int x = pair; x < npairs_tiles; x += npairs, ++tl) {
+        const int tr = 2 * x + static_cast<int>(rank);
+        const bool mine = tr < ntiles;
+        const int t = mine ? tr : ntiles - 1;
+        const int n = t / per_img, rem = t % per_img, pb = rem / g.qblocks, qb = rem % g.qblocks;
+        const uint32_t acc = tl & 1;
+        const int m = q * 32 + lane, p = pb * CV_TP + m / CV_TQ, qq = qb * CV_TQ + m % CV_TQ;
+        const int64_t rowoff = (mine && p < g.P) ? n * g.on + p * g.op + qq * g.oq : -1;
+        asm volatile("st.shared.s64 [%0], %1;" ::"r"(rtab + lane * 8), "l"(rowoff) : "memory");
+        tc::mbar_wait(&tfull[acc], (tl / 2) & 1);
+        tc::tc_fence_after();
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t rv[32];
+          tc::tmem_ld32(tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c0), rv);
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(stg + (lane * 33 + j) * 4), "r"(rv[j]) : "memory");
+          __syncwarp();
+          float* cc = g.O + c0 + lane;
+#pragma unroll
+          for (int rr = 0; rr < 32; ++rr) {
+            int64_t ro;
+            float v;
+            asm volatile("ld.shared.s64 %0, [%1];" : "=l"(ro) : "r"(rtab + rr * 8) : "memory");
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(stg + (rr * 33 + lane) * 4) : "memory");
+            if (ro >= 0) __stcs(cc + ro, v);
+          }
+          __syncwarp();
+        }
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty_leader0 + acc * 8) : "memory");
+      }
     }
   }
   tc::tc_fence_before();
@@ -457,9 +573,13 @@ class ConvRoutine final : public Routine {
        << static_cast<int64_t>(a_.N) * a_.P * a_.Q << ", \"N\": " << a_.K << ", \"K\": " << a_.R * a_.S * a_.C
        << ", \"tile\": \"16 p x 8 q x " << a_.K << " k\", \"patch\": [" << a_.HP << ", " << a_.WQ << ", 32]"
        << ", \"taps_per_patch\": " << a_.R * a_.S << ", \"tiles\": " << static_cast<int64_t>(a_.N) * a_.pblocks * a_.qblocks
-       << ", \"umma\": \"tcgen05.mma.cta_group::1.kind::" << (bf16_ ? "f16 (bf16) M128xN" : "tf32 M128xN") << a_.K
+       << ", \"patch_stages\": " << (two_sm_ ? pst2_ : pst_) << ", \"patch_layout\": \"" << (a_.sw ? "pixel-major 128B swizzle" : "[c-group][p][q][4c] no swizzle")
+       << "\", \"umma\": \"tcgen05.mma.cta_group::" << (two_sm_ ? "2" : "1") << ".kind::" << (bf16_ ? "f16 (bf16) M" : "tf32 M")
+       << (two_sm_ ? 256 : 128) << "xN" << a_.K
        << (bf16_ ? "xK16" : "xK8") << ", A no-swizzle shifted descriptors, B resident 128B-swizzled\", \"smem\": " << smem_
-       << (bf16_ ? ", \"conversion\": \"to_bf16 of input and filter per run\"" : "") << "}";
+       << (bf16_ ? ", \"conversion\": \"to_bf16 of input and filter per run\"" : "")
+       << ", \"epilogue\": \"" << (a_.tma_store ? "TMA tensor store (128B-swizzled 4p x 8q x 32k boxes)" : "smem transpose + st.global")
+       << "\"}";
     return os.str();
   }
 
@@ -499,25 +619,42 @@ class ConvRoutine final : public Routine {
     // pixel-major 128B-swizzled patch (shifted taps need no base offset: the
     // swizzle follows absolute smem address bits) -- bit-exact, measured
     // slower than the [c-group][p][q][4c] layout; selectable (MDHB_CONV_SW128=1)
-    a_.sw = std::getenv("MDHB_CONV_SW128") && !bf16_ ? 1 : 0;
+    // pixel-major 128B-swizzled patch (rows = 128-byte pixel slices) is the
+    // default; the [c-group][p][q][4c] no-swizzle layout stays selectable
+    a_.sw = std::getenv("MDHB_CONV_NOSW") ? 0 : 1;
     a_.bo_mode = std::getenv("MDHB_CONV_BO") ? std::atoi(std::getenv("MDHB_CONV_BO")) : 0;
+    a_.dbg = std::getenv("MDHB_CONV_DBG") ? std::atoi(std::getenv("MDHB_CONV_DBG")) : 0;
     if (a_.sw && (a_.WQ * 128) / 16 >= (1 << 14)) a_.sw = 0;
     const int ktiles = a_.R * a_.S * (a_.C / a_.ek);
     const size_t patch_slot = (8 * static_cast<size_t>(a_.plane) + 1023) / 1024 * 1024;
     pst_ = bf16_ ? 4 : 2;  // the bf16 filter is half the bytes: room for a deeper patch ring
-    smem_ = static_cast<size_t>(ktiles) * a_.K * CV_BKE * 4 + pst_ * patch_slot + 256 + 4 * (32 * 33 * 4 + 32 * 8) + 1024;
-    if (bf16_ && smem_ > 227 * 1024) {
-      pst_ = 2;
-      smem_ = static_cast<size_t>(ktiles) * a_.K * CV_BKE * 4 + pst_ * patch_slot + 256 + 4 * (32 * 33 * 4 + 32 * 8) + 1024;
+    // epilogue: TMA tensor stores of 128B-swizzled 4 p x 8 q x 32 k boxes from
+    // 8 KB per warp (needs 16-byte output strides), else the smem-transpose path
+    a_.tma_store = (oe[3] * 4) % 16 == 0 && !std::getenv("MDHB_CONV_NO_TMA_STORE") ? 1 : 0;
+    auto smem_of = [&](int pst) {
+      const size_t epi = a_.tma_store ? 1024 + 4 * 8192 : 4 * (32 * 33 * 4 + 32 * 8);
+      return static_cast<size_t>(ktiles) * a_.K * CV_BKE * 4 + pst * patch_slot + 256 + epi + 1024;
+    };
+    smem_ = smem_of(pst_);
+    if (bf16_ && smem_ > 227 * 1024) smem_ = smem_of(pst_ = 2);
+    if (smem_ > 227 * 1024 && a_.tma_store) {
+      a_.tma_store = 0;
+      smem_ = smem_of(pst_);
     }
     if (smem_ > 227 * 1024) return *why = "conv instance: filter + patches exceed shared memory", false;
-    // CTA-pair instance: half the filter per CTA, 3 patch stages
-    smem2_ = ((static_cast<size_t>(ktiles) * (a_.K / 2) * CV_BKE * 4 + 1023) / 1024 * 1024) + 3 * patch_slot + 256 +
-             4 * (32 * 33 * 4 + 32 * 8) + 1024;
-    // measured slower than the single-CTA kernel at conv2_x (0.242 vs 0.221 ms:
-    // N = 64 leaves the pair's saved B bandwidth small next to the extra
-    // cross-CTA synchronisation); selectable with MDHB_CONV_2SM=1
-    two_sm_ = smem2_ <= 227 * 1024 && std::getenv("MDHB_CONV_2SM") && !std::getenv("MDHB_TC_1SM") && !a_.sw && !bf16_;
+    // CTA-pair instance: half the filter per CTA, the freed shared memory
+    // deepens the patch ring (up to 6 stages)
+    auto smem2_of = [&](int pst) {
+      const size_t epi = a_.tma_store ? 1024 + 4 * 8192 : 4 * (32 * 33 * 4 + 32 * 8);
+      return ((static_cast<size_t>(ktiles) * (a_.K / 2) * CV_BKE * 4 + 1023) / 1024 * 1024) + pst * patch_slot + 256 + epi + 1024;
+    };
+    pst2_ = 6;
+    while (pst2_ > 3 && smem2_of(pst2_) > 227 * 1024) --pst2_;
+    smem2_ = smem2_of(pst2_);
+    // default for TF32 (0.121 vs 0.142 ms at conv2_x); the bf16 pair measured
+    // slower than the single-CTA bf16 instance (selectable: MDHB_CONV_2SM=1)
+    two_sm_ = smem2_ <= 227 * 1024 && !std::getenv("MDHB_CONV_1SM") && !std::getenv("MDHB_TC_1SM") &&
+              (!bf16_ || std::getenv("MDHB_CONV_2SM"));
     if (a_.plane / 16 >= (1u << 14)) return *why = "conv instance: patch plane too large for a descriptor", false;
     // input and filter extents for the tensor maps
     H_ = ie[1];
@@ -553,9 +690,21 @@ class ConvRoutine final : public Routine {
                                  static_cast<cuuint64_t>(H_ * W_ * C) * 2};
         cuuint32_t box[5] = {8, static_cast<cuuint32_t>(a_.WQ), static_cast<cuuint32_t>(a_.HP), 8, 1};
         cuuint32_t es[5] = {1, 1, 1, 1, 1};
-        CUresult r = conv_encoder()(&mi_, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, ibf_, dims, strides, box, es,
-                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        CUresult r;
+        if (a_.sw) {
+          // pixel-major: {C, W, H, N}, box {64 c, WQ, HP, 1}, 128-byte swizzle
+          cuuint64_t d4[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W_), static_cast<cuuint64_t>(H_),
+                              static_cast<cuuint64_t>(a_.N)};
+          cuuint64_t s4[3] = {static_cast<cuuint64_t>(C) * 2, static_cast<cuuint64_t>(W_ * C) * 2,
+                              static_cast<cuuint64_t>(H_ * W_ * C) * 2};
+          cuuint32_t b4[4] = {64, static_cast<cuuint32_t>(a_.WQ), static_cast<cuuint32_t>(a_.HP), 1};
+          r = conv_encoder()(&mi_, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, ibf_, d4, s4, b4, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        } else {
+          r = conv_encoder()(&mi_, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, ibf_, dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        }
         if (r != CUDA_SUCCESS) fail("CudaError", "cuTensorMapEncodeTiled (bf16 conv input) failed");
         cuuint64_t fd[2] = {static_cast<cuuint64_t>(FK_), static_cast<cuuint64_t>(a_.K)};
         cuuint64_t fs[1] = {static_cast<cuuint64_t>(FK_) * 2};
@@ -563,6 +712,10 @@ class ConvRoutine final : public Routine {
         r = conv_encoder()(&mf_, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, fbf_, fd, fs, fbx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) fail("CudaError", "cuTensorMapEncodeTiled (bf16 conv filter) failed");
+        fbx[1] = static_cast<cuuint32_t>(a_.K / 2);  // the CTA pair's filter halves
+        r = conv_encoder()(&mf2_, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, fbf_, fd, fs, fbx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) fail("CudaError", "cuTensorMapEncodeTiled (bf16 conv filter half) failed");
         bf_maps_ = true;
       }
       last_i_ = I;
@@ -613,6 +766,21 @@ class ConvRoutine final : public Routine {
       if (r != CUDA_SUCCESS) fail("CudaError", "cuTensorMapEncodeTiled (conv filter half) failed (" + std::to_string(static_cast<int>(r)) + ")");
       last_f_ = F;
     }
+    if (a_.tma_store && d_out[0] != last_o_) {
+      // O[N][P][Q][K] as {K, Q, P, N}, box {32 k, 8 q, 4 p, 1 n}, 128-byte swizzle
+      const auto& oe = p_.out_ext[0];
+      cuuint64_t dims[4] = {static_cast<cuuint64_t>(oe[3]), static_cast<cuuint64_t>(oe[2]), static_cast<cuuint64_t>(oe[1]),
+                            static_cast<cuuint64_t>(oe[0])};
+      cuuint64_t strides[3] = {static_cast<cuuint64_t>(oe[3]) * 4, static_cast<cuuint64_t>(oe[2] * oe[3]) * 4,
+                               static_cast<cuuint64_t>(oe[1] * oe[2] * oe[3]) * 4};
+      cuuint32_t box[4] = {32, CV_TQ, 4, 1};
+      cuuint32_t es[4] = {1, 1, 1, 1};
+      CUresult r = conv_encoder()(&mo_, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, d_out[0], dims, strides, box, es,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) fail("CudaError", "cuTensorMapEncodeTiled (conv output) failed (" + std::to_string(static_cast<int>(r)) + ")");
+      last_o_ = d_out[0];
+    }
     ConvArgs a = a_;
     a.O = static_cast<float*>(d_out[0]);
     const int sms = sm_count(p_.opt.device);
@@ -631,15 +799,18 @@ class ConvRoutine final : public Routine {
       at[0].val.clusterDim.z = 1;
       lc.attrs = at;
       lc.numAttrs = 1;
-      auto k = tc_conv_2sm<64, 3>;
+      auto k = bf16_ ? (pst2_ >= 6 ? tc_conv_2sm<64, 6, true> : pst2_ == 5 ? tc_conv_2sm<64, 5, true>
+                        : pst2_ == 4 ? tc_conv_2sm<64, 4, true> : tc_conv_2sm<64, 3, true>)
+                     : (pst2_ >= 6 ? tc_conv_2sm<64, 6> : pst2_ == 5 ? tc_conv_2sm<64, 5>
+                        : pst2_ == 4 ? tc_conv_2sm<64, 4> : tc_conv_2sm<64, 3>);
       MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2_)));
-      MDHB_CUDA(cudaLaunchKernelEx(&lc, k, mi_, mf2_, a));
+      MDHB_CUDA(cudaLaunchKernelEx(&lc, k, mi_, mf2_, mo_, a));
       return;
     }
     const int64_t tiles = static_cast<int64_t>(a_.N) * a_.pblocks * a_.qblocks;
     auto k = bf16_ ? (pst_ == 4 ? tc_conv_tf32<64, true, 4> : tc_conv_tf32<64, true, 2>) : tc_conv_tf32<64>;
     MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_)));
-    k<<<static_cast<unsigned>(std::min<int64_t>(sms, tiles)), 192, smem_, s>>>(mi_, mf_, a);
+    k<<<static_cast<unsigned>(std::min<int64_t>(sms, tiles)), 192, smem_, s>>>(mi_, mf_, mo_, a);
     MDHB_CUDA(cudaGetLastError());
   }
 
@@ -651,7 +822,7 @@ class ConvRoutine final : public Routine {
   size_t smem_ = 0, smem2_ = 0;
   bool two_sm_ = false;
   bool bf16_ = false, bf_maps_ = false;
-  int pst_ = 2;
+  int pst_ = 2, pst2_ = 3;
   void *ibf_ = nullptr, *fbf_ = nullptr;
 
  public:
@@ -661,7 +832,8 @@ class ConvRoutine final : public Routine {
   }
 
  private:
-  CUtensorMap mi_{}, mf_{}, mf2_{};
+  CUtensorMap mi_{}, mf_{}, mf2_{}, mo_{};
+  const void* last_o_ = nullptr;
   const void* last_i_ = nullptr;
   const void* last_f_ = nullptr;
 };

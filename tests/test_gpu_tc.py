@@ -151,16 +151,40 @@ def test_tf32_ccsdt_full_slices_exact():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("env", ["MDHB_CONV_2SM", "MDHB_CONV_SW128"])
-def test_tf32_conv_variants_bit_identical(env, monkeypatch):
-    """CTA-pair conv (cta_group::2, filter halves) and the swizzled pixel-major
-    patch layout give the default conv instance's bits."""
-    j = spec("mcc_nhwc", [3, 20, 16, 64, 3, 3, 64])
+@pytest.mark.parametrize("envs", [("MDHB_CONV_1SM",), ("MDHB_CONV_NOSW",), ("MDHB_CONV_1SM", "MDHB_CONV_NOSW"),
+                                  ("MDHB_CONV_NO_TMA_STORE",), ("MDHB_CONV_1SM", "MDHB_CONV_NO_TMA_STORE")])
+@pytest.mark.parametrize("sizes", [[3, 20, 16, 64, 3, 3, 64], [3, 56, 56, 64, 3, 3, 64]])
+def test_tf32_conv_variants_bit_identical(envs, sizes, monkeypatch):
+    """The single-CTA conv, the no-swizzle [c-group][p][q][4c] patch layout and
+    the smem-transpose epilogue give the default instance's bits (CTA pair,
+    128B-swizzled pixel-major patch, TMA-store epilogue); odd tile counts
+    exercise the pair's ragged last tile, P = 20 / 56 the clipped p-blocks."""
+    j = spec("mcc_nhwc", sizes)
     comp = mo.Computation.from_json(j)
     ins = exact_inputs(comp, 12)
     (base,) = run_device(plan_tf32(j), ins)
-    monkeypatch.setenv(env, "1")
+    for e in envs:
+        monkeypatch.setenv(e, "1")
     p = plan_tf32(j)
+    (var,) = run_device(p, ins)
+    assert np.array_equal(base, var), p.describe()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("envs", [("MDHB_CONV_2SM",), ("MDHB_CONV_NOSW",), ("MDHB_CONV_2SM", "MDHB_CONV_NOSW")])
+def test_bf16_conv_variants_bit_identical(envs, monkeypatch):
+    """The bf16 conv instances (CTA pair / single CTA, swizzled / plain patch)
+    agree bit for bit."""
+    from paper_2405_05118_b200 import mdh
+    j = spec("mcc_nhwc", [3, 20, 16, 64, 3, 3, 128])
+    comp = mo.Computation.from_json(j)
+    ins = exact_inputs(comp, 13)
+    p0 = mdh.Plan(j, math=mdh.MATH_BF16)
+    assert "cta_group::1" in p0.describe()["template"]["umma"]
+    (base,) = run_device(p0, ins)
+    for e in envs:
+        monkeypatch.setenv(e, "1")
+    p = mdh.Plan(j, math=mdh.MATH_BF16)
     (var,) = run_device(p, ins)
     assert np.array_equal(base, var), p.describe()
 
