@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* tmem_full = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = tc::warp_uniform(), lane = threadIdx.x & 31;
   // grouped raster over (tilesM x tilesN) for L2 reuse
   constexpr int GROUP_M = 8;
   const int x = blockIdx.x;
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps(RB, BN), 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   // per epilogue warp: a 32 x 33 staging square (row-major in, column-major out)
   float* stage_base = reinterpret_cast<float*>(smem + EPI_OFF(STAGES, BN, b_slots));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = tc::warp_uniform(), lane = threadIdx.x & 31;
   const int ntiles = g.tilesM * g.tilesN;
   constexpr int GROUP_M = 8;
   auto tile_mn = [&](int x, int& tm, int& tn) {
@@ -481,19 +481,19 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps(RB, BN), 1)
         kstep(dig, ka, kb);
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer
+  } else if (warp == 1) {
+    // ---------------- MMA issuer: whole warp, uniform operands, one elected lane issues
     constexpr uint32_t idesc = tc::instr_desc(BF16 ? 1 : 2, 0, B_MN ? 1 : 0, BM, BN);  // kind::f16 bf16 | kind::tf32
-    if (RB) tc::mbar_wait(bfull, 0);
+    if (RB) tc::mbar_wait_warp(bfull, 0);
     uint32_t it = 0, tl = 0;
     for (int x = blockIdx.x; x < ntiles; x += gridDim.x, ++tl) {
       const uint32_t acc = tl & 1;
-      if (tl >= 2) tc::mbar_wait(&tempty[acc], ((tl / 2) - 1) & 1);
+      if (tl >= 2) tc::mbar_wait_warp(&tempty[acc], ((tl / 2) - 1) & 1);
       tc::tc_fence_after();
       const uint32_t dtm = tmem + acc * BN;
       for (int kt = 0; kt < g.nk; ++kt, ++it) {
         const uint32_t s = it % STAGES;
-        tc::mbar_wait(&full[s], (it / STAGES) & 1);
+        tc::mbar_wait_warp(&full[s], (it / STAGES) & 1);
         tc::tc_fence_after();
         const uint32_t sa = tc::smem_u32(sA + s * A_BYTES);
         const uint32_t sb = tc::smem_u32(sB + (RB ? static_cast<uint32_t>(kt) : s) * B_BYTES);
@@ -501,11 +501,11 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps(RB, BN), 1)
         for (int k = 0; k < BKE / 8; ++k) {
           const uint64_t da = tc::sw128_desc(sa + k * 32, 16, 1024);
           const uint64_t db = B_MN ? tc::umma_desc(sb + k * 1024, BKE * 128, 512, 1) : tc::sw128_desc(sb + k * 32, 16, 1024);
-          tc::mma<!BF16>(dtm, da, db, idesc, (kt | k) != 0 ? 1u : 0u);
+          tc::mma_warp<!BF16>(dtm, da, db, idesc, (kt | k) != 0 ? 1u : 0u);
         }
-        tc::mma_commit(&empty[s]);
+        tc::mma_commit_warp(&empty[s]);
       }
-      tc::mma_commit(&tfull[acc]);
+      tc::mma_commit_warp(&tfull[acc]);
     }
   } else if (warp >= 2) {
     // ---------------- epilogue warps: TMEM -> registers -> 32x32 smem
@@ -617,7 +617,7 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* stage_base = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 256);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = tc::warp_uniform(), lane = threadIdx.x & 31;
   uint32_t rank;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   const bool leader = rank == 0;
@@ -704,18 +704,18 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
         }
       }
     }
-  } else if (warp == 1 && lane == 0 && leader) {
+  } else if (warp == 1 && leader) {
     // ---------------- MMA issuer (leader only): M = 256 across the pair
     constexpr uint32_t idesc = tc::instr_desc(BF16 ? 1 : 2, 0, 0, 2 * BM, BN);
     uint32_t it = 0, tl = 0;
     for (int x = pair; x < ntiles; x += npairs, ++tl) {
       const uint32_t acc = tl & 1;
-      if (tl >= 2) tc::mbar_wait(&tempty[acc], ((tl / 2) - 1) & 1);
+      if (tl >= 2) tc::mbar_wait_warp(&tempty[acc], ((tl / 2) - 1) & 1);
       tc::tc_fence_after();
       const uint32_t dtm = tmem + acc * BN;
       for (int kt = 0; kt < g.nk; ++kt, ++it) {
         const uint32_t s = it % STAGES;
-        tc::mbar_wait(&full[s], (it / STAGES) & 1);
+        tc::mbar_wait_warp(&full[s], (it / STAGES) & 1);
         tc::tc_fence_after();
         const uint32_t sa = tc::smem_u32(sA + s * A_BYTES);
         const uint32_t sb = tc::smem_u32(sB + s * B_BYTES);
@@ -726,19 +726,19 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
           const uint32_t accum = (kt | k) != 0 ? 1u : 0u;
           if (BF16)
             asm volatile(
-                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtm), "l"(da), "l"(db), "r"(idesc),
+                "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtm), "l"(da), "l"(db), "r"(idesc),
                 "r"(accum));
           else
             asm volatile(
-                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtm), "l"(da), "l"(db), "r"(idesc),
+                "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtm), "l"(da), "l"(db), "r"(idesc),
                 "r"(accum));
         }
-        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+        asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
                      ::"r"(tc::smem_u32(&empty[s])), "h"(static_cast<uint16_t>(3)) : "memory");
       }
-      asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+      asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
                    ::"r"(tc::smem_u32(&tfull[acc])), "h"(static_cast<uint16_t>(3)) : "memory");
     }
   } else if (warp >= 2) {
