@@ -1434,6 +1434,10 @@ std::unique_ptr<Routine> make_contraction(const Problem& p, const Config* cfg, C
   if (p.opt.math != Math::FFMA) {
     auto tc = make_tc_contraction(p, g, cfg, cfg_out, &tc_why);
     if (tc) return tc;
+  } else if (!cfg) {
+    // NHWC convolutions: the patch-reuse FFMA instance (ffma_conv.cu)
+    std::string w;
+    if (auto conv = make_ffma_conv(p, g, &w)) return conv;
   }
   auto r = std::make_unique<GemmRoutine>(p, g);
   r->note_ = tc_why;

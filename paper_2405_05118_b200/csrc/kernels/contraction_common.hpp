@@ -69,5 +69,21 @@ std::unique_ptr<Routine> make_tc_contraction(const Problem& p, const Groups& g, 
 // (kernels/tc_conv.cu).  nullptr when the md_hom is not such a convolution.
 std::unique_ptr<Routine> make_tc_conv(const Problem& p, const Groups& g, std::string* why);
 
+// NHWC convolution read off an md_hom (MCC's views): O[n][p][q][k] =
+// sum_{r,s,c} I[n][p+r][q+s][c] * F[k][r][s][c].  Extents are the views'
+// inferred extents; strides are row-major over them.
+struct ConvShape {
+  int ib = -1, fb = -1;                 // input / filter buffers
+  int N = 0, P = 0, Q = 0, K = 0, R = 0, S = 0, C = 0;
+  int64_t H = 0, W = 0;                 // input rows / columns
+  std::vector<int64_t> oe;              // output extents [N][P][Q][K]
+};
+// True when buffers (ib, fb) form such a convolution (kernels/tc_conv.cu).
+bool nhwc_conv_shape(const Problem& p, int ib, int fb, ConvShape* s, std::string* why);
+
+// FP32 FFMA instance for NHWC convolutions with K = 64, 3x3 taps, Q % 8 == 0
+// (kernels/ffma_conv.cu); nullptr when the md_hom is not such a convolution.
+std::unique_ptr<Routine> make_ffma_conv(const Problem& p, const Groups& g, std::string* why);
+
 }  // namespace ctr
 }  // namespace mdhb

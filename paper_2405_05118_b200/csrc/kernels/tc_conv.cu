@@ -840,6 +840,34 @@ class ConvRoutine final : public Routine {
 
 }  // namespace
 
+bool nhwc_conv_shape(const Problem& p, int ib, int fb, ConvShape* cs, std::string* why) {
+  const MdHom& e = p.e;
+  if (e.D() != 7 || e.in.size() != 2 || e.out.size() != 1) return *why = "not a 7-dim two-input md_hom", false;
+  const Buf& I = e.in[static_cast<size_t>(ib)];
+  const Buf& F = e.in[static_cast<size_t>(fb)];
+  const Buf& O = e.out[0];
+  if (I.rank != 4 || F.rank != 4 || O.rank != 4) return *why = "not an NHWC convolution", false;
+  const int dn = only_dim(O.acc[0].idx[0]), dp = only_dim(O.acc[0].idx[1]), dq = only_dim(O.acc[0].idx[2]),
+            dk = only_dim(O.acc[0].idx[3]);
+  const int dr = only_dim(F.acc[0].idx[1]), ds = only_dim(F.acc[0].idx[2]), dc = only_dim(F.acc[0].idx[3]);
+  if (dn < 0 || dp < 0 || dq < 0 || dk < 0 || dr < 0 || ds < 0 || dc < 0) return *why = "not an NHWC convolution", false;
+  if (!is_dim(F.acc[0].idx[0], dk) || !is_dim(I.acc[0].idx[0], dn) || !is_sum(I.acc[0].idx[1], dp, dr) ||
+      !is_sum(I.acc[0].idx[2], dq, ds) || !is_dim(I.acc[0].idx[3], dc))
+    return *why = "not an NHWC convolution", false;
+  auto sz = [&](int d) { return static_cast<int>(e.sizes[static_cast<size_t>(d)]); };
+  cs->ib = ib;
+  cs->fb = fb;
+  cs->N = sz(dn), cs->P = sz(dp), cs->Q = sz(dq), cs->K = sz(dk), cs->R = sz(dr), cs->S = sz(ds), cs->C = sz(dc);
+  const auto& ie = p.in_ext[static_cast<size_t>(ib)];
+  const auto& fe = p.in_ext[static_cast<size_t>(fb)];
+  cs->H = ie[1];
+  cs->W = ie[2];
+  cs->oe = p.out_ext[0];
+  if (ie[3] != cs->C || fe[0] != cs->K || fe[1] != cs->R || fe[2] != cs->S || fe[3] != cs->C || cs->oe[3] != cs->K)
+    return *why = "conv extents", false;
+  return true;
+}
+
 std::unique_ptr<Routine> make_tc_conv(const Problem& p, const Groups& g, std::string* why) {
   if (std::getenv("MDHB_TC_NO_CONV")) return nullptr;
   const MdHom& e = p.e;

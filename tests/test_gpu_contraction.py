@@ -13,8 +13,10 @@ SMALL = [
     ("matmul_fp32", [128, 128, 64], "sgemm"),
     ("matmul_fp32", [256, 192, 72], "sgemm"),
     ("matmul_fp32", [64, 64, 8], "sgemm"),
-    ("mcc_nhwc", [2, 8, 8, 64, 3, 3, 64], "sgemm"),
-    ("mcc_nhwc", [4, 8, 16, 64, 3, 3, 16], "sgemm"),
+    ("mcc_nhwc", [2, 8, 8, 64, 3, 3, 64], "ffma_conv"),
+    ("mcc_nhwc", [4, 8, 16, 64, 3, 3, 16], "ffma_conv"),
+    ("mcc_nhwc", [3, 10, 16, 64, 3, 3, 24], "ffma_conv"),      # P not a multiple of the 16-row block
+    ("mcc_nhwc", [2, 56, 56, 64, 3, 3, 64], "ffma_conv"),      # conv2_x images, 7 column groups
     ("ccsdt_abcdef_gdab_efgc", [4, 4, 4, 4, 4, 4, 8], "sgemm"),
     ("ccsdt_abcdef_gdab_efgc", [8, 4, 4, 4, 8, 4, 16], "sgemm"),
     ("matmul_resnet_fc", [16, 1000, 2048], "skinny_cluster<16>"),
@@ -102,6 +104,25 @@ def _full(name, slices):
         sl = tuple(slice(s, s + n) for s, n in zip(shifts[0], part.shape))
         got = out[sl].cpu().numpy().astype(np.float64)
         assert np.array_equal(got[dfd], part[dfd]), (name, box)
+
+
+@pytest.mark.gpu
+def test_mcc_ffma_conv_matches_implicit_gemm(monkeypatch):
+    """The patch-reuse conv instance and the table-driven implicit GEMM it
+    replaces agree bit for bit on exact inputs (and with the oracle)."""
+    from paper_2405_05118_b200 import mdh
+    j = spec("mcc_nhwc", [2, 12, 24, 64, 3, 3, 32])
+    comp = mo.Computation.from_json(j)
+    ins = exact_inputs(comp, 9)
+    p = mdh.Plan(j)
+    assert "ffma_conv" in p.describe()["template"]["kernel"]
+    (a,) = run_device(p, ins)
+    monkeypatch.setenv("MDHB_NO_FFMA_CONV", "1")
+    q = mdh.Plan(j)
+    assert "sgemm" in q.describe()["template"]["kernel"]
+    (b,) = run_device(q, ins)
+    ((want, dfd),) = mo.execute(comp, ins)
+    assert np.array_equal(a, b) and np.array_equal(a.astype(np.float64)[dfd], want[dfd])
 
 
 @pytest.mark.gpu
