@@ -23,6 +23,9 @@
  *     proj/include/mdh/autotuner.hpp:38
  *   mdh::validate(cfg, expr, model, constraints)          mdh_b200_validate_config
  *     proj/include/mdh/tuning.hpp:57
+ *   mdh::simcost_objective(expr, model, cfg)              mdh_b200_simcost (host only)
+ *     proj/include/mdh/autotuner.hpp:67;                  mdh_b200_tune_ex (objective choice,
+ *     tune(..., Objective::SimCost, ...)                    SimCost seeding, start config)
  *
  * Inputs are the reference's own JSON texts, unchanged: the computation
  * (proj/src/json_io.cpp:298-328), an ASM preset name or inline ASM JSON
@@ -120,6 +123,34 @@ int mdh_b200_validate_config(const char* computation_json, const char* asm_model
 int mdh_b200_tune(const char* computation_json, const char* asm_model, const mdh_b200_options* opt, int budget,
                   uint64_t seed, char* best_config, int64_t best_cap, char* history_csv, int64_t hist_cap,
                   double* best_seconds);
+
+/* Tuning objectives of mdh_b200_tune_ex (autotuner.hpp:16, Objective). */
+enum { MDH_B200_OBJ_TIME = 0, MDH_B200_OBJ_SIMCOST = 1 };
+
+/* mdh_b200_tune with the reference's objective choice and two seeding
+ * aids:
+ *   objective       MDH_B200_OBJ_TIME: device time (as mdh_b200_tune);
+ *                   MDH_B200_OBJ_SIMCOST: the input-free SimCost model
+ *                   (simcost_objective, autotuner.cpp:58-62) -- no kernel runs
+ *   simcost_seeded  non-zero: the random phase samples the cheapest quarter of
+ *                   the candidates by SimCost instead of the whole space
+ *   start_config    NULL or a configuration JSON (e.g. the published
+ *                   tvm_gpu / ppcg_gpu fixtures) evaluated first, so hill
+ *                   climbing can start from it
+ * History rows, tie-breaking and the budget rule are mdh_b200_tune's;
+ * *best_objective is seconds (TIME) or the SimCost value (SIMCOST). */
+int mdh_b200_tune_ex(const char* computation_json, const char* asm_model, const mdh_b200_options* opt, int budget,
+                     uint64_t seed, int objective, int simcost_seeded, const char* start_config, char* best_config,
+                     int64_t best_cap, char* history_csv, int64_t hist_cap, double* best_objective);
+
+/* SimCost of a configuration (NULL config = the baseline configuration,
+ * tuning.cpp:476-503): mdh::simcost_objective(expr, model, cfg)
+ * (autotuner.cpp:58-62 = cost(simulate_trace(lower(...)), default weights
+ * 2^(M-r+1), alpha 1), interpreter.cpp:70-241).  Host only, no GPU.  The
+ * trace totals are written as JSON {"reads", "writes", "parallel_depth",
+ * "regions": {name: elements}}. */
+int mdh_b200_simcost(const char* computation_json, const char* asm_model, const char* config_json, double* cost,
+                     char* trace_json, int64_t cap, int64_t* need);
 
 /* CUDA C++ source of the kernel the plan compiled at plan time (the emitted
  * family, NVRTC); "" for the precompiled template families.  The B200

@@ -226,8 +226,14 @@ def hash_config(cfg) -> int:
 
 def cmd_tune(a) -> int:
     spec = load_spec(a.spec, a.data)
-    best, hist, secs = mdh.tune(spec, a.asm, budget=a.budget, seed=a.seed, device=a.device,
-                                math=mdh.MATH_TF32 if a.tf32 else mdh.MATH_FFMA)
+    start = None
+    if a.start:
+        _, _, _, start = load_fixture(a.start, a.data)
+        start = json.dumps(start) if not isinstance(start, str) else start
+    objective = mdh.OBJ_SIMCOST if a.objective == "simcost" else mdh.OBJ_TIME
+    best, hist, secs = mdh.tune_ex(spec, a.asm, budget=a.budget, seed=a.seed, objective=objective,
+                                   simcost_seeded=a.seed_simcost, start_config=start, device=a.device,
+                                   math=mdh.MATH_TF32 if a.tf32 else mdh.MATH_FFMA)
     rows = [r for r in hist.strip().splitlines()[1:] if r]
     print(f"evaluations: {len(rows)}")
     print(f"best objective: {secs:.9g}")
@@ -332,7 +338,11 @@ def build_parser():
     t = sub.add_parser("tune", help="search the configuration space on the device")
     source(t, config=False)
     t.add_argument("--budget", type=int, default=20)
-    t.add_argument("--objective", default="compiled", choices=["compiled", "device"])
+    t.add_argument("--objective", default="compiled", choices=["compiled", "device", "simcost"],
+                   help="compiled/device: CUDA-event time; simcost: the reference's input-free cost model")
+    t.add_argument("--seed-simcost", action="store_true",
+                   help="random phase samples the cheapest quarter of the candidates by SimCost")
+    t.add_argument("--start", help="fixture (name or file) whose configuration is evaluated first")
     t.add_argument("--out")
     t.add_argument("--history")
     t.add_argument("--tf32", action="store_true")

@@ -25,6 +25,14 @@ namespace {
 
 thread_local std::string g_err;
 
+}  // namespace
+
+namespace mdhb {
+void set_last_error(const std::string& what) { g_err = what; }
+}  // namespace mdhb
+
+namespace {
+
 std::string json_escape(const std::string& x) {
   std::string o;
   for (char c : x) {
@@ -321,6 +329,18 @@ int mdh_b200_validate_config(const char* comp_json, const char* asm_model, const
     mdhb::Asm m = mdhb::resolve_asm(asm_model ? asm_model : "B200");
     mdhb::Config c = mdhb::parse_config(config_json, e, m);
     put(mdhb::config_violation(c, e, m, true), buf, cap, need);
+  });
+}
+
+int mdh_b200_simcost(const char* comp_json, const char* asm_model, const char* config_json, double* cost,
+                     char* trace_json, int64_t cap, int64_t* need) {
+  return guard([&] {
+    mdhb::MdHom e = mdhb::parse_md_hom(comp_json);
+    mdhb::Asm m = mdhb::resolve_asm(asm_model ? asm_model : "B200");
+    mdhb::Config c = config_json ? mdhb::parse_config(config_json, e, m) : mdhb::baseline_config(e, m);
+    mdhb::SimTrace t = mdhb::simulate(c, e, m);
+    if (cost) *cost = mdhb::simcost(t, m);
+    put(t.json(m), trace_json, cap, need);
   });
 }
 

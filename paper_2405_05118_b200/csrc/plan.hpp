@@ -7,6 +7,7 @@
 
 #include <cuda_runtime.h>
 
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -80,6 +81,20 @@ std::unique_ptr<Routine> make_contraction(const Problem& p, const Config* cfg, C
 std::unique_ptr<Routine> make_generic(const Problem& p, const Config* cfg, Config* cfg_out);
 std::unique_ptr<Routine> make_scan(const Problem& p, const Config* cfg, Config* cfg_out);
 std::unique_ptr<Routine> make_emitted(const Problem& p, const Config* cfg, Config* cfg_out);
+
+// SimCost (simcost.cpp): the reference's input-free trace of a configuration
+// (interpreter.cpp:70-210) and its cost (interpreter.cpp:232-241 with the
+// default weights 2^(M-r+1) and alpha 1, autotuner.cpp:58-62).
+struct SimTrace {
+  std::map<int, int64_t> traffic;  // region id -> elements moved
+  int64_t reads = 0, writes = 0, depth = 0;
+  std::string json(const Asm& m) const;
+};
+SimTrace simulate(const Config& c, const MdHom& e, const Asm& m);
+double simcost(const SimTrace& t, const Asm& m);
+
+// The C ABI's thread-local last-error slot (abi.cu).
+void set_last_error(const std::string& what);
 
 // The candidate configurations a family can instantiate for this problem
 // (the tuner's search space), canonical Table-1 form.

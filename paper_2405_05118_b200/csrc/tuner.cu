@@ -83,6 +83,14 @@ std::vector<Config> family_space(const Problem& p, const std::string& family) {
 extern "C" int mdh_b200_tune(const char* comp_json, const char* asm_model, const mdh_b200_options* o, int budget,
                              uint64_t seed, char* best_config, int64_t best_cap, char* history_csv, int64_t hist_cap,
                              double* best_seconds) {
+  return mdh_b200_tune_ex(comp_json, asm_model, o, budget, seed, MDH_B200_OBJ_TIME, 0, nullptr, best_config, best_cap,
+                          history_csv, hist_cap, best_seconds);
+}
+
+extern "C" int mdh_b200_tune_ex(const char* comp_json, const char* asm_model, const mdh_b200_options* o, int budget,
+                                uint64_t seed, int objective, int simcost_seeded, const char* start_config,
+                                char* best_config, int64_t best_cap, char* history_csv, int64_t hist_cap,
+                                double* best_seconds) {
   using namespace mdhb;
   mdh_b200_plan* probe = nullptr;
   if (mdh_b200_plan_create(comp_json, asm_model, nullptr, o, &probe)) return 1;
@@ -140,6 +148,39 @@ extern "C" int mdh_b200_tune(const char* comp_json, const char* asm_model, const
     if (space.empty()) space.push_back(baseline_config(prob.e, prob.m));
     std::vector<std::string> texts;
     for (auto& c : space) texts.push_back(config_json(c, prob.e, prob.m));
+    // a start configuration (e.g. a published fixture, tvm_gpu.json) joins the
+    // space if it is not already in it, and is evaluated first
+    int start_i = -1;
+    if (start_config) {
+      Config sc = parse_config(start_config, prob.e, prob.m);
+      std::string st = config_json(sc, prob.e, prob.m);
+      for (size_t i = 0; i < texts.size(); ++i)
+        if (texts[i] == st) start_i = static_cast<int>(i);
+      if (start_i < 0) {
+        space.push_back(sc);
+        texts.push_back(st);
+        start_i = static_cast<int>(space.size()) - 1;
+      }
+    }
+    // SimCost of every candidate (host only): the objective itself, or the
+    // seed order -- the random phase draws from the cheapest quarter
+    std::vector<double> sim(space.size(), std::numeric_limits<double>::infinity());
+    if (objective == MDH_B200_OBJ_SIMCOST || simcost_seeded)
+      for (size_t i = 0; i < space.size(); ++i) {
+        try {
+          sim[i] = simcost(simulate(space[i], prob.e, prob.m), prob.m);
+        } catch (const Error&) {
+        }
+      }
+    std::vector<int> pool(space.size());
+    for (size_t i = 0; i < pool.size(); ++i) pool[i] = static_cast<int>(i);
+    if (simcost_seeded) {
+      std::stable_sort(pool.begin(), pool.end(), [&](int a, int b) {
+        if (sim[static_cast<size_t>(a)] != sim[static_cast<size_t>(b)]) return sim[static_cast<size_t>(a)] < sim[static_cast<size_t>(b)];
+        return fnv1a(texts[static_cast<size_t>(a)]) < fnv1a(texts[static_cast<size_t>(b)]);
+      });
+      pool.resize(std::max<size_t>(1, (pool.size() + 3) / 4));
+    }
 
     std::mt19937_64 rng(seed);
     struct Ev {
@@ -157,6 +198,11 @@ extern "C" int mdh_b200_tune(const char* comp_json, const char* asm_model, const
       bool valid = true;
       if (memo[static_cast<size_t>(i)] >= 0) {
         obj = memo[static_cast<size_t>(i)];
+        valid = std::isfinite(obj);
+      } else if (objective == MDH_B200_OBJ_SIMCOST) {
+        obj = sim[static_cast<size_t>(i)];
+        valid = std::isfinite(obj);
+        memo[static_cast<size_t>(i)] = obj;
       } else {
         mdh_b200_plan* pl = nullptr;
         if (mdh_b200_plan_create(comp_json, asm_model, texts[static_cast<size_t>(i)].c_str(), o, &pl) == 0) {
@@ -178,8 +224,14 @@ extern "C" int mdh_b200_tune(const char* comp_json, const char* asm_model, const
       return obj;
     };
     const int n = static_cast<int>(space.size());
+    const int np = static_cast<int>(pool.size());
     int n_random = std::min(budget, std::max(1, budget * 3 / 10));
-    for (int k = 0; k < n_random; ++k) evaluate(static_cast<int>(rng() % static_cast<uint64_t>(n)));
+    int k0 = 0;
+    if (start_i >= 0) {
+      evaluate(start_i);
+      k0 = 1;
+    }
+    for (int k = k0; k < n_random; ++k) evaluate(pool[static_cast<size_t>(rng() % static_cast<uint64_t>(np))]);
     while (static_cast<int>(hist.size()) < budget) {
       bool improved = false;
       if (best_i >= 0) {
@@ -218,10 +270,7 @@ extern "C" int mdh_b200_tune(const char* comp_json, const char* asm_model, const
     if (best_seconds) *best_seconds = best;
   } catch (const Error& e) {
     rc = 1;
-    // surface through the ABI's last-error slot: re-run a failing call
-    mdh_b200_plan* dummy = nullptr;
-    mdh_b200_plan_create("{", asm_model, nullptr, o, &dummy);
-    (void)e;
+    set_last_error(e.what());
   }
   for (void* d : din) cudaFree(d);
   for (void* d : dout) cudaFree(d);

@@ -35,9 +35,10 @@ _NP = {F32: np.float32, F64: np.float64, I32: np.int32, I64: np.int64}
 EXPORTED = [
     "mdh_b200_default_options", "mdh_b200_plan_create", "mdh_b200_plan_destroy", "mdh_b200_buffer_count",
     "mdh_b200_buffer_info", "mdh_b200_run", "mdh_b200_run_host", "mdh_b200_time", "mdh_b200_describe",
-    "mdh_b200_validate_config", "mdh_b200_tune", "mdh_b200_launches_per_run", "mdh_b200_kernel_source", "mdh_b200_last_error",
-    "mdh_b200_version",
+    "mdh_b200_validate_config", "mdh_b200_tune", "mdh_b200_tune_ex", "mdh_b200_simcost", "mdh_b200_launches_per_run",
+    "mdh_b200_kernel_source", "mdh_b200_last_error", "mdh_b200_version",
 ]
+OBJ_TIME, OBJ_SIMCOST = 0, 1
 
 
 class MdhError(RuntimeError):
@@ -65,6 +66,11 @@ def lib():
         L = ctypes.CDLL(LIB_PATH)
         L.mdh_b200_last_error.restype = ctypes.c_char_p
         L.mdh_b200_version.restype = ctypes.c_char_p
+        c, v, i64, d = ctypes.c_char_p, ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_double)
+        L.mdh_b200_simcost.argtypes = [c, c, c, d, c, i64, ctypes.POINTER(ctypes.c_int64)]
+        L.mdh_b200_tune_ex.argtypes = [c, c, v, ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, c, c, i64, c,
+                                       i64, d]
+        L.mdh_b200_tune.argtypes = [c, c, v, ctypes.c_int, ctypes.c_uint64, c, i64, c, i64, d]
         _lib = L
     return _lib
 
@@ -237,6 +243,32 @@ def tune(spec, asm="B200", budget=20, seed=0, **kw):
     _check(lib().mdh_b200_tune(_text(spec), _text(asm), ctypes.byref(o), budget, ctypes.c_uint64(seed), best,
                                1 << 20, hist, 1 << 20, ctypes.byref(secs)))
     return best.value.decode(), hist.value.decode(), secs.value
+
+
+def tune_ex(spec, asm="B200", budget=20, seed=0, objective=OBJ_TIME, simcost_seeded=False, start_config=None, **kw):
+    """mdh::tune with the objective choice (device time | SimCost), SimCost
+    seeding of the random phase and an optional start configuration ->
+    (best_config_json, history_csv, best_objective)."""
+    o = options(**kw)
+    best = ctypes.create_string_buffer(1 << 20)
+    hist = ctypes.create_string_buffer(1 << 20)
+    val = ctypes.c_double()
+    _check(lib().mdh_b200_tune_ex(_text(spec), _text(asm), ctypes.byref(o), budget, ctypes.c_uint64(seed),
+                                  int(objective), int(bool(simcost_seeded)), _text(start_config) if start_config else None,
+                                  best, 1 << 20, hist, 1 << 20, ctypes.byref(val)))
+    return best.value.decode(), hist.value.decode(), val.value
+
+
+def simcost(spec, asm="B200", config=None):
+    """mdh::simcost_objective (autotuner.cpp:58-62) -> (cost, trace totals dict).
+    Host only: no GPU is touched."""
+    cost = ctypes.c_double()
+    need = ctypes.c_int64()
+    cfg = _text(config) if config is not None else None
+    _check(lib().mdh_b200_simcost(_text(spec), _text(asm), cfg, ctypes.byref(cost), None, 0, ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    _check(lib().mdh_b200_simcost(_text(spec), _text(asm), cfg, ctypes.byref(cost), buf, need.value, ctypes.byref(need)))
+    return cost.value, json.loads(buf.value.decode())
 
 
 def version() -> str:

@@ -56,3 +56,26 @@ def test_tvm_gpu_fixture_runs_through_config():
     (got,) = run_device(plan, ins)
     ((want, dfd),) = mo.execute(comp, ins)
     assert np.array_equal(got.astype(np.float64), want)
+
+
+@pytest.mark.gpu
+def test_tune_simcost_objective_and_seeding():
+    """Objective::SimCost runs no kernel and returns the candidate with the
+    lowest SimCost it visited (its objective equals mdh_b200_simcost of the
+    returned config); SimCost seeding and a start configuration keep the
+    history contract, and the start config is the first row."""
+    from paper_2405_05118_b200 import mdh
+    j = json.dumps(spec("matmul_fp32", [256, 256, 128]))
+    best, hist, val = mdh.tune_ex(j, "B200", budget=8, seed=3, objective=mdh.OBJ_SIMCOST)
+    rows = hist.strip().splitlines()
+    assert rows[0] == "eval_index,config_hash,objective,valid" and len(rows) == 9
+    assert val == mdh.simcost(j, "B200", best)[0]
+    assert val == min(float(r.split(",")[2]) for r in rows[1:] if r.split(",")[3] == "1")
+    # device-time objective, SimCost-seeded, starting from that best
+    best2, hist2, secs = mdh.tune_ex(j, "B200", budget=6, seed=3, simcost_seeded=True, start_config=best)
+    rows2 = hist2.strip().splitlines()
+    assert len(rows2) == 7 and secs > 0
+    # ties on the objective go to the lowest config hash (autotuner.cpp:263-271)
+    best_hash = str(min(int(r.split(",")[1]) for r in rows[1:] if r.split(",")[3] == "1" and float(r.split(",")[2]) == val))
+    assert rows2[1].split(",")[1] == best_hash  # the start configuration is evaluated first
+    assert mdh.validate_config(j, "B200", best2) == ""
