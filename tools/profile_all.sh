@@ -4,7 +4,7 @@
 # (tools/ncu_summary.py) + .hot.txt (tools/sass_hot.py) and deleted unless
 # KEEP_REP=1, so the results fit gpurun's 64 MiB return limit.  Here:
 #   python tools/ncu_summary.py --by-routine gpurun_out <tag>
-KRE='regex:star7|gemv|sgemm|skinny|tc_gemm|tc_conv|prl_main|vm_|scan_|layout|pack_'
+KRE='regex:star7|gemv|sgemm|skinny|tc_gemm|tc_conv|ffma_conv|prl_main|vm_|scan_|layout|pack_|mdh_emitted'
 for r in "$@"; do
   f=${r/:/__}
   timeout 600 ncu --set full --clock-control none --import-source on -k "$KRE" -c 8 \
