@@ -261,6 +261,194 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, TMEM_COLS);
 }
 
+// BF16 instance with the fp32 -> bf16 conversion fused (MDHB_CONV_BF16F):
+// the producer lands each 32-channel fp32 half-chunk of the patch with a 4-D
+// TMA box {32 c, WQ, HP, 1} into a 2-slot staging ring; four converter warps
+// turn two halves into one 64-channel bf16 patch slot -- pixel rows of 128
+// bytes written with the 128-byte swizzle TMA would apply (16-byte chunk
+// index XOR address bits 7..9) -- fence them into the async proxy and arrive
+// on the slot's full barrier.  The MMA warp and the TMA-store epilogue are
+// tc_conv_tf32<BF16>'s.  The input is read once as fp32; no bf16 copy of it
+// exists in HBM.
+template <int BN, int PST, int FS>
+__global__ void __launch_bounds__(320, 1)
+    tc_conv_bf16f(const __grid_constant__ CUtensorMap tma_i, const __grid_constant__ CUtensorMap tma_f,
+                  const __grid_constant__ CUtensorMap tma_o, ConvArgs g) {
+  constexpr uint32_t B_BYTES = BN * 128;  // one 64-channel bf16 k-tile of the filter
+  constexpr uint32_t TMEM_COLS = 2 * BN <= 128 ? 128 : 256;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int chunks = g.C / 64;
+  const int ktiles = g.R * g.S * chunks;
+  const int npx = g.HP * g.WQ;
+  const uint32_t patch_bytes = static_cast<uint32_t>(npx) * 128;
+  const uint32_t patch_slot = (patch_bytes + 1023) & ~1023u;
+  uint8_t* sB = smem;
+  uint8_t* sP = sB + static_cast<size_t>(ktiles) * B_BYTES;  // bf16 patch ring
+  uint8_t* sF = sP + static_cast<size_t>(PST) * patch_slot;  // fp32 staging ring
+  uint64_t* full = reinterpret_cast<uint64_t*>(sF + FS * patch_slot);
+  uint64_t* empty = full + PST;
+  uint64_t* sfull = empty + PST;
+  uint64_t* sempty = sfull + FS;
+  uint64_t* bfull = sempty + FS;
+  uint64_t* tfull = bfull + 1;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const uint32_t ostage = (tc::smem_u32(full) + 256 + 1023) & ~1023u;
+  const int warp = tc::warp_uniform(), lane = threadIdx.x & 31;
+  const int per_img = g.pblocks * g.qblocks;
+  const int ntiles = g.N * per_img;
+
+  if (threadIdx.x == 0) {
+    tc::tma_prefetch(&tma_i);
+    tc::tma_prefetch(&tma_f);
+    for (int s = 0; s < PST; ++s) {
+      tc::mbar_init(&full[s], 4);   // one arrival per converter warp
+      tc::mbar_init(&empty[s], 1);  // MMA commit
+    }
+    for (int s = 0; s < FS; ++s) {
+      tc::mbar_init(&sfull[s], 1);
+      tc::mbar_init(&sempty[s], 4);
+    }
+    tc::mbar_init(bfull, 1);
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 4);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, TMEM_COLS);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer: the bf16 filter once, then fp32 half-chunks
+    tc::mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(ktiles) * B_BYTES);
+    for (int kt = 0; kt < ktiles; ++kt) {
+      int c[5] = {kt * 64, 0, 0, 0, 0};
+      tc::tma_load(sB + static_cast<size_t>(kt) * B_BYTES, &tma_f, bfull, 2, c);
+    }
+    uint32_t it = 0;
+    for (int x = blockIdx.x; x < ntiles; x += gridDim.x) {
+      const int n = x / per_img, rem = x % per_img, pb = rem / g.qblocks, qb = rem % g.qblocks;
+      for (int h = 0; h < 2 * chunks; ++h, ++it) {
+        const uint32_t s = it % FS;
+        if (it >= FS) tc::mbar_wait(&sempty[s], ((it / FS) - 1) & 1);
+        tc::mbar_arrive_expect_tx(&sfull[s], patch_bytes);
+        int c[5] = {h * 32, qb * CV_TQ, pb * CV_TP, n, 0};
+        tc::tma_load(sF + s * patch_slot, &tma_i, &sfull[s], 4, c);
+      }
+    }
+  } else if (warp >= 6) {
+    // ---------------- converters: two fp32 halves -> one swizzled bf16 slot
+    const int ct = threadIdx.x - 192;  // 0..127
+    uint32_t it = 0, ps = 0;
+    for (int x = blockIdx.x; x < ntiles; x += gridDim.x) {
+      for (int cc = 0; cc < chunks; ++cc, ++ps) {
+        const uint32_t s = ps % PST;
+        if (ps >= PST) tc::mbar_wait(&empty[s], ((ps / PST) - 1) & 1);
+        const uint32_t dst = tc::smem_u32(sP + s * patch_slot);
+        for (int h = 0; h < 2; ++h, ++it) {
+          const uint32_t fs = it % FS;
+          tc::mbar_wait(&sfull[fs], (it / FS) & 1);
+          const uint32_t src = tc::smem_u32(sF + fs * patch_slot);
+          for (int i = ct; i < npx * 8; i += 128) {
+            const int px = i >> 3, c4 = i & 7;
+            float4 v;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                         : "r"(src + static_cast<uint32_t>(px) * 128 + c4 * 16));
+            __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+            const uint32_t row = dst + static_cast<uint32_t>(px) * 128;
+            const uint32_t chunk = static_cast<uint32_t>(h * 4 + (c4 >> 1)) ^ ((row >> 7) & 7u);
+            asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(row + chunk * 16 + (c4 & 1) * 8),
+                         "r"(*reinterpret_cast<uint32_t*>(&lo)), "r"(*reinterpret_cast<uint32_t*>(&hi))
+                         : "memory");
+          }
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&sempty[fs]);
+        }
+        tc::fence_proxy_async();  // generic-proxy writes -> visible to tcgen05 (async proxy)
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (whole warp, uniform descriptors)
+    constexpr uint32_t idesc = tc::instr_desc(1, 0, 0, CV_BM, BN);
+    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+    const uint64_t da0 = tc::umma_desc(tc::smem_u32(sP), 16, static_cast<uint32_t>(g.WQ) * 128, 2);
+    const uint64_t db0 = tc::sw128_desc(tc::smem_u32(sB), 16, 1024);
+    const uint32_t slot_u = patch_slot >> 4, btap_u = (static_cast<uint32_t>(chunks) * B_BYTES) >> 4;
+    tc::mbar_wait_warp(bfull, 0);
+    uint32_t it = 0, tl = 0;
+    for (int x = blockIdx.x; x < ntiles; x += gridDim.x, ++tl) {
+      const uint32_t acc = tl & 1;
+      if (tl >= 2) tc::mbar_wait_warp(&tempty[acc], ((tl / 2) - 1) & 1);
+      tc::tc_fence_after();
+      const uint32_t dtm = tm + acc * BN;
+      for (int cc = 0; cc < chunks; ++cc, ++it) {
+        const uint32_t s = it % PST;
+        tc::mbar_wait_warp(&full[s], (it / PST) & 1);
+        tc::tc_fence_after();
+        const uint64_t dA = da0 + s * slot_u;
+        uint64_t dB = db0 + ((static_cast<uint32_t>(cc) * B_BYTES) >> 4);
+        uint32_t first = cc == 0 ? 1u : 0u;
+        for (int r = 0; r < g.R; ++r)
+          for (int ss = 0; ss < g.S; ++ss, dB += btap_u) {
+            const uint64_t a = dA + static_cast<uint32_t>(r * g.WQ + ss) * 8;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              tc::mma_warp<false>(dtm, a + j * 2, dB + 2 * j, idesc, first ? 0u : 1u);
+              first = 0;
+            }
+          }
+        tc::mma_commit_warp(&empty[s]);
+      }
+      tc::mma_commit_warp(&tfull[acc]);
+    }
+  } else if (warp >= 2) {
+    // ---------------- epilogue (TMA tensor stores), as tc_conv_tf32
+    const int q = warp & 3;
+    const uint32_t stg = ostage + static_cast<uint32_t>(warp - 2) * 8192;
+    uint32_t tl = 0;
+    for (int x = blockIdx.x; x < ntiles; x += gridDim.x, ++tl) {
+      const int n = x / per_img, rem = x % per_img, pb = rem / g.qblocks, qb = rem % g.qblocks;
+      const uint32_t acc = tl & 1;
+      tc::mbar_wait(&tfull[acc], (tl / 2) & 1);
+      tc::tc_fence_after();
+      if (lane == 0) tc::bulk_wait_read0();
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < BN / 32; ++h) {
+        uint32_t rv[32];
+        tc::tmem_ld32(tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(h * 32), rv);
+        const uint32_t row = stg + static_cast<uint32_t>(h) * 4096 + static_cast<uint32_t>(lane) * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + ((c ^ (lane & 7)) << 4)), "r"(rv[4 * c]),
+                       "r"(rv[4 * c + 1]), "r"(rv[4 * c + 2]), "r"(rv[4 * c + 3])
+                       : "memory");
+      }
+      tc::tc_fence_before();
+      tc::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        tc::mbar_arrive(&tempty[acc]);
+#pragma unroll
+        for (int h = 0; h < BN / 32; ++h)
+          tc::tma_store4(&tma_o, stg + static_cast<uint32_t>(h) * 4096, h * 32, qb * CV_TQ, pb * CV_TP + q * 4, n);
+        tc::bulk_commit();
+      }
+    }
+    if (lane == 0) tc::bulk_wait0();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, TMEM_COLS);
+}
+
 // CTA-pair instance (cta_group::2): the two CTAs of a cluster take two
 // output tiles, each lands its own input patches, and each holds HALF of the
 // resident filter (32 of the 64 output channels); the leader issues
@@ -561,14 +749,14 @@ class ConvRoutine final : public Routine {
   ConvRoutine(const Problem& p, int ib, int fb) : p_(p), ib_(ib), fb_(fb) {}
   const char* family() const override { return "contraction"; }
   const char* bound() const override { return "tensor"; }
-  int launches() const override { return bf16_ ? 3 : 1; }
+  int launches() const override { return fused_ ? 2 : bf16_ ? 3 : 1; }
   double flops() const override {
     return 2.0 * a_.N * a_.P * a_.Q * static_cast<double>(a_.K) * a_.R * a_.S * a_.C;
   }
   double bytes() const override { return static_cast<double>(p_.in_bytes + p_.out_bytes); }
   std::string describe() const override {
     std::ostringstream os;
-    os << "{\"kernel\": \"" << (two_sm_ ? "tc_conv_2sm<" : bf16_ ? "tc_conv_bf16<" : "tc_conv_tf32<") << a_.K
+    os << "{\"kernel\": \"" << (two_sm_ ? "tc_conv_2sm<" : fused_ ? "tc_conv_bf16f<" : bf16_ ? "tc_conv_bf16<" : "tc_conv_tf32<") << a_.K
        << ">\", \"math\": \"" << (bf16_ ? "bf16" : "tf32") << "\", \"M\": "
        << static_cast<int64_t>(a_.N) * a_.P * a_.Q << ", \"N\": " << a_.K << ", \"K\": " << a_.R * a_.S * a_.C
        << ", \"tile\": \"16 p x 8 q x " << a_.K << " k\", \"patch\": [" << a_.HP << ", " << a_.WQ << ", 32]"
@@ -577,7 +765,8 @@ class ConvRoutine final : public Routine {
        << "\", \"umma\": \"tcgen05.mma.cta_group::" << (two_sm_ ? "2" : "1") << ".kind::" << (bf16_ ? "f16 (bf16) M" : "tf32 M")
        << (two_sm_ ? 256 : 128) << "xN" << a_.K
        << (bf16_ ? "xK16" : "xK8") << ", A no-swizzle shifted descriptors, B resident 128B-swizzled\", \"smem\": " << smem_
-       << (bf16_ ? ", \"conversion\": \"to_bf16 of input and filter per run\"" : "")
+       << (fused_ ? ", \"conversion\": \"input fp32 -> bf16 in-kernel (4 converter warps, 2 + 3 slot rings); to_bf16 of the filter per run\""
+                  : bf16_ ? ", \"conversion\": \"to_bf16 of input and filter per run\"" : "")
        << ", \"epilogue\": \"" << (a_.tma_store ? "TMA tensor store (128B-swizzled 4p x 8q x 32k boxes)" : "smem transpose + st.global")
        << "\"}";
     return os.str();
@@ -656,6 +845,20 @@ class ConvRoutine final : public Routine {
     two_sm_ = smem2_ <= 227 * 1024 && !std::getenv("MDHB_CONV_1SM") && !std::getenv("MDHB_TC_1SM") &&
               (!bf16_ || std::getenv("MDHB_CONV_2SM"));
     if (a_.plane / 16 >= (1u << 14)) return *why = "conv instance: patch plane too large for a descriptor", false;
+    // bf16 with the conversion fused into the conv kernel (default; measured
+    // 0.102 vs 0.128 ms with the separate to_bf16 pass; MDHB_CONV_NO_BF16F=1 off)
+    if (bf16_ && a_.sw && a_.tma_store && !std::getenv("MDHB_CONV_NO_BF16F") && !std::getenv("MDHB_CONV_2SM")) {
+      const size_t slot = (static_cast<size_t>(a_.HP) * a_.WQ * 128 + 1023) / 1024 * 1024;
+      auto fsm = [&](int pst) {
+        return static_cast<size_t>(ktiles) * a_.K * 128 + (pst + 2) * slot + 256 + 1024 + 4 * 8192 + 1024;  // pst + fs = 5
+      };
+      // 5 slots fit at conv2_x: 2 bf16 + 3 fp32 (MDHB_CONV_BF16F_PST=3: 3 + 2)
+      pstf_ = std::getenv("MDHB_CONV_BF16F_PST") ? std::atoi(std::getenv("MDHB_CONV_BF16F_PST")) : 2;
+      if (pstf_ != 3) pstf_ = 2;
+      if (fsm(3) > 227 * 1024) pstf_ = 2;
+      smemf_ = fsm(3);
+      fused_ = smemf_ <= 227 * 1024;
+    }
     // input and filter extents for the tensor maps
     H_ = ie[1];
     W_ = ie[2];
@@ -670,7 +873,39 @@ class ConvRoutine final : public Routine {
     const void* I = d_in[ib_];
     const void* F = d_in[fb_];
     const int sms0 = sm_count(p_.opt.device);
-    if (bf16_) {
+    if (fused_) {
+      // the filter alone is converted (147 KB); the input is read as fp32 by the kernel
+      const int64_t nf = FK_ * a_.K;
+      if (!fbf_) MDHB_CUDA(cudaMalloc(&fbf_, static_cast<size_t>(nf) * 2 + 16));
+      to_bf16<<<static_cast<unsigned>(std::min<int64_t>(8 * sms0, (nf / 8 + 255) / 256)), 256, 0, s>>>(
+          static_cast<const float*>(F), static_cast<__nv_bfloat16*>(fbf_), nf / 8);
+      MDHB_CUDA(cudaGetLastError());
+      if (!bf_maps_) {
+        cuuint64_t fd[2] = {static_cast<cuuint64_t>(FK_), static_cast<cuuint64_t>(a_.K)};
+        cuuint64_t fs[1] = {static_cast<cuuint64_t>(FK_) * 2};
+        cuuint32_t fbx[2] = {64, static_cast<cuuint32_t>(a_.K)};
+        cuuint32_t es[4] = {1, 1, 1, 1};
+        CUresult r = conv_encoder()(&mf_, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, fbf_, fd, fs, fbx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) fail("CudaError", "cuTensorMapEncodeTiled (bf16 conv filter) failed");
+        bf_maps_ = true;
+      }
+      if (I != last_i_) {
+        // fp32 input, pixel-major {C, W, H, N}, box {32 c, WQ, HP, 1}, no swizzle: [HP][WQ][32] staging
+        cuuint64_t d4[4] = {static_cast<cuuint64_t>(a_.C), static_cast<cuuint64_t>(W_), static_cast<cuuint64_t>(H_),
+                            static_cast<cuuint64_t>(a_.N)};
+        cuuint64_t s4[3] = {static_cast<cuuint64_t>(a_.C) * 4, static_cast<cuuint64_t>(W_ * a_.C) * 4,
+                            static_cast<cuuint64_t>(H_ * W_ * a_.C) * 4};
+        cuuint32_t b4[4] = {32, static_cast<cuuint32_t>(a_.WQ), static_cast<cuuint32_t>(a_.HP), 1};
+        cuuint32_t e4[4] = {1, 1, 1, 1};
+        CUresult r = conv_encoder()(&mi_, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(I), d4, s4, b4, e4,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) fail("CudaError", "cuTensorMapEncodeTiled (fused bf16 conv input) failed");
+        last_i_ = I;
+      }
+      last_f_ = F;
+    } else if (bf16_) {
       // operand conversion (layout_de): fp32 views -> bf16 copies of the same layout
       const int64_t ni = static_cast<int64_t>(a_.N) * H_ * W_ * a_.C, nf = FK_ * a_.K;
       if (!ibf_) {
@@ -808,6 +1043,13 @@ class ConvRoutine final : public Routine {
       return;
     }
     const int64_t tiles = static_cast<int64_t>(a_.N) * a_.pblocks * a_.qblocks;
+    if (fused_) {
+      auto kf = pstf_ == 3 ? tc_conv_bf16f<64, 3, 2> : tc_conv_bf16f<64, 2, 3>;
+      MDHB_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smemf_)));
+      kf<<<static_cast<unsigned>(std::min<int64_t>(sms, tiles)), 320, smemf_, s>>>(mi_, mf_, mo_, a);
+      MDHB_CUDA(cudaGetLastError());
+      return;
+    }
     auto k = bf16_ ? (pst_ == 4 ? tc_conv_tf32<64, true, 4> : tc_conv_tf32<64, true, 2>) : tc_conv_tf32<64>;
     MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_)));
     k<<<static_cast<unsigned>(std::min<int64_t>(sms, tiles)), 192, smem_, s>>>(mi_, mf_, mo_, a);
@@ -822,7 +1064,9 @@ class ConvRoutine final : public Routine {
   size_t smem_ = 0, smem2_ = 0;
   bool two_sm_ = false;
   bool bf16_ = false, bf_maps_ = false;
-  int pst_ = 2, pst2_ = 3;
+  int pst_ = 2, pst2_ = 3, pstf_ = 3;
+  bool fused_ = false;
+  size_t smemf_ = 0;
   void *ibf_ = nullptr, *fbf_ = nullptr;
 
  public:
