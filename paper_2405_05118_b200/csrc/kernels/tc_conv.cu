@@ -29,6 +29,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <sstream>
@@ -270,7 +271,7 @@ __global__ void __launch_bounds__(192, 1)
 // on the slot's full barrier.  The MMA warp and the TMA-store epilogue are
 // tc_conv_tf32<BF16>'s.  The input is read once as fp32; no bf16 copy of it
 // exists in HBM.
-template <int BN, int PST, int FS>
+template <int BN, int PST, int FS, int EH>
 __global__ void __launch_bounds__(320, 1)
     tc_conv_bf16f(const __grid_constant__ CUtensorMap tma_i, const __grid_constant__ CUtensorMap tma_f,
                   const __grid_constant__ CUtensorMap tma_o, ConvArgs g) {
@@ -282,7 +283,9 @@ __global__ void __launch_bounds__(320, 1)
   const int ktiles = g.R * g.S * chunks;
   const int npx = g.HP * g.WQ;
   const uint32_t patch_bytes = static_cast<uint32_t>(npx) * 128;
-  const uint32_t patch_slot = (patch_bytes + 1023) & ~1023u;
+  // slots need only 128-byte alignment: the bf16 slots' swizzle is a function
+  // of absolute address bits on both sides (converter stores, UMMA reads)
+  const uint32_t patch_slot = patch_bytes;
   uint8_t* sB = smem;
   uint8_t* sP = sB + static_cast<size_t>(ktiles) * B_BYTES;  // bf16 patch ring
   uint8_t* sF = sP + static_cast<size_t>(PST) * patch_slot;  // fp32 staging ring
@@ -409,38 +412,41 @@ __global__ void __launch_bounds__(320, 1)
       tc::mma_commit_warp(&tfull[acc]);
     }
   } else if (warp >= 2) {
-    // ---------------- epilogue (TMA tensor stores), as tc_conv_tf32
+    // ---------------- epilogue (TMA tensor stores), as tc_conv_tf32; EH = 32-channel
+    // halves buffered per warp (1: the second half waits for the first's smem read)
     const int q = warp & 3;
-    const uint32_t stg = ostage + static_cast<uint32_t>(warp - 2) * 8192;
+    const uint32_t stg = ostage + static_cast<uint32_t>(warp - 2) * 4096 * EH;
     uint32_t tl = 0;
     for (int x = blockIdx.x; x < ntiles; x += gridDim.x, ++tl) {
       const int n = x / per_img, rem = x % per_img, pb = rem / g.qblocks, qb = rem % g.qblocks;
       const uint32_t acc = tl & 1;
       tc::mbar_wait(&tfull[acc], (tl / 2) & 1);
       tc::tc_fence_after();
-      if (lane == 0) tc::bulk_wait_read0();
-      __syncwarp();
 #pragma unroll
       for (int h = 0; h < BN / 32; ++h) {
+        if (EH == 1 || h == 0) {
+          if (lane == 0) tc::bulk_wait_read0();
+          __syncwarp();
+        }
         uint32_t rv[32];
         tc::tmem_ld32(tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(h * 32), rv);
-        const uint32_t row = stg + static_cast<uint32_t>(h) * 4096 + static_cast<uint32_t>(lane) * 128;
+        const uint32_t hb = stg + static_cast<uint32_t>(EH == 1 ? 0 : h) * 4096;
+        const uint32_t row = hb + static_cast<uint32_t>(lane) * 128;
 #pragma unroll
         for (int c = 0; c < 8; ++c)
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + ((c ^ (lane & 7)) << 4)), "r"(rv[4 * c]),
                        "r"(rv[4 * c + 1]), "r"(rv[4 * c + 2]), "r"(rv[4 * c + 3])
                        : "memory");
+        tc::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          tc::tma_store4(&tma_o, hb, h * 32, qb * CV_TQ, pb * CV_TP + q * 4, n);
+          tc::bulk_commit();
+        }
       }
       tc::tc_fence_before();
-      tc::fence_proxy_async();
       __syncwarp();
-      if (lane == 0) {
-        tc::mbar_arrive(&tempty[acc]);
-#pragma unroll
-        for (int h = 0; h < BN / 32; ++h)
-          tc::tma_store4(&tma_o, stg + static_cast<uint32_t>(h) * 4096, h * 32, qb * CV_TQ, pb * CV_TP + q * 4, n);
-        tc::bulk_commit();
-      }
+      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
     }
     if (lane == 0) tc::bulk_wait0();
   }
@@ -765,7 +771,7 @@ class ConvRoutine final : public Routine {
        << "\", \"umma\": \"tcgen05.mma.cta_group::" << (two_sm_ ? "2" : "1") << ".kind::" << (bf16_ ? "f16 (bf16) M" : "tf32 M")
        << (two_sm_ ? 256 : 128) << "xN" << a_.K
        << (bf16_ ? "xK16" : "xK8") << ", A no-swizzle shifted descriptors, B resident 128B-swizzled\", \"smem\": " << smem_
-       << (fused_ ? ", \"conversion\": \"input fp32 -> bf16 in-kernel (4 converter warps, 2 + 3 slot rings); to_bf16 of the filter per run\""
+       << (fused_ ? ", \"conversion\": \"input fp32 -> bf16 in-kernel (4 converter warps, bf16 + fp32 slot rings); to_bf16 of the filter per run\""
                   : bf16_ ? ", \"conversion\": \"to_bf16 of input and filter per run\"" : "")
        << ", \"epilogue\": \"" << (a_.tma_store ? "TMA tensor store (128B-swizzled 4p x 8q x 32k boxes)" : "smem transpose + st.global")
        << "\"}";
@@ -849,14 +855,21 @@ class ConvRoutine final : public Routine {
     // 0.102 vs 0.128 ms with the separate to_bf16 pass; MDHB_CONV_NO_BF16F=1 off)
     if (bf16_ && a_.sw && a_.tma_store && !std::getenv("MDHB_CONV_NO_BF16F") && !std::getenv("MDHB_CONV_2SM")) {
       const size_t slot = (static_cast<size_t>(a_.HP) * a_.WQ * 128 + 1023) / 1024 * 1024;
-      auto fsm = [&](int pst) {
-        return static_cast<size_t>(ktiles) * a_.K * 128 + (pst + 2) * slot + 256 + 1024 + 4 * 8192 + 1024;  // pst + fs = 5
+      // rings: bf16 slots + fp32 staging slots (128-byte aligned) and the
+      // epilogue's per-warp buffer of 1 or 2 32-channel halves
+      const size_t slot128 = static_cast<size_t>(a_.HP) * a_.WQ * 128;
+      auto fsm = [&](int nslots, int eh) {
+        return static_cast<size_t>(ktiles) * a_.K * 128 + nslots * slot128 + 256 + 1024 + 4 * 4096 * eh + 1024;
       };
-      // 5 slots fit at conv2_x: 2 bf16 + 3 fp32 (MDHB_CONV_BF16F_PST=3: 3 + 2)
-      pstf_ = std::getenv("MDHB_CONV_BF16F_PST") ? std::atoi(std::getenv("MDHB_CONV_BF16F_PST")) : 2;
-      if (pstf_ != 3) pstf_ = 2;
-      if (fsm(3) > 227 * 1024) pstf_ = 2;
-      smemf_ = fsm(3);
+      (void)slot;
+      if (const char* v = std::getenv("MDHB_CONV_BF16F_CFG")) {  // "PST,FS,EH" (dev)
+        std::sscanf(v, "%d,%d,%d", &pstf_, &fsf_, &ehf_);
+      } else if (fsm(6, 1) <= 227 * 1024) {
+        pstf_ = 3, fsf_ = 3, ehf_ = 1;  // measured: 3 + 3 0.091 ms, 2 + 4 0.101, 2 + 3 (2 halves) 0.104
+      } else {
+        pstf_ = 2, fsf_ = 3, ehf_ = 2;
+      }
+      smemf_ = fsm(pstf_ + fsf_, ehf_);
       fused_ = smemf_ <= 227 * 1024;
     }
     // input and filter extents for the tensor maps
@@ -1044,7 +1057,12 @@ class ConvRoutine final : public Routine {
     }
     const int64_t tiles = static_cast<int64_t>(a_.N) * a_.pblocks * a_.qblocks;
     if (fused_) {
-      auto kf = pstf_ == 3 ? tc_conv_bf16f<64, 3, 2> : tc_conv_bf16f<64, 2, 3>;
+      auto kf = tc_conv_bf16f<64, 3, 3, 1>;
+      if (pstf_ == 2 && fsf_ == 3 && ehf_ == 2) kf = tc_conv_bf16f<64, 2, 3, 2>;
+      else if (pstf_ == 2 && fsf_ == 4 && ehf_ == 1) kf = tc_conv_bf16f<64, 2, 4, 1>;
+      else if (pstf_ == 4 && fsf_ == 2 && ehf_ == 1) kf = tc_conv_bf16f<64, 4, 2, 1>;
+      else if (pstf_ == 3 && fsf_ == 2 && ehf_ == 2) kf = tc_conv_bf16f<64, 3, 2, 2>;
+      else if (!(pstf_ == 3 && fsf_ == 3 && ehf_ == 1)) fail("Unsupported", "fused bf16 conv: slot configuration");
       MDHB_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smemf_)));
       kf<<<static_cast<unsigned>(std::min<int64_t>(sms, tiles)), 320, smemf_, s>>>(mi_, mf_, mo_, a);
       MDHB_CUDA(cudaGetLastError());
@@ -1064,7 +1082,7 @@ class ConvRoutine final : public Routine {
   size_t smem_ = 0, smem2_ = 0;
   bool two_sm_ = false;
   bool bf16_ = false, bf_maps_ = false;
-  int pst_ = 2, pst2_ = 3, pstf_ = 3;
+  int pst_ = 2, pst2_ = 3, pstf_ = 2, fsf_ = 4, ehf_ = 1;
   bool fused_ = false;
   size_t smemf_ = 0;
   void *ibf_ = nullptr, *fbf_ = nullptr;

@@ -172,11 +172,13 @@ def test_tf32_conv_variants_bit_identical(envs, sizes, monkeypatch):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("envs", [("MDHB_CONV_2SM",), ("MDHB_CONV_NOSW",), ("MDHB_CONV_2SM", "MDHB_CONV_NOSW"),
-                                  ("MDHB_CONV_NO_BF16F",), ("MDHB_CONV_BF16F_PST",)])
+                                  ("MDHB_CONV_NO_BF16F",), ("MDHB_CONV_BF16F_CFG=2,3,2",), ("MDHB_CONV_BF16F_CFG=3,2,2",),
+                                  ("MDHB_CONV_BF16F_CFG=2,4,1",), ("MDHB_CONV_BF16F_CFG=4,2,1",)])
 def test_bf16_conv_variants_bit_identical(envs, monkeypatch):
-    """The bf16 conv instances (fused fp32 -> bf16 conversion with 2 + 3 or
-    3 + 2 slots; separate conversion pass with CTA pair / single CTA,
-    swizzled / plain patch) agree bit for bit."""
+    """The bf16 conv instances (fused fp32 -> bf16 conversion with the default
+    3 bf16 + 3 fp32 slots or the other slot / epilogue-buffer splits; separate
+    conversion pass with CTA pair / single CTA, swizzled / plain patch) agree
+    bit for bit."""
     from paper_2405_05118_b200 import mdh
     j = spec("mcc_nhwc", [3, 20, 16, 64, 3, 3, 128])
     comp = mo.Computation.from_json(j)
@@ -185,7 +187,8 @@ def test_bf16_conv_variants_bit_identical(envs, monkeypatch):
     assert "cta_group::1" in p0.describe()["template"]["umma"]
     (base,) = run_device(p0, ins)
     for e in envs:
-        monkeypatch.setenv(e, "3" if e == "MDHB_CONV_BF16F_PST" else "1")
+        k, _, v = e.partition("=")
+        monkeypatch.setenv(k, v or "1")
     p = mdh.Plan(j, math=mdh.MATH_BF16)
     (var,) = run_device(p, ins)
     assert np.array_equal(base, var), p.describe()
