@@ -97,6 +97,26 @@ def test_tune_writes_history_with_reference_columns(tmp_path, capsys):
 
 
 @pytest.mark.gpu
+def test_tune_simcost_from_published_fixture(tmp_path, capsys):
+    """`tune --objective simcost --seed-simcost --start tvm_gpu`: the fixture's
+    configuration is the first history row and the best objective is the
+    SimCost of the written configuration."""
+    from paper_2405_05118_b200 import cli, mdh
+    hist = tmp_path / "h.csv"
+    best = tmp_path / "best.json"
+    rc, out, _ = run(["tune", "--spec", "matmul_resnet", "--asm", "CUDA", "--objective", "simcost", "--seed-simcost",
+                      "--start", "tvm_gpu", "--budget", "6", "--history", str(hist), "--out", str(best)], capsys)
+    assert rc == 0 and "evaluations: 6" in out, out
+    rows = hist.read_text().strip().splitlines()
+    assert len(rows) == 7
+    _, spec, model, cfg = cli.load_fixture("tvm_gpu")
+    start_cost, _ = mdh.simcost(cli.load_spec("matmul_resnet"), "CUDA", cfg)
+    assert float(rows[1].split(",")[2]) == start_cost
+    best_obj = float([l for l in out.splitlines() if l.startswith("best objective:")][0].split(":")[1])
+    assert abs(best_obj - mdh.simcost(cli.load_spec("matmul_resnet"), "CUDA", best.read_text())[0]) <= 1e-6 * best_obj
+
+
+@pytest.mark.gpu
 def test_run_reproduces_a_frozen_reference_vector(tmp_path, capsys):
     ref = os.path.join(REFDATA, "refs", "matmul.ref.json")
     out_file = tmp_path / "o.json"
