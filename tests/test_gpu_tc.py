@@ -180,18 +180,25 @@ def test_bf16_conv_variants_bit_identical(envs, monkeypatch):
     conversion pass with CTA pair / single CTA, swizzled / plain patch) agree
     bit for bit."""
     from paper_2405_05118_b200 import mdh
-    j = spec("mcc_nhwc", [3, 20, 16, 64, 3, 3, 128])
-    comp = mo.Computation.from_json(j)
-    ins = exact_inputs(comp, 13)
-    p0 = mdh.Plan(j, math=mdh.MATH_BF16)
-    assert "cta_group::1" in p0.describe()["template"]["umma"]
-    (base,) = run_device(p0, ins)
-    for e in envs:
-        k, _, v = e.partition("=")
-        monkeypatch.setenv(k, v or "1")
-    p = mdh.Plan(j, math=mdh.MATH_BF16)
-    (var,) = run_device(p, ins)
-    assert np.array_equal(base, var), p.describe()
+    # C = 64: the fused instance is the default (C = 128 does not fit its rings)
+    for sizes in ([3, 20, 16, 64, 3, 3, 64], [2, 56, 56, 64, 3, 3, 64]):
+        j = spec("mcc_nhwc", sizes)
+        comp = mo.Computation.from_json(j)
+        ins = exact_inputs(comp, 13)
+        monkeypatch.delenv("MDHB_CONV_2SM", raising=False)
+        for e in envs:
+            monkeypatch.delenv(e.partition("=")[0], raising=False)
+        p0 = mdh.Plan(j, math=mdh.MATH_BF16)
+        assert p0.describe()["template"]["kernel"].startswith("tc_conv_bf16f"), p0.describe()
+        (base,) = run_device(p0, ins)
+        ((part, dfd),), _ = mo.execute_box(comp, ins, {0: (0, 1)})  # image 0 against the oracle
+        assert np.array_equal(base[:1].astype(np.float64)[dfd], part[dfd])
+        for e in envs:
+            k, _, v = e.partition("=")
+            monkeypatch.setenv(k, v or "1")
+        p = mdh.Plan(j, math=mdh.MATH_BF16)
+        (var,) = run_device(p, ins)
+        assert np.array_equal(base, var), p.describe()
 
 
 BF16_CASES = [
