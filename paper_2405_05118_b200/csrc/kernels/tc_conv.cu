@@ -55,7 +55,6 @@ struct ConvArgs {
   int ek;                  // channels per k-tile row of 128 bytes (32 fp32 / 64 bf16)
   int sw;                  // 1: pixel-major 128B-swizzled patch (4-D box {32 c, WQ, HP, 1})
   int bo_mode;             // descriptor base-offset rule for shifted swizzled rows (dev)
-  int dbg;                 // dev bisection (MDHB_CONV_DBG): 1 no MMA, 2 no patch TMA, 4 no stores
   int tma_store;           // 1: output tiles leave through TMA tensor stores (NPQK view, clipped at P)
 };
 
@@ -123,10 +122,6 @@ __global__ void __launch_bounds__(192, 1)
       for (int cc = 0; cc < chunks; ++cc, ++it) {
         const uint32_t s = it % PSTAGES;
         if (it >= PSTAGES) tc::mbar_wait(&empty[s], ((it / PSTAGES) - 1) & 1);
-        if (g.dbg & 2) {
-          tc::mbar_arrive(&full[s]);
-          continue;
-        }
         tc::mbar_arrive_expect_tx(&full[s], patch_bytes);
         if (g.sw) {
           int c[5] = {cc * g.ek, qb * CV_TQ, pb * CV_TP, n, 0};
@@ -170,7 +165,7 @@ __global__ void __launch_bounds__(192, 1)
             const uint64_t a = dA + t * tap_u + (g.bo_mode ? static_cast<uint64_t>(t & 7) << 49 : 0);
 #pragma unroll
             for (int j = 0; j < CV_BKE / 8; ++j) {
-              if (!(g.dbg & 1)) tc::mma_warp<!BF16>(dtm, a + j * j_u, dB + 2 * j, idesc, first ? 0u : 1u);
+              tc::mma_warp<!BF16>(dtm, a + j * j_u, dB + 2 * j, idesc, first ? 0u : 1u);
               first = 0;
             }
           }
@@ -210,11 +205,9 @@ __global__ void __launch_bounds__(192, 1)
         __syncwarp();
         if (lane == 0) {
           tc::mbar_arrive(&tempty[acc]);
-          if (!(g.dbg & 4)) {
 #pragma unroll
-            for (int h = 0; h < BN / 32; ++h)
-              tc::tma_store4(&tma_o, stg + static_cast<uint32_t>(h) * 4096, h * 32, qb * CV_TQ, pb * CV_TP + q * 4, n);
-          }
+          for (int h = 0; h < BN / 32; ++h)
+            tc::tma_store4(&tma_o, stg + static_cast<uint32_t>(h) * 4096, h * 32, qb * CV_TQ, pb * CV_TP + q * 4, n);
           tc::bulk_commit();
         }
       }
@@ -247,7 +240,7 @@ __global__ void __launch_bounds__(192, 1)
           float v;
           asm volatile("ld.shared.s64 %0, [%1];" : "=l"(ro) : "r"(rtab + rr * 8) : "memory");
           asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(stg + (rr * 33 + lane) * 4) : "memory");
-          if (ro >= 0 && !(g.dbg & 4)) __stcs(cc + ro, v);
+          if (ro >= 0) __stcs(cc + ro, v);
         }
         __syncwarp();
       }
@@ -584,8 +577,7 @@ __global__ void __launch_bounds__(192, 1)
             const uint64_t a = dA + static_cast<uint32_t>(r * g.WQ + ss) * tap_u;
 #pragma unroll
             for (int j = 0; j < CV_BKE / 8; ++j) {
-              if (g.dbg & 1) {
-              } else if (BF16)
+              if (BF16)
                 asm volatile(
                     "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                     "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtm), "l"(a + j * j_u),
@@ -639,7 +631,7 @@ __global__ void __launch_bounds__(192, 1)
         __syncwarp();
         if (lane == 0) {
           asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty_leader0 + acc * 8) : "memory");
-          if (t < ntiles && !(g.dbg & 4)) {
+          if (t < ntiles) {
 #pragma unroll
             for (int h = 0; h < BN / 32; ++h)
               tc::tma_store4(&tma_o, stg + static_cast<uint32_t>(h) * 4096, h * 32, qb * CV_TQ, pb * CV_TP + q * 4, n);
@@ -818,7 +810,6 @@ class ConvRoutine final : public Routine {
     // default; the [c-group][p][q][4c] no-swizzle layout stays selectable
     a_.sw = std::getenv("MDHB_CONV_NOSW") ? 0 : 1;
     a_.bo_mode = std::getenv("MDHB_CONV_BO") ? std::atoi(std::getenv("MDHB_CONV_BO")) : 0;
-    a_.dbg = std::getenv("MDHB_CONV_DBG") ? std::atoi(std::getenv("MDHB_CONV_DBG")) : 0;
     if (a_.sw && (a_.WQ * 128) / 16 >= (1 << 14)) a_.sw = 0;
     const int ktiles = a_.R * a_.S * (a_.C / a_.ek);
     const size_t patch_slot = (8 * static_cast<size_t>(a_.plane) + 1023) / 1024 * 1024;
