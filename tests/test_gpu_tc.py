@@ -263,3 +263,25 @@ def test_bf16_matmul_8192_rows_exact():
     for lo in (0, 4097, 8191):
         ((part, dfd),), sh = mo.execute_box(comp, ins, {0: (lo, lo + 1)})
         assert np.array_equal(out[lo:lo + 1].cpu().numpy().astype(np.float64), part)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(12))
+def test_conv_random_shapes_exact_all_maths(seed):
+    """Seeded random NHWC convolution shapes (ragged P, Q in 8..64, channel
+    counts that select or skip each conv instance) through FFMA, TF32 and BF16:
+    exact-mode inputs give the oracle's values bit for bit on every path."""
+    from paper_2405_05118_b200 import mdh
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(1, 3))
+    p = int(rng.integers(3, 40))
+    q = 8 * int(rng.integers(1, 9))
+    c = int(rng.choice([8, 16, 32, 64, 96, 128]))
+    j = spec("mcc_nhwc", [n, p, q, 64, 3, 3, c])
+    comp = mo.Computation.from_json(j)
+    ins = exact_inputs(comp, seed)
+    ((want, dfd),) = mo.execute(comp, ins)
+    for math in (mdh.MATH_FFMA, mdh.MATH_TF32, mdh.MATH_BF16):
+        plan = mdh.Plan(j, math=math)
+        (got,) = run_device(plan, ins)
+        assert np.array_equal(got.astype(np.float64)[dfd], want[dfd]), (n, p, q, c, plan.describe()["template"])
