@@ -285,3 +285,22 @@ def test_conv_random_shapes_exact_all_maths(seed):
         plan = mdh.Plan(j, math=math)
         (got,) = run_device(plan, ins)
         assert np.array_equal(got.astype(np.float64)[dfd], want[dfd]), (n, p, q, c, plan.describe()["template"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(12))
+def test_matmul_random_shapes_exact_all_maths(seed):
+    """Seeded random MatMul shapes (tile-ragged M / N / K, including sizes no
+    tensor-core or FFMA template takes and that fall to another instance):
+    exact-mode inputs give the oracle's values bit for bit with every math."""
+    from paper_2405_05118_b200 import mdh
+    rng = np.random.default_rng(200 + seed)
+    m, n, k = (int(rng.integers(1, 700)), int(rng.integers(1, 700)), int(rng.integers(1, 400)))
+    j = spec("matmul_fp32", [m, n, k])
+    comp = mo.Computation.from_json(j)
+    ins = exact_inputs(comp, seed)
+    ((want, dfd),) = mo.execute(comp, ins)
+    for math in (mdh.MATH_FFMA, mdh.MATH_TF32, mdh.MATH_BF16):
+        plan = mdh.Plan(j, math=math)
+        (got,) = run_device(plan, ins)
+        assert np.array_equal(got.astype(np.float64)[dfd], want[dfd]), (m, n, k, plan.describe()["template"])
