@@ -806,24 +806,33 @@ __global__ void __launch_bounds__(256) bpack(const float* __restrict__ B, float*
 __global__ void __launch_bounds__(256) apack_t(const float* __restrict__ A, float* __restrict__ Ap,
                                                const int32_t* __restrict__ tAm, const int32_t* __restrict__ am,
                                                const int32_t* __restrict__ ak, int bml, int64_t mtot, int K) {
-  __shared__ float tile[32][33];
-  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * 32;
-  const int k0 = blockIdx.y * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  // 64 (m) x 64 (k) tile: 16-byte reads along k (the rows of A are
+  // K-contiguous with 16-byte aligned starts, host-checked), 16-byte writes
+  // along m
+  __shared__ float tile[64][65];
+  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * 64;
+  const int k0 = blockIdx.y * 64;
+  const int t = threadIdx.x, q = (t & 15) * 4, r = t >> 4;  // 16 quads x 16 rows
+  const int64_t kb = ak[k0];
 #pragma unroll
-  for (int j = 0; j < 32; j += 8) {
-    const int64_t m = m0 + ty + j;
-    const int k = k0 + tx;
-    float v = 0.f;
-    if (m < mtot && k < K) v = __ldg(A + tAm[m / bml] + am[m % bml] + ak[k]);
-    tile[ty + j][tx] = v;
+  for (int i = 0; i < 4; ++i) {
+    const int row = r + 16 * i;
+    const int64_t m = m0 + row;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (m < mtot && k0 + q < K) v = __ldg(reinterpret_cast<const float4*>(A + tAm[m / bml] + am[m % bml] + kb + q));
+    tile[q + 0][row] = v.x;
+    tile[q + 1][row] = v.y;
+    tile[q + 2][row] = v.z;
+    tile[q + 3][row] = v.w;
   }
   __syncthreads();
 #pragma unroll
-  for (int j = 0; j < 32; j += 8) {
-    const int k = k0 + ty + j;
-    const int64_t m = m0 + tx;
-    if (m < mtot && k < K) Ap[static_cast<int64_t>(k) * mtot + m] = tile[tx][ty + j];
+  for (int i = 0; i < 4; ++i) {
+    const int kr = r + 16 * i;
+    const int64_t m = m0 + q;
+    if (k0 + kr < K && m < mtot)
+      *reinterpret_cast<float4*>(Ap + static_cast<int64_t>(k0 + kr) * mtot + m) =
+          make_float4(tile[kr][q], tile[kr][q + 1], tile[kr][q + 2], tile[kr][q + 3]);
   }
 }
 
@@ -1021,9 +1030,9 @@ class GemmRoutine final : public Routine {
     // fills; measured 20.27 vs 21.12 ms at 8192^3 for the GEMM itself)
     if (amode_ == LD_K4 && tilesN_ >= 16 && BM % 32 == 0 && !std::getenv("MDHB_NO_APACK")) {
       const int64_t mtot = static_cast<int64_t>(tilesM_) * BM;
-      bool kcontig = true;
+      bool kcontig = K_ % 4 == 0 && all_mod4(tAm) && all_mod4(am) && ak[0] % 4 == 0;
       for (size_t k = 0; k < ak.size() && kcontig; ++k) kcontig = ak[k] == ak[0] + static_cast<int64_t>(k);
-      if (kcontig && K_ * mtot * 4 <= (int64_t(1) << 30) && K_ * mtot < INT32_MAX) {
+      if (kcontig && mtot % 64 == 0 && K_ * mtot * 4 <= (int64_t(1) << 30) && K_ * mtot < INT32_MAX) {
         ap_tAm_ = tAm;
         ap_am_ = am;
         ap_ak_ = ak;
@@ -1190,7 +1199,7 @@ class GemmRoutine final : public Routine {
     if (apack_m_) {
       const int32_t* ta = static_cast<const int32_t*>(ap_tab_);
       const int nt = static_cast<int>(ap_tAm_.size()), bml = static_cast<int>(ap_am_.size());
-      dim3 grid(static_cast<unsigned>((apack_m_ + 31) / 32), static_cast<unsigned>((K_ + 31) / 32));
+      dim3 grid(static_cast<unsigned>(apack_m_ / 64), static_cast<unsigned>((K_ + 63) / 64));
       apack_t<<<grid, 256, 0, s>>>(A, static_cast<float*>(ap_), ta, ta + nt, ta + nt + bml, bml, apack_m_, static_cast<int>(K_));
       MDHB_CUDA(cudaGetLastError());
       A = static_cast<const float*>(ap_);
