@@ -338,8 +338,9 @@ def build_parser():
     t = sub.add_parser("tune", help="search the configuration space on the device")
     source(t, config=False)
     t.add_argument("--budget", type=int, default=20)
-    t.add_argument("--objective", default="compiled", choices=["compiled", "device", "simcost"],
-                   help="compiled/device: CUDA-event time; simcost: the reference's input-free cost model")
+    t.add_argument("--objective", default="simcost", choices=["simcost", "compiled", "device"],
+                   help="simcost (the reference's default, mdh_main.cpp:306): the input-free cost model; "
+                        "compiled / device: CUDA-event time of the instantiated kernel on the B200")
     t.add_argument("--seed-simcost", action="store_true",
                    help="random phase samples the cheapest quarter of the candidates by SimCost")
     t.add_argument("--start", help="fixture (name or file) whose configuration is evaluated first")

@@ -86,10 +86,13 @@ def test_emit_prints_the_nvrtc_kernel(capsys):
 
 
 @pytest.mark.gpu
-def test_tune_writes_history_with_reference_columns(tmp_path, capsys):
+@pytest.mark.parametrize("objective", [None, "compiled"])  # None: the reference's default, simcost
+def test_tune_writes_history_with_reference_columns(objective, tmp_path, capsys):
     hist = tmp_path / "h.csv"
     best = tmp_path / "best.json"
-    rc, out, _ = run(["tune", "--spec", "matvec", "--budget", "3", "--history", str(hist), "--out", str(best)], capsys)
+    extra = ["--objective", objective] if objective else []
+    rc, out, _ = run(["tune", "--spec", "matvec", "--budget", "3", "--history", str(hist), "--out", str(best)] + extra,
+                     capsys)
     assert rc == 0 and "evaluations: 3" in out
     rows = hist.read_text().strip().splitlines()
     assert rows[0] == "eval_index,config_hash,objective,valid" and len(rows) == 4
