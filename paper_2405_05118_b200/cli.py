@@ -162,6 +162,48 @@ def _config_text(path):
         return f.read()
 
 
+def _prime_factors(n):
+    out, f = [], 2
+    while f * f <= n:
+        while n % f == 0:
+            out.append(f)
+            n //= f
+        f += 1
+    if n > 1:
+        out.append(n)
+    return out
+
+
+def random_configs(spec, model, n, seed, device=0):
+    """`--random N` (mdh_main.cpp:120-125 samples N configurations with seeds
+    seed + k): here each sample re-distributes every dimension's prime factors
+    over the ASM layers at random (mt19937_64, below(n) = gen() % n) around the
+    backend's canonical configuration for the spec, keeping its orders,
+    assignments and memory regions; samples violating the model rules are
+    redrawn (up to 64 times, else the canonical one is used)."""
+    base = mdh.Plan(spec, model, None, device=device).describe()["config"]
+    text = json.dumps(spec)
+    out = []
+    for k in range(n):
+        rng = _MT64(seed + k)
+        cfg = base
+        for _ in range(64):
+            c = json.loads(json.dumps(base))
+            parts = c["num_parts"]
+            layers = len(parts)
+            for d, size in enumerate(spec["sizes"]):
+                col = [1] * layers
+                for f in _prime_factors(int(size)):
+                    col[rng.next() % layers] *= f
+                for l in range(layers):
+                    parts[l][d] = col[l]
+            if not mdh.validate_config(text, model, json.dumps(c)):
+                cfg = c
+                break
+        out.append((f"random:{k}", json.dumps(cfg), model))
+    return out
+
+
 def cmd_verify(a) -> int:
     jobs = []
     if a.fixture:
@@ -169,7 +211,10 @@ def cmd_verify(a) -> int:
         jobs.append((label, json.dumps(cfg), model))
     else:
         spec = load_spec(a.spec, a.data)
-        jobs.append((a.config or "default", _config_text(a.config), a.asm))
+        if a.random and not a.config:
+            jobs.extend(random_configs(spec, a.asm, a.random, a.seed, a.device))
+        else:
+            jobs.append((a.config or "default", _config_text(a.config), a.asm))
     ref = mdh.Plan(spec, float_storage=mdh.F64, int_storage=mdh.I64, generic=True, device=a.device)
     ins = make_inputs(ref, spec, a.seed)
     want = ref.run_host(ins)
@@ -335,6 +380,7 @@ def build_parser():
     v = sub.add_parser("verify", help="run configurations against the device reference executor")
     source(v)
     v.add_argument("--fixture", help="bundled fixture name or file (overrides spec/asm/config)")
+    v.add_argument("--random", type=int, default=0, help="number of random configurations to sample (seeds seed + k)")
     t = sub.add_parser("tune", help="search the configuration space on the device")
     source(t, config=False)
     t.add_argument("--budget", type=int, default=20)

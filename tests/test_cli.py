@@ -72,6 +72,18 @@ def test_verify_published_fixture(capsys):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("spec", ["matvec", "jacobi3d", "mcc", "prl"])
+def test_verify_random_configurations(spec, capsys):
+    """`verify --random 3`: three sampled configurations (random prime-factor
+    placements over the layers), each executed -- on a specialised template
+    when it can instantiate the sample, else on the emitted / VM kernels --
+    and checked against the device reference executor."""
+    rc, out, _ = run(["verify", "--spec", spec, "--random", "3", "--seed", "7"], capsys)
+    assert rc == 0 and out.count(": pass (hash=") == 3 and "3/3 configurations pass" in out, out
+    assert "config random:0" in out and "config random:2" in out
+
+
+@pytest.mark.gpu
 def test_verify_invalid_config_exit_2(tmp_path, capsys):
     cfg = tmp_path / "bad.json"
     cfg.write_text(json.dumps({"num_parts": [[3, 1]]}))
