@@ -23,6 +23,8 @@
  *     proj/include/mdh/autotuner.hpp:38
  *   mdh::validate(cfg, expr, model, constraints)          mdh_b200_validate_config
  *     proj/include/mdh/tuning.hpp:57
+ *   mdh::lower(expr, model, cfg).pretty()                  mdh_b200_lowered (host only)
+ *     proj/include/mdh/lowering.hpp:71
  *   mdh::simcost_objective(expr, model, cfg)              mdh_b200_simcost (host only)
  *     proj/include/mdh/autotuner.hpp:67;                  mdh_b200_tune_ex (objective choice,
  *     tune(..., Objective::SimCost, ...)                    SimCost seeding, start config)
@@ -151,6 +153,12 @@ int mdh_b200_tune_ex(const char* computation_json, const char* asm_model, const 
  * "regions": {name: elements}}. */
 int mdh_b200_simcost(const char* computation_json, const char* asm_model, const char* config_json, double* cost,
                      char* trace_json, int64_t cap, int64_t* need);
+
+/* The lowered form of (computation, model, configuration) as the
+ * reference's LowLevelExpr::pretty() prints it (lowering.cpp:185-222; `mdh
+ * lower`): host only.  NULL config = the baseline configuration. */
+int mdh_b200_lowered(const char* computation_json, const char* asm_model, const char* config_json, char* buf,
+                     int64_t cap, int64_t* need);
 
 /* CUDA C++ source of the kernel the plan compiled at plan time (the emitted
  * family, NVRTC); "" for the precompiled template families.  The B200

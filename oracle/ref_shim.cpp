@@ -8,6 +8,7 @@
 //   ref_interpret      -> mdh::interpret(mdh::lower(...))  (include/mdh/interpreter.hpp:44-46)
 //   ref_emit           -> mdh::emit                        (include/mdh/codegen.hpp:38)
 //   ref_compiled_time  -> mdh::compiled_time_objective     (include/mdh/autotuner.hpp:73)
+//   ref_lowered        -> mdh::lower(...).pretty()                 (lowering.cpp:185-222)
 //   ref_simcost        -> mdh::simcost_objective           (include/mdh/autotuner.hpp:67)
 //   ref_sample_config  -> mdh::sample / ReducedSpace::sample (include/mdh/tuning.hpp:64,80)
 //   ref_validate       -> mdh::validate                    (include/mdh/tuning.hpp:57)
@@ -143,6 +144,15 @@ int ref_emit(const char* comp_json, const char* asm_arg, const char* cfg_json, c
     mdh::HighLevelExpr e = mdh::parse_computation_json(comp_json);
     mdh::AsmModel m = mdh::resolve_asm(asm_arg);
     put_string(mdh::emit(mdh::lower(e, m, config_of(e, m, cfg_json)), e), buf, cap, need);
+  });
+}
+
+int ref_lowered(const char* comp_json, const char* asm_arg, const char* cfg_json, char* buf, int64_t cap,
+                int64_t* need) {
+  return guard([&] {
+    mdh::HighLevelExpr e = mdh::parse_computation_json(comp_json);
+    mdh::AsmModel m = mdh::resolve_asm(asm_arg);
+    put_string(mdh::lower(e, m, config_of(e, m, cfg_json)).pretty(), buf, cap, need);
   });
 }
 

@@ -104,6 +104,11 @@ def emit(comp_json: str, asm: str, cfg_json: str = "") -> str:
     return _string_call(lib().ref_emit, _b(comp_json), _b(asm), _b(cfg_json))
 
 
+def lowered(comp_json: str, asm: str, cfg_json: str = "") -> str:
+    """mdh::lower(expr, model, cfg).pretty() (lowering.cpp:185-222)."""
+    return _string_call(lib().ref_lowered, _b(comp_json), _b(asm), _b(cfg_json))
+
+
 def sample_config(comp_json: str, asm: str, seed: int, reduced=True, model_rules=True) -> str:
     return _string_call(lib().ref_sample_config, _b(comp_json), _b(asm), ctypes.c_uint64(seed),
                         ctypes.c_int(int(reduced)), ctypes.c_int(int(model_rules)))

@@ -294,6 +294,24 @@ def cmd_tune(a) -> int:
     return 0
 
 
+def cmd_lower(a) -> int:
+    """`mdh lower` (mdh_main.cpp:293-295): the lowered expression of the
+    configuration (or fixture), as LowLevelExpr::pretty() prints it.  Host
+    only -- no GPU is touched."""
+    if a.fixture:
+        _, spec, model, cfg = load_fixture(a.fixture, a.data)
+        text = mdh.lowered(spec, model, json.dumps(cfg) if not isinstance(cfg, str) else cfg)
+    else:
+        spec = load_spec(a.spec, a.data)
+        text = mdh.lowered(spec, a.asm, _config_text(a.config))
+    if a.out:
+        with open(a.out, "w") as f:
+            f.write(text)
+    else:
+        sys.stdout.write(text)
+    return 0
+
+
 def cmd_emit(a) -> int:
     spec = load_spec(a.spec, a.data)
     plan = mdh.Plan(spec, a.asm, _config_text(a.config), float_storage=mdh.F64 if a.f64 else mdh.F32, device=a.device)
@@ -393,6 +411,10 @@ def build_parser():
     t.add_argument("--out")
     t.add_argument("--history")
     t.add_argument("--tf32", action="store_true")
+    lw = sub.add_parser("lower", help="print the lowered expression (LowLevelExpr::pretty)")
+    source(lw)
+    lw.add_argument("--fixture", help="bundled fixture name or file (overrides spec/asm/config)")
+    lw.add_argument("--out")
     e = sub.add_parser("emit", help="print the CUDA kernel compiled for the md_hom")
     source(e)
     e.add_argument("--out")
@@ -415,8 +437,8 @@ def main(argv=None) -> int:
         a = ap.parse_args(argv)
     except SystemExit as e:
         return 0 if e.code == 0 else 3
-    cmds = {"verify": cmd_verify, "tune": cmd_tune, "emit": cmd_emit, "describe": cmd_describe, "run": cmd_run,
-            "examples": cmd_examples}
+    cmds = {"verify": cmd_verify, "tune": cmd_tune, "lower": cmd_lower, "emit": cmd_emit, "describe": cmd_describe,
+            "run": cmd_run, "examples": cmd_examples}
     try:
         return cmds[a.cmd](a)
     except CliError as e:

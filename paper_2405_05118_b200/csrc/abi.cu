@@ -344,6 +344,16 @@ int mdh_b200_simcost(const char* comp_json, const char* asm_model, const char* c
   });
 }
 
+int mdh_b200_lowered(const char* comp_json, const char* asm_model, const char* config_json, char* buf, int64_t cap,
+                     int64_t* need) {
+  return guard([&] {
+    mdhb::MdHom e = mdhb::parse_md_hom(comp_json);
+    mdhb::Asm m = mdhb::resolve_asm(asm_model ? asm_model : "B200");
+    mdhb::Config c = config_json ? mdhb::parse_config(config_json, e, m) : mdhb::baseline_config(e, m);
+    put(mdhb::lowered_text(c, e, m), buf, cap, need);
+  });
+}
+
 int mdh_b200_launches_per_run(const mdh_b200_plan* p, int* launches) {
   return guard([&] { *launches = p->r->launches(); });
 }

@@ -92,6 +92,8 @@ struct SimTrace {
 };
 SimTrace simulate(const Config& c, const MdHom& e, const Asm& m);
 double simcost(const SimTrace& t, const Asm& m);
+// LowLevelExpr::pretty() of lower(e, m, c) (lowering.cpp:56-118, 185-222)
+std::string lowered_text(const Config& c, const MdHom& e, const Asm& m);
 
 // The C ABI's thread-local last-error slot (abi.cu).
 void set_last_error(const std::string& what);

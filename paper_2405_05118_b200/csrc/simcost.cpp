@@ -121,6 +121,73 @@ double simcost(const SimTrace& t, const Asm& m) {
   return total + 1.0 * static_cast<double>(t.depth);
 }
 
+// The lowered form's pretty text (LowLevelExpr::pretty, lowering.cpp:185-222;
+// steps as lower() builds them, lowering.cpp:56-118): one de line per level in
+// ord_de after the "iv" view stage, the scalar line, one re line per level in
+// ord_re, then the "ov" view stage.
+std::string lowered_text(const Config& c, const MdHom& e, const Asm& m) {
+  std::string why = config_violation(c, e, m, false);
+  if (!why.empty()) fail("InvalidConfig", "configuration violates \"" + why.substr(0, why.find(':')) + "\": " +
+                                              (why.find(": ") == std::string::npos ? why : why.substr(why.find(": ") + 2)));
+  const int D = e.D();
+  auto letter = [](int d) { return d == 1 ? std::string("x") : d == 2 ? std::string("y") : d == 3 ? std::string("z") : "d" + std::to_string(d); };
+  auto lvl = [&](const Level& l) { return "(" + std::to_string(l.layer) + "," + letter(l.dim) + ")"; };
+  auto tag = [&](const Level& a) { return "(" + m.layer(a.layer) + "," + letter(a.dim) + ")"; };
+  auto perm = [](const std::vector<int>& v) {
+    std::string s = "(";
+    for (size_t i = 0; i < v.size(); ++i) s += (i ? "," : "") + std::to_string(v[i]);
+    return s + ")";
+  };
+  auto rank = [&](const Level& l) { return (l.layer - 1) * D + (l.dim - 1); };
+  auto opname = [](Fold f) {
+    switch (f) {
+      case Fold::Add: return "+";
+      case Fold::Sub: return "-";
+      case Fold::Mul: return "*";
+      case Fold::Div: return "/";
+      case Fold::Min: return "min";
+      default: return "max";
+    }
+  };
+  auto comb = [&](int dim) {
+    const Combine& cb = e.comb[static_cast<size_t>(dim - 1)];
+    if (cb.kind == Combine::CC) return std::string("cc");
+    return std::string(cb.kind == Combine::PW ? "pw:" : "ps:") + opname(cb.op);
+  };
+  std::ostringstream o;
+  o << "lowered computation=" << e.name << " model=" << m.name << "\n";
+  auto step = [&](const char* ph, const Level& l, const Level& a, const std::string& op, const std::vector<Buf>& bufs,
+                  const std::vector<std::vector<int>>& mem, const std::vector<std::vector<std::vector<int>>>& lay) {
+    const int r = rank(l);
+    o << ph << " level=" << lvl(l) << " tag=" << tag(a) << " parts="
+      << c.parts[static_cast<size_t>(l.layer - 1)][static_cast<size_t>(l.dim - 1)] << " op=" << op << " mem=[";
+    for (size_t b = 0; b < bufs.size(); ++b)
+      o << (b ? ", " : "") << bufs[b].name << ":" << m.layer(mem[b][static_cast<size_t>(r)]);
+    o << "] layout=[";
+    for (size_t b = 0; b < bufs.size(); ++b)
+      o << (b ? ", " : "") << bufs[b].name << ":" << perm(lay[b][static_cast<size_t>(r)]);
+    o << "]\n";
+  };
+  o << "de level=(-) tag=(-) op=iv\n";
+  for (const Level& l : c.ord_de) step("de", l, c.ass_de[static_cast<size_t>(rank(l))], "cc_inv", e.in, c.mem_de, c.layout_de);
+  o << "scalar level=(-) tag=(-) op=f ord=[";
+  for (size_t i = 0; i < c.ord_scalar.size(); ++i) o << (i ? ", " : "") << lvl(c.ord_scalar[i]);
+  o << "] ass=[";
+  for (size_t i = 0; i < c.ass_scalar.size(); ++i) o << (i ? ", " : "") << tag(c.ass_scalar[i]);
+  o << "] mem=[";
+  for (size_t b = 0; b < e.in.size(); ++b) o << (b ? ", " : "") << "in " << e.in[b].name << ":" << m.layer(c.mem_scalar_in[b]);
+  for (size_t b = 0; b < e.out.size(); ++b)
+    o << (b || !e.in.empty() ? ", " : "") << "out " << e.out[b].name << ":" << m.layer(c.mem_scalar_out[b]);
+  o << "] layout=[";
+  for (size_t b = 0; b < e.in.size(); ++b) o << (b ? ", " : "") << "in " << e.in[b].name << ":" << perm(c.layout_scalar_in[b]);
+  for (size_t b = 0; b < e.out.size(); ++b)
+    o << (b || !e.in.empty() ? ", " : "") << "out " << e.out[b].name << ":" << perm(c.layout_scalar_out[b]);
+  o << "]\n";
+  for (const Level& l : c.ord_re) step("re", l, c.ass_re[static_cast<size_t>(rank(l))], comb(l.dim), e.out, c.mem_re, c.layout_re);
+  o << "re level=(-) tag=(-) op=ov\n";
+  return o.str();
+}
+
 std::string SimTrace::json(const Asm& m) const {
   std::ostringstream os;
   os << "{\"reads\": " << reads << ", \"writes\": " << writes << ", \"parallel_depth\": " << depth << ", \"regions\": {";

@@ -35,7 +35,8 @@ _NP = {F32: np.float32, F64: np.float64, I32: np.int32, I64: np.int64}
 EXPORTED = [
     "mdh_b200_default_options", "mdh_b200_plan_create", "mdh_b200_plan_destroy", "mdh_b200_buffer_count",
     "mdh_b200_buffer_info", "mdh_b200_run", "mdh_b200_run_host", "mdh_b200_time", "mdh_b200_describe",
-    "mdh_b200_validate_config", "mdh_b200_tune", "mdh_b200_tune_ex", "mdh_b200_simcost", "mdh_b200_launches_per_run",
+    "mdh_b200_validate_config", "mdh_b200_tune", "mdh_b200_tune_ex", "mdh_b200_simcost", "mdh_b200_lowered",
+    "mdh_b200_launches_per_run",
     "mdh_b200_kernel_source", "mdh_b200_last_error", "mdh_b200_version",
 ]
 OBJ_TIME, OBJ_SIMCOST = 0, 1
@@ -68,6 +69,7 @@ def lib():
         L.mdh_b200_version.restype = ctypes.c_char_p
         c, v, i64, d = ctypes.c_char_p, ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_double)
         L.mdh_b200_simcost.argtypes = [c, c, c, d, c, i64, ctypes.POINTER(ctypes.c_int64)]
+        L.mdh_b200_lowered.argtypes = [c, c, c, c, i64, ctypes.POINTER(ctypes.c_int64)]
         L.mdh_b200_tune_ex.argtypes = [c, c, v, ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, c, c, i64, c,
                                        i64, d]
         L.mdh_b200_tune.argtypes = [c, c, v, ctypes.c_int, ctypes.c_uint64, c, i64, c, i64, d]
@@ -269,6 +271,16 @@ def simcost(spec, asm="B200", config=None):
     buf = ctypes.create_string_buffer(need.value)
     _check(lib().mdh_b200_simcost(_text(spec), _text(asm), cfg, ctypes.byref(cost), buf, need.value, ctypes.byref(need)))
     return cost.value, json.loads(buf.value.decode())
+
+
+def lowered(spec, asm="B200", config=None) -> str:
+    """mdh::lower(expr, model, cfg).pretty() (lowering.cpp:185-222). Host only."""
+    need = ctypes.c_int64()
+    cfg = _text(config) if config is not None else None
+    _check(lib().mdh_b200_lowered(_text(spec), _text(asm), cfg, None, 0, ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    _check(lib().mdh_b200_lowered(_text(spec), _text(asm), cfg, buf, need.value, ctypes.byref(need)))
+    return buf.value.decode()
 
 
 def version() -> str:

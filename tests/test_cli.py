@@ -142,3 +142,17 @@ def test_run_reproduces_a_frozen_reference_vector(tmp_path, capsys):
     for name, g in want.items():
         w = np.array([0 if x is None else x for x in g["data"]], dtype=np.float64)
         assert np.array_equal(np.array(got[name]["data"], dtype=np.float64), w), name
+
+
+def test_lower_prints_the_reference_lowered_form(tmp_path, capsys):
+    """`lower --fixture tvm_gpu`: the reference's pretty form of the published
+    TVM configuration (host only; golden text from the unmodified reference
+    when oracle/_ref is built)."""
+    rc, out, _ = run(["lower", "--fixture", "tvm_gpu"], capsys)
+    assert rc == 0 and out.startswith("lowered computation=matmul_resnet model=CUDA\n"), out[:200]
+    assert out.splitlines()[1] == "de level=(-) tag=(-) op=iv" and out.rstrip().endswith("re level=(-) tag=(-) op=ov")
+    from oracle import refbind
+    if refbind.available():
+        from paper_2405_05118_b200 import cli
+        comp, cfg, asm = refbind.fixture("tvm_gpu")
+        assert out == refbind.lowered(comp, asm, cfg)

@@ -60,3 +60,20 @@ def test_simcost_equals_unmodified_reference_live(asm):
         for seed in range(3, 6):
             cfg = refbind.sample_config(text, asm, seed)
             assert mdh.simcost(text, asm, cfg)[0] == refbind.simcost(text, asm, cfg), (f, asm, seed)
+
+
+@pytest.mark.parametrize("case", [c for c in GOLD["configs"] if "lowered" in c],
+                         ids=lambda c: f'{c["computation"]}-{c["asm"]}')
+def test_lowered_form_matches_reference_golden(case):
+    """mdh_b200_lowered prints lower(e, m, cfg).pretty() byte for byte
+    (lowering.cpp:185-222)."""
+    assert mdh.lowered(_comp(case["computation"]), case["asm"], json.dumps(case["config"])) == case["lowered"]
+
+
+@pytest.mark.skipif(not refbind.available(), reason="oracle/_ref not built")
+def test_lowered_form_equals_unmodified_reference_live():
+    for f in sorted(os.listdir(os.path.join(DATA, "computations"))):
+        text = _comp(f)
+        for asm in ("CUDA", "MultiGPU"):
+            cfg = refbind.sample_config(text, asm, 11)
+            assert mdh.lowered(text, asm, cfg) == refbind.lowered(text, asm, cfg), (f, asm)
