@@ -314,7 +314,13 @@ def cmd_lower(a) -> int:
 
 def cmd_emit(a) -> int:
     spec = load_spec(a.spec, a.data)
-    plan = mdh.Plan(spec, a.asm, _config_text(a.config), float_storage=mdh.F64 if a.f64 else mdh.F32, device=a.device)
+    cfg = _config_text(a.config)
+    if cfg is not None:
+        why = mdh.validate_config(json.dumps(spec), a.asm, cfg)
+        if why:
+            print(f"config {a.config} is invalid ({why})", file=sys.stderr)
+            return 2
+    plan = mdh.Plan(spec, a.asm, cfg, float_storage=mdh.F64 if a.f64 else mdh.F32, device=a.device)
     src = plan.kernel_source()
     if not src:
         d = plan.describe()
@@ -325,6 +331,29 @@ def cmd_emit(a) -> int:
             f.write(src)
     else:
         sys.stdout.write(src)
+    if not a.gate_compile:
+        return 0
+    # --gate-compile (mdh_main.cpp:180-205): the kernel was compiled (NVRTC)
+    # when the plan was made; run it on the driver's inputs against the
+    # device reference executor
+    ref = mdh.Plan(spec, float_storage=mdh.F64, int_storage=mdh.I64, generic=True, device=a.device)
+    ins = make_inputs(ref, spec, a.seed)
+    want = ref.run_host(ins)
+    got = plan.run_host(ins)
+    K = 1
+    for n, c in zip(spec["sizes"], spec["combine"]):
+        if c != "cc":
+            K *= n
+    for g, w in zip(got, want):
+        if np.issubdtype(w.dtype, np.integer):
+            bad = np.flatnonzero(g.astype(np.int64) != w)
+        else:
+            w64 = w.astype(np.float64)
+            bad = np.flatnonzero(np.abs(g.astype(np.float64) - w64) > 1e-5 * np.sqrt(max(K, 1)) * np.maximum(np.abs(w64), 1.0))
+        if bad.size:
+            raise CliError("Mismatch", f"gate failed: cell {int(bad[0])}: {g.flat[int(bad[0])]} != {w.flat[int(bad[0])]}")
+    d = plan.describe()
+    print(f"gate passed: compiled with NVRTC (sm_100a), {d['family']} / {d['template']['kernel']}", file=sys.stderr)
     return 0
 
 
@@ -419,6 +448,8 @@ def build_parser():
     source(e)
     e.add_argument("--out")
     e.add_argument("--f64", action="store_true", help="f64 storage (the bit-exact mode)")
+    e.add_argument("--gate-compile", action="store_true",
+                   help="run the compiled kernel on the driver's inputs against the device reference executor")
     d = sub.add_parser("describe", help="print the plan (family, template, Table-1 config)")
     source(d)
     d.add_argument("--tf32", action="store_true")

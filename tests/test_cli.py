@@ -98,6 +98,15 @@ def test_emit_prints_the_nvrtc_kernel(capsys):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("spec", ["histo", "matvec", "scan"])
+def test_emit_gate_compile_runs_the_kernel(spec, capsys):
+    """`emit --gate-compile` (mdh_main.cpp:180-205): the compiled kernel is
+    run on the driver's inputs and checked against the device reference."""
+    rc, out, err = run(["emit", "--spec", spec, "--gate-compile", "--f64"], capsys)
+    assert rc == 0 and "gate passed" in err, err
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("objective", [None, "compiled"])  # None: the reference's default, simcost
 def test_tune_writes_history_with_reference_columns(objective, tmp_path, capsys):
     hist = tmp_path / "h.csv"
