@@ -15,7 +15,8 @@ formats unchanged:
     python -m paper_2405_05118_b200.cli examples [--data DIR]
 
 --spec takes a computation JSON file, or the name of one in --data
-(default: the reference's data dir when present, else specs/).
+(default: the package's data/ dir -- the reference's bundled computations
+and fixtures, unchanged, plus the BASELINE specs).
 
 `verify` is the reference's verify (interpret(lower(cfg)) against
 reference_execute, mdh_main.cpp:130-166) on the device: the plan
@@ -24,9 +25,10 @@ reference-semantics executor (the generic family in f64 storage: the
 reference's bytecode, lexicographic fold, bit-identical to reference_execute
 on the frozen vectors), on the driver's deterministic k/4 inputs
 (mdh_main.cpp:46-66).  `emit` prints the CUDA source the emitted family
-compiles with NVRTC (mdh emit prints C).  `tune --objective` is always the
-device time (compiled_time_objective's role); the history CSV has the
-reference's columns (autotuner.cpp:49-56).
+compiles with NVRTC (mdh emit prints C).  `tune --objective` is the
+SimCost model (default) or the device time (compiled_time_objective's role);
+the history CSV has the reference's columns (autotuner.cpp:49-56), and the
+printed best hash is the one of the best configuration's history row.
 """
 from __future__ import annotations
 
@@ -61,8 +63,9 @@ def _data_dirs(data):
     out = []
     if data:
         out.append(data)
-    out += ["/root/reference/proj/data", os.path.join(_REPO, "tests", "golden", "reference_data"),
-            os.path.join(_REPO, "specs")]
+    # the data shipped with the package: the reference's bundled computations
+    # and published fixtures (JSON, unchanged) plus the BASELINE specs
+    out.append(os.path.join(os.path.dirname(os.path.abspath(__file__)), "data"))
     return out
 
 
@@ -259,11 +262,12 @@ def cmd_verify(a) -> int:
 
 
 def hash_config(cfg) -> int:
-    """FNV-1a over the configuration JSON (config_hash, autotuner.cpp:39-47),
-    as this backend serialises it (the reference hashes its own
-    config_to_json text, so the two hashes are not interchangeable)."""
+    """FNV-1a over the configuration JSON text exactly as the library returned
+    it (config_hash, autotuner.cpp:39-47; the tuner's history rows hash the
+    same text, so the printed best hash matches its row)."""
+    text = cfg if isinstance(cfg, str) else json.dumps(cfg, separators=(", ", ": "))
     h = 14695981039346656037
-    for ch in json.dumps(cfg, separators=(", ", ": ")).encode():
+    for ch in text.encode():
         h ^= ch
         h = (h * 1099511628211) & 0xFFFFFFFFFFFFFFFF
     return h
@@ -282,7 +286,7 @@ def cmd_tune(a) -> int:
     rows = [r for r in hist.strip().splitlines()[1:] if r]
     print(f"evaluations: {len(rows)}")
     print(f"best objective: {secs:.9g}")
-    print(f"best hash: {hash_config(json.loads(best)):x}")
+    print(f"best hash: {hash_config(best):x}")
     if a.history:
         with open(a.history, "w") as f:
             f.write(hist)

@@ -284,25 +284,40 @@ int mdh_b200_time(mdh_b200_plan* p, const void* const* d_in, void* const* d_out,
     MDHB_CUDA(cudaSetDevice(p->prob.opt.device));
     cudaStream_t s = p->stream;
     for (int w = 0; w < warmup; ++w) p->r->launch(d_in, d_out, s);
-    std::vector<double> t;
-    cudaEvent_t a, b;
+    std::vector<double> t, tk;
+    cudaEvent_t a, b, ka, kb;
     MDHB_CUDA(cudaEventCreate(&a));
     MDHB_CUDA(cudaEventCreate(&b));
-    for (int k = 0; k < std::max(1, reps); ++k) {
-      if (flush) flush_l2(p, s);
-      MDHB_CUDA(cudaEventRecord(a, s));
-      p->r->launch(d_in, d_out, s);
-      MDHB_CUDA(cudaEventRecord(b, s));
-      MDHB_CUDA(cudaEventSynchronize(b));
-      float ms = 0.f;
-      MDHB_CUDA(cudaEventElapsedTime(&ms, a, b));
-      t.push_back(ms * 1e-3);
+    MDHB_CUDA(cudaEventCreate(&ka));
+    MDHB_CUDA(cudaEventCreate(&kb));
+    // the family records ka/kb around its dominant kernel (plan.hpp MarkScope)
+    p->r->set_marks(ka, kb);
+    try {
+      for (int k = 0; k < std::max(1, reps); ++k) {
+        if (flush) flush_l2(p, s);
+        MDHB_CUDA(cudaEventRecord(a, s));
+        p->r->launch(d_in, d_out, s);
+        MDHB_CUDA(cudaEventRecord(b, s));
+        MDHB_CUDA(cudaEventSynchronize(b));
+        float ms = 0.f;
+        MDHB_CUDA(cudaEventElapsedTime(&ms, a, b));
+        t.push_back(ms * 1e-3);
+        if (p->r->marked()) {
+          MDHB_CUDA(cudaEventElapsedTime(&ms, ka, kb));
+          tk.push_back(ms * 1e-3);
+        }
+      }
+    } catch (...) {
+      p->r->set_marks(nullptr, nullptr);
+      throw;
     }
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
+    p->r->set_marks(nullptr, nullptr);
+    for (cudaEvent_t e : {a, b, ka, kb}) cudaEventDestroy(e);
     std::sort(t.begin(), t.end());
+    std::sort(tk.begin(), tk.end());
     *median_s = t[t.size() / 2];
-    if (kernel_s) *kernel_s = *median_s;
+    // a family that did not mark runs a single kernel: the run is the kernel
+    if (kernel_s) *kernel_s = tk.size() == t.size() ? tk[tk.size() / 2] : *median_s;
   });
 }
 

@@ -1163,9 +1163,12 @@ class GemmRoutine final : public Routine {
                    static_cast<int>(N_), static_cast<int>(K_), ks_, splits_, 0, 0};
       dim3 grid(static_cast<unsigned>((N_ + 255) / 256), static_cast<unsigned>(splits_));
       size_t smem = static_cast<size_t>(M_) * ks_ * sizeof(float);
-      if (smem > 48 * 1024) MDHB_CUDA(cudaFuncSetAttribute(skinny_partial<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      if (M_ <= 16) skinny_partial<16><<<grid, 256, smem, s>>>(a);
-      else skinny_partial<32><<<grid, 256, smem, s>>>(a);
+      // the attribute goes on the instance actually launched
+      void (*kp)(SkinnyArgs) = M_ <= 16 ? skinny_partial<16> : skinny_partial<32>;
+      if (smem > 48 * 1024) MDHB_CUDA(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      mark_begin(s);
+      kp<<<grid, 256, smem, s>>>(a);
+      mark_end(s);
       MDHB_CUDA(cudaGetLastError());
       skinny_fold<<<static_cast<unsigned>((M_ * N_ + 255) / 256), 256, 0, s>>>(a);
       MDHB_CUDA(cudaGetLastError());
@@ -1215,7 +1218,9 @@ class GemmRoutine final : public Routine {
     }
     GemmArgs a{A, B, C, tab_[0], tab_[1], tab_[2], tab_[3], tab_[4], tab_[5], tab_[6], tab_[7], tab_[8], tab_[9],
                static_cast<int>(K_), tilesM_, tilesN_, psak_, psbk_};
+    mark_begin(s);
     dispatch(a, s);
+    mark_end(s);
     MDHB_CUDA(cudaGetLastError());
   }
 

@@ -440,6 +440,7 @@ class EmittedRoutine final : public Routine {
         MDHB_CUDA(cudaMemsetAsync(d_out[b], 0, static_cast<size_t>(out_cells_[b]) * store_bytes(p_.out_store[b]), s));
     }
     if (cells_ == 0) return;
+    MarkScope mark(this, s);
     if (G_) {
       void* args[] = {&ptr, &part_};
       MDHB_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(k_.kern), dim3(static_cast<unsigned>(cells_ * G_)), dim3(256),

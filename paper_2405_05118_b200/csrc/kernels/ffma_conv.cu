@@ -371,6 +371,7 @@ class FfmaConvRoutine final : public Routine {
     filter_ct<<<std::min(4 * sm_count(p_.opt.device), (nf + 255) / 256), 256, 0, s>>>(
         static_cast<const float*>(d_in[cs_.fb]), static_cast<float*>(ft_), cs_.R, cs_.S, cs_.C);
     MDHB_CUDA(cudaGetLastError());
+    MarkScope mark(this, s);  // the convolution kernel below is the dominant one
     FConvArgs a = a_;
     a.I = static_cast<const float*>(d_in[cs_.ib]);
     a.FT = static_cast<const float*>(ft_);

@@ -456,6 +456,7 @@ class GenericRoutine final : public Routine {
         MDHB_CUDA(cudaMemsetAsync(d_out[b], 0, static_cast<size_t>(n) * store_bytes(p_.out_store[b]), s));
       }
     unsigned grid = static_cast<unsigned>((P_.cells + 127) / 128);
+    MarkScope mark(this, s);
     if (f64_)
       vm_fold<double><<<grid, 128, 0, s>>>(P_, ptr, has_ps_ ? 0 : 1);
     else

@@ -368,11 +368,13 @@ class PrlRoutine final : public Routine {
     prl_pack<<<nparts_, 512, 0, s>>>(a, part_, nparts_);
     MDHB_CUDA(cudaGetLastError());
     dim3 grid(static_cast<unsigned>((a.nq + NT * a.qt - 1) / (NT * a.qt)), static_cast<unsigned>(a.rsplit));
+    mark_begin(s);
     switch (a.qt) {
       case 4: prl_main<4><<<grid, NT, 0, s>>>(a); break;
       case 16: prl_main<16><<<grid, NT, 0, s>>>(a); break;
       default: prl_main<8><<<grid, NT, 0, s>>>(a); break;
     }
+    mark_end(s);
     MDHB_CUDA(cudaGetLastError());
   }
 

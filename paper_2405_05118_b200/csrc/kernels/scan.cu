@@ -447,6 +447,7 @@ class ScanRoutine final : public Routine {
     a_.out = d_out[0];
     // cells of the output buffer the view does not reach stay zero (generic family rule)
     if (zero_out_) MDHB_CUDA(cudaMemsetAsync(d_out[0], 0, static_cast<size_t>(out_cells_) * store_bytes(st_), s));
+    MarkScope mark(this, s);
     switch (st_) {
       case Store::F32: go<float>(s); break;
       case Store::F64: go<double>(s); break;

@@ -939,6 +939,7 @@ class StencilRoutine final : public Routine {
     a.v = static_cast<const float*>(d_in[0]);
     a.w = static_cast<float*>(d_out[0]);
     const size_t smem = static_cast<size_t>(NSLOT) * 18 * BPITCH * sizeof(float);
+    MarkScope mark(this, s);
     if (pers_) {
       auto kern = minb_ == 2 ? star7_pers<2> : star7_pers<3>;
       MDHB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -1063,8 +1064,9 @@ std::unique_ptr<Routine> make_stencil(const Problem& p, const Config* cfg, Confi
   if (cfg) {
     // Instantiate from the configuration: i-planes per CTA = the parts on
     // DM x WRP x CC x SM x RM of dim i (everything below the grid).
-    auto P = parts_per_asm_layer(*cfg, e, p.m);
     int smx = p.m.id("SMX"), gpu = p.m.id("GPU");
+    if (smx < 0) fail("Unsupported", "stencil template needs an SMX layer");
+    auto P = parts_per_asm_layer(*cfg, e, p.m);
     int64_t grid_i = P[static_cast<size_t>(smx - 1)][0] * (gpu > 0 ? P[static_cast<size_t>(gpu - 1)][0] : 1);
     int64_t grid_j = P[static_cast<size_t>(smx - 1)][1], grid_k = P[static_cast<size_t>(smx - 1)][2];
     if (grid_j * TJ != a.n1 || grid_k * TK != a.n2)

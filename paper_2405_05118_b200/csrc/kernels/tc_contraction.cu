@@ -1365,6 +1365,7 @@ class TcRoutine final : public Routine {
       if (two_sm_) encode(vb2_, B, &mb2_);
       last_b_ = B;
     }
+    MarkScope mark(this, s);  // the GEMM kernel below is the dominant one
     TcArgs a = args_;
     a.C = static_cast<float*>(d_out[0]);
     if (two_sm_) {

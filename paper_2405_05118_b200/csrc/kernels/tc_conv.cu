@@ -1020,6 +1020,7 @@ class ConvRoutine final : public Routine {
       if (r != CUDA_SUCCESS) fail("CudaError", "cuTensorMapEncodeTiled (conv output) failed (" + std::to_string(static_cast<int>(r)) + ")");
       last_o_ = d_out[0];
     }
+    MarkScope mark(this, s);  // the convolution kernel below is the dominant one
     ConvArgs a = a_;
     a.O = static_cast<float*>(d_out[0]);
     const int sms = sm_count(p_.opt.device);

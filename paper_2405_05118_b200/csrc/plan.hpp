@@ -68,6 +68,38 @@ class Routine {
                                    cudaStream_t s) {
     (void)h_in; (void)h_out; (void)d_in; (void)d_out; (void)s;
   }
+  // Events recorded around the dominant kernel of launch() (mdh_b200_time's
+  // kernel_s); null = not recording.  marked() says whether the last launch
+  // recorded them (families whose run is one kernel leave it to the caller).
+  void set_marks(cudaEvent_t a, cudaEvent_t b) {
+    mark_a_ = a;
+    mark_b_ = b;
+    marked_ = false;
+  }
+  bool marked() const { return marked_; }
+
+ protected:
+  void mark_begin(cudaStream_t s) {
+    if (mark_a_) cudaEventRecord(mark_a_, s);
+  }
+  void mark_end(cudaStream_t s) {
+    if (mark_b_) {
+      cudaEventRecord(mark_b_, s);
+      marked_ = true;
+    }
+  }
+  // records mark_begin now and mark_end when the scope exits (every return
+  // path of a launch that follows the dominant kernel)
+  struct MarkScope {
+    Routine* r;
+    cudaStream_t s;
+    MarkScope(Routine* r_, cudaStream_t s_) : r(r_), s(s_) { r->mark_begin(s); }
+    ~MarkScope() { r->mark_end(s); }
+  };
+
+ private:
+  cudaEvent_t mark_a_ = nullptr, mark_b_ = nullptr;
+  bool marked_ = false;
 };
 
 // Family factories.  Each returns nullptr when the md_hom is not of its

@@ -126,6 +126,9 @@ extern "C" int mdh_b200_tune_ex(const char* comp_json, const char* asm_model, co
   bool ok = true;
   for (int b = 0; b < nin; ++b) ok = ok && alloc(0, b, din);
   for (int b = 0; b < nout; ++b) ok = ok && alloc(1, b, dout);
+  // the fills ran on the legacy stream; mdh_b200_time times on the plan's
+  // non-blocking stream, which does not order after them
+  ok = ok && cudaDeviceSynchronize() == cudaSuccess;
   // W of a PRL spec: small positive weights
   int rc = 0;
   try {
@@ -232,24 +235,38 @@ extern "C" int mdh_b200_tune_ex(const char* comp_json, const char* asm_model, co
       k0 = 1;
     }
     for (int k = k0; k < n_random; ++k) evaluate(pool[static_cast<size_t>(rng() % static_cast<uint64_t>(np))]);
+    // first-improving hill climb from the best; once a climb from the current
+    // best has converged ("settled", autotuner.cpp:290-300) the budget goes to
+    // random candidates until the best changes
+    int settled_i = -1;
     while (static_cast<int>(hist.size()) < budget) {
-      bool improved = false;
-      if (best_i >= 0) {
-        std::vector<int> nb;
-        for (int j = 0; j < n; ++j)
-          if (j != best_i && neighbours(space[static_cast<size_t>(best_i)], space[static_cast<size_t>(j)])) nb.push_back(j);
-        std::shuffle(nb.begin(), nb.end(), rng);
-        for (int j : nb) {
-          if (static_cast<int>(hist.size()) >= budget) break;
-          double before = best;
-          evaluate(j);
-          if (best < before) {
-            improved = true;
-            break;
+      if (best_i >= 0 && settled_i != best_i) {
+        bool converged = false, out_of_budget = false;
+        while (!converged && !out_of_budget) {
+          std::vector<int> nb;
+          for (int j = 0; j < n; ++j)
+            if (j != best_i && neighbours(space[static_cast<size_t>(best_i)], space[static_cast<size_t>(j)])) nb.push_back(j);
+          std::shuffle(nb.begin(), nb.end(), rng);
+          bool improved = false;
+          for (int j : nb) {
+            if (static_cast<int>(hist.size()) >= budget) {
+              out_of_budget = true;
+              break;
+            }
+            double before = best;
+            evaluate(j);
+            if (best < before) {
+              improved = true;
+              break;
+            }
           }
+          if (!improved && !out_of_budget) converged = true;
         }
+        if (out_of_budget) break;
+        settled_i = best_i;
+      } else {
+        evaluate(static_cast<int>(rng() % static_cast<uint64_t>(n)));
       }
-      if (!improved && static_cast<int>(hist.size()) < budget) evaluate(static_cast<int>(rng() % static_cast<uint64_t>(n)));
     }
     if (best_i < 0) fail("NoValidConfigFound", "every evaluated configuration failed");
     std::ostringstream csv;
