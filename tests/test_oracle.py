@@ -123,3 +123,119 @@ def test_oracle_equals_unmodified_reference(name):
         want = refbind.reference_execute(text, ins)
         ok, why = mo.buffers_match(got, want, 0.0)
         assert ok, why
+
+
+# ---- the BASELINE specs themselves (specs/*.json), shrunk -----------------
+# The GPU parity tests check the CUDA kernels against the restatement on
+# these specs (full size through ++ slices), so the restatement must agree
+# with the unmodified reference on exactly these files: the packed PRL key
+# (select/cmp/idx arithmetic), the NHWC MCC views, the reconstructed CCSD(T)
+# permutation, the 7-point Jacobi3D views and the ps:+ scan.
+SPEC_SIZES = {
+    "matvec_fp32": [16, 32],
+    "jacobi3d_fp32": [8, 8, 8],
+    "matmul_fp32": [8, 8, 16],
+    "matmul_resnet_fc": [4, 40, 64],
+    "mcc_nhwc": [2, 6, 6, 8, 3, 3, 8],
+    "ccsdt_abcdef_gdab_efgc": [3, 3, 3, 3, 3, 3, 8],
+    "prl_max": [64, 4096],
+    "scan_i32": [100],
+}
+
+
+def load_spec(name, sizes=None):
+    with open(os.path.join(SPECS_DIR, name + ".json")) as f:
+        j = json.load(f)
+    if sizes is not None:
+        j["sizes"] = list(sizes)
+    return json.dumps(j)
+
+
+def spec_inputs(name, comp, seed):
+    ins = mo.make_inputs(comp, seed)
+    if name == "prl_max":
+        # fields in [0, 3) (forces matches and ties, as bench.py), weights 1..9
+        rng = np.random.default_rng(seed)
+        ins = [rng.integers(0, 3, x.shape).astype(np.int64) for x in ins[:2]] + [np.array([3, 5, 7, 9], np.int64)]
+    return ins
+
+
+def test_specs_cover_every_baseline_workload():
+    assert sorted(SPEC_SIZES) == sorted(f[:-5] for f in os.listdir(SPECS_DIR) if f.endswith(".json"))
+
+
+@needs_ref
+@pytest.mark.parametrize("name", sorted(SPEC_SIZES))
+def test_oracle_equals_unmodified_reference_on_baseline_specs(name):
+    text = load_spec(name, SPEC_SIZES[name])
+    comp = mo.Computation.from_json(text)
+    for seed in (1, 2, 3):
+        ins = spec_inputs(name, comp, seed)
+        got = mo.execute(comp, ins)
+        want = refbind.reference_execute(text, ins)
+        ok, why = mo.buffers_match(got, want, 0.0)  # bit-for-bit
+        assert ok, f"{name} seed {seed}: {why}"
+
+
+@needs_ref
+@pytest.mark.parametrize("name", sorted(SPEC_SIZES))
+def test_oracle_equals_reference_interpreter_under_sampled_configs(name):
+    # interpret(lower(e, m, cfg)) folds in the configuration's order
+    # (interpreter.cpp:54-66); on the reference input distribution every
+    # BASELINE spec is exact, so every order gives the same bits.
+    text = load_spec(name, SPEC_SIZES[name])
+    comp = mo.Computation.from_json(text)
+    ins = spec_inputs(name, comp, 7)
+    want = mo.execute(comp, ins)
+    for asm in ("CUDA+WRP", "OpenMP"):
+        for seed in range(4):
+            cfg = refbind.sample_config(text, asm, seed)
+            got = refbind.interpret(text, asm, cfg, ins)
+            ok, why = mo.buffers_match(got, want, 0.0)
+            assert ok, f"{name} {asm} seed {seed}: {why}"
+
+
+@needs_ref
+@pytest.mark.parametrize("name", ["prl_max", "mcc_nhwc", "ccsdt_abcdef_gdab_efgc", "jacobi3d_fp32", "matmul_fp32"])
+def test_oracle_slices_equal_unmodified_reference(name):
+    # the GPU tests check full-size results through ++ slices of the oracle
+    # (execute_slice / execute_box); pin that slicing on the reference itself
+    text = load_spec(name, SPEC_SIZES[name])
+    comp = mo.Computation.from_json(text)
+    ins = spec_inputs(name, comp, 5)
+    (whole, wdef), = refbind.reference_execute(text, ins)
+    n0 = comp.sizes[0]
+    for lo, hi in [(0, 1), (n0 - 1, n0), (n0 // 2 - 1, n0 // 2 + 1)]:
+        ((part, pdef),), shifts = mo.execute_slice(comp, ins, 0, lo, hi)
+        sl = tuple(slice(s, s + n) for s, n in zip(shifts[0], part.shape))
+        assert np.array_equal(whole[sl], part) and pdef.all() and wdef[sl].all(), (name, lo, hi)
+
+
+def test_prl_packed_key_is_argmax_with_lowest_record():
+    # the packed key weight*2^20 + (2^20-1-r) folded with pw:max
+    # is the best weight with the lowest record id on ties (brute force).
+    text = load_spec("prl_max", [64, 512])
+    comp = mo.Computation.from_json(text)
+    Q, D, W = spec_inputs("prl_max", comp, 11)
+    (best, _), = mo.execute(comp, [Q, D, W])
+    # cmp yields -1/0/1 (scalar_expr.cpp:396-405), select(c, a, b) = c ? a : b,
+    # so select(cmp(q, d), 0, w) adds w for every EQUAL field
+    wt = np.where(Q[:, None, :] == D[None, :, :], W[None, None, :], 0).sum(-1)
+    top = wt.max(1)
+    first = np.argmax(wt == top[:, None], axis=1)
+    assert np.array_equal(best >> 20, top) and np.array_equal((1 << 20) - 1 - (best & ((1 << 20) - 1)), first)
+
+
+@needs_ref
+def test_reference_emitted_openmp_kernel_matches_oracle_on_jacobi3d():
+    # the CPU reference arm of bench.py runs the reference's own emitted
+    # OpenMP kernel; it must compute the same md_hom as the oracle
+    import bench
+    text = load_spec("jacobi3d_fp32", [16, 12, 10])
+    comp = mo.Computation.from_json(text)
+    ins = mo.make_inputs(comp, 3)
+    cfg, _ = bench.openmp_config(text, 4)
+    out = np.zeros(mo.output_shapes(comp)[0])
+    refbind.EmittedKernel(text, "OpenMP", cfg)(ins, [out])
+    (want, _), = mo.execute(comp, ins)
+    assert np.array_equal(out, want)
