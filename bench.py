@@ -259,41 +259,104 @@ def openmp_config(comp_json, threads):
     return json.dumps({"num_parts": parts, "ass_de": ass, "ass_scalar": ass, "ass_re": ass}), t
 
 
-def cpu_reference_run(name, sample_planes, threads, reps):
-    """Times the reference's emitted OpenMP kernel (f64) on an i-slab sample.
-    Returns (seconds per run, sample description, kind, cores)."""
+def omp_threads(n):
+    """omp_set_num_threads on the process's libgomp (the emitted kernels link
+    the same libgomp.so.1, so this sets their team size)."""
+    import ctypes
+    try:
+        ctypes.CDLL("libgomp.so.1").omp_set_num_threads(int(n))
+    except OSError:
+        os.environ["OMP_NUM_THREADS"] = str(n)
+
+
+def cpu_inputs(name, planes=None):
+    """The reference's own input generator (support.hpp:32-51) on the spec,
+    full size or an i-slab of `planes` planes; f64/i64 as the reference
+    computes, with zeroed outputs."""
     from oracle import mdh_oracle as mo
-    from oracle import refbind
     j = spec(name)
-    j["sizes"][0] = sample_planes
+    if planes:
+        j["sizes"][0] = planes
     text = json.dumps(j)
     comp = mo.Computation.from_json(text)
     ins = [x.astype(np.float64) if vb.type == "f64" else x for vb, x in zip(comp.inputs, mo.make_inputs(comp, 1))]
     outs = [np.zeros(s, dtype=np.float64 if vb.type == "f64" else np.int64)
             for vb, s in zip(comp.outputs, mo.output_shapes(comp))]
-    try:
-        cfg, t = openmp_config(text, threads)
-        os.environ["OMP_NUM_THREADS"] = str(threads)
-        k = refbind.EmittedKernel(text, "OpenMP", cfg)
-        k(ins, outs)  # warm-up
-        ts = []
-        for _ in range(reps):
-            t0 = time.perf_counter()
-            k(ins, outs)
-            ts.append(time.perf_counter() - t0)
-        return statistics.median(ts), f"reference emitted OpenMP kernel (f64), {sample_planes}-plane i-slab of {name}", \
-            "reference", threads
-    except Exception as e:  # reference not built here: the C restatement, 1 thread
-        plan = mo.pw_outer_plan(comp)
+    return text, comp, ins, outs
+
+
+def cpu_reference_kernel(name, threads, planes=None):
+    """The reference's emitted OpenMP kernel (mdh::emit of a blocked OpenMP
+    configuration, built with compile_and_run's flags) on the FULL workload
+    (planes=None) or an i-slab.  Returns (call, description)."""
+    from oracle import refbind
+    text, comp, ins, outs = cpu_inputs(name, planes)
+    cfg, _ = openmp_config(text, threads)
+    k = refbind.EmittedKernel(text, "OpenMP", cfg)
+    what = f"reference emitted OpenMP kernel (f64), {'full ' + str(comp.sizes) if not planes else str(planes) + '-plane i-slab'}"
+    return (lambda: k(ins, outs)), what
+
+
+def time_calls(fn, reps):
+    fn()  # warm-up (first touch of the outputs, thread team start)
+    ts = []
+    for _ in range(reps):
         t0 = time.perf_counter()
-        mo.execute(comp, ins, plan)
-        return time.perf_counter() - t0, f"oracle C restatement (f64, 1 thread; reference unavailable: {e})", "port", 1
+        fn()
+        ts.append(time.perf_counter() - t0)
+    return statistics.median(ts)
 
 
-def cpu_points_bytes(name, planes):
-    j = spec(name)
-    full = j["sizes"][0]
-    return planes / full
+def cpu_baseline_line(name, reps=3):
+    """cpu_baseline of our arm: the reference's emitted OpenMP kernel on the
+    same full workload with every host thread (the value), beside it the same
+    kernel on one thread and the single-threaded reference_execute
+    (highlevel.cpp:110-113) on an 8-plane slab, extrapolated and labelled so."""
+    from oracle import refbind
+    full_bytes = bytes_of_spec(name)
+    threads = os.cpu_count() or 1
+    try:
+        call, what = cpu_reference_kernel(name, threads)
+        omp_threads(threads)
+        s_all = time_calls(call, reps)
+        omp_threads(1)
+        s_one = time_calls(call, 1)
+        omp_threads(threads)
+        del call
+        _, comp, ins, _ = cpu_inputs(name, 8)
+        text = json.dumps(comp.to_json())
+        t0 = time.perf_counter()
+        refbind.reference_execute(text, ins)
+        s_ref = (time.perf_counter() - t0) * spec(name)["sizes"][0] / 8
+        return {"value": round(full_bytes / s_all / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
+                "sample": f"{what}, {threads} threads, median of {reps}; GB/s counted with the fp32 algorithmic "
+                          "bytes of the same points (same config as the GPU arm)",
+                "ms_per_step": round(s_all * 1e3, 2), "host_cpu": host_cpu(),
+                "one_thread": {"value": round(full_bytes / s_one / 1e9, 3), "ms_per_step": round(s_one * 1e3, 2),
+                               "sample": what + ", 1 thread"},
+                "reference_execute": {"value": round(full_bytes / s_ref / 1e9, 4), "s_per_step": round(s_ref, 2),
+                                      "sample": "mdh::reference_execute (single-threaded by contract), 8-plane "
+                                                "i-slab, extrapolated to the full workload"}}
+    except Exception as e:  # reference not built: the C restatement, 1 thread, on a slab
+        from oracle import mdh_oracle as mo
+        _, comp, ins, _ = cpu_inputs(name, 8)
+        t0 = time.perf_counter()
+        mo.execute(comp, ins, mo.pw_outer_plan(comp))
+        s = (time.perf_counter() - t0) * spec(name)["sizes"][0] / 8
+        return {"value": round(full_bytes / s / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "port",
+                "sample": f"oracle C restatement (f64, 1 thread) on an 8-plane slab, extrapolated "
+                          f"(reference unavailable: {e})"}
+
+
+def host_cpu():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 # ------------------------------------------------------------------ main
@@ -313,29 +376,33 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
     if args.impl == "reference":
+        # the reference's own CPU implementation of the path, on the SAME
+        # workload as our arm (full size), every host thread, one run per step
         if rank != 0:
             return
+        base = args.routine.partition(":")[0]
         threads = os.cpu_count() or 1
-        planes = 32
-        per, sample, kind, cores = None, None, None, None
+        omp_threads(threads)
+        call, what = cpu_reference_kernel(base, threads)
+        for _ in range(max(1, args.warmup)):
+            call()
         runs = []
-        for _ in range(max(1, args.warmup // 3)):
-            cpu_reference_run(args.routine, planes, threads, 1)
         for _ in range(args.steps):
-            s, sample, kind, cores = cpu_reference_run(args.routine, planes, threads, 1)
-            runs.append(s)
-        per = statistics.median(runs)
-        frac = cpu_points_bytes(args.routine, planes)
-        full_bytes = bytes_of_spec(args.routine)
-        value = full_bytes * frac / per / 1e9
+            t0 = time.perf_counter()
+            call()
+            runs.append(time.perf_counter() - t0)
+        tot = sum(runs)
+        per = tot / len(runs)
+        value = bytes_of_spec(base) / per / 1e9
         line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(per * 1e3, 3), "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator)",
                 "impl": "reference",
-                "config": {"workload": f"{args.routine} ({planes}-plane i-slab sample per step)",
-                           "sample_fraction": frac, "threads": threads},
-                "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": cores, "kind": kind,
-                                 "sample": sample},
+                "config": {"workload": f"{base} {spec(base)['sizes']} (full, same as the GPU arm)", "threads": threads,
+                           "host_cpu": host_cpu()},
+                "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
+                                 "sample": what + f", {threads} threads; GB/s counted with the fp32 algorithmic "
+                                                  "bytes of the same points"},
                 "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -389,12 +456,7 @@ def main():
             "roofline": roof, "clocks": clocks, "e2e": e2e,
             "gpu_launches": plan.launches * args.steps}
     if rank == 0 and world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        planes = 32
-        s, sample, kind, cores = cpu_reference_run(base, planes, threads, 3)
-        cpu_val = bytes_of_spec(base) * cpu_points_bytes(base, planes) / s / 1e9
-        line["cpu_baseline"] = {"value": round(cpu_val, 3), "unit": unit, "cores": cores, "kind": kind,
-                                "sample": sample + "; GB/s counted with the fp32 algorithmic bytes of the same points"}
+        line["cpu_baseline"] = cpu_baseline_line(base)
     if not args.no_routines:
         line["routines"] = routines_table(device, pk, world, exclude=args.routine)
         line["gpu_launches"] += sum(r.get("launches", 0) for r in line["routines"])

@@ -165,6 +165,24 @@ int mdh_b200_lowered(const char* computation_json, const char* asm_model, const 
  * counterpart of mdh::emit (codegen.hpp:38-53, `mdh emit`). */
 int mdh_b200_kernel_source(const mdh_b200_plan* plan, char* buf, int64_t cap, int64_t* need);
 
+/* Custom combine operators (API extension, SURVEY §8(b) "Custom combine").
+ * The reference's BinOpKind is closed (proj/include/mdh/mda.hpp:52) and its
+ * JSON accepts only pw:/ps: over + * min max - / (proj/src/json_io.cpp:58-64,
+ * proj/src/mda.cpp:75-83).  Here a registered operator is usable as
+ * "pw:<name>" / "ps:<name>" in a computation's "combine" list.  It folds the
+ * TUPLE of all output components of the scalar function jointly: `cuda_body`
+ * is CUDA C statements over a0..a{arity-1} (the accumulator, lvalues) and
+ * b0..b{arity-1} (the next value), compiled into the md_hom's kernel by NVRTC
+ * (the emitted family).  md_hom validity (Lemma 2.9) requires assoc and comm.
+ * Built in: "max_prl" (arity 2: larger weight, lower record on ties --
+ * PRL's custom combine), also implemented by the PRL
+ * template and the device VM.  Registering an existing user operator's name
+ * replaces it; plans already created keep their compiled kernel. */
+int mdh_b200_register_combine(const char* name, int arity, const char* cuda_body, const char* identity_csv,
+                              int assoc, int comm, const char* description);
+/* JSON array describing every registered custom operator. */
+int mdh_b200_combine_info(char* buf, int64_t cap, int64_t* need);
+
 /* Number of kernel launches one mdh_b200_run issues. */
 int mdh_b200_launches_per_run(const mdh_b200_plan* plan, int* launches);
 

@@ -369,6 +369,47 @@ int mdh_b200_lowered(const char* comp_json, const char* asm_model, const char* c
   });
 }
 
+int mdh_b200_register_combine(const char* name, int arity, const char* cuda_body, const char* identity_csv,
+                              int assoc, int comm, const char* description) {
+  return guard([&] {
+    if (!name || !cuda_body) mdhb::fail("InvalidConfig", "null argument");
+    mdhb::CustomCombine c;
+    c.name = name;
+    c.arity = arity;
+    c.body = cuda_body;
+    c.assoc = assoc != 0;
+    c.comm = comm != 0;
+    c.description = description ? description : "";
+    std::string id = identity_csv ? identity_csv : "";
+    size_t st = 0;
+    while (!id.empty()) {
+      size_t k = id.find(',', st);
+      c.identity.push_back(id.substr(st, k == std::string::npos ? std::string::npos : k - st));
+      if (k == std::string::npos) break;
+      st = k + 1;
+    }
+    mdhb::register_combine(c);
+  });
+}
+
+int mdh_b200_combine_info(char* buf, int64_t cap, int64_t* need) {
+  return guard([&] {
+    std::ostringstream os;
+    os << "[";
+    auto names = mdhb::combine_names();
+    for (size_t k = 0; k < names.size(); ++k) {
+      const mdhb::CustomCombine& c = mdhb::combine_at(static_cast<int>(k));
+      os << (k ? ", " : "") << "{\"name\": \"" << json_escape(c.name) << "\", \"arity\": " << c.arity
+         << ", \"assoc\": " << (c.assoc ? "true" : "false") << ", \"comm\": " << (c.comm ? "true" : "false")
+         << ", \"builtin\": " << (c.vm_op ? "true" : "false") << ", \"identity\": [";
+      for (size_t i = 0; i < c.identity.size(); ++i) os << (i ? ", " : "") << "\"" << json_escape(c.identity[i]) << "\"";
+      os << "], \"body\": \"" << json_escape(c.body) << "\", \"description\": \"" << json_escape(c.description) << "\"}";
+    }
+    os << "]";
+    put(os.str(), buf, cap, need);
+  });
+}
+
 int mdh_b200_launches_per_run(const mdh_b200_plan* p, int* launches) {
   return guard([&] { *launches = p->r->launches(); });
 }

@@ -177,8 +177,18 @@ class Emitter {
     s << ind << "if (" << first << ") {\n";
     for (size_t c = 0; c < e_.assigns.size(); ++c) s << ind << "  " << acc << c << " = " << val << c << ";\n";
     s << ind << "} else {\n";
-    for (size_t c = 0; c < e_.assigns.size(); ++c)
-      s << ind << "  " << acc << c << " = " << fold_expr(fold, acc + std::to_string(c), val + std::to_string(c)) << ";\n";
+    if (fold >= kCustomFoldBase) {
+      // registered custom operator: its body folds the whole component tuple
+      // (a0.. = accumulator lvalues, b0.. = the next value)
+      const CustomCombine& op = combine_at(fold - kCustomFoldBase);
+      s << ind << "  {\n";
+      for (size_t c = 0; c < e_.assigns.size(); ++c)
+        s << ind << "    auto& a" << c << " = " << acc << c << ";\n" << ind << "    const auto b" << c << " = " << val << c << ";\n";
+      s << ind << "    " << op.body << "\n" << ind << "  }\n";
+    } else {
+      for (size_t c = 0; c < e_.assigns.size(); ++c)
+        s << ind << "  " << acc << c << " = " << fold_expr(fold, acc + std::to_string(c), val + std::to_string(c)) << ";\n";
+    }
     s << ind << "}\n" << ind << first << " = false;\n";
     return s.str();
   }
@@ -310,7 +320,7 @@ class Emitter {
     const int64_t C = cells();
     if (L < 1024 || C >= 16384) return 0;
     // re-association is invisible for integers and min/max; FP32 storage is tolerance mode
-    bool ok = true;
+    bool ok = true;  // (custom operators are declared associative + commutative by md_hom validity)
     for (auto& a : e_.assigns)
       if (a.e.type == Ty::F64 && (fold == 0 || fold == 2) && p_.opt.fstore == Store::F64) ok = false;
     if (!ok) return 0;

@@ -53,6 +53,7 @@ struct VmParams {
   int32_t pw_dims[kMaxD];
   int64_t cells;
   int fold;  // Fold enum, -1 none
+  int custom_vm;  // built-in custom operator compiled into the VM (1 = max_prl), 0 none
   int n_in_acc;
   const VmAccess* in_acc;
   int n_comp;
@@ -156,6 +157,19 @@ __device__ __forceinline__ void fold_into(int fold, bool is_f, Slot& acc, Slot v
   }
 }
 
+// built-in custom operators fold the whole component tuple; b better than a?
+__device__ __forceinline__ bool tuple_better(int op, const int32_t* comp_float, const Slot* a, const Slot* b) {
+  switch (op) {
+    case 1: {  // max_prl: larger key (component 0), lower payload (component 1) on ties
+      const bool gt = comp_float[0] ? b[0].f > a[0].f : b[0].i > a[0].i;
+      const bool eq = comp_float[0] ? b[0].f == a[0].f : b[0].i == a[0].i;
+      const bool lt1 = comp_float[1] ? b[1].f < a[1].f : b[1].i < a[1].i;
+      return gt || (eq && lt1);
+    }
+    default: return false;
+  }
+}
+
 __device__ __forceinline__ void store_out(void* base, int store, int64_t off, Slot v, bool is_f) {
   switch (store) {
     case 0: static_cast<float*>(base)[off] = static_cast<float>(is_f ? v.f : static_cast<double>(v.i)); break;
@@ -205,6 +219,9 @@ __global__ void __launch_bounds__(128) vm_fold(VmParams P, Ptrs ptr, int direct)
     if (first) {
       for (int c = 0; c < P.n_comp; ++c) acc[c] = v[c];
       first = false;
+    } else if (P.custom_vm) {
+      if (tuple_better(P.custom_vm, P.comp_float, acc, v))
+        for (int c = 0; c < P.n_comp; ++c) acc[c] = v[c];
     } else {
       for (int c = 0; c < P.n_comp; ++c) fold_into<FT>(P.fold, P.comp_float[c] != 0, acc[c], v[c]);
     }
@@ -248,6 +265,18 @@ __global__ void vm_prefix(VmParams P, int d, int64_t lines) {
     rem /= P.sizes[e];
   }
   int64_t st = P.cstride[d];
+  if (P.custom_vm) {  // tuple operator: the running best tuple carries forward
+    Slot prev[kMaxComp], cur[kMaxComp];
+    for (int c = 0; c < P.n_comp; ++c) prev[c].i = P.acc[static_cast<int64_t>(c) * P.cells + base];
+    for (int64_t t = 1; t < P.sizes[d]; ++t) {
+      for (int c = 0; c < P.n_comp; ++c) cur[c].i = P.acc[static_cast<int64_t>(c) * P.cells + base + t * st];
+      if (tuple_better(P.custom_vm, P.comp_float, cur, prev))
+        for (int c = 0; c < P.n_comp; ++c) cur[c] = prev[c];
+      for (int c = 0; c < P.n_comp; ++c) P.acc[static_cast<int64_t>(c) * P.cells + base + t * st] = cur[c].i;
+      for (int c = 0; c < P.n_comp; ++c) prev[c] = cur[c];
+    }
+    return;
+  }
   for (int c = 0; c < P.n_comp; ++c) {
     int64_t* a = P.acc + static_cast<int64_t>(c) * P.cells;
     Slot prev;
@@ -342,6 +371,14 @@ class GenericRoutine final : public Routine {
     std::memset(&P_, 0, sizeof P_);
     P_.D = D;
     P_.fold = e.fold();
+    if (P_.fold >= kCustomFoldBase) {
+      const CustomCombine& op = combine_at(P_.fold - kCustomFoldBase);
+      if (!op.vm_op)
+        fail("Unsupported", "custom combine operator '" + op.name +
+                                "' has no device-VM implementation (it runs through the emitted family, NVRTC, "
+                                "which does not take ps dimensions)");
+      P_.custom_vm = op.vm_op;
+    }
     std::vector<int64_t> coll = e.collapsed();
     int64_t cells = 1;
     for (int d = D - 1; d >= 0; --d) {

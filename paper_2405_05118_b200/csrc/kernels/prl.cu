@@ -18,6 +18,18 @@
 // + IMAD (key) + IMNMX (fold) -- six instructions for four field compares.
 // When the data does not fit that encoding the same kernel takes an exact
 // 64-bit path (a device-side flag decides; no host round trip).
+//
+// The same template also runs the UNPACKED form with the registered custom
+// combine operator max_prl (mdh_model.cpp registry; specs/prl_max_prl.json):
+//
+//   (weight[q], record[q]) = max_prl over r of ( sum_f select(...), r )
+//
+// i.e. two output buffers folded jointly -- larger weight, lower record on
+// ties.  Internally the fast paths pack (w, r) exactly like the spec form
+// with S = 2^ceil(log2(max(records, 128))); every thread's best is unpacked
+// to a (w, r) pair and committed with a 128-bit compare-and-swap (lexicographic
+// max, order-independent); the exact path folds pairs without packing, so
+// no weight range is excluded.  prl_unpack writes the two outputs.
 #include <climits>
 #include <cstdlib>
 #include <cstring>
@@ -52,6 +64,13 @@ struct PrlArgs {
   int allow5;     // five-instruction path permitted (MDHB_PRL_5=1)
   uint32_t one;   // 1 (keeps the byte-compare add an IMAD, see add7f_fma)
   int rsplit;     // record splits (grid.y)
+  // max_prl (unpacked pair) mode
+  int pair;                  // 1: fold (w, r) pairs with max_prl
+  int lgS;                   // S = 2^lgS, C = S - 1 internally
+  unsigned long long* pairs;  // [nq][2] (w, r), 16-byte aligned scratch
+  void* out_r;                // record output (weight output is `best`)
+  int r_is64;
+  int64_t r_stride;
 };
 
 __device__ __forceinline__ int64_t ld(const void* p, int is64, int64_t i) {
@@ -152,8 +171,14 @@ __global__ void __launch_bounds__(512) prl_pack(PrlArgs a, const long long* part
         w |= static_cast<uint32_t>(ld(a.Q, a.q_is64, q * a.qs + a.qf[t]) - base) << (8 * t);
       a.qp[q] = w;
     }
-    if (a.out_is64) a.best[q * a.out_stride] = LLONG_MIN;
-    else reinterpret_cast<int32_t*>(a.best)[q * a.out_stride] = INT_MIN;
+    if (a.pair) {
+      a.pairs[2 * q] = static_cast<unsigned long long>(LLONG_MIN);  // max_prl identity (-inf, +inf)
+      a.pairs[2 * q + 1] = static_cast<unsigned long long>(LLONG_MAX);
+    } else if (a.out_is64) {
+      a.best[q * a.out_stride] = LLONG_MIN;
+    } else {
+      reinterpret_cast<int32_t*>(a.best)[q * a.out_stride] = INT_MIN;
+    }
   }
   if (!fast) return;
   for (int64_t r = i; r < a.nr; r += stride) {
@@ -172,6 +197,36 @@ __device__ __forceinline__ uint32_t add7f_fma(uint32_t xm, uint32_t one) {
   uint32_t t;
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(xm), "r"(one), "r"(0x7F7F7F7Fu));
   return t;
+}
+
+// max_prl commit: lexicographic max of (w, -r) by 128-bit compare-and-swap
+__device__ __forceinline__ void commit_pair(unsigned long long* slot, long long w, long long r) {
+  unsigned __int128* p = reinterpret_cast<unsigned __int128*>(slot);
+  unsigned __int128 cur = *reinterpret_cast<volatile unsigned __int128*>(p);
+  for (;;) {
+    const long long cw = static_cast<long long>(static_cast<unsigned long long>(cur));
+    const long long cr = static_cast<long long>(static_cast<unsigned long long>(cur >> 64));
+    if (!(w > cw || (w == cw && r < cr))) return;
+    const unsigned __int128 nv = (static_cast<unsigned __int128>(static_cast<unsigned long long>(r)) << 64) |
+                                 static_cast<unsigned long long>(w);
+    const unsigned __int128 prev = atomicCAS(p, cur, nv);
+    if (prev == cur) return;
+    cur = prev;
+  }
+}
+
+// max_prl: unpack each thread's packed best key (fast paths) and commit
+template <int QT>
+__device__ __forceinline__ void commit_pairs_packed(const PrlArgs& a, int64_t q0, const long long (&best)[QT]) {
+  const long long S = 1LL << a.lgS;
+#pragma unroll
+  for (int j = 0; j < QT; ++j) {
+    int64_t q = q0 + static_cast<int64_t>(j) * NT;
+    if (q >= a.nq) continue;
+    const long long w = best[j] >> a.lgS;  // floor: the low part is in [0, S)
+    const long long r = (S - 1) - (best[j] & (S - 1));
+    commit_pair(a.pairs + 2 * q, w, r);
+  }
 }
 
 template <int QT>
@@ -198,6 +253,7 @@ __global__ void __launch_bounds__(NT) prl_main(PrlArgs a) {
   const int64_t per = (a.nr + a.rsplit - 1) / a.rsplit;
   const int64_t r_begin = static_cast<int64_t>(blockIdx.y) * per;
   const int64_t r_end = min(a.nr, r_begin + per);
+  if (r_end <= r_begin) return;  // empty record split: nothing to fold
   long long best64[QT];
   if (a.info[4]) {
     // ---- five instructions per pair: LOP3 (xor & mask) + IADD + LOP3 (byte
@@ -280,6 +336,37 @@ __global__ void __launch_bounds__(NT) prl_main(PrlArgs a) {
     }
 #pragma unroll
     for (int j = 0; j < QT; ++j) best64[j] = best[j];
+  } else if (a.pair) {
+    // ---- exact max_prl path: (w, r) pairs folded without packing
+    long long bw[QT], br[QT];
+#pragma unroll
+    for (int j = 0; j < QT; ++j) {
+      bw[j] = LLONG_MIN;
+      br[j] = LLONG_MAX;
+    }
+    for (int64_t r = r_begin; r < r_end; ++r) {
+#pragma unroll
+      for (int j = 0; j < QT; ++j) {
+        int64_t q = q0 + static_cast<int64_t>(j) * NT;
+        if (q >= a.nq) continue;
+        long long w = 0;
+        for (int t = 0; t < a.F; ++t) {
+          long long x = ld(a.Q, a.q_is64, q * a.qs + a.qf[t]);
+          long long y = ld(a.D, a.d_is64, r * a.ds + a.df[t]);
+          w += x == y ? ld(a.W, a.w_is64, a.wf[t]) : 0;
+        }
+        if (w > bw[j] || r == r_begin) {  // ascending r: ties keep the lower record
+          bw[j] = w;
+          br[j] = r;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < QT; ++j) {
+      int64_t q = q0 + static_cast<int64_t>(j) * NT;
+      if (q < a.nq) commit_pair(a.pairs + 2 * q, bw[j], br[j]);
+    }
+    return;
   } else {
     // ---- exact 64-bit path: the scalar function as written, per pair
 #pragma unroll
@@ -301,7 +388,19 @@ __global__ void __launch_bounds__(NT) prl_main(PrlArgs a) {
       }
     }
   }
-  commit_best<QT>(a, q0, best64);
+  if (a.pair) commit_pairs_packed<QT>(a, q0, best64);
+  else commit_best<QT>(a, q0, best64);
+}
+
+// max_prl: the folded pairs -> the two output buffers (storage i64 or i32)
+__global__ void prl_unpack(PrlArgs a) {
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= a.nq) return;
+  const long long w = static_cast<long long>(a.pairs[2 * q]), r = static_cast<long long>(a.pairs[2 * q + 1]);
+  if (a.out_is64) a.best[q * a.out_stride] = w;
+  else reinterpret_cast<int32_t*>(a.best)[q * a.out_stride] = static_cast<int32_t>(w);
+  if (a.r_is64) static_cast<int64_t*>(a.out_r)[q * a.r_stride] = r;
+  else static_cast<int32_t*>(a.out_r)[q * a.r_stride] = static_cast<int32_t>(r);
 }
 
 // ---------------------------------------------------------------- host
@@ -339,13 +438,16 @@ class PrlRoutine final : public Routine {
     part_ = reinterpret_cast<long long*>(static_cast<char*>(scratch_) + 256);
     a_.qp = reinterpret_cast<uint32_t*>(static_cast<char*>(scratch_) + head);
     a_.dp = a_.qp + a.nq;
+    if (a_.pair) MDHB_CUDA(cudaMalloc(&pairs_, static_cast<size_t>(a.nq) * 16 + 16));
+    a_.pairs = static_cast<unsigned long long*>(pairs_);
   }
   ~PrlRoutine() override {
     if (scratch_) cudaFree(scratch_);
+    if (pairs_) cudaFree(pairs_);
   }
   const char* family() const override { return "prl"; }
   const char* bound() const override { return "int"; }
-  int launches() const override { return 3; }
+  int launches() const override { return a_.pair ? 4 : 3; }
   double bytes() const override { return static_cast<double>(p_.in_bytes + p_.out_bytes); }
   // integer work: F compares + F selects + F adds + key + fold per pair
   double flops() const override { return static_cast<double>(a_.nq) * static_cast<double>(a_.nr) * (3.0 * a_.F + 3.0); }
@@ -354,7 +456,9 @@ class PrlRoutine final : public Routine {
     std::ostringstream os;
     os << "{\"kernel\": \"prl_main<" << a_.qt << ">\", \"queries\": " << a_.nq << ", \"records\": " << a_.nr
        << ", \"fields\": " << a_.F << ", \"queries_per_thread\": " << a_.qt << ", \"threads\": " << NT
-       << ", \"record_splits\": " << a_.rsplit << ", \"record_tile\": 2048, \"pairs\": " << pairs() << "}";
+       << ", \"record_splits\": " << a_.rsplit << ", \"record_tile\": 2048, \"pairs\": " << pairs()
+       << ", \"combine\": \"" << (a_.pair ? "pw:max_prl (weight, record) pairs, 128-bit CAS" : "pw:max packed key, 64-bit atomicMax")
+       << "\"}";
     return os.str();
   }
   void launch(const void* const* d_in, void* const* d_out, cudaStream_t s) override {
@@ -363,6 +467,7 @@ class PrlRoutine final : public Routine {
     a.D = d_in[ib_[1]];
     a.W = d_in[ib_[2]];
     a.best = static_cast<int64_t*>(d_out[0]);
+    if (a.pair) a.out_r = d_out[1];
     prl_range<<<nparts_, 512, 0, s>>>(a, part_);
     MDHB_CUDA(cudaGetLastError());
     prl_pack<<<nparts_, 512, 0, s>>>(a, part_, nparts_);
@@ -376,11 +481,16 @@ class PrlRoutine final : public Routine {
     }
     mark_end(s);
     MDHB_CUDA(cudaGetLastError());
+    if (a.pair) {
+      prl_unpack<<<static_cast<unsigned>((a.nq + 255) / 256), 256, 0, s>>>(a);
+      MDHB_CUDA(cudaGetLastError());
+    }
   }
 
  private:
   const Problem& p_;
   PrlArgs a_;
+  void* pairs_ = nullptr;
   int ib_[3];
   int nparts_ = 0;
   long long* part_ = nullptr;
@@ -413,14 +523,34 @@ bool split_key(const Expr& e, const Expr** sum, int64_t* S, int64_t* C, int* rdi
 
 std::unique_ptr<Routine> make_prl(const Problem& p, const Config* cfg, Config* cfg_out) {
   const MdHom& e = p.e;
-  if (e.D() != 2 || e.in.size() != 3 || e.out.size() != 1 || e.out[0].acc.size() != 1 || e.assigns.size() != 1)
-    return nullptr;
+  if (e.D() != 2 || e.in.size() != 3) return nullptr;
   int rdim = -1;
   const Expr* sum = nullptr;
   int64_t S = 0, C = 0;
-  if (!split_key(e.assigns[0].e, &sum, &S, &C, &rdim)) return nullptr;
+  bool pair = false;
+  if (e.out.size() == 1 && e.out[0].acc.size() == 1 && e.assigns.size() == 1) {
+    // packed form: best = weight * S + (C - idx(r)) folded with pw:max
+    if (!split_key(e.assigns[0].e, &sum, &S, &C, &rdim)) return nullptr;
+    if (e.comb[static_cast<size_t>(rdim)].kind != Combine::PW || e.comb[static_cast<size_t>(rdim)].op != Fold::Max)
+      return nullptr;
+  } else if (e.out.size() == 2 && e.out[0].acc.size() == 1 && e.out[1].acc.size() == 1 && e.assigns.size() == 2) {
+    // unpacked form: (weight, idx(r)) folded with the custom pw:max_prl
+    rdim = e.comb[0].kind == Combine::PW ? 0 : 1;
+    const Combine& c = e.comb[static_cast<size_t>(rdim)];
+    if (c.kind != Combine::PW || c.op != Fold::Custom || combine_at(c.custom).name != "max_prl") return nullptr;
+    const Expr& id = e.assigns[1].e;
+    if (id.k != EK::Idx || id.dim != rdim + 1 || e.out[1].type != Ty::I64) return nullptr;
+    sum = &e.assigns[0].e;
+    int lg = 7;
+    while ((int64_t(1) << lg) < e.sizes[static_cast<size_t>(rdim)]) ++lg;
+    if (lg > 40) return nullptr;
+    S = int64_t(1) << lg;
+    C = S - 1;
+    pair = true;
+  } else {
+    return nullptr;
+  }
   const int qdim = 1 - rdim;
-  if (e.comb[static_cast<size_t>(rdim)].kind != Combine::PW || e.comb[static_cast<size_t>(rdim)].op != Fold::Max) return nullptr;
   if (e.comb[static_cast<size_t>(qdim)].kind != Combine::CC) return nullptr;
   std::vector<Term> terms;
   if (!collect_terms(*sum, terms) || terms.empty() || terms.size() > static_cast<size_t>(kMaxF)) return nullptr;
@@ -463,9 +593,18 @@ std::unique_ptr<Routine> make_prl(const Problem& p, const Config* cfg, Config* c
     a.wf[t] = wc;
   }
   if (ib[0] == ib[1] || ib[0] == ib[2] || ib[1] == ib[2]) return nullptr;
-  // output: best[q]
-  const Affine& o = e.out[0].acc[0].idx[0];
-  if (e.out[0].rank != 1 || o.c0 != 0 || o.coeff[static_cast<size_t>(qdim)] != 1) return nullptr;
+  // output(s): best[q] (pair mode: weight[q], record[q])
+  for (size_t b = 0; b < e.out.size(); ++b) {
+    const Affine& o = e.out[b].acc[0].idx[0];
+    if (e.out[b].rank != 1 || o.c0 != 0 || o.coeff[static_cast<size_t>(qdim)] != 1) return nullptr;
+  }
+  a.pair = pair ? 1 : 0;
+  if (pair) {
+    a.lgS = 0;
+    while ((int64_t(1) << a.lgS) < S) ++a.lgS;
+    a.r_is64 = p.out_store[1] == Store::I64;
+    a.r_stride = 1;
+  }
   a.nq = e.sizes[static_cast<size_t>(qdim)];
   a.nr = e.sizes[static_cast<size_t>(rdim)];
   a.qs = p.in_ext[static_cast<size_t>(ib[0])][1];

@@ -2,6 +2,8 @@
 
 #include <algorithm>
 #include <cctype>
+#include <deque>
+#include <mutex>
 #include <set>
 
 #include "json.hpp"
@@ -312,14 +314,25 @@ Combine parse_combine(const std::string& s, int d) {
     else if (op == "/") { c.op = Fold::Div; }
     else fail("UnknownOperator", "unknown binary operator '" + op + "'");
   };
+  auto named = [&](const std::string& op) {
+    const int k = combine_index(op);
+    if (k >= 0) {  // registered custom operator
+      const CustomCombine& cc = combine_at(k);
+      c.op = Fold::Custom;
+      c.custom = k;
+      c.assoc_comm = cc.assoc && cc.comm;
+      return;
+    }
+    bin(op);
+  };
   if (s.rfind("pw:", 0) == 0) {
     c.kind = Combine::PW;
-    bin(s.substr(3));
+    named(s.substr(3));
     return c;
   }
   if (s.rfind("ps:", 0) == 0) {
     c.kind = Combine::PS;
-    bin(s.substr(3));
+    named(s.substr(3));
     return c;
   }
   fail("ParseError", "combine operator " + std::to_string(d) + ": '" + s + "' is not cc, pw:<op>, or ps:<op>");
@@ -345,8 +358,73 @@ std::vector<int64_t> MdHom::collapsed() const {
 
 int MdHom::fold() const {
   for (auto& c : comb)
-    if (c.kind != Combine::CC) return static_cast<int>(c.op);
+    if (c.kind != Combine::CC) return c.op == Fold::Custom ? kCustomFoldBase + c.custom : static_cast<int>(c.op);
   return -1;
+}
+
+// ---- custom combine registry ------------------------------------------------
+namespace {
+// a deque keeps references stable while operators are appended; entries are
+// never removed (a plan holds its operator's index)
+std::mutex g_registry_mu;
+std::deque<CustomCombine>& registry() {
+  static std::deque<CustomCombine> r = [] {
+    std::deque<CustomCombine> v;
+    CustomCombine m;
+    m.name = "max_prl";
+    m.arity = 2;
+    // (weight, record): larger weight wins, the lower record on ties
+    m.body = "if (b0 > a0 || (b0 == a0 && b1 < a1)) { a0 = b0; a1 = b1; }";
+    m.identity = {"INT64_MIN", "INT64_MAX"};
+    m.assoc = m.comm = true;
+    m.description = "PRL max: lexicographic max of (weight, -record) over the (out 1, out 2) pair";
+    m.vm_op = 1;
+    v.push_back(m);
+    return v;
+  }();
+  return r;
+}
+}  // namespace
+
+int register_combine(const CustomCombine& c) {
+  std::lock_guard<std::mutex> lk(g_registry_mu);
+  auto& r = registry();
+  if (c.name.empty() || c.name.find_first_of(" :,\"") != std::string::npos)
+    fail("ParseError", "combine operator name '" + c.name + "' is empty or contains a separator");
+  static const std::set<std::string> builtin = {"+", "*", "mul", "min", "max", "-", "/"};
+  if (builtin.count(c.name)) fail("InvalidConfig", "'" + c.name + "' is a built-in operator of the reference");
+  if (c.arity < 1 || c.arity > 8) fail("OutOfRange", "combine operator arity must be in [1, 8]");
+  if (c.body.empty()) fail("ParseError", "combine operator '" + c.name + "' has no body");
+  for (size_t k = 0; k < r.size(); ++k)
+    if (r[k].name == c.name) {
+      if (r[k].vm_op) fail("InvalidConfig", "'" + c.name + "' is a built-in custom operator");
+      r[k] = c;
+      r[k].vm_op = 0;
+      return static_cast<int>(k);
+    }
+  r.push_back(c);
+  r.back().vm_op = 0;
+  return static_cast<int>(r.size() - 1);
+}
+
+int combine_index(const std::string& name) {
+  std::lock_guard<std::mutex> lk(g_registry_mu);
+  auto& r = registry();
+  for (size_t k = 0; k < r.size(); ++k)
+    if (r[k].name == name) return static_cast<int>(k);
+  return -1;
+}
+
+const CustomCombine& combine_at(int index) {
+  std::lock_guard<std::mutex> lk(g_registry_mu);
+  return registry().at(static_cast<size_t>(index));
+}
+
+std::vector<std::string> combine_names() {
+  std::lock_guard<std::mutex> lk(g_registry_mu);
+  std::vector<std::string> n;
+  for (auto& c : registry()) n.push_back(c.name);
+  return n;
 }
 
 int MdHom::n_in_access() const {
@@ -460,6 +538,14 @@ MdHom parse_md_hom(const std::string& text) {
           fail("IndexOutOfBounds", "out(" + std::to_string(b + 1) + "," + std::to_string(k + 1) + ") never assigned");
     std::stable_sort(h.assigns.begin(), h.assigns.end(),
                      [](const Assign& x, const Assign& y) { return x.buf != y.buf ? x.buf < y.buf : x.acc < y.acc; });
+    for (auto& c : h.comb)
+      if (c.op == Fold::Custom && c.kind != Combine::CC) {
+        const CustomCombine& op = combine_at(c.custom);
+        if (static_cast<int>(h.assigns.size()) != op.arity)
+          fail("MixedIncompatibleOperators", "combine operator '" + op.name + "' folds " + std::to_string(op.arity) +
+                                                 " output components jointly; the scalar function assigns " +
+                                                 std::to_string(h.assigns.size()));
+      }
     return h;
   });
 }
@@ -475,7 +561,7 @@ std::string md_hom_violation(const MdHom& e) {
       first = d;
       continue;
     }
-    if (e.comb[static_cast<size_t>(first)].op != c.op)
+    if (e.comb[static_cast<size_t>(first)].op != c.op || e.comb[static_cast<size_t>(first)].custom != c.custom)
       return "dimensions " + std::to_string(first + 1) + " and " + std::to_string(d + 1) +
              " fold with different operators";
   }

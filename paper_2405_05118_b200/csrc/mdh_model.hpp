@@ -58,12 +58,36 @@ struct Assign {
   Expr e;
 };
 
-enum class Fold { Add = 0, Sub = 1, Mul = 2, Div = 3, Min = 4, Max = 5 };  // mda.hpp:52
+enum class Fold { Add = 0, Sub = 1, Mul = 2, Div = 3, Min = 4, Max = 5, Custom = 6 };  // mda.hpp:52 (+ Custom)
 struct Combine {
   enum Kind { CC, PW, PS } kind = CC;
   Fold op = Fold::Add;
   bool assoc_comm = false;  // mda.cpp:75-83: + * min max are declared assoc+comm
+  int custom = -1;          // registry index when op == Fold::Custom
 };
+
+// ---- custom combine operators (API extension; the reference's BinOpKind is
+// closed, mda.hpp:52, and its JSON accepts only the six named operators,
+// json_io.cpp:58-64 / mda.cpp:75-83).  A registered operator folds the TUPLE
+// of all output components of the scalar function jointly -- e.g. max_prl
+// keeps the (weight, record) pair with the larger weight and, on ties, the
+// lower record: PRL's custom combine.  It is used as
+// pw:<name> or ps:<name> like a built-in operator.
+struct CustomCombine {
+  std::string name;
+  int arity = 0;                      // output components folded jointly
+  std::string body;                   // CUDA C statements over a0.. (accumulator, lvalues) and b0.. (next value)
+  std::vector<std::string> identity;  // per component (C literal text), documentation + seeding
+  bool assoc = false, comm = false;
+  std::string description;
+  int vm_op = 0;                      // > 0: also compiled into the generic device VM (built-ins)
+};
+constexpr int kCustomFoldBase = 100;  // MdHom::fold() of custom operator k = kCustomFoldBase + k
+// registers (or replaces a same-named, not built-in) operator; returns its index
+int register_combine(const CustomCombine& c);
+int combine_index(const std::string& name);  // -1 when not registered
+const CustomCombine& combine_at(int index);
+std::vector<std::string> combine_names();
 
 struct MdHom {
   std::string name;
@@ -76,7 +100,8 @@ struct MdHom {
 
   int D() const { return static_cast<int>(sizes.size()); }
   std::vector<int64_t> collapsed() const;  // pw dims -> 1 (highlevel.cpp:65-75)
-  int fold() const;                        // shared fold op of non-cc dims, -1 if none
+  int fold() const;                        // shared fold op of non-cc dims, -1 if none;
+                                           // kCustomFoldBase + k for custom operator k
   int n_in_access() const;
   int in_comp(int buf, int acc) const;     // flat (buffer, access) position, 1-based args
 };

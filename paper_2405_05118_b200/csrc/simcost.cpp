@@ -152,7 +152,8 @@ std::string lowered_text(const Config& c, const MdHom& e, const Asm& m) {
   auto comb = [&](int dim) {
     const Combine& cb = e.comb[static_cast<size_t>(dim - 1)];
     if (cb.kind == Combine::CC) return std::string("cc");
-    return std::string(cb.kind == Combine::PW ? "pw:" : "ps:") + opname(cb.op);
+    return std::string(cb.kind == Combine::PW ? "pw:" : "ps:") +
+           (cb.op == Fold::Custom ? combine_at(cb.custom).name : std::string(opname(cb.op)));
   };
   std::ostringstream o;
   o << "lowered computation=" << e.name << " model=" << m.name << "\n";

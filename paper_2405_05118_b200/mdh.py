@@ -36,7 +36,7 @@ EXPORTED = [
     "mdh_b200_default_options", "mdh_b200_plan_create", "mdh_b200_plan_destroy", "mdh_b200_buffer_count",
     "mdh_b200_buffer_info", "mdh_b200_run", "mdh_b200_run_host", "mdh_b200_time", "mdh_b200_describe",
     "mdh_b200_validate_config", "mdh_b200_tune", "mdh_b200_tune_ex", "mdh_b200_simcost", "mdh_b200_lowered",
-    "mdh_b200_launches_per_run",
+    "mdh_b200_launches_per_run", "mdh_b200_register_combine", "mdh_b200_combine_info",
     "mdh_b200_kernel_source", "mdh_b200_last_error", "mdh_b200_version",
 ]
 OBJ_TIME, OBJ_SIMCOST = 0, 1
@@ -281,6 +281,24 @@ def lowered(spec, asm="B200", config=None) -> str:
     buf = ctypes.create_string_buffer(need.value)
     _check(lib().mdh_b200_lowered(_text(spec), _text(asm), cfg, buf, need.value, ctypes.byref(need)))
     return buf.value.decode()
+
+
+def register_combine(name, arity, cuda_body, identity=(), assoc=True, comm=True, description=""):
+    """Registers a custom combine operator usable as "pw:<name>" / "ps:<name>"
+    (API extension; the reference's operator set is closed, mda.hpp:52).
+    `cuda_body` folds the component tuple: statements over a0.. (accumulator
+    lvalues) and b0.. (next value)."""
+    _check(lib().mdh_b200_register_combine(_text(name), int(arity), _text(cuda_body),
+                                           _text(",".join(identity)), int(bool(assoc)), int(bool(comm)),
+                                           _text(description)))
+
+
+def combine_info() -> list:
+    need = ctypes.c_int64()
+    _check(lib().mdh_b200_combine_info(None, 0, ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    _check(lib().mdh_b200_combine_info(buf, need.value, ctypes.byref(need)))
+    return json.loads(buf.value.decode())
 
 
 def version() -> str:
