@@ -72,9 +72,10 @@ typedef struct {
   int math;          /* enum mdh_b200_math, contraction family only */
   int device;        /* CUDA device ordinal the plan lives on */
   int family;        /* 0 = auto; 1 = force the generic md_hom kernel */
+  int split_dim;     /* DEV layer (mplan / rank plans): 1-based dimension the GPU layer splits, 0 = automatic */
 } mdh_b200_options;
 
-/* Fills the defaults: F32 / I64 storage, FFMA math, device 0, auto family. */
+/* Fills the defaults: F32 / I64 storage, FFMA math, device 0, auto family, automatic split. */
 void mdh_b200_default_options(mdh_b200_options* opt);
 
 /* Builds a plan: parses + validates the md_hom, checks the configuration
@@ -182,6 +183,58 @@ int mdh_b200_register_combine(const char* name, int arity, const char* cuda_body
                               int assoc, int comm, const char* description);
 /* JSON array describing every registered custom operator. */
 int mdh_b200_combine_info(char* buf, int64_t cap, int64_t* need);
+
+/* ---- the multi-GPU DEV layer (the reference declares the
+ * MultiGPU ASM, proj/src/asm_model.cpp:36-37, and GPU partials combining in
+ * host memory, but never executes them).
+ *
+ * The md_hom is split over the GPU layer: along the dimension a MultiB200
+ * configuration gives GPU-layer parts to, else the outermost ++ dimension that
+ * splits uniformly (every output depending on it), else the outermost
+ * point-wise one.  A ++ split needs no communication; a point-wise split
+ * combines the shards' partial outputs with the dimension's operator in device
+ * memory -- ncclAllReduce over NVLink (+ * min max, distinct devices) or the
+ * peer-memory combine kernel (any operator incl. max_prl; several shards may
+ * share one device).  Shard g reads the slab of each global input that starts
+ * at `start` along `slab_rank` (-1: the whole buffer) and, for a ++ split,
+ * writes the matching slab of each output; a point-wise split leaves the
+ * combined result in shard 0's outputs. */
+typedef struct mdh_b200_mplan mdh_b200_mplan;
+int mdh_b200_mplan_create(const char* computation_json, const char* asm_model, const char* config_json,
+                          const mdh_b200_options* opt, int n_gpus, const int* device_ids, mdh_b200_mplan** out);
+int mdh_b200_mplan_destroy(mdh_b200_mplan* mplan);
+/* JSON: split dimension/kind, combine path ("none" | "nccl" | "peer"), each shard's range and plan. */
+int mdh_b200_mplan_describe(const mdh_b200_mplan* mplan, char* buf, int64_t cap, int64_t* need);
+/* Shard g's local buffer (side 0 in, 1 out): its slab of the global buffer and its shape. */
+int mdh_b200_mplan_shard_buffer(const mdh_b200_mplan* mplan, int g, int side, int b, int* slab_rank, int64_t* start,
+                                int64_t* dims, int* rank, int* dtype, int64_t* bytes);
+int mdh_b200_mplan_shard_plan(const mdh_b200_mplan* mplan, int g, mdh_b200_plan** plan);
+/* d_in[g][b] / d_out[g][b]: shard-local device buffers; streams[g] (NULL = plan-owned). */
+int mdh_b200_mplan_run(mdh_b200_mplan* mplan, const void* const* const* d_in, void* const* const* d_out,
+                       void* const* streams);
+/* End to end on GLOBAL host buffers: slabs scattered to the devices, run, outputs gathered. */
+int mdh_b200_mplan_run_host(mdh_b200_mplan* mplan, const void* const* h_in, void* const* h_out);
+/* `sweeps` iterations of a halo-1 stencil (one input = output + 1-cell halo,
+ * split along dimension 1): after each sweep the output is written back into
+ * the input's interior and each shard's two ghost planes are exchanged with
+ * its neighbours (grouped ncclSend/Recv, or peer copies; MDHB_DEV_PEER=1
+ * forces the latter). */
+int mdh_b200_mplan_iterate(mdh_b200_mplan* mplan, void* const* const* d_v, void* const* const* d_w, int sweeps,
+                           void* const* streams);
+/* Median over `reps` of the MAX over shards of each shard's event-timed run. */
+int mdh_b200_mplan_time(mdh_b200_mplan* mplan, const void* const* const* d_in, void* const* const* d_out, int warmup,
+                        int reps, double* median_s);
+
+/* One process per GPU (torch.distributed / torchrun): rank `rank` of `world`
+ * builds the plan of its shard (same split rule as mdh_b200_mplan_create).
+ * With `nccl_id` (128 bytes from mdh_b200_nccl_unique_id on one rank,
+ * broadcast by the caller) a point-wise split all-reduces its outputs over
+ * NCCL inside mdh_b200_run; with NULL the caller combines.  describe() gains
+ * a "shard" member (range, per-buffer slab rank and start). */
+int mdh_b200_nccl_unique_id(unsigned char* id128);
+int mdh_b200_rank_plan_create(const char* computation_json, const char* asm_model, const char* config_json,
+                              const mdh_b200_options* opt, int world, int rank, const unsigned char* nccl_id,
+                              mdh_b200_plan** out);
 
 /* Number of kernel launches one mdh_b200_run issues. */
 int mdh_b200_launches_per_run(const mdh_b200_plan* plan, int* launches);

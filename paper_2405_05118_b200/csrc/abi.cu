@@ -149,6 +149,7 @@ void mdh_b200_default_options(mdh_b200_options* o) {
   o->math = MDH_B200_MATH_FFMA;
   o->device = 0;
   o->family = 0;
+  o->split_dim = 0;
 }
 
 const char* mdh_b200_last_error(void) { return g_err.c_str(); }
@@ -193,6 +194,32 @@ int mdh_b200_plan_create(const char* comp_json, const char* asm_model, const cha
     p->r = select_routine(prob, cfg.get(), &p->cfg, &p->note);
     MDHB_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
     *out = p.release();
+  });
+}
+
+int mdh_b200_rank_plan_create(const char* comp_json, const char* asm_model, const char* config_json,
+                              const mdh_b200_options* opt, int world, int rank, const unsigned char* nccl_id,
+                              mdh_b200_plan** out) {
+  return guard([&] {
+    if (!comp_json || !out) mdhb::fail("InvalidConfig", "null argument");
+    if (world < 1 || rank < 0 || rank >= world) mdhb::fail("OutOfRange", "rank must be in [0, world)");
+    mdhb::Asm m = mdhb::resolve_asm(asm_model ? asm_model : "MultiB200");
+    std::string cfg_out, desc;
+    int fold = -1;
+    bool pw = false;
+    std::string sj = mdhb::rank_shard(comp_json, m, config_json ? config_json : "", world, rank, opt ? opt->split_dim : 0,
+                                      &cfg_out, &desc, &fold, &pw);
+    const char* shard_asm = (config_json && *config_json) ? m.name.c_str() : (m.name == "MultiB200" ? "B200" : m.name.c_str());
+    mdh_b200_plan* p = nullptr;
+    if (mdh_b200_plan_create(sj.c_str(), shard_asm, cfg_out.empty() ? nullptr : cfg_out.c_str(), opt, &p))
+      throw mdhb::Error(g_err.substr(0, g_err.find(':')), g_err.substr(std::min(g_err.size(), g_err.find(':') + 2)));
+    try {
+      p->r = mdhb::wrap_rank(std::move(p->r), p->prob, desc, fold, pw, nccl_id, world, rank);
+    } catch (...) {
+      mdh_b200_plan_destroy(p);
+      throw;
+    }
+    *out = p;
   });
 }
 

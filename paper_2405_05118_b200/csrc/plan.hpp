@@ -127,6 +127,15 @@ double simcost(const SimTrace& t, const Asm& m);
 // LowLevelExpr::pretty() of lower(e, m, c) (lowering.cpp:56-118, 185-222)
 std::string lowered_text(const Config& c, const MdHom& e, const Asm& m);
 
+// The DEV layer for one process per GPU (dev_layer.cu): the rank's shard of
+// the md_hom (computation JSON, shard config, a JSON "shard" member for
+// describe()), and the routine wrapper that all-reduces a point-wise split's
+// outputs over NCCL inside run().
+std::string rank_shard(const std::string& comp_json, const Asm& m, const std::string& cfg_json, int world, int rank,
+                       int split_dim, std::string* cfg_out, std::string* desc, int* fold, bool* pw);
+std::unique_ptr<Routine> wrap_rank(std::unique_ptr<Routine> inner, const Problem& p, const std::string& desc, int fold,
+                                   bool pw, const unsigned char* nccl_id, int world, int rank);
+
 // The C ABI's thread-local last-error slot (abi.cu).
 void set_last_error(const std::string& what);
 

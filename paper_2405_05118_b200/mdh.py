@@ -37,6 +37,9 @@ EXPORTED = [
     "mdh_b200_buffer_info", "mdh_b200_run", "mdh_b200_run_host", "mdh_b200_time", "mdh_b200_describe",
     "mdh_b200_validate_config", "mdh_b200_tune", "mdh_b200_tune_ex", "mdh_b200_simcost", "mdh_b200_lowered",
     "mdh_b200_launches_per_run", "mdh_b200_register_combine", "mdh_b200_combine_info",
+    "mdh_b200_mplan_create", "mdh_b200_mplan_destroy", "mdh_b200_mplan_describe", "mdh_b200_mplan_shard_buffer",
+    "mdh_b200_mplan_shard_plan", "mdh_b200_mplan_run", "mdh_b200_mplan_run_host", "mdh_b200_mplan_iterate",
+    "mdh_b200_mplan_time", "mdh_b200_nccl_unique_id", "mdh_b200_rank_plan_create",
     "mdh_b200_kernel_source", "mdh_b200_last_error", "mdh_b200_version",
 ]
 OBJ_TIME, OBJ_SIMCOST = 0, 1
@@ -52,7 +55,7 @@ class MdhError(RuntimeError):
 
 class Options(ctypes.Structure):
     _fields_ = [("float_storage", ctypes.c_int), ("int_storage", ctypes.c_int), ("math", ctypes.c_int),
-                ("device", ctypes.c_int), ("family", ctypes.c_int)]
+                ("device", ctypes.c_int), ("family", ctypes.c_int), ("split_dim", ctypes.c_int)]
 
 
 _lib = None
@@ -88,10 +91,11 @@ def _text(spec) -> bytes:
     return spec.encode() if isinstance(spec, str) else spec
 
 
-def options(float_storage=F32, int_storage=I64, math=MATH_FFMA, device=0, generic=False) -> Options:
+def options(float_storage=F32, int_storage=I64, math=MATH_FFMA, device=0, generic=False, split_dim=0) -> Options:
     o = Options()
     lib().mdh_b200_default_options(ctypes.byref(o))
     o.float_storage, o.int_storage, o.math, o.device, o.family = float_storage, int_storage, math, device, int(generic)
+    o.split_dim = split_dim
     return o
 
 
@@ -103,13 +107,16 @@ class Plan:
     """An md_hom bound to an instantiated sm_100a kernel template."""
 
     def __init__(self, spec, asm: str = "B200", config=None, float_storage=F32, int_storage=I64,
-                 math=MATH_FFMA, device=0, generic=False):
+                 math=MATH_FFMA, device=0, generic=False, _handle=None):
         self.spec = spec if isinstance(spec, str) else json.dumps(spec)
         self._h = ctypes.c_void_p()
         self.opts = options(float_storage, int_storage, math, device, generic)
-        cfg = None if config is None else _text(config)
-        _check(lib().mdh_b200_plan_create(_text(self.spec), _text(asm), cfg, ctypes.byref(self.opts),
-                                          ctypes.byref(self._h)))
+        if _handle is not None:  # built by another constructor (rank plans)
+            self._h = _handle
+        else:
+            cfg = None if config is None else _text(config)
+            _check(lib().mdh_b200_plan_create(_text(self.spec), _text(asm), cfg, ctypes.byref(self.opts),
+                                              ctypes.byref(self._h)))
         self.device = device
         self.inputs = [self.buffer_info(0, b) for b in range(self._count(0))]
         self.outputs = [self.buffer_info(1, b) for b in range(self._count(1))]
@@ -203,6 +210,127 @@ class Plan:
             h_out = [np.empty(i["shape"], dtype=i["np"]) for i in self.outputs]
         _check(lib().mdh_b200_run_host(self._h, _ptr_array([a.ctypes.data for a in ins]),
                                        _ptr_array([a.ctypes.data for a in h_out]), None))
+        return h_out
+
+
+# ---------------------------------------------------------------- DEV layer
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId (128 bytes) -- made on one rank, broadcast by the caller."""
+    buf = (ctypes.c_ubyte * 128)()
+    _check(lib().mdh_b200_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def rank_plan(spec, world, rank, device=0, nccl_id: Optional[bytes] = None, asm="MultiB200", config=None,
+              split_dim=0, **kw) -> Plan:
+    """One process per GPU: rank `rank`'s shard of the md_hom split over the
+    GPU layer (mdh_b200_rank_plan_create).  With `nccl_id` a point-wise split
+    all-reduces its outputs over NCCL inside run(); without, the caller
+    combines (describe()["template"]["shard"] says how)."""
+    o = options(device=device, split_dim=split_dim, **kw)
+    h = ctypes.c_void_p()
+    idb = None if nccl_id is None else (ctypes.c_ubyte * 128)(*nccl_id)
+    text = spec if isinstance(spec, str) else json.dumps(spec)
+    _check(lib().mdh_b200_rank_plan_create(_text(text), _text(asm), None if config is None else _text(config),
+                                           ctypes.byref(o), int(world), int(rank), idb, ctypes.byref(h)))
+    p = Plan(text, device=device, _handle=h)
+    p.opts = o
+    return p
+
+
+class MultiPlan:
+    """mdh_b200_mplan_*: one process drives G shards of the md_hom (device_ids
+    may repeat -- shards then share a device and combine through the peer
+    kernel)."""
+
+    def __init__(self, spec, n_gpus, device_ids=None, asm="MultiB200", config=None, split_dim=0, **kw):
+        self.spec = spec if isinstance(spec, str) else json.dumps(spec)
+        self.G = int(n_gpus)
+        self.devices = list(device_ids) if device_ids is not None else list(range(self.G))
+        o = options(split_dim=split_dim, **kw)
+        self._h = ctypes.c_void_p()
+        devs = (ctypes.c_int * self.G)(*self.devices)
+        _check(lib().mdh_b200_mplan_create(_text(self.spec), _text(asm), None if config is None else _text(config),
+                                           ctypes.byref(o), self.G, devs, ctypes.byref(self._h)))
+        n_in, n_out = len(json.loads(self.spec)["inputs"]), len(json.loads(self.spec)["outputs"])
+        self.inputs = [[self.shard_buffer(g, 0, b) for b in range(n_in)] for g in range(self.G)]
+        self.outputs = [[self.shard_buffer(g, 1, b) for b in range(n_out)] for g in range(self.G)]
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.mdh_b200_mplan_destroy(h)
+            self._h = ctypes.c_void_p()
+
+    def describe(self) -> dict:
+        need = ctypes.c_int64()
+        _check(lib().mdh_b200_mplan_describe(self._h, None, 0, ctypes.byref(need)))
+        buf = ctypes.create_string_buffer(need.value)
+        _check(lib().mdh_b200_mplan_describe(self._h, buf, need.value, ctypes.byref(need)))
+        return json.loads(buf.value.decode())
+
+    def shard_buffer(self, g, side, b):
+        dims = (ctypes.c_int64 * 16)()
+        sr, st, rank, dt, nb = ctypes.c_int(), ctypes.c_int64(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int64()
+        _check(lib().mdh_b200_mplan_shard_buffer(self._h, g, side, b, ctypes.byref(sr), ctypes.byref(st), dims,
+                                                 ctypes.byref(rank), ctypes.byref(dt), ctypes.byref(nb)))
+        return {"slab_rank": sr.value, "start": st.value, "shape": tuple(dims[r] for r in range(rank.value)),
+                "dtype": dt.value, "bytes": nb.value, "np": _NP[dt.value]}
+
+    def empty(self, side):
+        import torch
+        tdt = {F32: torch.float32, F64: torch.float64, I32: torch.int32, I64: torch.int64}
+        infos = self.inputs if side == 0 else self.outputs
+        return [[torch.empty(i["shape"], dtype=tdt[i["dtype"]], device=f"cuda:{self.devices[g]}") for i in infos[g]]
+                for g in range(self.G)]
+
+    def slab(self, g, side, b, array):
+        """Shard g's slab of a GLOBAL buffer (numpy or torch)."""
+        i = (self.inputs if side == 0 else self.outputs)[g][b]
+        if i["slab_rank"] < 0:
+            return array
+        idx = [slice(None)] * array.ndim
+        r = i["slab_rank"]
+        idx[r] = slice(i["start"], i["start"] + i["shape"][r])
+        return array[tuple(idx)]
+
+    def _pp(self, bufs):
+        rows = [_ptr_array([t.data_ptr() for t in row]) for row in bufs]
+        arr = (ctypes.c_void_p * self.G)(*[ctypes.cast(r, ctypes.c_void_p) for r in rows])
+        return arr, rows
+
+    def run(self, d_in, d_out):
+        a, ka = self._pp(d_in)
+        b, kb = self._pp(d_out)
+        _check(lib().mdh_b200_mplan_run(self._h, a, b, None))
+
+    def iterate(self, d_v, d_w, sweeps):
+        a, ka = self._pp(d_v)
+        b, kb = self._pp(d_w)
+        _check(lib().mdh_b200_mplan_iterate(self._h, a, b, int(sweeps), None))
+
+    def time(self, d_in, d_out, warmup=2, reps=5):
+        a, ka = self._pp(d_in)
+        b, kb = self._pp(d_out)
+        med = ctypes.c_double()
+        _check(lib().mdh_b200_mplan_time(self._h, a, b, warmup, reps, ctypes.byref(med)))
+        return med.value
+
+    def run_host(self, h_in, h_out=None):
+        """GLOBAL host buffers in, GLOBAL host outputs out (slabs scattered / gathered)."""
+        spec = json.loads(self.spec)
+        ins = [np.ascontiguousarray(x, dtype=i["np"]) for x, i in zip(h_in, self.inputs[0])]
+        if h_out is None:
+            h_out = []
+            for b in range(len(spec["outputs"])):
+                i = self.outputs[0][b]
+                shp = list(i["shape"])
+                if i["slab_rank"] >= 0:
+                    shp[i["slab_rank"]] = max(self.outputs[g][b]["start"] + self.outputs[g][b]["shape"][i["slab_rank"]]
+                                              for g in range(self.G))
+                h_out.append(np.empty(shp, dtype=i["np"]))
+        _check(lib().mdh_b200_mplan_run_host(self._h, _ptr_array([a.ctypes.data for a in ins]),
+                                             _ptr_array([a.ctypes.data for a in h_out])))
         return h_out
 
 
