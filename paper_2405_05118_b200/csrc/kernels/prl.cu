@@ -69,6 +69,7 @@ struct PrlArgs {
   int lgS;                   // S = 2^lgS, C = S - 1 internally
   unsigned long long* pairs;  // [nq][2] (w, r), 16-byte aligned scratch
   void* out_r;                // record output (weight output is `best`)
+  int64_t roff;               // global index of local record 0 (a DEV-layer shard's offset)
   int r_is64;
   int64_t r_stride;
 };
@@ -396,7 +397,7 @@ __global__ void __launch_bounds__(NT) prl_main(PrlArgs a) {
 __global__ void prl_unpack(PrlArgs a) {
   const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (q >= a.nq) return;
-  const long long w = static_cast<long long>(a.pairs[2 * q]), r = static_cast<long long>(a.pairs[2 * q + 1]);
+  const long long w = static_cast<long long>(a.pairs[2 * q]), r = static_cast<long long>(a.pairs[2 * q + 1]) + a.roff;
   if (a.out_is64) a.best[q * a.out_stride] = w;
   else reinterpret_cast<int32_t*>(a.best)[q * a.out_stride] = static_cast<int32_t>(w);
   if (a.r_is64) static_cast<int64_t*>(a.out_r)[q * a.r_stride] = r;
@@ -498,20 +499,43 @@ class PrlRoutine final : public Routine {
 };
 
 // matches  <const> - idx(r)  and  <lit> * <sum>  / <sum> * <lit>
+// idx(r) or idx(r) + lit / lit + idx(r) (a DEV-layer shard rebases idx(r) to
+// the global record index): the dim and the constant offset
+bool idx_plus(const Expr& e, int* dim, int64_t* off) {
+  if (e.k == EK::Idx) {
+    *dim = e.dim - 1;
+    *off = 0;
+    return true;
+  }
+  if (e.k != EK::Add) return false;
+  for (int s = 0; s < 2; ++s) {
+    const Expr& a = e.args[static_cast<size_t>(s)];
+    const Expr& b = e.args[static_cast<size_t>(1 - s)];
+    if (a.k == EK::Idx && b.k == EK::Lit && !b.flit) {
+      *dim = a.dim - 1;
+      *off = b.iv;
+      return true;
+    }
+  }
+  return false;
+}
+
 bool split_key(const Expr& e, const Expr** sum, int64_t* S, int64_t* C, int* rdim) {
   if (e.k != EK::Add) return false;
   for (int s = 0; s < 2; ++s) {
     const Expr& m = e.args[static_cast<size_t>(s)];
     const Expr& c = e.args[static_cast<size_t>(1 - s)];
     if (m.k != EK::Mul || c.k != EK::Sub) continue;
-    if (c.args[0].k != EK::Lit || c.args[0].flit || c.args[1].k != EK::Idx) continue;
+    int dim = -1;
+    int64_t off = 0;
+    if (c.args[0].k != EK::Lit || c.args[0].flit || !idx_plus(c.args[1], &dim, &off)) continue;
     for (int t = 0; t < 2; ++t) {
       const Expr& lit = m.args[static_cast<size_t>(t)];
       if (lit.k == EK::Lit && !lit.flit) {
         *sum = &m.args[static_cast<size_t>(1 - t)];
         *S = lit.iv;
-        *C = c.args[0].iv;
-        *rdim = c.args[1].dim - 1;
+        *C = c.args[0].iv - off;  // C - (r + off) = (C - off) - r
+        *rdim = dim;
         return true;
       }
     }
@@ -526,7 +550,7 @@ std::unique_ptr<Routine> make_prl(const Problem& p, const Config* cfg, Config* c
   if (e.D() != 2 || e.in.size() != 3) return nullptr;
   int rdim = -1;
   const Expr* sum = nullptr;
-  int64_t S = 0, C = 0;
+  int64_t S = 0, C = 0, roff = 0;
   bool pair = false;
   if (e.out.size() == 1 && e.out[0].acc.size() == 1 && e.assigns.size() == 1) {
     // packed form: best = weight * S + (C - idx(r)) folded with pw:max
@@ -538,8 +562,8 @@ std::unique_ptr<Routine> make_prl(const Problem& p, const Config* cfg, Config* c
     rdim = e.comb[0].kind == Combine::PW ? 0 : 1;
     const Combine& c = e.comb[static_cast<size_t>(rdim)];
     if (c.kind != Combine::PW || c.op != Fold::Custom || combine_at(c.custom).name != "max_prl") return nullptr;
-    const Expr& id = e.assigns[1].e;
-    if (id.k != EK::Idx || id.dim != rdim + 1 || e.out[1].type != Ty::I64) return nullptr;
+    int idim = -1;
+    if (!idx_plus(e.assigns[1].e, &idim, &roff) || idim != rdim || e.out[1].type != Ty::I64) return nullptr;
     sum = &e.assigns[0].e;
     int lg = 7;
     while ((int64_t(1) << lg) < e.sizes[static_cast<size_t>(rdim)]) ++lg;
@@ -604,6 +628,7 @@ std::unique_ptr<Routine> make_prl(const Problem& p, const Config* cfg, Config* c
     while ((int64_t(1) << a.lgS) < S) ++a.lgS;
     a.r_is64 = p.out_store[1] == Store::I64;
     a.r_stride = 1;
+    a.roff = roff;
   }
   a.nq = e.sizes[static_cast<size_t>(qdim)];
   a.nr = e.sizes[static_cast<size_t>(rdim)];
