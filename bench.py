@@ -12,10 +12,13 @@ between steps.  Every other §8 routine is measured too (one line, key
 "routines"), each with its own roofline; those whose inputs fit in L2 are
 timed with an L2 flush between runs.
 
-Multi-GPU (torchrun, one rank per GPU, NCCL only for the barrier and the
-max-over-ranks timing): weak scaling -- rank r owns z-slab r of a
-(512*N) x 512 x 512 Jacobi3D, its input slab carrying the 1-plane halos
-(placed at distribution, no exchange in a single sweep).
+Multi-GPU (torchrun, one rank per GPU): STRONG scaling of the same global
+512^3 Jacobi3D -- rank r's plan is the DEV layer's shard r
+(mdh_b200_rank_plan_create: 512/N output planes, its input slab carrying the
+1-plane halos of the one global input, placed at distribution; a single sweep
+exchanges nothing).  Every rank fills its slab from the same global
+index-hashed data, so the shards' halos agree.  NCCL carries the barrier, the
+max-over-ranks timing and (for point-wise splits) the in-plan all-reduce.
 
 --impl reference times the reference's own CPU implementation of the path:
 the OpenMP C kernel its code generator emits (oracle/_ref, built from
@@ -125,20 +128,43 @@ def prl_weights(d_in):
     d_in[2].copy_(d_in[2].new_tensor([3, 5, 7, 9]))
 
 
-def make_plan(name, device, world=1, rank=0):
+def make_plan(name, device, world=1, rank=0, nccl_id=None):
     """Plan for routine `name` ("<spec>[:tf32]").  With world > 1 the rank's
-    shard of the weak-scaled global problem (dim 0 grown world-fold, split
-    into world ++-parts by the GPU layer, paper_2405_05118_b200/shard.py)."""
+    shard of the GLOBAL problem split over the GPU layer by the DEV layer
+    (strong scaling; mdh_b200_rank_plan_create)."""
     from paper_2405_05118_b200 import mdh
-    from paper_2405_05118_b200.shard import shard_spec
     base, _, math = name.partition(":")
     m = {"": mdh.MATH_FFMA, "tf32": mdh.MATH_TF32, "bf16": mdh.MATH_BF16}[math]
     j = spec(base)
     if world > 1:
-        j["sizes"][0] *= world
-        j, _, _, op = shard_spec(j, 0, world, rank)
-        assert op is None, "dim 0 of the BASELINE specs is a ++ dimension"
+        return mdh.rank_plan(j, world, rank, device=device, nccl_id=nccl_id, math=m, int_storage=mdh.I32), \
+            base, math or "ffma"
     return mdh.Plan(j, math=m, int_storage=mdh.I32, device=device), base, math or "ffma"
+
+
+def fill_global(plan, seed):
+    """Inputs of this rank's shard filled from ONE global array: value =
+    hash(global linear index), so every rank's halo planes hold the same
+    values as its neighbours' edge planes (the shard describes its slab)."""
+    import torch
+    d_in = plan.empty(0)
+    sh = plan.describe()["template"].get("shard")
+    for b, t in enumerate(d_in):
+        if not t.is_floating_point():
+            t.random_(0, 3)
+            continue
+        shape = list(t.shape)
+        gshape = list(shape)
+        start = 0
+        if sh and sh["in"][b][0] == 0:  # the DEV layer slabs along rank 0 here
+            start = sh["in"][b][1]
+        inner = int(np.prod(shape[1:])) if len(shape) > 1 else 1
+        idx = torch.arange(start * inner, (start + shape[0]) * inner, device=t.device, dtype=torch.int64)
+        x = (idx * 2654435761 + seed) % 4294967296
+        x = ((x ^ (x >> 13)) * 1597334677) % 4294967296
+        x = x ^ (x >> 16)
+        t.copy_((x.to(torch.float64) / 2147483648.0 - 1.0).view(gshape).to(t.dtype))
+    return d_in
 
 
 def roofline_of(desc, kernel_s, pk, clock_mhz, traffic):
@@ -420,9 +446,16 @@ def main():
     pk = peaks()
 
     # ---- headline: device-resident steps
-    plan, base, math = make_plan(args.routine, device, world, rank)
+    nccl_id = None
+    if world > 1:
+        import torch.distributed as dist
+        from paper_2405_05118_b200 import mdh
+        box = [mdh.nccl_unique_id() if rank == 0 and dist.get_backend() == "nccl" else None]
+        dist.broadcast_object_list(box, src=0)
+        nccl_id = box[0]
+    plan, base, math = make_plan(args.routine, device, world, rank, nccl_id)
     desc = plan.describe()
-    d_in = fill(plan.empty(0), 1234 + rank)
+    d_in = fill_global(plan, 1234)
     if base == "prl_max":
         prl_weights(d_in)
     d_out = plan.empty(1)
@@ -433,23 +466,26 @@ def main():
         tot, copies = time_device(plan, d_in, d_out, args.steps, args.warmup, rotate)
     tot = max_over_ranks(tot, world)
     ms = tot / args.steps * 1e3
-    value = desc["bytes"] * world / (tot / args.steps) / 1e9 if desc["bound"] == "hbm" else \
-        desc["flops"] * world / (tot / args.steps) / 1e9
+    gdesc = desc if world == 1 else make_plan(args.routine, device)[0].describe()  # the global problem's work
+    value = gdesc["bytes"] / (tot / args.steps) / 1e9 if desc["bound"] == "hbm" else \
+        gdesc["flops"] / (tot / args.steps) / 1e9
     unit = "GB/s" if desc["bound"] == "hbm" else "GFLOP/s"
     kernel_s = tot / args.steps
     clocks = clk.summary()
     roof = roofline_of(desc, kernel_s, pk, clocks["sm_mhz"], traffic_of(args.routine, desc["template"]["kernel"]))
 
     # ---- e2e through the C ABI with pinned host buffers
-    e2e = e2e_measure(plan, d_in, max(3, min(args.steps, 10)), world)
+    e2e = e2e_measure(plan, d_in, max(3, min(args.steps, 10)), world, gdesc)
 
     line = {"metric": METRIC, "value": round(value, 2), "unit": unit, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32" if base != "prl_max" else "i32",
-            "data": "synthetic (uniform(-1,1) fp32, seeded per rank)",
-            "config": {"workload": f"{base} {spec(base)['sizes']} per GPU ({math})", "family": desc["family"],
+            "data": "synthetic (one global array, uniform(-1,1) fp32 from a hash of the global index)",
+            "config": {"workload": f"{base} {spec(base)['sizes']} ({math}), global problem over all GPUs",
+                       "family": desc["family"],
                        "kernel": desc["template"]["kernel"],
-                       "parallelism": f"++-sharded z-slabs x{world} (weak)" if world > 1 else "single GPU",
+                       "parallelism": (f"DEV layer: ++ dim {desc['template']['shard']['split_dim']} split into "
+                                       f"{world} shards (strong), rank plans" if world > 1 else "single GPU"),
                        "l2": f"inputs rotated over {copies} copies (> 3x L2)" if rotate else
                        f"inputs ({in_bytes >> 20} MB) larger than L2",
                        "timing": "K runs replayed from one CUDA graph, CUDA events on the replay stream"},
@@ -457,7 +493,7 @@ def main():
             "gpu_launches": plan.launches * args.steps}
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_line(base)
-    if not args.no_routines:
+    if not args.no_routines and world == 1:
         line["routines"] = routines_table(device, pk, world, exclude=args.routine)
         line["gpu_launches"] += sum(r.get("launches", 0) for r in line["routines"])
     if rank == 0:
@@ -493,7 +529,7 @@ def max_over_ranks(x, world):
     return float(t.item())
 
 
-def e2e_measure(plan, d_in, reps, world):
+def e2e_measure(plan, d_in, reps, world, gdesc=None):
     """Host (pinned) inputs -> mdh_b200_run_host -> host outputs, wall clock."""
     import torch
     h_in = [t.cpu().pin_memory() for t in d_in]
@@ -508,10 +544,10 @@ def e2e_measure(plan, d_in, reps, world):
         plan.run_host(np_in, np_out)
     dt = (time.perf_counter() - t0) / reps
     dt = max_over_ranks(dt, world)
-    desc = plan.describe()
+    desc = gdesc or plan.describe()
     work = desc["bytes"] if desc["bound"] == "hbm" else desc["flops"]
     unit = "GB/s" if desc["bound"] == "hbm" else "GFLOP/s"
-    return {"value": round(work * world / dt / 1e9, 2), "unit": unit,
+    return {"value": round(work / dt / 1e9, 2), "unit": unit,
             "h2d_bytes_per_step": int(sum(a.nbytes for a in np_in)),
             "d2h_bytes_per_step": int(sum(a.nbytes for a in np_out)), "ms_per_step": round(dt * 1e3, 3)}
 

@@ -1,5 +1,6 @@
 """bench.py contract on one GPU: the single-GPU JSON line, and the N>1
-(torchrun) weak-scaling path exercised with 2 ranks sharing the GPU over gloo."""
+(torchrun) strong-scaling path (DEV-layer rank plans on one global problem)
+exercised with 2 ranks sharing the GPU over gloo."""
 import json
 import os
 import subprocess
@@ -28,7 +29,7 @@ def test_bench_single_gpu_line():
 
 
 @pytest.mark.gpu
-def test_bench_two_ranks_weak_scaling_path():
+def test_bench_two_ranks_strong_scaling_path():
     env = dict(os.environ, MDHB_BENCH_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
            "127.0.0.1", "--master-port", "29533", "bench.py", "--gpus", "2", "--steps", "5", "--warmup", "3",
@@ -36,4 +37,6 @@ def test_bench_two_ranks_weak_scaling_path():
     p = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=600, env=env)
     assert p.returncode == 0, p.stderr[-2000:]
     d = _last_json(p.stdout)
-    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and "x2" in d["config"]["parallelism"]
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and "2 shards" in d["config"]["parallelism"]
+    # whole-job value over the GLOBAL problem: the same algorithmic bytes as one GPU
+    assert d["config"]["workload"].startswith("jacobi3d_fp32 [512, 512, 512]")
