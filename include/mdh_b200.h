@@ -108,6 +108,13 @@ int mdh_b200_run_host(mdh_b200_plan* plan, const void* const* h_in, void* const*
 int mdh_b200_time(mdh_b200_plan* plan, const void* const* d_in, void* const* d_out, int warmup, int reps,
                   int flush_l2, double* median_s, double* kernel_s);
 
+/* compiled_time_objective exactly (proj/src/autotuner.cpp:64-129): synthetic
+ * inputs owned by the plan, element t = t % 7 + 1 as that function's
+ * generated main() fills them, then mdh_b200_time on them.  What the
+ * reference-side EvaluateFn binding calls. */
+int mdh_b200_time_synthetic(mdh_b200_plan* plan, int warmup, int reps, int flush_l2, double* median_s,
+                            double* kernel_s);
+
 /* JSON describing the plan: family, kernel template + its parameters, the
  * normalised Table-1 configuration, launches per run, algorithmic bytes and
  * flops per run. */

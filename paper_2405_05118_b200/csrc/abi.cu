@@ -19,6 +19,7 @@ struct mdh_b200_plan {
   void* flush_r = nullptr;
   float* flush_sink = nullptr;
   size_t flush_bytes = 0;
+  std::vector<void*> syn_in, syn_out;  // synthetic buffers of mdh_b200_time_synthetic
 };
 
 namespace {
@@ -94,6 +95,21 @@ __global__ void flush_read(const float4* __restrict__ p, size_t n, float* sink) 
     acc += v.x + v.y + v.z + v.w;
   }
   if (acc == 12345.678f) *sink = acc;  // keeps the loads alive
+}
+
+// compiled_time_objective's synthetic inputs (autotuner.cpp:72-119): element
+// t of every input holds t % 7 + 1
+__global__ void fill_t7(void* p, int store, int64_t n) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t v = t % 7 + 1;
+    switch (store) {
+      case 0: static_cast<float*>(p)[t] = static_cast<float>(v); break;
+      case 1: static_cast<double*>(p)[t] = static_cast<double>(v); break;
+      case 2: static_cast<int32_t*>(p)[t] = static_cast<int32_t>(v); break;
+      default: static_cast<int64_t*>(p)[t] = v; break;
+    }
+  }
 }
 
 void flush_l2(mdh_b200_plan* p, cudaStream_t s) {
@@ -233,6 +249,8 @@ int mdh_b200_plan_destroy(mdh_b200_plan* p) {
     if (p->flush_w) cudaFree(p->flush_w);
     if (p->flush_r) cudaFree(p->flush_r);
     if (p->flush_sink) cudaFree(p->flush_sink);
+    for (void* d : p->syn_in) cudaFree(d);
+    for (void* d : p->syn_out) cudaFree(d);
     if (p->stream) cudaStreamDestroy(p->stream);
     delete p;
   });
@@ -346,6 +364,34 @@ int mdh_b200_time(mdh_b200_plan* p, const void* const* d_in, void* const* d_out,
     // a family that did not mark runs a single kernel: the run is the kernel
     if (kernel_s) *kernel_s = tk.size() == t.size() ? tk[tk.size() / 2] : *median_s;
   });
+}
+
+int mdh_b200_time_synthetic(mdh_b200_plan* p, int warmup, int reps, int flush, double* median_s, double* kernel_s) {
+  int rc = guard([&] {
+    MDHB_CUDA(cudaSetDevice(p->prob.opt.device));
+    if (p->syn_in.empty()) {
+      auto alloc = [&](const std::vector<std::vector<int64_t>>& ext, const std::vector<mdhb::Store>& st,
+                       std::vector<void*>& dst, bool fill) {
+        for (size_t b = 0; b < ext.size(); ++b) {
+          int64_t n = 1;
+          for (int64_t x : ext[b]) n *= x;
+          void* d = nullptr;
+          MDHB_CUDA(cudaMalloc(&d, std::max<size_t>(16, static_cast<size_t>(n) * mdhb::store_bytes(st[b]))));
+          dst.push_back(d);
+          if (fill) {
+            fill_t7<<<4 * mdhb::sm_count(p->prob.opt.device), 256, 0, p->stream>>>(d, static_cast<int>(st[b]), n);
+            MDHB_CUDA(cudaGetLastError());
+          }
+        }
+      };
+      alloc(p->prob.in_ext, p->prob.in_store, p->syn_in, true);
+      alloc(p->prob.out_ext, p->prob.out_store, p->syn_out, false);
+      MDHB_CUDA(cudaStreamSynchronize(p->stream));
+    }
+  });
+  if (rc) return rc;
+  return mdh_b200_time(p, const_cast<const void* const*>(p->syn_in.data()), p->syn_out.data(), warmup, reps, flush,
+                       median_s, kernel_s);
 }
 
 int mdh_b200_describe(const mdh_b200_plan* p, char* buf, int64_t cap, int64_t* need) {

@@ -39,7 +39,7 @@ EXPORTED = [
     "mdh_b200_launches_per_run", "mdh_b200_register_combine", "mdh_b200_combine_info",
     "mdh_b200_mplan_create", "mdh_b200_mplan_destroy", "mdh_b200_mplan_describe", "mdh_b200_mplan_shard_buffer",
     "mdh_b200_mplan_shard_plan", "mdh_b200_mplan_run", "mdh_b200_mplan_run_host", "mdh_b200_mplan_iterate",
-    "mdh_b200_mplan_time", "mdh_b200_nccl_unique_id", "mdh_b200_rank_plan_create",
+    "mdh_b200_mplan_time", "mdh_b200_nccl_unique_id", "mdh_b200_rank_plan_create", "mdh_b200_time_synthetic",
     "mdh_b200_kernel_source", "mdh_b200_last_error", "mdh_b200_version",
 ]
 OBJ_TIME, OBJ_SIMCOST = 0, 1
