@@ -153,6 +153,15 @@ int mdh_b200_tune_ex(const char* computation_json, const char* asm_model, const 
                      uint64_t seed, int objective, int simcost_seeded, const char* start_config, char* best_config,
                      int64_t best_cap, char* history_csv, int64_t hist_cap, double* best_objective);
 
+/* The tuner's enumerated search space for a kernel family ("stencil",
+ * "contraction", "prl", ...; host only): a JSON array of the canonical Table-1
+ * configurations of every template instance the family offers for this
+ * md_hom (the random phase samples it; hill climbing moves with the
+ * reference's four neighbourhood moves and projects each neighbour onto the
+ * instance it instantiates). */
+int mdh_b200_tune_space(const char* computation_json, const char* asm_model, const mdh_b200_options* opt,
+                        const char* family, char* buf, int64_t cap, int64_t* need);
+
 /* SimCost of a configuration (NULL config = the baseline configuration,
  * tuning.cpp:476-503): mdh::simcost_objective(expr, model, cfg)
  * (autotuner.cpp:58-62 = cost(simulate_trace(lower(...)), default weights

@@ -1580,10 +1580,20 @@ std::unique_ptr<Routine> make_contraction(const Problem& p, const Config* cfg, C
 namespace mdhb {
 // Tuning space of the FFMA contraction template: the (BM, BN) tile menu,
 // each instance reported through its canonical Table-1 configuration.
+bool contraction_project(const Problem& p, const Config& c, Config* canon) {
+  Groups g;
+  if (!analyze_contraction(p, g)) return false;
+  return tc_project(p, g, c, canon);
+}
+
 std::vector<Config> contraction_space(const Problem& p) {
   std::vector<Config> out;
   Groups g;
   if (!analyze_contraction(p, g)) return out;
+  if (p.opt.math != Math::FFMA) {
+    out = tc_space(p, g);
+    if (!out.empty()) return out;
+  }
   const int menu[4][2] = {{128, 128}, {128, 64}, {64, 128}, {64, 64}};
   for (auto& t : menu) {
     GemmRoutine r(p, g);

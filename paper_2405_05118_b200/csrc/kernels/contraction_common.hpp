@@ -64,6 +64,14 @@ inline std::vector<int64_t> factor_box(const MdHom& e, const std::vector<int>& d
 std::unique_ptr<Routine> make_tc_contraction(const Problem& p, const Groups& g, const Config* cfg, Config* cfg_out,
                                              std::string* why);
 
+// The tensor-core GEMM template's instances for a MatMul-shaped md_hom, as
+// canonical Table-1 configurations (empty for other shapes).
+std::vector<Config> tc_space(const Problem& p, const Groups& g);
+// The tensor-core instance a configuration instantiates, as its canonical
+// configuration (false: not MatMul-shaped / FFMA; throws Unsupported when
+// the configuration is outside the template).
+bool tc_project(const Problem& p, const Groups& g, const Config& c, Config* canon);
+
 // Tensor-core instance for NHWC convolutions (MCC): one input patch per
 // 32-channel chunk, all R*S taps issued from it through shifted descriptors
 // (kernels/tc_conv.cu).  nullptr when the md_hom is not such a convolution.

@@ -845,12 +845,20 @@ bool linear_terms(const Expr& e, std::vector<std::pair<double, int>>& terms) {
   return false;
 }
 
+// Schedules of the star-7 template (which kernel streams the planes):
+//   LEAN     TMA-bulk producer warp + smem plane ring, centre columns in registers (star7_lean)
+//   LEAN_TS  LEAN with the output staged in smem and written by TMA stores
+//   WS       producer warp + ring, every neighbour read from smem (star7_ws)
+//   PERS     WS on persistent CTAs striding over (tile, i-chunk) items (star7_pers)
+//   PLAIN    no producer: the compute warps load their rows themselves (star7_kernel)
+enum StencilSched { S_LEAN = 0, S_LEAN_TS = 1, S_WS = 2, S_PERS = 3, S_PLAIN = 4 };
+
 class StencilRoutine final : public Routine {
  public:
-  StencilRoutine(const Problem& p, StencilArgs a, int tj, bool bulk)
-      : p_(p), a_(a), tj_(tj), bulk_(bulk), ws_(bulk && !std::getenv("MDHB_STENCIL_V2")),
-        pers_(ws_ && std::getenv("MDHB_STENCIL_PERS") != nullptr) {
-    if (!ws_ || pers_) lean_ = 0;
+  StencilRoutine(const Problem& p, StencilArgs a, int tj, bool bulk, int sched)
+      : p_(p), a_(a), tj_(tj), bulk_(bulk && sched != S_PLAIN), ws_(bulk_ && sched != S_PLAIN),
+        pers_(ws_ && sched == S_PERS), ts_(sched == S_LEAN_TS) {
+    if (sched == S_WS || sched == S_PERS || !ws_) lean_ = 0;
   }
   const char* family() const override { return "stencil"; }
   std::string describe() const override {
@@ -992,13 +1000,76 @@ class StencilRoutine final : public Routine {
   int minb_ = std::getenv("MDHB_STENCIL_MINB") ? std::atoi(std::getenv("MDHB_STENCIL_MINB")) : 2;
   // lean-register variant (default): 5 ring slots, 4 CTAs per SM (NS*10+MINB; 0 = star7_ws)
   int lean_ = std::getenv("MDHB_STENCIL_LEAN") ? std::atoi(std::getenv("MDHB_STENCIL_LEAN")) : 54;
-  // TMA-store variant: full tiles, 16-byte aligned output rows (MDHB_STENCIL_TS=1)
-  bool ts_ok() const {
-    return std::getenv("MDHB_STENCIL_TS") && a_.n2 % TK == 0 && a_.n1 % 16 == 0 && (a_.n2 * 4) % 16 == 0;
-  }
+  bool ts_ = false;
+  // TMA-store variant: full tiles, 16-byte aligned output rows
+  bool ts_ok() const { return ts_ && a_.n2 % TK == 0 && a_.n1 % 16 == 0 && (a_.n2 * 4) % 16 == 0; }
 };
 
 }  // namespace
+
+// ---- Table-1 instantiation (B200 ASM {DM, SM, RM | SMX, WRP, CC}; MDH
+// layer order SMX -> DM -> WRP -> CC -> SM -> RM):
+//   SMX(i, j, k) = grid (i-chunks, j/16, k/128); DM(i) = ti planes streamed
+//   per CTA; DM(j) > 1 = CTAs walk several tiles (persistent); WRP(j) 8 x
+//   RM(j) 2 = 16 rows, CC(k) 32 x RM(k) 4 = 128 columns per CTA.
+//   Regions of v: at the SM layer SM = staged by the TMA producer, DM = read
+//   by the compute warps (PLAIN); at the RM layer RM = centre columns held in
+//   registers (LEAN), SM = re-read from the ring (WS).  Region of w at the SM
+//   layer: SM = staged for TMA stores (LEAN_TS), else stored from registers.
+struct StencilKnobs {
+  int ti = 32;
+  int sched = S_LEAN;
+};
+
+int region_at(const Config& c, const std::vector<std::vector<int>>& mem, size_t buf, int asm_layer, bool re, int D) {
+  const auto& ass = re ? c.ass_re : c.ass_de;
+  for (size_t r = 0; r < ass.size(); ++r)
+    if (ass[r].layer == asm_layer && static_cast<int>(r) % D == 0) return mem[buf][r];
+  return 0;
+}
+
+StencilKnobs stencil_knobs(const Problem& p, const Config& c) {
+  const MdHom& e = p.e;
+  const int smx = p.m.id("SMX"), dm = p.m.id("DM"), sm = p.m.id("SM"), rm = p.m.id("RM");
+  if (smx < 0 || dm < 0 || sm < 0 || rm < 0) fail("Unsupported", "stencil template needs SMX, DM, SM and RM layers");
+  auto P = parts_per_asm_layer(c, e, p.m);
+  for (const char* other : {"GPU", "HM"})
+    if (p.m.id(other) > 0)
+      for (int64_t x : P[static_cast<size_t>(p.m.id(other) - 1)])
+        if (x != 1) fail("Unsupported", std::string("stencil template: ") + other + " parts belong to the DEV layer");
+  auto at = [&](int layer, int d) { return P[static_cast<size_t>(layer - 1)][static_cast<size_t>(d)]; };
+  StencilKnobs k;
+  if (e.sizes[1] % (at(smx, 1) * at(dm, 1)) || e.sizes[1] / (at(smx, 1) * at(dm, 1)) != 16 ||
+      e.sizes[2] % (at(smx, 2) * at(dm, 2)) || e.sizes[2] / (at(smx, 2) * at(dm, 2)) != TK)
+    fail("Unsupported", "stencil template tiles (j, k) by (16, 128) per CTA");
+  if (e.sizes[0] % at(smx, 0)) fail("Unsupported", "stencil template needs uniform i-chunks");
+  k.ti = static_cast<int>(e.sizes[0] / at(smx, 0));
+  const bool persistent = at(dm, 1) > 1 || at(dm, 2) > 1;
+  const int D = e.D();
+  const int v_sm = region_at(c, c.mem_de, 0, sm, false, D), v_rm = region_at(c, c.mem_de, 0, rm, false, D);
+  const int w_sm = region_at(c, c.mem_re, 0, sm, true, D);
+  if (persistent) k.sched = S_PERS;
+  else if (v_sm == dm) k.sched = S_PLAIN;
+  else if (v_rm == rm) k.sched = w_sm == sm ? S_LEAN_TS : S_LEAN;
+  else k.sched = S_WS;
+  return k;
+}
+
+Config stencil_canonical(const Problem& p, const StencilKnobs& k) {
+  const MdHom& e = p.e;
+  const int64_t gj = e.sizes[1] / 16, gk = e.sizes[2] / TK;
+  const bool pers = k.sched == S_PERS && gj % 2 == 0;
+  std::vector<LayerParts> lp = {{"SMX", {e.sizes[0] / k.ti, pers ? gj / 2 : gj, gk}}, {"DM", {k.ti, pers ? 2 : 1, 1}},
+                                {"WRP", {1, 8, 1}}, {"CC", {1, 1, 32}}, {"SM", {1, 1, 1}}, {"RM", {1, 2, 4}}};
+  Config c = make_config(p, lp, {{e.in[0].name, k.sched == S_PLAIN ? "DM" : "SM"}}, "RM");
+  const int D = e.D(), sm = p.m.id("SM"), rm = p.m.id("RM"), dm = p.m.id("DM");
+  for (size_t r = 0; r < c.ass_de.size(); ++r) {
+    if (c.ass_de[r].layer == rm) c.mem_de[0][r] = (k.sched == S_LEAN || k.sched == S_LEAN_TS) ? rm : (k.sched == S_PLAIN ? dm : sm);
+    if (c.ass_re[r].layer == sm && k.sched == S_LEAN_TS) c.mem_re[0][r] = sm;
+  }
+  (void)D;
+  return c;
+}
 
 std::unique_ptr<Routine> make_stencil(const Problem& p, const Config* cfg, Config* cfg_out) {
   const MdHom& e = p.e;
@@ -1061,57 +1132,54 @@ std::unique_ptr<Routine> make_stencil(const Problem& p, const Config* cfg, Confi
 
   const int TJ = 16;
   int ti = 32;
+  int sched = S_LEAN;
+  if (std::getenv("MDHB_STENCIL_V1") || std::getenv("MDHB_STENCIL_V2")) sched = S_PLAIN;  // dev aids
+  if (std::getenv("MDHB_STENCIL_PERS")) sched = S_PERS;
+  if (std::getenv("MDHB_STENCIL_TS")) sched = S_LEAN_TS;
   if (cfg) {
-    // Instantiate from the configuration: i-planes per CTA = the parts on
-    // DM x WRP x CC x SM x RM of dim i (everything below the grid).
-    int smx = p.m.id("SMX"), gpu = p.m.id("GPU");
-    if (smx < 0) fail("Unsupported", "stencil template needs an SMX layer");
-    auto P = parts_per_asm_layer(*cfg, e, p.m);
-    int64_t grid_i = P[static_cast<size_t>(smx - 1)][0] * (gpu > 0 ? P[static_cast<size_t>(gpu - 1)][0] : 1);
-    int64_t grid_j = P[static_cast<size_t>(smx - 1)][1], grid_k = P[static_cast<size_t>(smx - 1)][2];
-    if (grid_j * TJ != a.n1 || grid_k * TK != a.n2)
-      fail("Unsupported", "stencil template tiles (j, k) by (16, 128) per CTA");
-    ti = static_cast<int>(a.n0 / grid_i);
-    if (ti < 1 || a.n0 % grid_i != 0) fail("Unsupported", "stencil template needs uniform i-chunks");
+    StencilKnobs k = stencil_knobs(p, *cfg);
+    ti = k.ti;
+    sched = k.sched;
   }
   if (const char* f = std::getenv("MDHB_STENCIL_TI")) ti = std::max(1, std::atoi(f));
   a.ti = ti;
-  if (cfg_out) {
-    int64_t gi = (a.n0 + ti - 1) / ti;
-    // i: SMX chunks x DM planes; j: SMX x WRP(8) x RM(2); k: SMX x CC(32) x RM(4)
-    if (a.n1 % TJ || a.n2 % TK || a.n0 % ti) {
-      *cfg_out = baseline_config(e, p.m);
-    } else {
-      std::vector<LayerParts> lp = {{"SMX", {gi, a.n1 / TJ, a.n2 / TK}}, {"DM", {ti, 1, 1}}, {"WRP", {1, 8, 1}},
-                                    {"CC", {1, 1, 32}},                   {"SM", {1, 1, 1}},  {"RM", {1, 2, 4}}};
-      if (p.m.id("WRP") < 0 || p.m.id("SMX") < 0)
-        *cfg_out = baseline_config(e, p.m);
-      else
-        *cfg_out = make_config(p, lp, {{in.name, "SM"}}, "RM");
-    }
-  }
   // TMA bulk row copies need every copied span inside the allocation: the
   // buffer size must be 16-byte rounded (rows overrun at most to the next
   // 16-byte boundary) and the k tiles must not reach past the row end.
   const int64_t vbytes = p.in_ext[0][0] * a.e1 * a.e2 * 4;
-  const bool bulk = vbytes % 16 == 0 && a.n2 % TK == 0 && !std::getenv("MDHB_STENCIL_V1");
-  return std::make_unique<StencilRoutine>(p, a, TJ, bulk);
+  const bool bulk = vbytes % 16 == 0 && a.n2 % TK == 0;
+  if (cfg && sched != S_PLAIN && !bulk) fail("Unsupported", "stencil producer schedules need 16-byte rows and full k tiles");
+  if (cfg && sched == S_LEAN_TS && (a.n1 % 16 || (a.n2 * 4) % 16)) fail("Unsupported", "TMA-store epilogue needs full tiles");
+  if (cfg_out) {
+    if (a.n1 % TJ || a.n2 % TK || a.n0 % ti || p.m.id("WRP") < 0 || p.m.id("SMX") < 0)
+      *cfg_out = baseline_config(e, p.m);
+    else
+      *cfg_out = stencil_canonical(p, {ti, sched});
+  }
+  return std::make_unique<StencilRoutine>(p, a, TJ, bulk, sched);
 }
 
 }  // namespace mdhb
 
 namespace mdhb {
-// Tuning space of the stencil template: i-planes per CTA (the DM parts of i).
+bool stencil_project(const Problem& p, const Config& c, Config* canon) {
+  *canon = stencil_canonical(p, stencil_knobs(p, c));
+  return true;
+}
+
+// Tuning space of the stencil template: i-planes per CTA (every divisor of
+// the i extent) x the five schedules, as canonical configurations.
 std::vector<Config> stencil_space(const Problem& p) {
   std::vector<Config> out;
   const MdHom& e = p.e;
-  if (p.m.id("SMX") < 0 || p.m.id("WRP") < 0) return out;
-  for (int64_t ti : {4, 8, 16, 32, 64, 128}) {
-    if (e.sizes[0] % ti || e.sizes[1] % 16 || e.sizes[2] % 128) continue;
-    std::vector<LayerParts> lp = {{"SMX", {e.sizes[0] / ti, e.sizes[1] / 16, e.sizes[2] / 128}}, {"DM", {ti, 1, 1}},
-                                  {"WRP", {1, 8, 1}}, {"CC", {1, 1, 32}}, {"SM", {1, 1, 1}}, {"RM", {1, 2, 4}}};
-    out.push_back(make_config(p, lp, {{e.in[0].name, "SM"}}, "RM"));
-  }
+  if (p.m.id("SMX") < 0 || p.m.id("WRP") < 0 || e.D() != 3) return out;
+  if (e.sizes[1] % 16 || e.sizes[2] % 128) return out;
+  for (int sched = S_LEAN; sched <= S_PLAIN; ++sched)
+    for (int64_t ti = 1; ti <= e.sizes[0]; ti *= 2) {
+      if (e.sizes[0] % ti) continue;
+      if (sched == S_PERS && (e.sizes[1] / 16) % 2) continue;
+      out.push_back(stencil_canonical(p, {static_cast<int>(ti), sched}));
+    }
   return out;
 }
 }  // namespace mdhb

@@ -54,6 +54,11 @@ struct TcArgs {
   int nkd;
   int kext[MAXKD], kstep[MAXKD];
   int kca[MAXKD][MAXR], kcb[MAXKD][MAXR];
+  // Table-1 instantiation (plan-time knobs): M tiles per raster group (the
+  // SMX parts of the M dim, 0 = 8), and the K-split's starting coordinates
+  // (SMX parts of the K dim: split s starts at ka0 / kb0)
+  int group_m;
+  int ka0[MAXR], kb0[MAXR];
 };
 
 template <int BN, int STAGES, bool B_MN>
@@ -72,7 +77,7 @@ __global__ void __launch_bounds__(192, 1)
 
   const int warp = tc::warp_uniform(), lane = threadIdx.x & 31;
   // grouped raster over (tilesM x tilesN) for L2 reuse
-  constexpr int GROUP_M = 8;
+  const int GROUP_M = g.group_m > 0 ? g.group_m : 8;
   const int x = blockIdx.x;
   const int per_group = GROUP_M * g.tilesN;
   const int first_m = (x / per_group) * GROUP_M;
@@ -103,8 +108,8 @@ __global__ void __launch_bounds__(192, 1)
     for (int r = 0; r < MAXR; ++r) {
       am0[r] = g.a_mc[tm * MAXR + r];
       bn0[r] = g.b_nc[tn * MAXR + r];
-      ka[r] = 0;
-      kb[r] = 0;
+      ka[r] = g.ka0[r];
+      kb[r] = g.kb0[r];
     }
 #pragma unroll
     for (int q = 0; q < MAXKD; ++q) dig[q] = 0;
@@ -381,7 +386,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps(RB, BN), 1)
   float* stage_base = reinterpret_cast<float*>(smem + EPI_OFF(STAGES, BN, b_slots));
   const int warp = tc::warp_uniform(), lane = threadIdx.x & 31;
   const int ntiles = g.tilesM * g.tilesN;
-  constexpr int GROUP_M = 8;
+  const int GROUP_M = g.group_m > 0 ? g.group_m : 8;
   auto tile_mn = [&](int x, int& tm, int& tn) {
     const int per_group = GROUP_M * g.tilesN;
     const int first_m = (x / per_group) * GROUP_M;
@@ -431,7 +436,12 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps(RB, BN), 1)
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer
     if (RB) {  // all of B for the (single) N tile, once
-      int dig[MAXKD] = {0, 0, 0, 0, 0, 0}, ka[MAXR] = {0, 0, 0, 0, 0}, kb[MAXR] = {0, 0, 0, 0, 0};
+      int dig[MAXKD] = {0, 0, 0, 0, 0, 0}, ka[MAXR], kb[MAXR];
+#pragma unroll
+      for (int r = 0; r < MAXR; ++r) {
+        ka[r] = g.ka0[r];
+        kb[r] = g.kb0[r];
+      }
       tc::mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(g.nk) * B_BYTES);
       for (int kt = 0; kt < g.nk; ++kt) {
         int c[MAXR];
@@ -450,8 +460,8 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps(RB, BN), 1)
       for (int r = 0; r < MAXR; ++r) {
         am0[r] = g.a_mc[tm * MAXR + r];
         bn0[r] = g.b_nc[tn * MAXR + r];
-        ka[r] = 0;
-        kb[r] = 0;
+        ka[r] = g.ka0[r];
+        kb[r] = g.kb0[r];
       }
 #pragma unroll
       for (int q = 0; q < MAXKD; ++q) dig[q] = 0;
@@ -624,7 +634,7 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
   const int pair = static_cast<int>(blockIdx.x) >> 1, npairs = static_cast<int>(gridDim.x) >> 1;
   const int tilesM2 = g.tilesM / 2;  // 256-row tiles
   const int ntiles = tilesM2 * g.tilesN;
-  constexpr int GROUP_M = 8;
+  const int GROUP_M = g.group_m > 0 ? g.group_m : 8;
   auto tile_mn = [&](int x, int& tm, int& tn) {
     const int per_group = GROUP_M * g.tilesN;
     const int first_m = (x / per_group) * GROUP_M;
@@ -669,8 +679,8 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
       for (int r = 0; r < MAXR; ++r) {
         am0[r] = g.a_mc[ta * MAXR + r];
         bn0[r] = g.b_nc[tn * MAXR + r] + (r == b_row_rank ? static_cast<int>(rank) * (BN / 2) : 0);
-        ka[r] = 0;
-        kb[r] = 0;
+        ka[r] = g.ka0[r];
+        kb[r] = g.kb0[r];
       }
 #pragma unroll
       for (int q = 0; q < MAXKD; ++q) dig[q] = 0;
@@ -926,10 +936,33 @@ std::vector<int32_t> coords(const View& v, const std::vector<int64_t>& origin, b
   return c;
 }
 
+// Template parameters a Table-1 configuration sets (tc_knobs below):
+// N tile, kernel form, M-tiles per raster group, K split, B layout pass.
+struct TcKnobs {
+  bool set = false;   // read from a configuration (else the planner's menu)
+  int bn = 0;         // N tile = RM parts of the N dim
+  int form = -1;      // 0 one CTA per tile, 1 persistent CTAs (DM parts of M > 1), 2 CTA pair (256-row tiles)
+  int group = 0;      // M tiles per raster group = SMX parts of M (persistent forms), 0 = 8
+  int split = 1;      // K split = SMX parts of K (SMXs combine in DM: ordered reduction)
+  int transpose = -1; // B rewritten K-major (layout_de of B = [2, 1]) 1, read as stored 0
+};
+
+// split-K combine: C += ws[0] + ws[1] + ... in split order (the k order of
+// the unsplit fold)
+__global__ void splitk_reduce(float* __restrict__ C, const float* __restrict__ ws, int parts, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float acc = C[i];
+    for (int s = 0; s < parts; ++s) acc += ws[static_cast<int64_t>(s) * n + i];
+    C[i] = acc;
+  }
+}
+
 class TcRoutine final : public Routine {
  public:
-  TcRoutine(const Problem& p, const Groups& g) : p_(p), g_(g) {}
+  TcRoutine(const Problem& p, const Groups& g, const TcKnobs& k = {}) : p_(p), g_(g), kn_(k) {}
   ~TcRoutine() override {
+    if (ws_) cudaFree(ws_);
     if (blob_) cudaFree(blob_);
     if (bt_) cudaFree(bt_);
     if (pa_) cudaFree(pa_);
@@ -937,7 +970,9 @@ class TcRoutine final : public Routine {
   }
   const char* family() const override { return "contraction"; }
   const char* bound() const override { return "tensor"; }
-  int launches() const override { return packed_ ? 3 : (transposeB_ ? 2 : 1); }
+  int launches() const override {
+    return (packed_ ? 3 : (transposeB_ ? 2 : 1)) + (kn_.split > 1 ? kn_.split : 0);
+  }
   double flops() const override { return 2.0 * static_cast<double>(M_) * static_cast<double>(N_) * static_cast<double>(K_); }
   double bytes() const override { return static_cast<double>(p_.in_bytes + p_.out_bytes); }
   std::string describe() const override {
@@ -954,6 +989,8 @@ class TcRoutine final : public Routine {
        << "\"";
     if (packed_) os << ", \"K_padded\": " << Kp_;
     if (two_sm_) os << ", \"cta_pair\": \"tc_gemm_2sm<" << BN_ << "," << st2_ << ">: tcgen05.mma.cta_group::2 M256xN" << BN_ << (bf16_ ? "xK16 (bf16)" : "xK8") << "\"";
+    os << ", \"raster_group_m\": " << (kn_.group > 0 ? kn_.group : 8) << ", \"k_split\": " << kn_.split
+       << ", \"from_config\": " << (kn_.set ? "true" : "false");
     os << "}";
     return os.str();
   }
@@ -972,7 +1009,7 @@ class TcRoutine final : public Routine {
       *why = w + "; packed: " + *why;
       return false;
     }
-    if (vb_.mn && g_.Nd.size() == 1 && g_.Kd.size() == 1 && !std::getenv("MDHB_TC_NO_TRANSPOSE")) {
+    if (vb_.mn && g_.Nd.size() == 1 && g_.Kd.size() == 1 && !std::getenv("MDHB_TC_NO_TRANSPOSE") && kn_.transpose != 0) {
       // rewrite B K-major into scratch: Bt[n][k]
       const int dn = g_.Nd[0], dk = g_.Kd[0];
       const int64_t Nn = e.sizes[static_cast<size_t>(dn)], Kk = e.sizes[static_cast<size_t>(dk)];
@@ -1121,7 +1158,27 @@ class TcRoutine final : public Routine {
     pstages_ = rb_ ? rb_st : pers_stages(BN);
     psmem_ = rb_ ? rb_bytes : static_cast<size_t>(pstages_) * (BM + BN) * BKE * 4 + 1024 + 256 + epi_bytes(false, BN);
     pers_ = !std::getenv("MDHB_TC_NONPERSISTENT");
+    return finish_knobs(why);
+  }
+
+  // The configuration's knobs on top of the instance: kernel form, raster
+  // group, K split (workspace for the partials)
+  bool finish_knobs(std::string* why) {
+    if (kn_.set) {
+      pers_ = kn_.form >= 1;
+      if (kn_.transpose == 1 && vb_.mn && !transposeB_) return *why = "K-major B copy unavailable", false;
+    }
     decide_2sm();
+    if (kn_.set && (kn_.form == 2) != two_sm_) return *why = "CTA-pair instance unavailable for this tile", false;
+    if (!pers_ && BN_ == 192) return *why = "no one-CTA-per-tile instance with BN 192", false;
+    args_.group_m = kn_.group;
+    if (kn_.split > 1) {
+      if (args_.kext[0] % kn_.split) return *why = "K split does not divide the outer K digit", false;
+      int64_t n = 1;
+      for (int64_t x : p_.out_ext[0]) n *= x;
+      ws_n_ = n;
+      MDHB_CUDA(cudaMalloc(&ws_, static_cast<size_t>(n) * static_cast<size_t>(kn_.split - 1) * sizeof(float)));
+    }
     return true;
   }
 
@@ -1257,8 +1314,7 @@ class TcRoutine final : public Routine {
     pstages_ = pers_stages(BN);
     psmem_ = static_cast<size_t>(pstages_) * (BM + BN) * BKE * 4 + 1024 + 256 + epi_bytes(false, BN);
     pers_ = !std::getenv("MDHB_TC_NONPERSISTENT");
-    decide_2sm();
-    return true;
+    return finish_knobs(why);
   }
 
   // CTA-pair instance: K-major B whose tile rows live in one TMA rank (the
@@ -1266,6 +1322,7 @@ class TcRoutine final : public Routine {
   void decide_2sm() {
     two_sm_ = false;
     if (std::getenv("MDHB_TC_1SM") || !pers_ || rb_ || vb_.mn || (BN_ != 256 && BN_ != 128) || tilesM_ % 2) return;
+    if (kn_.set && kn_.form != 2) return;
     int row_rank = -1;
     for (int t = 1; t < vb_.rank; ++t) {
       if (vb_.box[t] == static_cast<cuuint32_t>(BN_)) {
@@ -1284,6 +1341,17 @@ class TcRoutine final : public Routine {
     two_sm_ = smem2_ <= 227 * 1024;
   }
   bool packed() const { return packed_; }
+  // the knobs of the planner's default instance (for its canonical config)
+  bool knobs_default(TcKnobs* k) const {
+    k->set = true;
+    k->form = two_sm_ ? 2 : pers_ ? 1 : 0;
+    k->bn = BN_;
+    k->group = k->form == 0 ? (two_sm_ ? tilesM_ / 2 : tilesM_) : 8;
+    if (k->form != 0 && (two_sm_ ? tilesM_ / 2 : tilesM_) % 8) return false;
+    k->split = 1;
+    k->transpose = bf16_ ? -1 : (transposeB_ ? 1 : 0);
+    return true;
+  }
   int64_t c_run() const { return c_run_; }
   static int64_t run_of(const std::vector<int64_t>& cn) {
     int64_t n = 1;
@@ -1365,9 +1433,30 @@ class TcRoutine final : public Routine {
       if (two_sm_) encode(vb2_, B, &mb2_);
       last_b_ = B;
     }
-    MarkScope mark(this, s);  // the GEMM kernel below is the dominant one
-    TcArgs a = args_;
-    a.C = static_cast<float*>(d_out[0]);
+    MarkScope mark(this, s);  // the GEMM kernel(s) below are the dominant ones
+    float* C = static_cast<float*>(d_out[0]);
+    const int S = kn_.split;
+    for (int sp = 0; sp < S; ++sp) {
+      TcArgs a = args_;
+      a.C = sp == 0 ? C : static_cast<float*>(ws_) + static_cast<int64_t>(sp - 1) * ws_n_;
+      if (S > 1) {  // split sp: the outer K digit's range [sp, sp + 1) * kext / S
+        const int part = args_.kext[0] / S;
+        a.kext[0] = part;
+        a.nk = args_.nk / S;
+        for (int r = 0; r < MAXR; ++r) {
+          a.ka0[r] = args_.kca[0][r] * args_.kstep[0] * part * sp;
+          a.kb0[r] = args_.kcb[0][r] * args_.kstep[0] * part * sp;
+        }
+      }
+      launch_gemm(a, s);
+    }
+    if (S > 1) {
+      splitk_reduce<<<4 * sm_count(p_.opt.device), 256, 0, s>>>(C, static_cast<const float*>(ws_), S - 1, ws_n_);
+      MDHB_CUDA(cudaGetLastError());
+    }
+  }
+
+  void launch_gemm(TcArgs& a, cudaStream_t s) {
     if (two_sm_) {
       const int sms = sm_count(p_.opt.device);
       const int pairs = std::min(sms / 2, (tilesM_ / 2) * tilesN_);
@@ -1437,6 +1526,9 @@ class TcRoutine final : public Routine {
 
   const Problem& p_;
   Groups g_;
+  TcKnobs kn_;
+  void* ws_ = nullptr;
+  int64_t ws_n_ = 0;
   View va_, vb_;
   int64_t M_ = 0, N_ = 0, K_ = 0;
   int BN_ = 0, stages_ = 0, nk_ = 0, tilesM_ = 0, tilesN_ = 0;
@@ -1472,6 +1564,137 @@ class TcRoutine final : public Routine {
 
 }  // namespace
 
+// ---- Table-1 instantiation of the tensor-core GEMM (MatMul-shaped md_homs:
+// one M, one N, one K dim).  ASM layers, MDH layer order DM -> SMX -> WRP ->
+// CC -> SM -> RM (the persistent schedule: a CTA's sequential tile loop is
+// the DM layer around the concurrent SMX layer):
+//   SMX(m) x DM(m) = M tiles; SMX(m) = M tiles per raster group; DM(m) > 1
+//     = persistent CTAs walking groups, DM(m) = 1 = one CTA per tile
+//   WRP(m) x CC(m) = rows per tile: 128 (4 epilogue warps x 32 TMEM lanes), 256 = CTA pair
+//   SMX(n) = N tiles, RM(n) = BN (TMEM columns each epilogue thread drains)
+//   SM(k) = the 128-byte k-tile (32 TF32 / 64 BF16), DM(k) = k-tiles per split,
+//   SMX(k) = K split, partials combined in DM ("SMXs combine in DM")
+//   layout_de of B = [2, 1]: B rewritten K-major by a layout pass
+bool gemm_shaped(const Groups& g) { return g.Md.size() == 1 && g.Nd.size() == 1 && g.Kd.size() == 1; }
+int k_tile(const Problem& p) { return p.opt.math == Math::BF16 ? 2 * BKE : BKE; }
+bool b_mn_major(const Groups& g) { return std::llabs(g.lb.cj[static_cast<size_t>(g.Nd[0])]) == 1; }
+
+TcKnobs tc_knobs(const Problem& p, const Groups& g, const Config& c) {
+  const MdHom& e = p.e;
+  const Asm& m = p.m;
+  const int smx = m.id("SMX"), dm = m.id("DM"), wrp = m.id("WRP"), cc = m.id("CC"), sm = m.id("SM"), rm = m.id("RM");
+  if (smx < 0 || dm < 0 || wrp < 0 || cc < 0 || sm < 0 || rm < 0) fail("Unsupported", "tensor-core template needs the B200 (CUDA+WRP) layers");
+  auto P = parts_per_asm_layer(c, e, m);
+  for (const char* other : {"GPU", "HM"})
+    if (m.id(other) > 0)
+      for (int64_t x : P[static_cast<size_t>(m.id(other) - 1)])
+        if (x != 1) fail("Unsupported", std::string("tensor-core template: ") + other + " parts belong to the DEV layer");
+  const int dm_ = g.Md[0], dn = g.Nd[0], dk = g.Kd[0];
+  auto at = [&](int layer, int d) { return P[static_cast<size_t>(layer - 1)][static_cast<size_t>(d)]; };
+  auto below = [&](int d) { return at(wrp, d) * at(cc, d) * at(sm, d) * at(rm, d); };
+  TcKnobs k;
+  k.set = true;
+  const int64_t tm = below(dm_);
+  if (tm != BM && tm != 2 * BM) fail("Unsupported", "tensor-core tile rows (WRP x CC x SM x RM of M) must be 128 or 256");
+  k.bn = static_cast<int>(below(dn));
+  if (k.bn != 64 && k.bn != 128 && k.bn != 192 && k.bn != 256) fail("Unsupported", "tensor-core N tile must be 64, 128, 192 or 256");
+  if (below(dk) != k_tile(p)) fail("Unsupported", "tensor-core k-tile (SM x ... of K) must be one 128-byte row");
+  if (at(dm, dn) != 1) fail("Unsupported", "tensor-core template rasters groups along M only (DM parts of N must be 1)");
+  k.split = static_cast<int>(at(smx, dk));
+  const int64_t rows = e.sizes[static_cast<size_t>(dm_)] / tm;
+  if (tm == 2 * BM) {
+    k.form = 2;
+    k.group = static_cast<int>(at(smx, dm_));
+  } else if (at(dm, dm_) > 1) {
+    k.form = 1;
+    k.group = static_cast<int>(at(smx, dm_));
+  } else {
+    k.form = 0;
+    k.group = static_cast<int>(rows);
+  }
+  k.transpose = 0;
+  const auto& lay = c.layout_de[static_cast<size_t>(g.b_buf)];
+  for (auto& l : lay)
+    if (l.size() == 2 && l[0] == 2 && l[1] == 1) k.transpose = 1;
+  if (p.opt.math == Math::BF16) k.transpose = -1;  // bf16 operands are always packed K-major
+  else if (!b_mn_major(g) && k.transpose == 1) fail("Unsupported", "B is stored K-major already");
+  return k;
+}
+
+Config tc_canonical(const Problem& p, const Groups& g, const TcKnobs& k) {
+  const MdHom& e = p.e;
+  const int D = e.D(), dm_ = g.Md[0], dn = g.Nd[0], dk = g.Kd[0];
+  const int64_t tm = k.form == 2 ? 2 * BM : BM, ek = k_tile(p);
+  const int64_t rows = e.sizes[static_cast<size_t>(dm_)] / tm, cols = e.sizes[static_cast<size_t>(dn)] / k.bn;
+  const int64_t grp = k.form == 0 ? rows : k.group;
+  std::vector<int64_t> DMv(static_cast<size_t>(D), 1), SMXv(DMv), WRPv(DMv), CCv(DMv), SMv(DMv), RMv(DMv);
+  DMv[static_cast<size_t>(dm_)] = rows / grp;
+  SMXv[static_cast<size_t>(dm_)] = grp;
+  SMXv[static_cast<size_t>(dn)] = cols;
+  SMXv[static_cast<size_t>(dk)] = k.split;
+  DMv[static_cast<size_t>(dk)] = e.sizes[static_cast<size_t>(dk)] / ek / k.split;
+  WRPv[static_cast<size_t>(dm_)] = tm / 32;
+  CCv[static_cast<size_t>(dm_)] = 32;
+  SMv[static_cast<size_t>(dk)] = ek;
+  RMv[static_cast<size_t>(dn)] = k.bn;
+  Config c = make_config(p, {{"DM", DMv}, {"SMX", SMXv}, {"WRP", WRPv}, {"CC", CCv}, {"SM", SMv}, {"RM", RMv}},
+                         {{e.in[static_cast<size_t>(g.a_buf)].name, "SM"}, {e.in[static_cast<size_t>(g.b_buf)].name, "SM"}}, "RM");
+  if (k.transpose == 1)
+    for (auto& l : c.layout_de[static_cast<size_t>(g.b_buf)]) l = {2, 1};
+  return c;
+}
+
+// Every instance the tensor-core GEMM template offers for this problem, as
+// canonical configurations (the tuner's search space).
+std::vector<Config> tc_space(const Problem& p, const Groups& g) {
+  std::vector<Config> out;
+  if (!gemm_shaped(g) || p.m.id("WRP") < 0 || p.m.id("SMX") < 0) return out;
+  const MdHom& e = p.e;
+  const int64_t M = e.sizes[static_cast<size_t>(g.Md[0])], N = e.sizes[static_cast<size_t>(g.Nd[0])],
+                K = e.sizes[static_cast<size_t>(g.Kd[0])], ek = k_tile(p);
+  if (K % ek) return out;
+  const bool bf16 = p.opt.math == Math::BF16, mn = b_mn_major(g);
+  for (int form = 0; form < 3; ++form)
+    for (int bn : {256, 192, 128, 64}) {
+      if (N % bn) continue;
+      if ((form == 0 && bn == 192) || (form == 2 && bn != 256 && bn != 128)) continue;
+      const int64_t tm = form == 2 ? 2 * BM : BM;
+      if (M % tm) continue;
+      const int64_t rows = M / tm;
+      for (int tr : {0, 1}) {
+        if (bf16 && tr) continue;
+        if (!bf16 && !mn && tr) continue;
+        if (!bf16 && mn && !tr && (form == 2 || bn == 192 || bn == 64 && form == 1)) continue;  // no MN-major instance
+        for (int split : {1, 2, 4}) {
+          if ((K / ek) % split) continue;
+          std::vector<int64_t> groups;
+          if (form == 0) groups = {rows};
+          else
+            for (int64_t gp = 1; gp < rows && gp <= 64; gp *= 2)
+              if (rows % gp == 0) groups.push_back(gp);
+          for (int64_t gp : groups) {
+            TcKnobs k;
+            k.set = true;
+            k.form = form;
+            k.bn = bn;
+            k.group = static_cast<int>(gp);
+            k.split = split;
+            k.transpose = bf16 ? -1 : (mn ? tr : 0);
+            Config c = tc_canonical(p, g, k);
+            if (config_violation(c, e, p.m, true).empty()) out.push_back(c);
+          }
+        }
+      }
+    }
+  return out;
+}
+
+bool tc_project(const Problem& p, const Groups& g, const Config& c, Config* canon) {
+  if (!gemm_shaped(g) || p.opt.math == Math::FFMA) return false;
+  *canon = tc_canonical(p, g, tc_knobs(p, g, c));
+  return true;
+}
+
 std::unique_ptr<Routine> make_tc_contraction(const Problem& p, const Groups& g, const Config* cfg, Config* cfg_out,
                                              std::string* why) {
   // N-tile menu; among the instances that set up, prefer a direct TMA view
@@ -1484,12 +1707,15 @@ std::unique_ptr<Routine> make_tc_contraction(const Problem& p, const Groups& g, 
       return conv;
     }
   }
+  TcKnobs kn;
+  if (cfg && gemm_shaped(g)) kn = tc_knobs(p, g, *cfg);  // Unsupported when outside the template
   std::vector<int> menu = {256, 192, 128, 64};
   if (const char* f = std::getenv("MDHB_TC_BN")) menu = {std::atoi(f)};
+  if (kn.set) menu = {kn.bn};
   std::unique_ptr<TcRoutine> best;
   int64_t best_score = -1;
   for (int bn : menu) {
-    auto r = std::make_unique<TcRoutine>(p, g);
+    auto r = std::make_unique<TcRoutine>(p, g, kn);
     std::string w;
     if (!r->setup(bn, &w)) {
       *why = w;
@@ -1498,7 +1724,13 @@ std::unique_ptr<Routine> make_tc_contraction(const Problem& p, const Groups& g, 
     const int64_t score = (r->packed() ? 0 : 1000000) + r->c_run() * 1000 + bn;
     if (score > best_score) best_score = score, best = std::move(r);
   }
-  if (best && cfg_out) *cfg_out = cfg ? *cfg : baseline_config(p.e, p.m);
+  if (kn.set && !best) fail("Unsupported", "tensor-core template cannot instantiate this configuration: " + *why);
+  if (best && cfg_out) {
+    if (gemm_shaped(g) && p.m.id("WRP") > 0 && p.m.id("SMX") > 0 && (kn.set || best->knobs_default(&kn)))
+      *cfg_out = tc_canonical(p, g, kn);
+    else
+      *cfg_out = cfg ? *cfg : baseline_config(p.e, p.m);
+  }
   return best;
 }
 

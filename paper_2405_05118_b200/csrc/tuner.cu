@@ -7,7 +7,9 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <map>
 #include <random>
+#include <set>
 #include <sstream>
 
 #include "../../include/mdh_b200.h"
@@ -43,33 +45,85 @@ __global__ void fill_small_int(void* p, int64_t n, int is64, uint32_t seed) {
   }
 }
 
-// two configurations are neighbours when one prime factor moved between two
-// layers of one dimension (default_neighborhood, autotuner.cpp:131-212)
-bool neighbours(const Config& a, const Config& b) {
-  if (a.parts.size() != b.parts.size()) return false;
-  int diffs = 0;
-  for (size_t d = 0; d < a.parts[0].size(); ++d) {
-    std::vector<size_t> ls;
-    for (size_t l = 0; l < a.parts.size(); ++l)
-      if (a.parts[l][d] != b.parts[l][d]) ls.push_back(l);
-    if (ls.empty()) continue;
-    if (ls.size() != 2) return false;
-    ++diffs;
-    int64_t x = a.parts[ls[0]][d], y = b.parts[ls[0]][d];
-    int64_t r = x > y ? x / y : y / x;
-    if ((x > y ? x % y : y % x) != 0 || r < 2) return false;
-    for (int64_t q = 2; q * q <= r; ++q)
-      if (r % q == 0) return false;  // must be a prime factor
-  }
-  return diffs == 1;
+std::vector<int64_t> distinct_primes(int64_t n) {
+  std::vector<int64_t> out;
+  for (int64_t q = 2; q * q <= n; ++q)
+    if (n % q == 0) {
+      out.push_back(q);
+      while (n % q == 0) n /= q;
+    }
+  if (n > 1) out.push_back(n);
+  return out;
 }
 
 }  // namespace
+
+// The reference's neighbourhood (default_neighborhood, autotuner.cpp:131-212):
+// one prime factor moved between adjacent layers (both directions, per
+// dimension), adjacent transpositions of each phase order, image swaps of
+// each assignment, single region changes in the de/re memory maps and the
+// scalar-phase regions; candidates failing validation are dropped.
+std::vector<Config> reference_neighbours(const Config& c, const MdHom& e, const Asm& m) {
+  std::vector<Config> out;
+  auto admit = [&](Config&& cand) {
+    if (config_violation(cand, e, m, true).empty()) out.push_back(std::move(cand));
+  };
+  const int L = static_cast<int>(c.parts.size()), D = e.D();
+  for (int l = 0; l + 1 < L; ++l)
+    for (int d = 0; d < D; ++d) {
+      for (int64_t q : distinct_primes(c.parts[static_cast<size_t>(l)][static_cast<size_t>(d)])) {
+        Config x = c;
+        x.parts[static_cast<size_t>(l)][static_cast<size_t>(d)] /= q;
+        x.parts[static_cast<size_t>(l + 1)][static_cast<size_t>(d)] *= q;
+        admit(std::move(x));
+      }
+      for (int64_t q : distinct_primes(c.parts[static_cast<size_t>(l + 1)][static_cast<size_t>(d)])) {
+        Config x = c;
+        x.parts[static_cast<size_t>(l + 1)][static_cast<size_t>(d)] /= q;
+        x.parts[static_cast<size_t>(l)][static_cast<size_t>(d)] *= q;
+        admit(std::move(x));
+      }
+    }
+  for (auto field : {&Config::ord_de, &Config::ord_scalar, &Config::ord_re})
+    for (size_t k = 0; k + 1 < (c.*field).size(); ++k) {
+      Config x = c;
+      std::swap((x.*field)[k], (x.*field)[k + 1]);
+      admit(std::move(x));
+    }
+  for (auto field : {&Config::ass_de, &Config::ass_scalar, &Config::ass_re})
+    for (size_t a = 0; a < (c.*field).size(); ++a)
+      for (size_t b = a + 1; b < (c.*field).size(); ++b) {
+        Config x = c;
+        std::swap((x.*field)[a], (x.*field)[b]);
+        admit(std::move(x));
+      }
+  const int regions = m.M();
+  for (auto field : {&Config::mem_de, &Config::mem_re})
+    for (size_t b = 0; b < (c.*field).size(); ++b)
+      for (size_t r = 0; r < (c.*field)[b].size(); ++r)
+        for (int reg = 1; reg <= regions; ++reg) {
+          if (reg == (c.*field)[b][r]) continue;
+          Config x = c;
+          (x.*field)[b][r] = reg;
+          admit(std::move(x));
+        }
+  for (auto field : {&Config::mem_scalar_in, &Config::mem_scalar_out})
+    for (size_t b = 0; b < (c.*field).size(); ++b)
+      for (int reg = 1; reg <= regions; ++reg) {
+        if (reg == (c.*field)[b]) continue;
+        Config x = c;
+        (x.*field)[b] = reg;
+        admit(std::move(x));
+      }
+  return out;
+}
 
 // per-family candidate spaces live next to each template
 std::vector<Config> stencil_space(const Problem& p);
 std::vector<Config> contraction_space(const Problem& p);
 std::vector<Config> prl_space(const Problem& p);
+bool stencil_project(const Problem& p, const Config& c, Config* canon);
+bool contraction_project(const Problem& p, const Config& c, Config* canon);
 
 std::vector<Config> family_space(const Problem& p, const std::string& family) {
   if (family == "stencil") return stencil_space(p);
@@ -78,7 +132,57 @@ std::vector<Config> family_space(const Problem& p, const std::string& family) {
   return {baseline_config(p.e, p.m)};
 }
 
+// The template instance a configuration instantiates, as its canonical
+// configuration (false: outside the template -- for families without a
+// parameter reader, membership in the enumerated space decides).
+bool family_project(const Problem& p, const std::string& family, const Config& c, Config* canon) {
+  try {
+    if (family == "stencil") return stencil_project(p, c, canon);
+    if (family == "contraction" && contraction_project(p, c, canon)) return true;
+  } catch (const Error& e) {
+    if (e.code != "Unsupported") throw;
+    return false;
+  }
+  return false;
+}
+
 }  // namespace mdhb
+
+// The tuner's enumerated candidates for `family` (host only): JSON array of
+// canonical Table-1 configurations.
+extern "C" int mdh_b200_tune_space(const char* comp_json, const char* asm_model, const mdh_b200_options* o,
+                                   const char* family, char* buf, int64_t cap, int64_t* need) {
+  using namespace mdhb;
+  try {
+    Problem prob;
+    prob.e = parse_md_hom(comp_json);
+    prob.m = resolve_asm(asm_model ? asm_model : "B200");
+    prob.in_ext = infer_extents(prob.e.in, prob.e.sizes);
+    prob.out_ext = infer_extents(prob.e.out, prob.e.collapsed());
+    if (o) {
+      prob.opt.fstore = static_cast<Store>(o->float_storage);
+      prob.opt.istore = static_cast<Store>(o->int_storage);
+      prob.opt.math = static_cast<Math>(o->math);
+      prob.opt.device = o->device;
+    }
+    for (auto& b : prob.e.in) prob.in_store.push_back(prob.store_of(b.type));
+    for (auto& b : prob.e.out) prob.out_store.push_back(prob.store_of(b.type));
+    std::string out = "[";
+    auto sp = family_space(prob, family ? family : "");
+    for (size_t i = 0; i < sp.size(); ++i) out += (i ? ", " : "") + config_json(sp[i], prob.e, prob.m);
+    out += "]";
+    if (need) *need = static_cast<int64_t>(out.size()) + 1;
+    if (buf && cap > 0) {
+      size_t k = std::min<size_t>(out.size(), static_cast<size_t>(cap - 1));
+      std::memcpy(buf, out.data(), k);
+      buf[k] = '\0';
+    }
+    return 0;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return 1;
+  }
+}
 
 extern "C" int mdh_b200_tune(const char* comp_json, const char* asm_model, const mdh_b200_options* o, int budget,
                              uint64_t seed, char* best_config, int64_t best_cap, char* history_csv, int64_t hist_cap,
@@ -193,17 +297,33 @@ extern "C" int mdh_b200_tune_ex(const char* comp_json, const char* asm_model, co
       bool valid;
     };
     std::vector<Ev> hist;
-    std::vector<double> memo(space.size(), -1.0);
+    std::map<std::string, int> index;  // canonical text -> candidate index
+    for (size_t i = 0; i < texts.size(); ++i) index.emplace(texts[i], static_cast<int>(i));
+    auto intern = [&](const Config& c) {
+      std::string t = config_json(c, prob.e, prob.m);
+      auto it = index.find(t);
+      if (it != index.end()) return it->second;
+      space.push_back(c);
+      texts.push_back(t);
+      sim.push_back(std::numeric_limits<double>::infinity());
+      index.emplace(t, static_cast<int>(space.size()) - 1);
+      return static_cast<int>(space.size()) - 1;
+    };
+    std::vector<double> memo;
     double best = std::numeric_limits<double>::infinity();
     int best_i = -1;
     auto evaluate = [&](int i) {
+      if (memo.size() < space.size()) memo.resize(space.size(), -1.0);
       double obj = std::numeric_limits<double>::infinity();
       bool valid = true;
       if (memo[static_cast<size_t>(i)] >= 0) {
         obj = memo[static_cast<size_t>(i)];
         valid = std::isfinite(obj);
       } else if (objective == MDH_B200_OBJ_SIMCOST) {
-        obj = sim[static_cast<size_t>(i)];
+        try {
+          obj = simcost(simulate(space[static_cast<size_t>(i)], prob.e, prob.m), prob.m);
+        } catch (const Error&) {
+        }
         valid = std::isfinite(obj);
         memo[static_cast<size_t>(i)] = obj;
       } else {
@@ -220,21 +340,55 @@ extern "C" int mdh_b200_tune_ex(const char* comp_json, const char* asm_model, co
       }
       uint64_t h = fnv1a(texts[static_cast<size_t>(i)]);
       hist.push_back({static_cast<int>(hist.size()), h, obj, valid && std::isfinite(obj)});
-      if (valid && (obj < best || (obj == best && best_i >= 0 && h < fnv1a(texts[static_cast<size_t>(best_i)])))) {
+      if (valid && std::isfinite(obj) &&
+          (obj < best || (obj == best && best_i >= 0 && h < fnv1a(texts[static_cast<size_t>(best_i)])))) {
         best = obj;
         best_i = i;
       }
       return obj;
     };
-    const int n = static_cast<int>(space.size());
+    // the reference's moves from the incumbent, each projected onto the
+    // template instance it instantiates (its canonical configuration);
+    // moves that leave the instance unchanged or leave the template drop out
+    auto neighbourhood = [&](int i) {
+      std::vector<int> nb;
+      std::set<int> seen;
+      for (const Config& cand : reference_neighbours(space[static_cast<size_t>(i)], prob.e, prob.m)) {
+        Config canon;
+        int j = -1;
+        if (family_project(prob, family, cand, &canon)) {
+          j = intern(canon);
+        } else {
+          auto it = index.find(config_json(cand, prob.e, prob.m));
+          if (it != index.end()) j = it->second;
+        }
+        if (j >= 0 && j != i && seen.insert(j).second) nb.push_back(j);
+      }
+      return nb;
+    };
     const int np = static_cast<int>(pool.size());
+    const int n_enum = static_cast<int>(space.size());
     int n_random = std::min(budget, std::max(1, budget * 3 / 10));
     int k0 = 0;
     if (start_i >= 0) {
       evaluate(start_i);
       k0 = 1;
     }
-    for (int k = k0; k < n_random; ++k) evaluate(pool[static_cast<size_t>(rng() % static_cast<uint64_t>(np))]);
+    // random draws take unvisited candidates first (a seeded permutation of the
+    // pool, then of the whole enumerated space): a memo hit would spend budget
+    // without information
+    std::vector<int> perm_pool(pool), perm_all(static_cast<size_t>(n_enum));
+    for (int i = 0; i < n_enum; ++i) perm_all[static_cast<size_t>(i)] = i;
+    std::shuffle(perm_pool.begin(), perm_pool.end(), rng);
+    std::shuffle(perm_all.begin(), perm_all.end(), rng);
+    size_t next_pool = 0, next_all = 0;
+    auto visited = [&](int i) { return static_cast<size_t>(i) < memo.size() && memo[static_cast<size_t>(i)] >= 0; };
+    auto draw = [&](std::vector<int>& perm, size_t& next, int n) {
+      while (next < perm.size() && visited(perm[next])) ++next;
+      if (next < perm.size()) return perm[next++];
+      return perm[static_cast<size_t>(rng() % static_cast<uint64_t>(n))];
+    };
+    for (int k = k0; k < n_random; ++k) evaluate(draw(perm_pool, next_pool, np));
     // first-improving hill climb from the best; once a climb from the current
     // best has converged ("settled", autotuner.cpp:290-300) the budget goes to
     // random candidates until the best changes
@@ -243,9 +397,7 @@ extern "C" int mdh_b200_tune_ex(const char* comp_json, const char* asm_model, co
       if (best_i >= 0 && settled_i != best_i) {
         bool converged = false, out_of_budget = false;
         while (!converged && !out_of_budget) {
-          std::vector<int> nb;
-          for (int j = 0; j < n; ++j)
-            if (j != best_i && neighbours(space[static_cast<size_t>(best_i)], space[static_cast<size_t>(j)])) nb.push_back(j);
+          std::vector<int> nb = neighbourhood(best_i);
           std::shuffle(nb.begin(), nb.end(), rng);
           bool improved = false;
           for (int j : nb) {
@@ -265,7 +417,7 @@ extern "C" int mdh_b200_tune_ex(const char* comp_json, const char* asm_model, co
         if (out_of_budget) break;
         settled_i = best_i;
       } else {
-        evaluate(static_cast<int>(rng() % static_cast<uint64_t>(n)));
+        evaluate(draw(perm_all, next_all, n_enum));
       }
     }
     if (best_i < 0) fail("NoValidConfigFound", "every evaluated configuration failed");

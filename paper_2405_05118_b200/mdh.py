@@ -39,7 +39,7 @@ EXPORTED = [
     "mdh_b200_launches_per_run", "mdh_b200_register_combine", "mdh_b200_combine_info",
     "mdh_b200_mplan_create", "mdh_b200_mplan_destroy", "mdh_b200_mplan_describe", "mdh_b200_mplan_shard_buffer",
     "mdh_b200_mplan_shard_plan", "mdh_b200_mplan_run", "mdh_b200_mplan_run_host", "mdh_b200_mplan_iterate",
-    "mdh_b200_mplan_time", "mdh_b200_nccl_unique_id", "mdh_b200_rank_plan_create", "mdh_b200_time_synthetic",
+    "mdh_b200_mplan_time", "mdh_b200_nccl_unique_id", "mdh_b200_rank_plan_create", "mdh_b200_time_synthetic", "mdh_b200_tune_space",
     "mdh_b200_kernel_source", "mdh_b200_last_error", "mdh_b200_version",
 ]
 OBJ_TIME, OBJ_SIMCOST = 0, 1
@@ -387,6 +387,17 @@ def tune_ex(spec, asm="B200", budget=20, seed=0, objective=OBJ_TIME, simcost_see
                                   int(objective), int(bool(simcost_seeded)), _text(start_config) if start_config else None,
                                   best, 1 << 20, hist, 1 << 20, ctypes.byref(val)))
     return best.value.decode(), hist.value.decode(), val.value
+
+
+def tune_space(spec, family, asm="B200", **kw) -> list:
+    """The tuner's enumerated candidates for a kernel family (host only)."""
+    o = options(**kw)
+    need = ctypes.c_int64()
+    _check(lib().mdh_b200_tune_space(_text(spec), _text(asm), ctypes.byref(o), _text(family), None, 0, ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    _check(lib().mdh_b200_tune_space(_text(spec), _text(asm), ctypes.byref(o), _text(family), buf, need.value,
+                                     ctypes.byref(need)))
+    return json.loads(buf.value.decode())
 
 
 def simcost(spec, asm="B200", config=None):

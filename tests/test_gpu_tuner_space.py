@@ -1,0 +1,69 @@
+"""Kernels instantiated from Table-1 configurations (SURVEY 8(a) a11/a12,
+a14): every instance of the tuner's space runs the template the
+configuration names and matches the oracle; the tuner (the reference's 3/10
+random phase + first-improving climb over its four neighbourhood moves,
+projected onto template instances) visits >= 50 distinct instances."""
+import json
+
+import numpy as np
+import pytest
+
+from helpers import exact_inputs, run_device, spec, uniform_inputs
+from oracle import mdh_oracle as mo
+
+SCHED = {  # schedule -> kernel name prefix (stencil.cu)
+    "lean": "star7_lean<5,4>", "ts": "star7_lean<4,4,tma_store>", "ws": "star7_ws", "pers": "star7_pers",
+    "plain": "star7_kernel"}
+
+
+@pytest.mark.gpu
+def test_every_stencil_instance_matches_the_oracle():
+    from paper_2405_05118_b200 import mdh
+    j = spec("jacobi3d_fp32", [512, 32, 128])
+    comp = mo.Computation.from_json(j)
+    ins = uniform_inputs(comp, 3)
+    ((want, dfd),) = mo.execute(comp, ins)
+    seen = set()
+    for c in mdh.tune_space(j, "stencil"):
+        plan = mdh.Plan(j, "B200", c)
+        d = plan.describe()
+        assert d["family"] == "stencil" and d["template"]["TI"] == 512 // c["num_parts"][0][0], d
+        assert json.loads(json.dumps(d["config"]))["num_parts"] == c["num_parts"]  # the instance's canonical config
+        seen.add((d["template"]["kernel"], d["template"]["TI"]))
+        (got,) = run_device(plan, ins)
+        assert np.abs(got.astype(np.float64) - want)[dfd].max() <= 1e-5 * 4, d["template"]
+    assert len(seen) == 50 and {k.split("<")[0] for k, _ in seen} == {"star7_lean", "star7_ws", "star7_pers", "star7_kernel"}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("math", [1, 2])
+def test_every_tensor_core_gemm_instance_is_exact(math):
+    from paper_2405_05118_b200 import mdh
+    j = spec("matmul_fp32", [1024, 1024, 256])
+    comp = mo.Computation.from_json(j)
+    ins = exact_inputs(comp, 5)
+    ((want, _),) = mo.execute(comp, ins)
+    kinds = set()
+    sp = mdh.tune_space(j, "contraction", math=math)
+    assert len(sp) >= 50
+    for c in sp:
+        plan = mdh.Plan(j, "B200", c, math=math)
+        t = plan.describe()["template"]
+        assert t["from_config"] and t["k_split"] == c["num_parts"][1][2] and t["BN"] == c["num_parts"][5][1], t
+        kinds.add((t["kernel"].split("<")[0], t["BN"], t["raster_group_m"], t["k_split"]))
+        (got,) = run_device(plan, ins)
+        assert np.array_equal(got.astype(np.float64), want), t
+    assert {k[0] for k in kinds} == {"tc_gemm_tf32", "tc_gemm_pers", "tc_gemm_2sm"}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,sizes,math", [("jacobi3d_fp32", [512, 32, 128], 0), ("matmul_fp32", [1024, 1024, 256], 1)])
+def test_tuner_visits_fifty_distinct_instances(name, sizes, math):
+    from paper_2405_05118_b200 import mdh
+    j = json.dumps(spec(name, sizes))
+    best, hist, secs = mdh.tune(j, "B200", budget=64, seed=5, math=math)
+    rows = [r.split(",") for r in hist.strip().splitlines()[1:]]
+    assert len(rows) == 64
+    distinct = {r[1] for r in rows if r[3] == "1"}
+    assert len(distinct) >= 50, len(distinct)
+    assert mdh.validate_config(j, "B200", best) == "" and secs > 0
