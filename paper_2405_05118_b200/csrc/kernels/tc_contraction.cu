@@ -1171,6 +1171,7 @@ class TcRoutine final : public Routine {
     decide_2sm();
     if (kn_.set && (kn_.form == 2) != two_sm_) return *why = "CTA-pair instance unavailable for this tile", false;
     if (!pers_ && BN_ == 192) return *why = "no one-CTA-per-tile instance with BN 192", false;
+    if (!pers_ && bf16_) return *why = "no one-CTA-per-tile kind::f16 instance", false;
     args_.group_m = kn_.group;
     if (kn_.split > 1) {
       if (args_.kext[0] % kn_.split) return *why = "K split does not divide the outer K digit", false;
@@ -1657,7 +1658,7 @@ std::vector<Config> tc_space(const Problem& p, const Groups& g) {
   for (int form = 0; form < 3; ++form)
     for (int bn : {256, 192, 128, 64}) {
       if (N % bn) continue;
-      if ((form == 0 && bn == 192) || (form == 2 && bn != 256 && bn != 128)) continue;
+      if ((form == 0 && (bn == 192 || bf16)) || (form == 2 && bn != 256 && bn != 128)) continue;
       const int64_t tm = form == 2 ? 2 * BM : BM;
       if (M % tm) continue;
       const int64_t rows = M / tm;
