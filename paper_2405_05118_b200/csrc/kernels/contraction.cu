@@ -285,6 +285,7 @@ struct SkinnyArgs {
   int M, N, K, ks;  // ks = k per split
   int splits;
   int64_t sak, sbk;  // affine k strides of A and B (skinny_cluster)
+  int* counter;      // per N strip arrival counters (skinny_cluster<..., LAST>)
 };
 
 template <int MT>
@@ -338,7 +339,14 @@ __global__ void __launch_bounds__(256) skinny_fold(SkinnyArgs g) {
 // Re-composition of K: k-quarters meet in shared memory (WRP -> SM), the CS
 // slices meet over DSMEM (SM -> cluster), each CTA folding 1/CS of the
 // outputs in fixed slice order -- deterministic, single writer per C cell.
-template <int MT, int KS>
+//
+// LAST = true (no cluster): the k-slices meet in global memory instead -- each
+// CTA writes its folded [MT][NW] partial to the plan's workspace, fences, and
+// bumps the strip's arrival counter; the CTA that arrives last folds the
+// strip's partials in slice order (deterministic, single writer) and resets
+// the counter for the next run.  CTAs that finish early leave at once (no
+// cluster barrier waits on the slowest slice).
+template <int MT, int KS, bool LAST = false>
 __global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g) {
   constexpr int NW = 32, NSTG = 4, R = MT / 8, SL = KS / NSTG, KQ = SL / 4, AKQ = SL / 4, AP = KS + 4;
   static_assert(KQ % 4 == 0, "k per thread per stage must be a multiple of 4");
@@ -353,7 +361,7 @@ __global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g) {
   const int kbase = blockIdx.y * KS;
   // every CTA of the cluster must be running before anyone writes into its
   // shared memory: arrive now, wait just before the DSMEM pushes
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  if (!LAST) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   // ---- issue every stage's copies up front (NSTG commit groups).  k offsets
   // are affine (g.sak == 1, g.sbk per k), so one table read per row / column
   // precedes the copies and nothing serialises the issue on load latency.
@@ -435,6 +443,28 @@ __global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g) {
   for (int i = 0; i < R; ++i)
     *reinterpret_cast<float4*>(red + (kq * MT + mg * R + i) * NW + cq * 4) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
   __syncthreads();
+  if (LAST) {
+    // ---- k-slices meet in global memory, the last arrival folds
+    __shared__ int last;
+    float* mine = g.part + (static_cast<int64_t>(blockIdx.x) * gridDim.y + blockIdx.y) * (MT * NW);
+    for (int o = tid; o < MT * NW; o += 256)
+      mine[o] = ((red[o] + red[MT * NW + o]) + red[2 * MT * NW + o]) + red[3 * MT * NW + o];
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) last = atomicAdd(g.counter + blockIdx.x, 1) == static_cast<int>(gridDim.y) - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const float* strip = g.part + static_cast<int64_t>(blockIdx.x) * gridDim.y * (MT * NW);
+    for (int o = tid; o < MT * NW; o += 256) {
+      float v = 0.f;
+      for (int c = 0; c < static_cast<int>(gridDim.y); ++c) v += __ldcg(strip + c * (MT * NW) + o);
+      const int m = o / NW, n = n0 + o % NW;
+      if (m < g.M && n < g.N) g.C[g.cm[m] + g.cn[n]] = v;
+    }
+    if (tid == 0) g.counter[blockIdx.x] = 0;  // ready for the next run (stream order)
+    return;
+  }
   // ---- k-slices meet over DSMEM: output o belongs to CTA o / per of the
   // cluster; every CTA pushes its partial of o into slot [my rank] of the
   // owner's inbox (remote stores, no round trips), one cluster barrier, then
@@ -866,6 +896,8 @@ class GemmRoutine final : public Routine {
   ~GemmRoutine() override {
     if (blob_) cudaFree(blob_);
     if (part_) cudaFree(part_);
+    if (lpart_) cudaFree(lpart_);
+    if (lcnt_) cudaFree(lcnt_);
     if (bp_tab_) cudaFree(bp_tab_);
     if (bp_) cudaFree(bp_);
     if (ap_tab_) cudaFree(ap_tab_);
@@ -926,6 +958,13 @@ class GemmRoutine final : public Routine {
           skinny_ = cluster_ = true;
           ks_ = static_cast<int>(ks);
           splits_ = cs;
+          last_ = std::getenv("MDHB_SKINNY_LAST") != nullptr;
+          if (last_) {  // workspace [strips][splits][mt * 32] + per-strip counters (zeroed once)
+            const int64_t strips = (N_ + 31) / 32;
+            MDHB_CUDA(cudaMalloc(&lpart_, static_cast<size_t>(strips * cs * mt * 32) * sizeof(float)));
+            MDHB_CUDA(cudaMalloc(&lcnt_, static_cast<size_t>(strips) * sizeof(int)));
+            MDHB_CUDA(cudaMemset(lcnt_, 0, static_cast<size_t>(strips) * sizeof(int)));
+          }
           tables(am, ak, bk, bn, cm, cn, {}, {}, {}, {});
           return true;
         }
@@ -1096,7 +1135,7 @@ class GemmRoutine final : public Routine {
     std::ostringstream os;
     const char* mn[] = {"scalar", "k4", "mn4"};
     if (cluster_) {
-      os << "{\"kernel\": \"skinny_cluster<" << (M_ <= 16 ? 16 : 32) << ">\", \"M\": " << M_ << ", \"N\": " << N_
+      os << "{\"kernel\": \"skinny_cluster<" << (M_ <= 16 ? 16 : 32) << (last_ ? ",last_block>" : ">") << "\", \"M\": " << M_ << ", \"N\": " << N_
          << ", \"K\": " << K_ << ", \"k_per_cta\": " << ks_ << ", \"cluster\": " << splits_
          << ", \"ctas\": " << (N_ + 31) / 32 * splits_ << ", \"threads\": 256}";
       return os.str();
@@ -1132,8 +1171,8 @@ class GemmRoutine final : public Routine {
     const float* B = static_cast<const float*>(d_in[g_.b_buf]);
     float* C = static_cast<float*>(d_out[0]);
     if (cluster_) {
-      SkinnyArgs a{A, B, nullptr, C, tab_[0], tab_[1], tab_[2], tab_[3], tab_[4], tab_[5], static_cast<int>(M_),
-                   static_cast<int>(N_), static_cast<int>(K_), ks_, splits_, sak_, sbk_};
+      SkinnyArgs a{A, B, lpart_, C, tab_[0], tab_[1], tab_[2], tab_[3], tab_[4], tab_[5], static_cast<int>(M_),
+                   static_cast<int>(N_), static_cast<int>(K_), ks_, splits_, sak_, sbk_, lcnt_};
       const int mt = M_ <= 16 ? 16 : 32;
       const size_t smem = (static_cast<size_t>(ks_) * 32 + static_cast<size_t>(mt) * (ks_ + 4) + 5 * mt * 32) * sizeof(float);
       cudaLaunchConfig_t lc = {};
@@ -1147,14 +1186,16 @@ class GemmRoutine final : public Routine {
       at[0].val.clusterDim.y = static_cast<unsigned>(splits_);
       at[0].val.clusterDim.z = 1;
       lc.attrs = at;
-      lc.numAttrs = 1;  // PDL measured slower for the cluster kernel (6.6 -> 7.7 us)
+      lc.numAttrs = last_ ? 0 : 1;  // PDL measured slower for the cluster kernel (6.6 -> 7.7 us)
       void (*kern)(SkinnyArgs) = nullptr;
-#define MDHB_SK(KS) \
-  if (ks_ == KS) kern = mt == 16 ? skinny_cluster<16, KS> : skinny_cluster<32, KS>;
+#define MDHB_SK(KS)                                                                                          \
+  if (ks_ == KS)                                                                                             \
+    kern = last_ ? (mt == 16 ? skinny_cluster<16, KS, true> : skinny_cluster<32, KS, true>)                  \
+                 : (mt == 16 ? skinny_cluster<16, KS> : skinny_cluster<32, KS>);
       MDHB_SK(64) MDHB_SK(128) MDHB_SK(256) MDHB_SK(512) MDHB_SK(1024)
 #undef MDHB_SK
       if (smem > 48 * 1024) MDHB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      if (splits_ > 8) MDHB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      if (splits_ > 8 && !last_) MDHB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       MDHB_CUDA(cudaLaunchKernelEx(&lc, kern, a));
       return;
     }
@@ -1322,7 +1363,9 @@ class GemmRoutine final : public Routine {
   int BM_ = 0, BN_ = 0, tilesM_ = 0, tilesN_ = 0;
   std::vector<int64_t> Tm_, Tn_;
   int amode_ = 0, bmode_ = 0;
-  bool cvec_ = false, gemv_ = false, skinny_ = false, cluster_ = false;
+  bool cvec_ = false, gemv_ = false, skinny_ = false, cluster_ = false, last_ = false;
+  float* lpart_ = nullptr;
+  int* lcnt_ = nullptr;
   int ks_ = 0, splits_ = 0;
   int64_t sak_ = 0, sbk_ = 0;
   bool tile_affine_ = false;
