@@ -610,7 +610,7 @@ __device__ __forceinline__ void tma_load_2sm(void* dst, const void* tmap, uint32
   }
 }
 
-template <int BN, int STAGES, bool BF16 = false>
+template <int BN, int STAGES, bool BF16 = false, bool B_MN = false>
 __global__ void __launch_bounds__(64 + 32 * 4, 1)
     tc_gemm_2sm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, TcArgs g, int b_row_rank) {
   constexpr int EPW = 4;
@@ -695,7 +695,18 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
         tma_load_2sm(sA + s * A_BYTES, &tma_a, fb, g.a_rank, c);
 #pragma unroll
         for (int r = 0; r < MAXR; ++r) c[r] = bn0[r] + kb[r];
-        tma_load_2sm(sB + s * B_BYTES, &tma_b, fb, g.b_rank, c);
+        if (B_MN) {  // MN-major B: this CTA's BN/2 columns as 32-column slabs (no layout pass)
+#pragma unroll
+          for (int j = 0; j < BN / 64; ++j) {
+            int cj[MAXR];
+#pragma unroll
+            for (int r = 0; r < MAXR; ++r) cj[r] = c[r];
+            cj[0] += 32 * j;
+            tma_load_2sm(sB + s * B_BYTES + j * (BKE * 128), &tma_b, fb, g.b_rank, cj);
+          }
+        } else {
+          tma_load_2sm(sB + s * B_BYTES, &tma_b, fb, g.b_rank, c);
+        }
         for (int q = g.nkd - 1; q >= 0; --q) {
           if (++dig[q] < g.kext[q]) {
 #pragma unroll
@@ -716,7 +727,7 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
     }
   } else if (warp == 1 && leader) {
     // ---------------- MMA issuer (leader only): M = 256 across the pair
-    constexpr uint32_t idesc = tc::instr_desc(BF16 ? 1 : 2, 0, 0, 2 * BM, BN);
+    constexpr uint32_t idesc = tc::instr_desc(BF16 ? 1 : 2, 0, B_MN ? 1 : 0, 2 * BM, BN);
     uint32_t it = 0, tl = 0;
     for (int x = pair; x < ntiles; x += npairs, ++tl) {
       const uint32_t acc = tl & 1;
@@ -732,7 +743,7 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
 #pragma unroll
         for (int k = 0; k < BKE / 8; ++k) {
           const uint64_t da = tc::sw128_desc(sa + k * 32, 16, 1024);
-          const uint64_t db = tc::sw128_desc(sb + k * 32, 16, 1024);
+          const uint64_t db = B_MN ? tc::umma_desc(sb + k * 1024, BKE * 128, 512, 1) : tc::sw128_desc(sb + k * 32, 16, 1024);
           const uint32_t accum = (kt | k) != 0 ? 1u : 0u;
           if (BF16)
             asm volatile(
@@ -1322,8 +1333,19 @@ class TcRoutine final : public Routine {
   // half-box split), an even number of 128-row tiles, BN 128 / 256
   void decide_2sm() {
     two_sm_ = false;
-    if (std::getenv("MDHB_TC_1SM") || !pers_ || rb_ || vb_.mn || (BN_ != 256 && BN_ != 128) || tilesM_ % 2) return;
+    if (std::getenv("MDHB_TC_1SM") || !pers_ || rb_ || (BN_ != 256 && BN_ != 128) || tilesM_ % 2) return;
     if (kn_.set && kn_.form != 2) return;
+    if (vb_.mn) {
+      // MN-major B (TF32, no layout pass): 32-column slabs, this CTA's half
+      // of the N tile from column rank * BN / 2 of the innermost TMA dim
+      if (bf16_ || vb_.box[0] != 32 || BN_ != 256 || std::getenv("MDHB_TC_2SM_NO_MN")) return;
+      b_row_rank_ = 0;
+      vb2_ = vb_;
+      st2_ = 6;
+      smem2_ = static_cast<size_t>(st2_) * (BM + BN_ / 2) * BKE * 4 + 1024 + 256 + 4 * (32 * 33 * 4 + 32 * 8);
+      two_sm_ = smem2_ <= 227 * 1024;
+      return;
+    }
     int row_rank = -1;
     for (int t = 1; t < vb_.rank; ++t) {
       if (vb_.box[t] == static_cast<cuuint32_t>(BN_)) {
@@ -1474,8 +1496,9 @@ class TcRoutine final : public Routine {
       lc.attrs = at;
       lc.numAttrs = 1;
       void (*k)(const CUtensorMap, const CUtensorMap, TcArgs, int) =
-          bf16_ ? (BN_ == 256 ? tc_gemm_2sm<256, 6, true> : tc_gemm_2sm<128, 8, true>)
-                : (BN_ == 256 ? tc_gemm_2sm<256, 6> : tc_gemm_2sm<128, 8>);
+          vb_.mn ? tc_gemm_2sm<256, 6, false, true>
+          : bf16_ ? (BN_ == 256 ? tc_gemm_2sm<256, 6, true> : tc_gemm_2sm<128, 8, true>)
+                  : (BN_ == 256 ? tc_gemm_2sm<256, 6> : tc_gemm_2sm<128, 8>);
       MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2_)));
       MDHB_CUDA(cudaLaunchKernelEx(&lc, k, ma_, mb2_, a, b_row_rank_));
       return;
@@ -1665,7 +1688,7 @@ std::vector<Config> tc_space(const Problem& p, const Groups& g) {
       for (int tr : {0, 1}) {
         if (bf16 && tr) continue;
         if (!bf16 && !mn && tr) continue;
-        if (!bf16 && mn && !tr && (form == 2 || bn == 192 || bn == 64 && form == 1)) continue;  // no MN-major instance
+        if (!bf16 && mn && !tr && ((form == 2 && bn != 256) || bn == 192 || (bn == 64 && form == 1))) continue;  // no MN-major instance
         for (int split : {1, 2, 4}) {
           if ((K / ek) % split) continue;
           std::vector<int64_t> groups;

@@ -351,8 +351,10 @@ def b200_time_objective(spec, asm="B200", config=None, reps=5, **kw) -> float:
         else:
             t.random_(0, 3)
     outs = p.empty(1)
-    med, _ = p.time(ins, outs, warmup=1, reps=reps)
+    # the fills ran on torch's stream; mdh_b200_time times on the plan's own
+    # non-blocking stream, which does not order after them
     torch.cuda.synchronize()
+    med, _ = p.time(ins, outs, warmup=1, reps=reps)
     return med
 
 
