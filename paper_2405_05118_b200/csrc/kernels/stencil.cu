@@ -15,13 +15,10 @@
 //          plane row is read from shared memory once per use class.
 // Algorithmic traffic per run: every input cell read once + every output cell
 // written once = 4 * (514^3 + 512^3) B for the BASELINE size.
-#include <cuda.h>
-
 #include <algorithm>
 #include <array>
 #include <cstdlib>
 #include <cstring>
-#include <mutex>
 #include <sstream>
 
 #include "../plan.hpp"
@@ -653,26 +650,23 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) star7_lean(StencilArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// v5 (1-D TMA rows, conflict-free): the lean kernel's shared-memory traffic
-// is the binding resource (ncu: l1tex 90%, mio_throttle) -- each lane owns 4
-// consecutive k, so its 6-wide window (halo included) costs three 8-byte
-// reads at a 16-byte lane stride: 4-way bank conflicts.  Here the producer
-// fetches every plane row with a 1-D TMA *tensor* copy (element-granular
-// start coordinate, unlike the 16-byte-aligned bulk copy), starting 3
-// elements before the tile, so each lane's 4 centre values land 16-byte
-// aligned: one conflict-free LDS.128 per row; the k-halo values come from
-// the neighbouring lanes by shuffle, only lanes 0 / 31 read one more float.
-constexpr int T1_PITCH = 160;  // floats per smem row: 640 B (128-byte aligned TMA destinations)
-constexpr int T1_BOX = 136;    // floats per row copy: v columns k0-3 .. k0+132
-
-struct Rows4v {
-  float4 r[2];
+// v5 (strided lanes, conflict-free): the lean kernel is bound by shared
+// memory wavefronts (ncu: l1tex 90%, mio_throttle) because each lane owns 4
+// consecutive k -- its windows are 8-byte reads at a 16-byte lane stride,
+// 4-way bank conflicts.  Here lane l owns columns l, l+32, l+64, l+96 of the
+// tile: every read of a row is one 4-byte word per lane at consecutive
+// addresses (one wavefront per 32 values, whatever the row's alignment
+// shift), the k-halos are plain reads one word left / right, and each store
+// instruction writes 128 contiguous bytes.  Same ring, producer and
+// register rotation along i as star7_lean.
+struct Rows8 {
+  float r[2][4];
 };
 
 template <int NS, int MINB>
-__global__ void __launch_bounds__(WS_THREADS, MINB) star7_t1d(const __grid_constant__ CUtensorMap tv, StencilArgs a) {
+__global__ void __launch_bounds__(WS_THREADS, MINB) star7_s32(StencilArgs a) {
   constexpr int TJ = 16, ROWS = TJ + 2;
-  extern __shared__ __align__(128) float sring[];  // [NS][ROWS][T1_PITCH]
+  extern __shared__ __align__(128) float sring[];  // [NS][ROWS][BPITCH]
   __shared__ __align__(8) uint64_t full[NS], empty[NS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t k0 = static_cast<int64_t>(blockIdx.x) * TK;
@@ -680,7 +674,9 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) star7_t1d(const __grid_const
   const int64_t i0 = static_cast<int64_t>(blockIdx.z) * a.ti;
   const int iend = static_cast<int>(a.n0 - i0 < a.ti ? a.n0 - i0 : a.ti);
   const int nplanes = iend + 2;
-  float* ring = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(sring) + 127) & ~uintptr_t(127));
+  const uint32_t pstride = static_cast<uint32_t>(a.e1 * a.e2);
+  const uint32_t base0 = static_cast<uint32_t>((i0 * a.e1 + j0) * a.e2 + k0);
+  const uint32_t rstride = static_cast<uint32_t>(a.e2);
 
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -692,104 +688,87 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) star7_t1d(const __grid_const
   __syncthreads();
 
   if (warp == 8) {
-    if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(&tv) : "memory");
-      const int64_t row0 = (i0 * a.e1 + j0) * a.e2 + k0 - 3;  // element of smem column 0, row 0, plane 0
-      for (int p = 0; p < nplanes; ++p) {
-        const int s = p % NS;
-        if (p >= NS) mbar_wait_parity(&empty[s], static_cast<uint32_t>((p / NS - 1) & 1));
-        const bool in = i0 + p < a.e0;
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(&full[s])),
-                     "r"(in ? static_cast<uint32_t>(ROWS * T1_BOX * 4) : 0u) : "memory");
-        if (!in) continue;
-        for (int r = 0; r < ROWS; ++r) {
-          const int c = static_cast<int>(row0 + static_cast<int64_t>(p) * (a.e1 * a.e2) + static_cast<int64_t>(r) * a.e2);
-          float* dst = ring + (static_cast<size_t>(s) * ROWS + r) * T1_PITCH;
-          asm volatile("cp.async.bulk.tensor.1d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2}], [%3];"
-                       ::"r"(s_u32(dst)), "l"(&tv), "r"(c), "r"(s_u32(&full[s])) : "memory");
-        }
+    const float* vbase = a.v + ((i0 * a.e1 + j0) * a.e2 + k0);
+    for (int p = 0; p < nplanes; ++p) {
+      const int s = p % NS;
+      if (p >= NS) mbar_wait_parity(&empty[s], static_cast<uint32_t>((p / NS - 1) & 1));
+      uint32_t bytes = 0, sh = 0;
+      if (lane < ROWS) {
+        sh = (base0 + static_cast<uint32_t>(p) * pstride + static_cast<uint32_t>(lane) * rstride) & 3u;
+        bytes = (sh * 4 + (TK + 2) * 4 + 15) & ~15u;
+      }
+      uint32_t total = bytes;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(&full[s])), "r"(total) : "memory");
+      __syncwarp();
+      if (lane < ROWS && i0 + p < a.e0) {
+        const float* src = vbase + static_cast<int64_t>(p) * (a.e1 * a.e2) + static_cast<int64_t>(lane) * a.e2 - sh;
+        float* dst = sring + (static_cast<size_t>(s) * ROWS + lane) * BPITCH;
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(s_u32(dst)), "l"(src), "r"(bytes), "r"(s_u32(&full[s])) : "memory");
       }
     }
     return;
   }
 
-  const int kl = lane * 4, jl = warp * 2;
-  // 32-bit shared addresses: this lane's centre column of row r of plane p
-  const uint32_t tbase = s_u32(ring) + static_cast<uint32_t>(kl + 4) * 4u;
-  auto row = [&](int p, int r) {
-    return tbase + static_cast<uint32_t>(((p % NS) * ROWS + r) * T1_PITCH) * 4u;
-  };
-  auto ld4 = [](uint32_t addr) {
-    float4 v;
-    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
-    return v;
+  const int jl = warp * 2;
+  // 32-bit shared address of (plane p, smem row r, the column left of this lane's first centre)
+  const uint32_t ring0 = s_u32(sring) + static_cast<uint32_t>(lane) * 4u;
+  auto rowaddr = [&](int p, int r) {
+    const uint32_t sh = (base0 + static_cast<uint32_t>(p) * pstride + static_cast<uint32_t>(r) * rstride) & 3u;
+    return ring0 + (static_cast<uint32_t>(((p % NS) * ROWS + r) * BPITCH) + sh) * 4u;
   };
   auto ld1 = [](uint32_t addr) {
     float v;
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
     return v;
   };
-  auto load_centre = [&](int p, Rows4v& R) {
-    R.r[0] = ld4(row(p, jl + 1));
-    R.r[1] = ld4(row(p, jl + 2));
+  auto load_row = [&](uint32_t ra, float (&x)[4]) {  // centres of columns lane + 32 m
+#pragma unroll
+    for (int m = 0; m < 4; ++m) x[m] = ld1(ra + static_cast<uint32_t>(32 * m + 1) * 4u);
+  };
+  auto load_centre = [&](int p, Rows8& R) {
+    load_row(rowaddr(p, jl + 1), R.r[0]);
+    load_row(rowaddr(p, jl + 2), R.r[1]);
   };
   auto release = [&](int p) {
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(&empty[p % NS])) : "memory");
   };
-  float* wout = a.w + (i0 * a.n1 + j0 + jl) * a.n2 + k0 + kl;
+  float* wout = a.w + (i0 * a.n1 + j0 + jl) * a.n2 + k0 + lane;
   const int64_t wplane = a.n1 * a.n2;
-  const bool kin = k0 + kl + 4 <= a.n2;
 
-  auto step = [&](int t, const Rows4v& P, const Rows4v& C, Rows4v& N) {
+  auto step = [&](int t, const Rows8& P, const Rows8& C, Rows8& N) {
     mbar_wait_parity(&full[(t + 2) % NS], static_cast<uint32_t>(((t + 2) / NS) & 1));
     load_centre(t + 2, N);
-    const float4 jm = ld4(row(t + 1, jl));
-    const float4 jp = ld4(row(t + 1, jl + 3));
-    // k-halos: the neighbouring lanes' centre values; the tile edges from smem
-    float hl[2], hr[2];
-    hl[0] = __shfl_up_sync(0xffffffffu, C.r[0].w, 1);
-    hl[1] = __shfl_up_sync(0xffffffffu, C.r[1].w, 1);
-    hr[0] = __shfl_down_sync(0xffffffffu, C.r[0].x, 1);
-    hr[1] = __shfl_down_sync(0xffffffffu, C.r[1].x, 1);
-    if (lane == 0) {
-      hl[0] = ld1(row(t + 1, jl + 1) - 4u);
-      hl[1] = ld1(row(t + 1, jl + 2) - 4u);
-    } else if (lane == 31) {
-      hr[0] = ld1(row(t + 1, jl + 1) + 16u);
-      hr[1] = ld1(row(t + 1, jl + 2) + 16u);
-    }
-    release(t + 1);
+    // plane t + 1 stays resident until every read below is done: the j /
+    // k neighbours are read just in time (few live registers)
 #pragma unroll
     for (int jj = 0; jj < 2; ++jj) {
-      const float4& c = C.r[jj];
-      const float4& up = jj == 0 ? jm : C.r[0];
-      const float4& dn = jj == 1 ? jp : C.r[1];
-      auto g = [](const float4& v, int q) { return q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w; };
-      float o[4];
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const float km = kk == 0 ? hl[jj] : g(c, kk - 1);
-        const float kp = kk == 3 ? hr[jj] : g(c, kk + 1);
-        float acc = a.wc * g(c, kk);
-        acc = fmaf(a.wim, g(P.r[jj], kk), acc);
-        acc = fmaf(a.wip, g(N.r[jj], kk), acc);
-        acc = fmaf(a.wjm, g(up, kk), acc);
-        acc = fmaf(a.wjp, g(dn, kk), acc);
-        acc = fmaf(a.wkm, km, acc);
-        acc = fmaf(a.wkp, kp, acc);
-        o[kk] = acc;
-      }
+      float nb[4];  // the row outside the register window: j-1 for jj = 0, j+2 for jj = 1
+      load_row(rowaddr(t + 1, jj == 0 ? jl : jl + 3), nb);
+      const uint32_t ra = rowaddr(t + 1, jl + 1 + jj);
       const int64_t j = j0 + jl + jj;
-      if (j < a.n1 && kin) {
-        __stcs(reinterpret_cast<float4*>(wout + t * wplane + jj * a.n2), make_float4(o[0], o[1], o[2], o[3]));
-      } else if (j < a.n1) {
-        for (int kk = 0; kk < 4 && k0 + kl + kk < a.n2; ++kk) wout[t * wplane + jj * a.n2 + kk] = o[kk];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const float up = jj == 0 ? nb[m] : C.r[0][m];
+        const float dn = jj == 1 ? nb[m] : C.r[1][m];
+        float acc = a.wc * C.r[jj][m];
+        acc = fmaf(a.wim, P.r[jj][m], acc);
+        acc = fmaf(a.wip, N.r[jj][m], acc);
+        acc = fmaf(a.wjm, up, acc);
+        acc = fmaf(a.wjp, dn, acc);
+        acc = fmaf(a.wkm, ld1(ra + static_cast<uint32_t>(32 * m) * 4u), acc);
+        acc = fmaf(a.wkp, ld1(ra + static_cast<uint32_t>(32 * m + 2) * 4u), acc);
+        if (j < a.n1 && k0 + lane + 32 * m < a.n2) __stcs(wout + t * wplane + jj * a.n2 + 32 * m, acc);
       }
     }
+    release(t + 1);
   };
 
-  Rows4v R0, R1, R2;
+  Rows8 R0, R1, R2;
   mbar_wait_parity(&full[0], 0);
   mbar_wait_parity(&full[1], 0);
   load_centre(0, R0);
@@ -1001,24 +980,6 @@ bool linear_terms(const Expr& e, std::vector<std::pair<double, int>>& terms) {
   return false;
 }
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-EncodeTiledFn tmap_encoder() {
-  static EncodeTiledFn fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q{};
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  });
-  if (!fn) fail("CudaError", "cuTensorMapEncodeTiled unavailable");
-  return fn;
-}
-
 // Schedules of the star-7 template (which kernel streams the planes):
 //   LEAN     TMA-bulk producer warp + smem plane ring, centre columns in registers (star7_lean)
 //   LEAN_TS  LEAN with the output staged in smem and written by TMA stores
@@ -1037,7 +998,7 @@ class StencilRoutine final : public Routine {
   const char* family() const override { return "stencil"; }
   std::string describe() const override {
     std::ostringstream os;
-    const std::string kname = t1d_ && lean_ && !ts_ok() ? "star7_t1d<" + std::to_string(t1d_ / 10) + "," + std::to_string(t1d_ % 10) + ">"
+    const std::string kname = s32_ && lean_ && !ts_ok() ? "star7_s32<" + std::to_string(s32_ / 10) + "," + std::to_string(s32_ % 10) + ">"
                               : lean_ && ts_ok() ? std::string("star7_lean<4,4,tma_store>")
                               : lean_ ? "star7_lean<" + std::to_string(lean_ / 10) + "," + std::to_string(lean_ % 10) + ">"
                                     : std::string(pers_ ? "star7_pers<" : ws_ ? "star7_ws<" : bulk_ ? "star7_bulk<" : "star7_kernel<") +
@@ -1137,22 +1098,11 @@ class StencilRoutine final : public Routine {
       const int64_t items = tiles * ((a.n0 + a.ti - 1) / a.ti);
       const int grid_p = static_cast<int>(std::min<int64_t>(ctas_, mode ? items : std::max<int64_t>(1, total / 4)));
       kern<<<grid_p, WS_THREADS, smem, s>>>(a, tiles_k, total, mode);
-    } else if (t1d_ && lean_) {
-      if (a.v != t1d_v_) {  // 1-D tensor map over the whole input (element-granular row starts)
-        const cuuint64_t dims[1] = {static_cast<cuuint64_t>(a.e0 * a.e1 * a.e2)};
-        const cuuint64_t strides[1] = {4};
-        const cuuint32_t box[1] = {static_cast<cuuint32_t>(T1_BOX)}, estr[1] = {1};
-        CUresult r = tmap_encoder()(&t1d_map_, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 1, const_cast<float*>(a.v), dims, strides, box,
-                                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) fail("CudaError", "1-D tensor map encode failed (" + std::to_string(static_cast<int>(r)) + ")");
-        t1d_v_ = a.v;
-      }
-      const int ns = t1d_ / 10;
-      void (*k)(const CUtensorMap, StencilArgs) = ns == 5 ? star7_t1d<5, 3> : ns == 3 ? star7_t1d<3, 4> : star7_t1d<4, 4>;
-      const size_t tsmem = static_cast<size_t>(ns) * 18 * T1_PITCH * sizeof(float) + 128;
-      MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsmem)));
-      k<<<grid(), WS_THREADS, tsmem, s>>>(t1d_map_, a);
+    } else if (s32_ && lean_ && !ts_ok()) {
+      void (*k)(StencilArgs) = s32_ == 53 ? star7_s32<5, 3> : s32_ == 44 ? star7_s32<4, 4> : star7_s32<5, 4>;
+      const size_t lsmem = static_cast<size_t>(s32_ / 10) * 18 * BPITCH * sizeof(float);
+      MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lsmem)));
+      k<<<grid(), WS_THREADS, lsmem, s>>>(a);
     } else if (lean_) {
       void (*k)(StencilArgs) = nullptr;
       const bool ts = ts_ok();
@@ -1186,10 +1136,8 @@ class StencilRoutine final : public Routine {
   bool ws_;
   bool pers_;
   int ctas_ = 0;
-  // 1-D TMA row variant (star7_t1d): NS*10+MINB, 0 = off
-  int t1d_ = std::getenv("MDHB_STENCIL_T1D") ? std::atoi(std::getenv("MDHB_STENCIL_T1D")) : 0;
-  CUtensorMap t1d_map_{};
-  const float* t1d_v_ = nullptr;
+  // strided-lane variant (star7_s32): NS*10+MINB, 0 = off
+  int s32_ = std::getenv("MDHB_STENCIL_S32") ? std::atoi(std::getenv("MDHB_STENCIL_S32")) : 0;
   cudaStream_t h2d_ = nullptr, d2h_ = nullptr;
   cudaEvent_t ev_in_[18] = {}, ev_cmp_[18] = {};
   int minb_ = std::getenv("MDHB_STENCIL_MINB") ? std::atoi(std::getenv("MDHB_STENCIL_MINB")) : 2;
