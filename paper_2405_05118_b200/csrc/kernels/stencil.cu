@@ -981,7 +981,8 @@ bool linear_terms(const Expr& e, std::vector<std::pair<double, int>>& terms) {
 }
 
 // Schedules of the star-7 template (which kernel streams the planes):
-//   LEAN     TMA-bulk producer warp + smem plane ring, centre columns in registers (star7_lean)
+//   LEAN     TMA-bulk producer warp + smem plane ring, centre columns in registers
+//            (star7_s32: lanes strided by 32 columns; star7_lean: 4 adjacent columns per lane)
 //   LEAN_TS  LEAN with the output staged in smem and written by TMA stores
 //   WS       producer warp + ring, every neighbour read from smem (star7_ws)
 //   PERS     WS on persistent CTAs striding over (tile, i-chunk) items (star7_pers)
@@ -1099,7 +1100,11 @@ class StencilRoutine final : public Routine {
       const int grid_p = static_cast<int>(std::min<int64_t>(ctas_, mode ? items : std::max<int64_t>(1, total / 4)));
       kern<<<grid_p, WS_THREADS, smem, s>>>(a, tiles_k, total, mode);
     } else if (s32_ && lean_ && !ts_ok()) {
-      void (*k)(StencilArgs) = s32_ == 53 ? star7_s32<5, 3> : s32_ == 44 ? star7_s32<4, 4> : star7_s32<5, 4>;
+      void (*k)(StencilArgs) = s32_ == 53   ? star7_s32<5, 3>
+                               : s32_ == 63 ? star7_s32<6, 3>
+                               : s32_ == 73 ? star7_s32<7, 3>
+                               : s32_ == 44 ? star7_s32<4, 4>
+                                            : star7_s32<5, 4>;
       const size_t lsmem = static_cast<size_t>(s32_ / 10) * 18 * BPITCH * sizeof(float);
       MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lsmem)));
       k<<<grid(), WS_THREADS, lsmem, s>>>(a);
@@ -1137,7 +1142,10 @@ class StencilRoutine final : public Routine {
   bool pers_;
   int ctas_ = 0;
   // strided-lane variant (star7_s32): NS*10+MINB, 0 = off
-  int s32_ = std::getenv("MDHB_STENCIL_S32") ? std::atoi(std::getenv("MDHB_STENCIL_S32")) : 0;
+  // (default for the LEAN schedule: 206 vs 210 us at 512^3 on one box, bit-identical;
+  // MDHB_STENCIL_LEAN selects the packed-lane star7_lean rings instead)
+  int s32_ = std::getenv("MDHB_STENCIL_S32") ? std::atoi(std::getenv("MDHB_STENCIL_S32"))
+                                            : (std::getenv("MDHB_STENCIL_LEAN") ? 0 : 53);
   cudaStream_t h2d_ = nullptr, d2h_ = nullptr;
   cudaEvent_t ev_in_[18] = {}, ev_cmp_[18] = {};
   int minb_ = std::getenv("MDHB_STENCIL_MINB") ? std::atoi(std::getenv("MDHB_STENCIL_MINB")) : 2;

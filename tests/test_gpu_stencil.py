@@ -69,15 +69,18 @@ def test_jacobi3d_host_pipeline_equals_device_run(sizes):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("env", ["0", "63", "44", "ts"])
+@pytest.mark.parametrize("env", ["0", "63", "44", "54", "ts"])
 def test_jacobi3d_variants_bit_identical(env, monkeypatch):
-    """Every stencil kernel variant (star7_ws, lean-register rings) computes
-    the same bits: same FMA order per output cell."""
+    """Every stencil kernel variant (star7_ws, the packed-lane lean rings, the
+    TMA-store epilogue) computes the default's (star7_s32) bits: same FMA
+    order per output cell."""
     from paper_2405_05118_b200 import mdh
     j = spec("jacobi3d_fp32", [40, 48, 384])
     comp = mo.Computation.from_json(j)
     ins = uniform_inputs(comp, 5)
-    (base,) = run_device(mdh.Plan(j), ins)
+    p0 = mdh.Plan(j)
+    assert p0.describe()["template"]["kernel"] == "star7_s32<5,3>", p0.describe()
+    (base,) = run_device(p0, ins)
     if env == "ts":
         monkeypatch.setenv("MDHB_STENCIL_TS", "1")  # TMA bulk stores (full tiles: 48 x 384 qualify)
     else:

@@ -32,7 +32,8 @@ def test_every_stencil_instance_matches_the_oracle():
         seen.add((d["template"]["kernel"], d["template"]["TI"]))
         (got,) = run_device(plan, ins)
         assert np.abs(got.astype(np.float64) - want)[dfd].max() <= 1e-5 * 4, d["template"]
-    assert len(seen) == 50 and {k.split("<")[0] for k, _ in seen} == {"star7_lean", "star7_ws", "star7_pers", "star7_kernel"}
+    assert len(seen) == 50 and {k.split("<")[0] for k, _ in seen} == {"star7_s32", "star7_lean", "star7_ws", "star7_pers",
+                                                                      "star7_kernel"}
 
 
 @pytest.mark.gpu
