@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round evidence on one GPU (run under gpurun): GPU tests, the bench line, the
 # ncu launch list of the bench command, one ncu --set full summary per routine.
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3 > gpurun_out/gpu_tests.log
+timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -3 > gpurun_out/gpu_tests.log
 timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err
 bash tools/launch_list.sh
 bash tools/profile_all.sh jacobi3d_fp32 matvec_fp32 matmul_fp32 matmul_fp32:tf32 matmul_resnet_fc mcc_nhwc mcc_nhwc:tf32 \
