@@ -38,6 +38,7 @@ struct StencilArgs {
   int ti;                 // output planes per CTA
   // weights of the 7-point star, in slot order: centre, i-1, i+1, j-1, j+1, k-1, k+1
   float wc, wim, wip, wjm, wjp, wkm, wkp;
+  int pf;                 // star7_s32: L2 prefetch distance in planes (0 = off)
 };
 
 // Star-7 stencil with the centre at offset (1,1,1): reads v[i+1+di][j+1+dj][k+1+dk].
@@ -708,6 +709,11 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) star7_s32(StencilArgs a) {
         float* dst = sring + (static_cast<size_t>(s) * ROWS + lane) * BPITCH;
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                      ::"r"(s_u32(dst)), "l"(src), "r"(bytes), "r"(s_u32(&full[s])) : "memory");
+        // L2 prefetch `pf` planes ahead of the ring: more DRAM requests in
+        // flight than the ring's shared memory holds
+        if (a.pf > 0 && p + a.pf < nplanes && i0 + p + a.pf < a.e0)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + static_cast<int64_t>(a.pf) * (a.e1 * a.e2)),
+                       "r"(bytes) : "memory");
       }
     }
     return;
@@ -1100,6 +1106,7 @@ class StencilRoutine final : public Routine {
       const int grid_p = static_cast<int>(std::min<int64_t>(ctas_, mode ? items : std::max<int64_t>(1, total / 4)));
       kern<<<grid_p, WS_THREADS, smem, s>>>(a, tiles_k, total, mode);
     } else if (s32_ && lean_ && !ts_ok()) {
+      a.pf = pf_;
       void (*k)(StencilArgs) = s32_ == 53   ? star7_s32<5, 3>
                                : s32_ == 63 ? star7_s32<6, 3>
                                : s32_ == 73 ? star7_s32<7, 3>
@@ -1146,6 +1153,7 @@ class StencilRoutine final : public Routine {
   // MDHB_STENCIL_LEAN selects the packed-lane star7_lean rings instead)
   int s32_ = std::getenv("MDHB_STENCIL_S32") ? std::atoi(std::getenv("MDHB_STENCIL_S32"))
                                             : (std::getenv("MDHB_STENCIL_LEAN") ? 0 : 53);
+  int pf_ = std::getenv("MDHB_STENCIL_PF") ? std::atoi(std::getenv("MDHB_STENCIL_PF")) : 0;
   cudaStream_t h2d_ = nullptr, d2h_ = nullptr;
   cudaEvent_t ev_in_[18] = {}, ev_cmp_[18] = {};
   int minb_ = std::getenv("MDHB_STENCIL_MINB") ? std::atoi(std::getenv("MDHB_STENCIL_MINB")) : 2;
