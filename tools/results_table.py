@@ -36,7 +36,7 @@ def main():
     for name, label in LABEL.items():
         meas, frac, kern = [], [], []
         for r in rows.get(name, []):
-            math = r["routine"].split(":")[1] if ":" in r["routine"] else "ffma"
+            math = r["routine"].split(":")[1] if ":" in r["routine"] else ("int" if name == "prl_max" else "fp32")
             rf = r["roofline"]
             unit = rf.get("unit", "")
             ach = rf.get("achieved")
