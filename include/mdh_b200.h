@@ -248,6 +248,11 @@ int mdh_b200_mplan_time(mdh_b200_mplan* mplan, const void* const* const* d_in, v
  * NCCL inside mdh_b200_run; with NULL the caller combines.  describe() gains
  * a "shard" member (range, per-buffer slab rank and start). */
 int mdh_b200_nccl_unique_id(unsigned char* id128);
+/* Host only: rank `rank`'s shard as the rank plan would build it -- JSON
+ * {"computation": <shard md_hom>, "config": <shard config or null>,
+ *  "shard": {split_dim, split_kind, range, in/out: [slab rank, start]}}. */
+int mdh_b200_shard_spec(const char* computation_json, const char* asm_model, const char* config_json, int world,
+                        int rank, int split_dim, char* buf, int64_t cap, int64_t* need);
 int mdh_b200_rank_plan_create(const char* computation_json, const char* asm_model, const char* config_json,
                               const mdh_b200_options* opt, int world, int rank, const unsigned char* nccl_id,
                               mdh_b200_plan** out);

@@ -239,6 +239,23 @@ int mdh_b200_rank_plan_create(const char* comp_json, const char* asm_model, cons
   });
 }
 
+int mdh_b200_shard_spec(const char* comp_json, const char* asm_model, const char* config_json, int world, int rank,
+                        int split_dim, char* buf, int64_t cap, int64_t* need) {
+  return guard([&] {
+    if (!comp_json) mdhb::fail("InvalidConfig", "null argument");
+    if (world < 1 || rank < 0 || rank >= world) mdhb::fail("OutOfRange", "rank must be in [0, world)");
+    mdhb::Asm m = mdhb::resolve_asm(asm_model ? asm_model : "MultiB200");
+    std::string cfg_out, desc;
+    int fold = -1;
+    bool pw = false;
+    std::string sj = mdhb::rank_shard(comp_json, m, config_json ? config_json : "", world, rank, split_dim, &cfg_out,
+                                      &desc, &fold, &pw);
+    std::string out = "{\"computation\": " + sj + ", \"config\": " + (cfg_out.empty() ? std::string("null") : cfg_out) +
+                      ", " + desc + "}";
+    put(out, buf, cap, need);
+  });
+}
+
 int mdh_b200_plan_destroy(mdh_b200_plan* p) {
   return guard([&] {
     if (!p) return;

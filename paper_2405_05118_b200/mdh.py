@@ -39,7 +39,7 @@ EXPORTED = [
     "mdh_b200_launches_per_run", "mdh_b200_register_combine", "mdh_b200_combine_info",
     "mdh_b200_mplan_create", "mdh_b200_mplan_destroy", "mdh_b200_mplan_describe", "mdh_b200_mplan_shard_buffer",
     "mdh_b200_mplan_shard_plan", "mdh_b200_mplan_run", "mdh_b200_mplan_run_host", "mdh_b200_mplan_iterate",
-    "mdh_b200_mplan_time", "mdh_b200_nccl_unique_id", "mdh_b200_rank_plan_create", "mdh_b200_time_synthetic", "mdh_b200_tune_space",
+    "mdh_b200_mplan_time", "mdh_b200_nccl_unique_id", "mdh_b200_rank_plan_create", "mdh_b200_time_synthetic", "mdh_b200_tune_space", "mdh_b200_shard_spec",
     "mdh_b200_kernel_source", "mdh_b200_last_error", "mdh_b200_version",
 ]
 OBJ_TIME, OBJ_SIMCOST = 0, 1
@@ -219,6 +219,17 @@ def nccl_unique_id() -> bytes:
     buf = (ctypes.c_ubyte * 128)()
     _check(lib().mdh_b200_nccl_unique_id(buf))
     return bytes(buf)
+
+
+def shard_spec(spec, world, rank, split_dim=0, asm="MultiB200", config=None) -> dict:
+    """Host only: the DEV layer's shard `rank` of `world` (the C++ split rule
+    of mdh_b200_rank_plan_create) -> {"computation", "config", "shard"}."""
+    need = ctypes.c_int64()
+    args = (_text(spec), _text(asm), None if config is None else _text(config), int(world), int(rank), int(split_dim))
+    _check(lib().mdh_b200_shard_spec(*args, None, 0, ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    _check(lib().mdh_b200_shard_spec(*args, buf, need.value, ctypes.byref(need)))
+    return json.loads(buf.value.decode())
 
 
 def rank_plan(spec, world, rank, device=0, nccl_id: Optional[bytes] = None, asm="MultiB200", config=None,
