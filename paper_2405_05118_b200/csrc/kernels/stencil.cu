@@ -664,13 +664,31 @@ struct Rows8 {
   float r[2][4];
 };
 
-template <int NS, int MINB>
+// TKC = k columns per CTA tile (128, 256 or 512): wider tiles read longer
+// contiguous row segments (528 / 1040 / 2064 bytes) at the price of more
+// j-halo rows per output (TJ = 2048 / TKC rows: 16 / 8 / 4).  Each warp owns
+// RW rows x CW columns, lane l the columns l + 32 m of them (M = CW / 32).
+template <int TKC>
+__host__ __device__ constexpr int CWDIV() { return (TKC * (2048 / TKC)) / 8; }
+
+template <int TKC>
+struct S32Shape {
+  static constexpr int TJ = 2048 / TKC;                 // rows per CTA
+  static constexpr int RW = TJ >= 8 ? TJ / 8 : 1;       // rows per warp
+  static constexpr int CW = TJ >= 8 ? TKC : TKC * TJ / 8;  // columns per warp
+  static constexpr int M = CW / 32;                     // columns per lane
+  static constexpr int PITCH = TKC + 8;                 // smem row pitch (floats)
+  static_assert(RW * M == 8, "8 output values per thread per plane");
+};
+
+template <int NS, int MINB, int TKC = 128>
 __global__ void __launch_bounds__(WS_THREADS, MINB) star7_s32(StencilArgs a) {
-  constexpr int TJ = 16, ROWS = TJ + 2;
-  extern __shared__ __align__(128) float sring[];  // [NS][ROWS][BPITCH]
+  using SH = S32Shape<TKC>;
+  constexpr int TJ = SH::TJ, ROWS = TJ + 2, RW = SH::RW, M = SH::M, PITCH = SH::PITCH;
+  extern __shared__ __align__(128) float sring[];  // [NS][ROWS][PITCH]
   __shared__ __align__(8) uint64_t full[NS], empty[NS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * TK;
+  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * TKC;
   const int64_t j0 = static_cast<int64_t>(blockIdx.y) * TJ;
   const int64_t i0 = static_cast<int64_t>(blockIdx.z) * a.ti;
   const int iend = static_cast<int>(a.n0 - i0 < a.ti ? a.n0 - i0 : a.ti);
@@ -696,7 +714,7 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) star7_s32(StencilArgs a) {
       uint32_t bytes = 0, sh = 0;
       if (lane < ROWS) {
         sh = (base0 + static_cast<uint32_t>(p) * pstride + static_cast<uint32_t>(lane) * rstride) & 3u;
-        bytes = (sh * 4 + (TK + 2) * 4 + 15) & ~15u;
+        bytes = (sh * 4 + (TKC + 2) * 4 + 15) & ~15u;
       }
       uint32_t total = bytes;
 #pragma unroll
@@ -706,75 +724,79 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) star7_s32(StencilArgs a) {
       __syncwarp();
       if (lane < ROWS && i0 + p < a.e0) {
         const float* src = vbase + static_cast<int64_t>(p) * (a.e1 * a.e2) + static_cast<int64_t>(lane) * a.e2 - sh;
-        float* dst = sring + (static_cast<size_t>(s) * ROWS + lane) * BPITCH;
+        float* dst = sring + (static_cast<size_t>(s) * ROWS + lane) * PITCH;
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                      ::"r"(s_u32(dst)), "l"(src), "r"(bytes), "r"(s_u32(&full[s])) : "memory");
-        // L2 prefetch `pf` planes ahead of the ring: more DRAM requests in
-        // flight than the ring's shared memory holds
-        if (a.pf > 0 && p + a.pf < nplanes && i0 + p + a.pf < a.e0)
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + static_cast<int64_t>(a.pf) * (a.e1 * a.e2)),
-                       "r"(bytes) : "memory");
       }
     }
     return;
   }
 
-  const int jl = warp * 2;
-  // 32-bit shared address of (plane p, smem row r, the column left of this lane's first centre)
-  const uint32_t ring0 = s_u32(sring) + static_cast<uint32_t>(lane) * 4u;
+  // this warp's rows and columns
+  const int jl = TJ >= 8 ? warp * RW : (warp * CWDIV<TKC>()) / TKC;
+  const int cl = TJ >= 8 ? 0 : (warp * CWDIV<TKC>()) % TKC;
+  const uint32_t ring0 = s_u32(sring) + static_cast<uint32_t>(cl + lane) * 4u;
   auto rowaddr = [&](int p, int r) {
     const uint32_t sh = (base0 + static_cast<uint32_t>(p) * pstride + static_cast<uint32_t>(r) * rstride) & 3u;
-    return ring0 + (static_cast<uint32_t>(((p % NS) * ROWS + r) * BPITCH) + sh) * 4u;
+    return ring0 + (static_cast<uint32_t>(((p % NS) * ROWS + r) * PITCH) + sh) * 4u;
   };
   auto ld1 = [](uint32_t addr) {
     float v;
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
     return v;
   };
-  auto load_row = [&](uint32_t ra, float (&x)[4]) {  // centres of columns lane + 32 m
+  auto load_row = [&](uint32_t ra, float (&x)[M]) {  // centres of columns lane + 32 m
 #pragma unroll
-    for (int m = 0; m < 4; ++m) x[m] = ld1(ra + static_cast<uint32_t>(32 * m + 1) * 4u);
+    for (int m = 0; m < M; ++m) x[m] = ld1(ra + static_cast<uint32_t>(32 * m + 1) * 4u);
   };
-  auto load_centre = [&](int p, Rows8& R) {
-    load_row(rowaddr(p, jl + 1), R.r[0]);
-    load_row(rowaddr(p, jl + 2), R.r[1]);
+  struct RowsW {
+    float r[RW][M];
+  };
+  auto load_centre = [&](int p, RowsW& R) {
+#pragma unroll
+    for (int q = 0; q < RW; ++q) load_row(rowaddr(p, jl + 1 + q), R.r[q]);
   };
   auto release = [&](int p) {
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(&empty[p % NS])) : "memory");
   };
-  float* wout = a.w + (i0 * a.n1 + j0 + jl) * a.n2 + k0 + lane;
+  float* wout = a.w + (i0 * a.n1 + j0 + jl) * a.n2 + k0 + cl + lane;
   const int64_t wplane = a.n1 * a.n2;
 
-  auto step = [&](int t, const Rows8& P, const Rows8& C, Rows8& N) {
+  auto step = [&](int t, const RowsW& P, const RowsW& C, RowsW& N) {
     mbar_wait_parity(&full[(t + 2) % NS], static_cast<uint32_t>(((t + 2) / NS) & 1));
     load_centre(t + 2, N);
     // plane t + 1 stays resident until every read below is done: the j /
     // k neighbours are read just in time (few live registers)
 #pragma unroll
-    for (int jj = 0; jj < 2; ++jj) {
-      float nb[4];  // the row outside the register window: j-1 for jj = 0, j+2 for jj = 1
-      load_row(rowaddr(t + 1, jj == 0 ? jl : jl + 3), nb);
+    for (int jj = 0; jj < RW; ++jj) {
+      float up[M], dn[M];
+      if (jj == 0) load_row(rowaddr(t + 1, jl), up);
+      else
+#pragma unroll
+        for (int m = 0; m < M; ++m) up[m] = C.r[jj - 1][m];
+      if (jj == RW - 1) load_row(rowaddr(t + 1, jl + RW + 1), dn);
+      else
+#pragma unroll
+        for (int m = 0; m < M; ++m) dn[m] = C.r[jj + 1][m];
       const uint32_t ra = rowaddr(t + 1, jl + 1 + jj);
       const int64_t j = j0 + jl + jj;
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const float up = jj == 0 ? nb[m] : C.r[0][m];
-        const float dn = jj == 1 ? nb[m] : C.r[1][m];
+      for (int m = 0; m < M; ++m) {
         float acc = a.wc * C.r[jj][m];
         acc = fmaf(a.wim, P.r[jj][m], acc);
         acc = fmaf(a.wip, N.r[jj][m], acc);
-        acc = fmaf(a.wjm, up, acc);
-        acc = fmaf(a.wjp, dn, acc);
+        acc = fmaf(a.wjm, up[m], acc);
+        acc = fmaf(a.wjp, dn[m], acc);
         acc = fmaf(a.wkm, ld1(ra + static_cast<uint32_t>(32 * m) * 4u), acc);
         acc = fmaf(a.wkp, ld1(ra + static_cast<uint32_t>(32 * m + 2) * 4u), acc);
-        if (j < a.n1 && k0 + lane + 32 * m < a.n2) __stcs(wout + t * wplane + jj * a.n2 + 32 * m, acc);
+        if (j < a.n1 && k0 + cl + lane + 32 * m < a.n2) __stcs(wout + t * wplane + jj * a.n2 + 32 * m, acc);
       }
     }
     release(t + 1);
   };
 
-  Rows8 R0, R1, R2;
+  RowsW R0, R1, R2;
   mbar_wait_parity(&full[0], 0);
   mbar_wait_parity(&full[1], 0);
   load_centre(0, R0);
@@ -1005,7 +1027,9 @@ class StencilRoutine final : public Routine {
   const char* family() const override { return "stencil"; }
   std::string describe() const override {
     std::ostringstream os;
-    const std::string kname = s32_ && lean_ && !ts_ok() ? "star7_s32<" + std::to_string(s32_ / 10) + "," + std::to_string(s32_ % 10) + ">"
+    const std::string kname = s32_ && lean_ && !ts_ok() ? "star7_s32<" + std::to_string(tkc_ != 128 ? 5 : s32_ / 10) + "," +
+                                                                std::to_string(tkc_ != 128 ? 3 : s32_ % 10) +
+                                                                (tkc_ != 128 ? "," + std::to_string(tkc_) : std::string()) + ">"
                               : lean_ && ts_ok() ? std::string("star7_lean<4,4,tma_store>")
                               : lean_ ? "star7_lean<" + std::to_string(lean_ / 10) + "," + std::to_string(lean_ % 10) + ">"
                                     : std::string(pers_ ? "star7_pers<" : ws_ ? "star7_ws<" : bulk_ ? "star7_bulk<" : "star7_kernel<") +
@@ -1107,14 +1131,19 @@ class StencilRoutine final : public Routine {
       kern<<<grid_p, WS_THREADS, smem, s>>>(a, tiles_k, total, mode);
     } else if (s32_ && lean_ && !ts_ok()) {
       a.pf = pf_;
-      void (*k)(StencilArgs) = s32_ == 53   ? star7_s32<5, 3>
-                               : s32_ == 63 ? star7_s32<6, 3>
-                               : s32_ == 73 ? star7_s32<7, 3>
-                               : s32_ == 44 ? star7_s32<4, 4>
-                                            : star7_s32<5, 4>;
-      const size_t lsmem = static_cast<size_t>(s32_ / 10) * 18 * BPITCH * sizeof(float);
+      void (*k)(StencilArgs) = tkc_ == 256 ? star7_s32<5, 3, 256>
+                               : tkc_ == 512 ? star7_s32<5, 3, 512>
+                               : s32_ == 53  ? star7_s32<5, 3>
+                               : s32_ == 63  ? star7_s32<6, 3>
+                               : s32_ == 73  ? star7_s32<7, 3>
+                               : s32_ == 44  ? star7_s32<4, 4>
+                                             : star7_s32<5, 4>;
+      const int ns = tkc_ != 128 ? 5 : s32_ / 10;
+      const size_t lsmem = static_cast<size_t>(ns) * (2048 / tkc_ + 2) * (tkc_ + 8) * sizeof(float);
       MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lsmem)));
-      k<<<grid(), WS_THREADS, lsmem, s>>>(a);
+      const dim3 g(static_cast<unsigned>((a.n2 + tkc_ - 1) / tkc_), static_cast<unsigned>((a.n1 + 2048 / tkc_ - 1) / (2048 / tkc_)),
+                   static_cast<unsigned>((a.n0 + a.ti - 1) / a.ti));
+      k<<<g, WS_THREADS, lsmem, s>>>(a);
     } else if (lean_) {
       void (*k)(StencilArgs) = nullptr;
       const bool ts = ts_ok();
@@ -1154,6 +1183,8 @@ class StencilRoutine final : public Routine {
   int s32_ = std::getenv("MDHB_STENCIL_S32") ? std::atoi(std::getenv("MDHB_STENCIL_S32"))
                                             : (std::getenv("MDHB_STENCIL_LEAN") ? 0 : 53);
   int pf_ = std::getenv("MDHB_STENCIL_PF") ? std::atoi(std::getenv("MDHB_STENCIL_PF")) : 0;
+  // star7_s32 k columns per CTA tile (128 / 256 / 512; rows 16 / 8 / 4)
+  int tkc_ = std::getenv("MDHB_STENCIL_TKC") ? std::atoi(std::getenv("MDHB_STENCIL_TKC")) : 128;
   cudaStream_t h2d_ = nullptr, d2h_ = nullptr;
   cudaEvent_t ev_in_[18] = {}, ev_cmp_[18] = {};
   int minb_ = std::getenv("MDHB_STENCIL_MINB") ? std::atoi(std::getenv("MDHB_STENCIL_MINB")) : 2;
