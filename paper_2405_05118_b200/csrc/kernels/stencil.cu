@@ -1019,7 +1019,7 @@ enum StencilSched { S_LEAN = 0, S_LEAN_TS = 1, S_WS = 2, S_PERS = 3, S_PLAIN = 4
 
 class StencilRoutine final : public Routine {
  public:
-  StencilRoutine(const Problem& p, StencilArgs a, int tj, bool bulk, int sched)
+  StencilRoutine(const Problem& p, StencilArgs a, int tj, bool bulk, int sched, int tkc = 128)
       : p_(p), a_(a), tj_(tj), bulk_(bulk && sched != S_PLAIN), ws_(bulk_ && sched != S_PLAIN),
         pers_(ws_ && sched == S_PERS), ts_(sched == S_LEAN_TS) {
     if (sched == S_WS || sched == S_PERS || !ws_) lean_ = 0;
@@ -1034,10 +1034,12 @@ class StencilRoutine final : public Routine {
                               : lean_ ? "star7_lean<" + std::to_string(lean_ / 10) + "," + std::to_string(lean_ % 10) + ">"
                                     : std::string(pers_ ? "star7_pers<" : ws_ ? "star7_ws<" : bulk_ ? "star7_bulk<" : "star7_kernel<") +
                                           std::to_string(tj_) + ">";
-    os << "{\"kernel\": \"" << kname << "\", \"TK\": " << TK << ", \"TJ\": " << tj_ << ", \"TI\": " << a_.ti
+    const bool s32 = s32_ && lean_ && !ts_ok();
+    const int tk = s32 ? tkc_ : TK, tj = s32 ? 2048 / tkc_ : tj_;
+    os << "{\"kernel\": \"" << kname << "\", \"TK\": " << tk << ", \"TJ\": " << tj << ", \"TI\": " << a_.ti
        << ", \"threads\": " << (ws_ ? WS_THREADS : NTHREADS) << ", \"smem_ring_slots\": " << (lean_ ? lean_ / 10 : bulk_ ? NSLOT : 4)
-       << ", \"ctas_per_sm\": " << (lean_ ? lean_ % 10 : 3) << ", \"grid\": [" << grid().x << ", " << grid().y
-       << ", " << grid().z << "]}";
+       << ", \"ctas_per_sm\": " << (lean_ ? lean_ % 10 : 3) << ", \"grid\": [" << (a_.n2 + tk - 1) / tk << ", "
+       << (a_.n1 + tj - 1) / tj << ", " << grid().z << "]}";
     return os.str();
   }
   dim3 grid() const {
@@ -1184,7 +1186,7 @@ class StencilRoutine final : public Routine {
                                             : (std::getenv("MDHB_STENCIL_LEAN") ? 0 : 53);
   int pf_ = std::getenv("MDHB_STENCIL_PF") ? std::atoi(std::getenv("MDHB_STENCIL_PF")) : 0;
   // star7_s32 k columns per CTA tile (128 / 256 / 512; rows 16 / 8 / 4)
-  int tkc_ = std::getenv("MDHB_STENCIL_TKC") ? std::atoi(std::getenv("MDHB_STENCIL_TKC")) : 128;
+  int tkc_ = 128;
   cudaStream_t h2d_ = nullptr, d2h_ = nullptr;
   cudaEvent_t ev_in_[18] = {}, ev_cmp_[18] = {};
   int minb_ = std::getenv("MDHB_STENCIL_MINB") ? std::atoi(std::getenv("MDHB_STENCIL_MINB")) : 2;
@@ -1209,6 +1211,7 @@ class StencilRoutine final : public Routine {
 struct StencilKnobs {
   int ti = 32;
   int sched = S_LEAN;
+  int tkc = 128;  // k columns per CTA tile (LEAN: 128 / 256 / 512 with 16 / 8 / 4 rows; other schedules 128)
 };
 
 int region_at(const Config& c, const std::vector<std::vector<int>>& mem, size_t buf, int asm_layer, bool re, int D) {
@@ -1229,9 +1232,11 @@ StencilKnobs stencil_knobs(const Problem& p, const Config& c) {
         if (x != 1) fail("Unsupported", std::string("stencil template: ") + other + " parts belong to the DEV layer");
   auto at = [&](int layer, int d) { return P[static_cast<size_t>(layer - 1)][static_cast<size_t>(d)]; };
   StencilKnobs k;
-  if (e.sizes[1] % (at(smx, 1) * at(dm, 1)) || e.sizes[1] / (at(smx, 1) * at(dm, 1)) != 16 ||
-      e.sizes[2] % (at(smx, 2) * at(dm, 2)) || e.sizes[2] / (at(smx, 2) * at(dm, 2)) != TK)
-    fail("Unsupported", "stencil template tiles (j, k) by (16, 128) per CTA");
+  const int64_t tj = e.sizes[1] % (at(smx, 1) * at(dm, 1)) ? 0 : e.sizes[1] / (at(smx, 1) * at(dm, 1));
+  const int64_t tk = e.sizes[2] % (at(smx, 2) * at(dm, 2)) ? 0 : e.sizes[2] / (at(smx, 2) * at(dm, 2));
+  if (!((tj == 16 && tk == 128) || (tj == 8 && tk == 256) || (tj == 4 && tk == 512)))
+    fail("Unsupported", "stencil template tiles (j, k) by (16, 128), (8, 256) or (4, 512) per CTA");
+  k.tkc = static_cast<int>(tk);
   if (e.sizes[0] % at(smx, 0)) fail("Unsupported", "stencil template needs uniform i-chunks");
   k.ti = static_cast<int>(e.sizes[0] / at(smx, 0));
   const bool persistent = at(dm, 1) > 1 || at(dm, 2) > 1;
@@ -1242,15 +1247,21 @@ StencilKnobs stencil_knobs(const Problem& p, const Config& c) {
   else if (v_sm == dm) k.sched = S_PLAIN;
   else if (v_rm == rm) k.sched = w_sm == sm ? S_LEAN_TS : S_LEAN;
   else k.sched = S_WS;
+  if (k.tkc != 128 && k.sched != S_LEAN) fail("Unsupported", "only the LEAN schedule takes 256- / 512-column tiles");
   return k;
 }
 
 Config stencil_canonical(const Problem& p, const StencilKnobs& k) {
   const MdHom& e = p.e;
-  const int64_t gj = e.sizes[1] / 16, gk = e.sizes[2] / TK;
+  const int64_t tj = 2048 / k.tkc;
+  const int64_t gj = e.sizes[1] / tj, gk = e.sizes[2] / k.tkc;
   const bool pers = k.sched == S_PERS && gj % 2 == 0;
+  // threads: 8 warps over j (x 2 column halves at 512), 32 lanes over k, per
+  // thread 8 values: 2 rows x 4 columns (128), 1 x 8 (256, 512)
+  const std::vector<int64_t> wrp = k.tkc == 512 ? std::vector<int64_t>{1, 4, 2} : std::vector<int64_t>{1, 8, 1};
+  const std::vector<int64_t> rmv = k.tkc == 128 ? std::vector<int64_t>{1, 2, 4} : std::vector<int64_t>{1, 1, 8};
   std::vector<LayerParts> lp = {{"SMX", {e.sizes[0] / k.ti, pers ? gj / 2 : gj, gk}}, {"DM", {k.ti, pers ? 2 : 1, 1}},
-                                {"WRP", {1, 8, 1}}, {"CC", {1, 1, 32}}, {"SM", {1, 1, 1}}, {"RM", {1, 2, 4}}};
+                                {"WRP", wrp}, {"CC", {1, 1, 32}}, {"SM", {1, 1, 1}}, {"RM", rmv}};
   Config c = make_config(p, lp, {{e.in[0].name, k.sched == S_PLAIN ? "DM" : "SM"}}, "RM");
   const int D = e.D(), sm = p.m.id("SM"), rm = p.m.id("RM"), dm = p.m.id("DM");
   for (size_t r = 0; r < c.ass_de.size(); ++r) {
@@ -1326,27 +1337,40 @@ std::unique_ptr<Routine> make_stencil(const Problem& p, const Config* cfg, Confi
   if (std::getenv("MDHB_STENCIL_V1") || std::getenv("MDHB_STENCIL_V2")) sched = S_PLAIN;  // dev aids
   if (std::getenv("MDHB_STENCIL_PERS")) sched = S_PERS;
   if (std::getenv("MDHB_STENCIL_TS")) sched = S_LEAN_TS;
+  // LEAN: the widest k tile whose full tiles cover the output (longer
+  // contiguous row reads: 172 vs 207 us at 512^3 for 512 vs 128 columns)
+  int tkc = 128;
+  for (int c : {512, 256})
+    if (a.n2 % c == 0 && a.n1 % (2048 / c) == 0) {
+      tkc = c;
+      break;
+    }
+  if (const char* f = std::getenv("MDHB_STENCIL_TKC")) tkc = std::atoi(f);
   if (cfg) {
     StencilKnobs k = stencil_knobs(p, *cfg);
     ti = k.ti;
     sched = k.sched;
+    tkc = k.tkc;
   }
+  if (sched != S_LEAN) tkc = 128;
   if (const char* f = std::getenv("MDHB_STENCIL_TI")) ti = std::max(1, std::atoi(f));
   a.ti = ti;
   // TMA bulk row copies need every copied span inside the allocation: the
   // buffer size must be 16-byte rounded (rows overrun at most to the next
   // 16-byte boundary) and the k tiles must not reach past the row end.
   const int64_t vbytes = p.in_ext[0][0] * a.e1 * a.e2 * 4;
-  const bool bulk = vbytes % 16 == 0 && a.n2 % TK == 0;
-  if (cfg && sched != S_PLAIN && !bulk) fail("Unsupported", "stencil producer schedules need 16-byte rows and full k tiles");
+  // the producer copies whole (tile + halo) rows: full j and k tiles keep every
+  // copy inside the buffer (ragged shapes take the PLAIN schedule)
+  const bool bulk = vbytes % 16 == 0 && a.n2 % tkc == 0 && a.n1 % (2048 / tkc) == 0;
+  if (cfg && sched != S_PLAIN && !bulk) fail("Unsupported", "stencil producer schedules need 16-byte rows and full j / k tiles");
   if (cfg && sched == S_LEAN_TS && (a.n1 % 16 || (a.n2 * 4) % 16)) fail("Unsupported", "TMA-store epilogue needs full tiles");
   if (cfg_out) {
-    if (a.n1 % TJ || a.n2 % TK || a.n0 % ti || p.m.id("WRP") < 0 || p.m.id("SMX") < 0)
+    if (a.n1 % (2048 / tkc) || a.n2 % tkc || a.n0 % ti || p.m.id("WRP") < 0 || p.m.id("SMX") < 0)
       *cfg_out = baseline_config(e, p.m);
     else
-      *cfg_out = stencil_canonical(p, {ti, sched});
+      *cfg_out = stencil_canonical(p, {ti, sched, bulk ? tkc : 128});
   }
-  return std::make_unique<StencilRoutine>(p, a, TJ, bulk, sched);
+  return std::make_unique<StencilRoutine>(p, a, TJ, bulk, sched, tkc);
 }
 
 }  // namespace mdhb
@@ -1365,10 +1389,13 @@ std::vector<Config> stencil_space(const Problem& p) {
   if (p.m.id("SMX") < 0 || p.m.id("WRP") < 0 || e.D() != 3) return out;
   if (e.sizes[1] % 16 || e.sizes[2] % 128) return out;
   for (int sched = S_LEAN; sched <= S_PLAIN; ++sched)
-    for (int64_t ti = 1; ti <= e.sizes[0]; ti *= 2) {
-      if (e.sizes[0] % ti) continue;
-      if (sched == S_PERS && (e.sizes[1] / 16) % 2) continue;
-      out.push_back(stencil_canonical(p, {static_cast<int>(ti), sched}));
+    for (int tkc : {128, 256, 512}) {
+      if (tkc != 128 && (sched != S_LEAN || e.sizes[2] % tkc || e.sizes[1] % (2048 / tkc))) continue;
+      for (int64_t ti = 1; ti <= e.sizes[0]; ti *= 2) {
+        if (e.sizes[0] % ti) continue;
+        if (sched == S_PERS && (e.sizes[1] / 16) % 2) continue;
+        out.push_back(stencil_canonical(p, {static_cast<int>(ti), sched, tkc}));
+      }
     }
   return out;
 }

@@ -7,7 +7,8 @@ from oracle import mdh_oracle as mo
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("sizes", [[8, 8, 16], [3, 16, 128], [5, 32, 256], [7, 20, 130], [40, 48, 384]])
+@pytest.mark.parametrize("sizes", [[8, 8, 16], [3, 16, 128], [5, 32, 256], [7, 20, 130], [40, 48, 384], [6, 8, 256],
+                                   [5, 4, 512], [9, 12, 512], [4, 20, 256]])
 def test_jacobi3d_small_vs_oracle(sizes):
     from paper_2405_05118_b200 import mdh
     j = spec("jacobi3d_fp32", sizes)

@@ -17,6 +17,25 @@ SCHED = {  # schedule -> kernel name prefix (stencil.cu)
 
 
 @pytest.mark.gpu
+def test_wide_tile_stencil_instances_match_the_oracle():
+    """The LEAN schedule's 256- and 512-column tiles (8 / 4 rows per CTA)."""
+    from paper_2405_05118_b200 import mdh
+    j = spec("jacobi3d_fp32", [16, 64, 512])
+    comp = mo.Computation.from_json(j)
+    ins = uniform_inputs(comp, 4)
+    ((want, dfd),) = mo.execute(comp, ins)
+    tiles = set()
+    for c in mdh.tune_space(j, "stencil"):
+        plan = mdh.Plan(j, "B200", c)
+        t = plan.describe()["template"]
+        tiles.add((t["kernel"], t["TK"], t["TJ"]))
+        (got,) = run_device(plan, ins)
+        assert np.abs(got.astype(np.float64) - want)[dfd].max() <= 1e-5 * 4, t
+    assert {(128, 16), (256, 8), (512, 4)} <= {(tk, tj) for _, tk, tj in tiles}
+    assert mdh.Plan(j).describe()["template"]["kernel"] == "star7_s32<5,3,512>"  # the default: widest tile
+
+
+@pytest.mark.gpu
 def test_every_stencil_instance_matches_the_oracle():
     from paper_2405_05118_b200 import mdh
     j = spec("jacobi3d_fp32", [512, 32, 128])
