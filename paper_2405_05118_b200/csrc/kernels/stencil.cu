@@ -1023,6 +1023,7 @@ class StencilRoutine final : public Routine {
       : p_(p), a_(a), tj_(tj), bulk_(bulk && sched != S_PLAIN), ws_(bulk_ && sched != S_PLAIN),
         pers_(ws_ && sched == S_PERS), ts_(sched == S_LEAN_TS) {
     if (sched == S_WS || sched == S_PERS || !ws_) lean_ = 0;
+    tkc_ = tkc;
   }
   const char* family() const override { return "stencil"; }
   std::string describe() const override {
