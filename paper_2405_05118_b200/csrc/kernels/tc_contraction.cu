@@ -1184,6 +1184,7 @@ class TcRoutine final : public Routine {
     if (!pers_ && BN_ == 192) return *why = "no one-CTA-per-tile instance with BN 192", false;
     if (!pers_ && bf16_) return *why = "no one-CTA-per-tile kind::f16 instance", false;
     args_.group_m = kn_.group;
+    if (const char* f = std::getenv("MDHB_TC_GROUP")) args_.group_m = std::atoi(f);  // dev aid
     if (kn_.split > 1) {
       if (args_.kext[0] % kn_.split) return *why = "K split does not divide the outer K digit", false;
       int64_t n = 1;
