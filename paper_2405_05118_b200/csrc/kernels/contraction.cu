@@ -346,17 +346,19 @@ __global__ void __launch_bounds__(256) skinny_fold(SkinnyArgs g) {
 // strip's partials in slice order (deterministic, single writer) and resets
 // the counter for the next run.  CTAs that finish early leave at once (no
 // cluster barrier waits on the slowest slice).
-template <int MT, int KS, bool LAST = false>
+template <int MT, int KS, bool LAST = false, int NW = 32>
 __global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g) {
-  constexpr int NW = 32, NSTG = 4, R = MT / 8, SL = KS / NSTG, KQ = SL / 4, AKQ = SL / 4, AP = KS + 4;
-  static_assert(KQ % 4 == 0, "k per thread per stage must be a multiple of 4");
+  // NW columns per CTA strip: 256 threads = KQN k-parts x 8 m-groups x NW/4 column quads
+  constexpr int CQN = NW / 4, KQN = 256 / (8 * CQN);
+  constexpr int NSTG = 4, R = MT / 8, SL = KS / NSTG, KQ = SL / KQN, AKQ = SL / 4, AP = KS + 4;
+  static_assert(KQN >= 1 && KQ % 4 == 0, "k per thread per stage must be a multiple of 4");
   extern __shared__ __align__(16) float sm[];
   float* Bs = sm;                 // [KS][NW]
   float* As = Bs + KS * NW;       // [MT][KS + 4]
-  float* red = As + MT * AP;      // [4][MT][NW]   k-quarter partials
-  float* inbox = red + 4 * MT * NW;  // [CS][MT*NW/CS]  slices pushed by the cluster's CTAs
+  float* red = As + MT * AP;      // [KQN][MT][NW]   k-part partials
+  float* inbox = red + KQN * MT * NW;  // [CS][MT*NW/CS]  slices pushed by the cluster's CTAs
   const int tid = threadIdx.x;
-  const int kq = tid >> 6, mg = (tid >> 3) & 7, cq = tid & 7;
+  const int kq = tid / (8 * CQN), mg = (tid / CQN) % 8, cq = tid % CQN;
   const int n0 = blockIdx.x * NW;
   const int kbase = blockIdx.y * KS;
   // every CTA of the cluster must be running before anyone writes into its
@@ -447,8 +449,12 @@ __global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g) {
     // ---- k-slices meet in global memory, the last arrival folds
     __shared__ int last;
     float* mine = g.part + (static_cast<int64_t>(blockIdx.x) * gridDim.y + blockIdx.y) * (MT * NW);
-    for (int o = tid; o < MT * NW; o += 256)
-      mine[o] = ((red[o] + red[MT * NW + o]) + red[2 * MT * NW + o]) + red[3 * MT * NW + o];
+    for (int o = tid; o < MT * NW; o += 256) {
+      float v = red[o];
+#pragma unroll
+      for (int q = 1; q < KQN; ++q) v += red[q * MT * NW + o];
+      mine[o] = v;
+    }
     __threadfence();
     __syncthreads();
     if (tid == 0) last = atomicAdd(g.counter + blockIdx.x, 1) == static_cast<int>(gridDim.y) - 1;
@@ -475,7 +481,9 @@ __global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g) {
   const int per = MT * NW / static_cast<int>(cs);
   asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   for (int o = tid; o < MT * NW; o += 256) {
-    const float v = ((red[o] + red[MT * NW + o]) + red[2 * MT * NW + o]) + red[3 * MT * NW + o];
+    float v = red[o];
+#pragma unroll
+    for (int q = 1; q < KQN; ++q) v += red[q * MT * NW + o];
     const uint32_t owner = static_cast<uint32_t>(o / per);
     const uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(inbox + rank * per + o % per));
     uint32_t remote;
@@ -959,6 +967,8 @@ class GemmRoutine final : public Routine {
           ks_ = static_cast<int>(ks);
           splits_ = cs;
           last_ = std::getenv("MDHB_SKINNY_LAST") != nullptr;
+          if (const char* f = std::getenv("MDHB_SKINNY_NW")) nw_ = std::atoi(f);
+          if (nw_ != 32 && (mt != 16 || last_ || (ks != 128 && ks != 256) || N_ % 4)) nw_ = 32;
           if (last_) {  // workspace [strips][splits][mt * 32] + per-strip counters (zeroed once)
             const int64_t strips = (N_ + 31) / 32;
             MDHB_CUDA(cudaMalloc(&lpart_, static_cast<size_t>(strips * cs * mt * 32) * sizeof(float)));
@@ -1174,9 +1184,10 @@ class GemmRoutine final : public Routine {
       SkinnyArgs a{A, B, lpart_, C, tab_[0], tab_[1], tab_[2], tab_[3], tab_[4], tab_[5], static_cast<int>(M_),
                    static_cast<int>(N_), static_cast<int>(K_), ks_, splits_, sak_, sbk_, lcnt_};
       const int mt = M_ <= 16 ? 16 : 32;
-      const size_t smem = (static_cast<size_t>(ks_) * 32 + static_cast<size_t>(mt) * (ks_ + 4) + 5 * mt * 32) * sizeof(float);
+      const int nw = nw_, kqn = 256 / (8 * (nw / 4));
+      const size_t smem = (static_cast<size_t>(ks_) * nw + static_cast<size_t>(mt) * (ks_ + 4) + (kqn + 1) * mt * nw) * sizeof(float);
       cudaLaunchConfig_t lc = {};
-      lc.gridDim = dim3(static_cast<unsigned>((N_ + 31) / 32), static_cast<unsigned>(splits_));
+      lc.gridDim = dim3(static_cast<unsigned>((N_ + nw - 1) / nw), static_cast<unsigned>(splits_));
       lc.blockDim = dim3(256);
       lc.dynamicSmemBytes = smem;
       lc.stream = s;
@@ -1192,8 +1203,14 @@ class GemmRoutine final : public Routine {
   if (ks_ == KS)                                                                                             \
     kern = last_ ? (mt == 16 ? skinny_cluster<16, KS, true> : skinny_cluster<32, KS, true>)                  \
                  : (mt == 16 ? skinny_cluster<16, KS> : skinny_cluster<32, KS>);
-      MDHB_SK(64) MDHB_SK(128) MDHB_SK(256) MDHB_SK(512) MDHB_SK(1024)
+      if (nw == 32) {
+        MDHB_SK(64) MDHB_SK(128) MDHB_SK(256) MDHB_SK(512) MDHB_SK(1024)
+      }
 #undef MDHB_SK
+      // wider column strips (longer contiguous B row segments): MT 16 only
+      if (nw == 64 && mt == 16) kern = ks_ == 128 ? skinny_cluster<16, 128, false, 64> : ks_ == 256 ? skinny_cluster<16, 256, false, 64> : nullptr;
+      if (nw == 128 && mt == 16) kern = ks_ == 128 ? skinny_cluster<16, 128, false, 128> : ks_ == 256 ? skinny_cluster<16, 256, false, 128> : nullptr;
+      if (!kern) fail("Unsupported", "no skinny_cluster instance for this strip / slice");
       if (smem > 48 * 1024) MDHB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       if (splits_ > 8 && !last_) MDHB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       MDHB_CUDA(cudaLaunchKernelEx(&lc, kern, a));
@@ -1366,6 +1383,7 @@ class GemmRoutine final : public Routine {
   bool cvec_ = false, gemv_ = false, skinny_ = false, cluster_ = false, last_ = false;
   float* lpart_ = nullptr;
   int* lcnt_ = nullptr;
+  int nw_ = 32;  // skinny_cluster column strip width
   int ks_ = 0, splits_ = 0;
   int64_t sak_ = 0, sbk_ = 0;
   bool tile_affine_ = false;
