@@ -610,7 +610,24 @@ __device__ __forceinline__ void tma_load_2sm(void* dst, const void* tmap, uint32
   }
 }
 
-template <int BN, int STAGES, bool BF16 = false, bool B_MN = false>
+// 2-D TMA load into this CTA AND the CTAs of `mask` (same smem offsets);
+// with cta_group::2 each destination's complete_tx lands on its pair
+// leader's barrier (the even CTA of the pair)
+__device__ __forceinline__ void tma_load_2sm_mc(void* dst, const void* tmap, uint32_t mbar_cluster, uint16_t mask,
+                                                const int* c) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.cta_group::2"
+      " [%0], [%1, {%3, %4}], [%2], %5;"
+      ::"r"(tc::smem_u32(dst)), "l"(tmap), "r"(mbar_cluster), "r"(c[0]), "r"(c[1]), "h"(mask) : "memory");
+}
+
+// MC: a cluster of FOUR CTAs = two CTA pairs on the tiles (tm, 2n) and
+// (tm, 2n + 1), which share their A rows: CTA r lands half of its A tile
+// (64 rows, multicast) in itself and in CTA r ^ 2, so each A row crosses
+// from L2 once per cluster instead of once per pair.  A stage is reused only
+// after BOTH pairs' MMAs released it (empty[s] counts two commits, each
+// multicast to all four CTAs).
+template <int BN, int STAGES, bool BF16 = false, bool B_MN = false, bool MC = false>
 __global__ void __launch_bounds__(64 + 32 * 4, 1)
     tc_gemm_2sm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, TcArgs g, int b_row_rank) {
   constexpr int EPW = 4;
@@ -628,26 +645,32 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* stage_base = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 256);
   const int warp = tc::warp_uniform(), lane = threadIdx.x & 31;
-  uint32_t rank;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  uint32_t crank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  const uint32_t rank = crank & 1u;           // rank within the CTA pair
+  const uint32_t lead_rank = crank & ~1u;     // the pair leader's cluster rank
+  const int pp = static_cast<int>(crank >> 1);  // MC: pair index within the cluster
   const bool leader = rank == 0;
-  const int pair = static_cast<int>(blockIdx.x) >> 1, npairs = static_cast<int>(gridDim.x) >> 1;
+  const int pair = MC ? static_cast<int>(blockIdx.x) >> 2 : static_cast<int>(blockIdx.x) >> 1;
+  const int npairs = MC ? static_cast<int>(gridDim.x) >> 2 : static_cast<int>(gridDim.x) >> 1;
   const int tilesM2 = g.tilesM / 2;  // 256-row tiles
-  const int ntiles = tilesM2 * g.tilesN;
+  const int tilesNs = MC ? g.tilesN / 2 : g.tilesN;  // MC: pairs of N tiles per cluster work item
+  const int ntiles = tilesM2 * tilesNs;
   const int GROUP_M = g.group_m > 0 ? g.group_m : 8;
   auto tile_mn = [&](int x, int& tm, int& tn) {
-    const int per_group = GROUP_M * g.tilesN;
+    const int per_group = GROUP_M * tilesNs;
     const int first_m = (x / per_group) * GROUP_M;
     const int gsz = min(tilesM2 - first_m, GROUP_M);
     tm = first_m + (x % per_group) % gsz;
     tn = (x % per_group) / gsz;
+    if (MC) tn = 2 * tn + pp;
   };
   if (threadIdx.x == 0) {
     tc::tma_prefetch(&tma_a);
     tc::tma_prefetch(&tma_b);
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], 1);
+      tc::mbar_init(&empty[s], MC ? 2 : 1);
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
@@ -668,7 +691,7 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer (both CTAs): own A rows, own half of B
-    const uint32_t full_leader0 = peer_addr(tc::smem_u32(&full[0]), 0);
+    const uint32_t full_leader0 = peer_addr(tc::smem_u32(&full[0]), lead_rank);
     uint32_t it = 0;
     for (int x = pair; x < ntiles; x += npairs) {
       int tm, tn;
@@ -692,7 +715,13 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
         int c[MAXR];
 #pragma unroll
         for (int r = 0; r < MAXR; ++r) c[r] = am0[r] + ka[r];
-        tma_load_2sm(sA + s * A_BYTES, &tma_a, fb, g.a_rank, c);
+        if (MC) {  // half pp of this CTA's A rows, into this CTA and its twin in the other pair
+          c[1] += pp * (BM / 2);
+          tma_load_2sm_mc(sA + s * A_BYTES + pp * (A_BYTES / 2), &tma_a, fb,
+                          static_cast<uint16_t>((1u << crank) | (1u << (crank ^ 2u))), c);
+        } else {
+          tma_load_2sm(sA + s * A_BYTES, &tma_a, fb, g.a_rank, c);
+        }
 #pragma unroll
         for (int r = 0; r < MAXR; ++r) c[r] = bn0[r] + kb[r];
         if (B_MN) {  // MN-major B: this CTA's BN/2 columns as 32-column slabs (no layout pass)
@@ -757,17 +786,17 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
                 "r"(accum));
         }
         asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
-                     ::"r"(tc::smem_u32(&empty[s])), "h"(static_cast<uint16_t>(3)) : "memory");
+                     ::"r"(tc::smem_u32(&empty[s])), "h"(static_cast<uint16_t>(MC ? 0xF : 3)) : "memory");
       }
       asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
-                   ::"r"(tc::smem_u32(&tfull[acc])), "h"(static_cast<uint16_t>(3)) : "memory");
+                   ::"r"(tc::smem_u32(&tfull[acc])), "h"(static_cast<uint16_t>(3u << lead_rank)) : "memory");
     }
   } else if (warp >= 2) {
     // ---------------- epilogue warps (both CTAs): own 128 TMEM lanes
     const int q = warp & 3;
     const uint32_t stg = tc::smem_u32(stage_base) + static_cast<uint32_t>(warp - 2) * (32 * 33 * 4 + 32 * 8);
     const uint32_t rtab = stg + 32 * 33 * 4;
-    const uint32_t tempty_leader0 = peer_addr(tc::smem_u32(&tempty[0]), 0);
+    const uint32_t tempty_leader0 = peer_addr(tc::smem_u32(&tempty[0]), lead_rank);
     uint32_t tl = 0;
     for (int x = pair; x < ntiles; x += npairs, ++tl) {
       int tm, tn;
@@ -1000,6 +1029,7 @@ class TcRoutine final : public Routine {
        << "\"";
     if (packed_) os << ", \"K_padded\": " << Kp_;
     if (two_sm_) os << ", \"cta_pair\": \"tc_gemm_2sm<" << BN_ << "," << st2_ << ">: tcgen05.mma.cta_group::2 M256xN" << BN_ << (bf16_ ? "xK16 (bf16)" : "xK8") << "\"";
+    if (mc_) os << ", \"a_multicast\": \"clusters of 4 (two pairs on adjacent N tiles), A halves multicast\"";
     os << ", \"raster_group_m\": " << (kn_.group > 0 ? kn_.group : 8) << ", \"k_split\": " << kn_.split
        << ", \"from_config\": " << (kn_.set ? "true" : "false");
     os << "}";
@@ -1363,6 +1393,13 @@ class TcRoutine final : public Routine {
     st2_ = BN_ == 256 ? 6 : 8;
     smem2_ = static_cast<size_t>(st2_) * (BM + BN_ / 2) * BKE * 4 + 1024 + 256 + 4 * (32 * 33 * 4 + 32 * 8);
     two_sm_ = smem2_ <= 227 * 1024;
+    // clusters of two pairs sharing A by multicast (plain 2-D A views)
+    mc_ = two_sm_ && BN_ == 256 && tilesN_ % 2 == 0 && va_.rank == 2 && va_.row_dims.size() <= 1 && va_.box[1] == BM &&
+          std::getenv("MDHB_TC_MC") != nullptr;
+    if (mc_) {
+      vaH_ = va_;
+      vaH_.box[1] = BM / 2;
+    }
   }
   bool packed() const { return packed_; }
   // the knobs of the planner's default instance (for its canonical config)
@@ -1451,7 +1488,10 @@ class TcRoutine final : public Routine {
       MDHB_CUDA(cudaGetLastError());
       B = bt_;
     }
-    if (A != last_a_) encode(va_, A, &ma_), last_a_ = A;
+    if (A != last_a_) {
+      encode(mc_ ? vaH_ : va_, A, &ma_);
+      last_a_ = A;
+    }
     if (B != last_b_) {
       encode(vb_, B, &mb_);
       if (two_sm_) encode(vb2_, B, &mb2_);
@@ -1481,6 +1521,27 @@ class TcRoutine final : public Routine {
   }
 
   void launch_gemm(TcArgs& a, cudaStream_t s) {
+    if (two_sm_ && mc_) {
+      const int sms = sm_count(p_.opt.device);
+      const int clusters = std::min(sms / 4, (tilesM_ / 2) * (tilesN_ / 2));
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3(static_cast<unsigned>(4 * clusters));
+      lc.blockDim = dim3(64 + 32 * 4);
+      lc.dynamicSmemBytes = smem2_;
+      lc.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 4;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      void (*k)(const CUtensorMap, const CUtensorMap, TcArgs, int) =
+          bf16_ ? tc_gemm_2sm<256, 6, true, false, true> : tc_gemm_2sm<256, 6, false, false, true>;
+      MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2_)));
+      MDHB_CUDA(cudaLaunchKernelEx(&lc, k, ma_, mb2_, a, b_row_rank_));
+      return;
+    }
     if (two_sm_) {
       const int sms = sm_count(p_.opt.device);
       const int pairs = std::min(sms / 2, (tilesM_ / 2) * tilesN_);
@@ -1573,6 +1634,8 @@ class TcRoutine final : public Routine {
   bool packed_ = false;
   int64_t Kp_ = 0, c_run_ = 1;
   bool two_sm_ = false;
+  bool mc_ = false;  // CTA-pair clusters of 4 sharing A by TMA multicast
+  View vaH_;
   bool bf16_ = false, a_rowfast_ = false, b_rowfast_ = false;
   struct PlainPack {
     int kind = 0;  // 0 table gather, 1 vectorised convert (k unit-stride), 2 64x64 transpose (rows unit-stride)
