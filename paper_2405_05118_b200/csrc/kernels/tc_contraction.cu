@@ -1029,7 +1029,7 @@ class TcRoutine final : public Routine {
        << "\"";
     if (packed_) os << ", \"K_padded\": " << Kp_;
     if (two_sm_) os << ", \"cta_pair\": \"tc_gemm_2sm<" << BN_ << "," << st2_ << ">: tcgen05.mma.cta_group::2 M256xN" << BN_ << (bf16_ ? "xK16 (bf16)" : "xK8") << "\"";
-    if (mc_) os << ", \"a_multicast\": \"clusters of 4 (two pairs on adjacent N tiles), A halves multicast\"";
+    if (mc_) os << ", \"a_multicast\": \"clusters of 4 (two pairs on adjacent N tiles), A halves multicast\", \"clusters\": " << mc_clusters_;
     os << ", \"raster_group_m\": " << (kn_.group > 0 ? kn_.group : 8) << ", \"k_split\": " << kn_.split
        << ", \"from_config\": " << (kn_.set ? "true" : "false");
     os << "}";
@@ -1522,10 +1522,7 @@ class TcRoutine final : public Routine {
 
   void launch_gemm(TcArgs& a, cudaStream_t s) {
     if (two_sm_ && mc_) {
-      const int sms = sm_count(p_.opt.device);
-      const int clusters = std::min(sms / 4, (tilesM_ / 2) * (tilesN_ / 2));
       cudaLaunchConfig_t lc = {};
-      lc.gridDim = dim3(static_cast<unsigned>(4 * clusters));
       lc.blockDim = dim3(64 + 32 * 4);
       lc.dynamicSmemBytes = smem2_;
       lc.stream = s;
@@ -1539,6 +1536,13 @@ class TcRoutine final : public Routine {
       void (*k)(const CUtensorMap, const CUtensorMap, TcArgs, int) =
           bf16_ ? tc_gemm_2sm<256, 6, true, false, true> : tc_gemm_2sm<256, 6, false, false, true>;
       MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2_)));
+      if (!mc_clusters_) {  // co-resident clusters of 4 (GPC-limited, fewer than SMs / 4)
+        lc.gridDim = dim3(4 * 64);
+        MDHB_CUDA(cudaOccupancyMaxActiveClusters(&mc_clusters_, reinterpret_cast<const void*>(k), &lc));
+        mc_clusters_ = std::max(1, mc_clusters_);
+      }
+      const int clusters = std::min(mc_clusters_, (tilesM_ / 2) * (tilesN_ / 2));
+      lc.gridDim = dim3(static_cast<unsigned>(4 * clusters));
       MDHB_CUDA(cudaLaunchKernelEx(&lc, k, ma_, mb2_, a, b_row_rank_));
       return;
     }
@@ -1635,6 +1639,7 @@ class TcRoutine final : public Routine {
   int64_t Kp_ = 0, c_run_ = 1;
   bool two_sm_ = false;
   bool mc_ = false;  // CTA-pair clusters of 4 sharing A by TMA multicast
+  int mc_clusters_ = 0;
   View vaH_;
   bool bf16_ = false, a_rowfast_ = false, b_rowfast_ = false;
   struct PlainPack {

@@ -1,6 +1,5 @@
-for v in "MDHB_SKINNY_NW=64" "MDHB_SKINNY_NW=128" "MDHB_SKINNY_NW=128 MDHB_SKINNY_CS=16"; do
-  echo "T $v"; env $v timeout 300 python -m pytest tests/test_gpu_contraction.py -m gpu -q -k "resnet or skinny or fc" 2>&1 | tail -1
-done
-for v in "" "MDHB_SKINNY_NW=64" "MDHB_SKINNY_NW=128" "MDHB_SKINNY_NW=64 MDHB_SKINNY_CS=16" "MDHB_SKINNY_NW=128 MDHB_SKINNY_CS=16" "MDHB_SKINNY_NW=128 MDHB_SKINNY_CS=4" ""; do
-  echo "FC $v"; env $v timeout 120 python tools/graph_time.py matmul_resnet_fc 400 2>&1 | tail -1 | cut -c1-120
+MDHB_TC_MC=1 timeout 300 python -m pytest tests/test_gpu_tc.py -m gpu -q -x -k "matmul" 2>&1 | grep -E "passed|failed|Error|^E" | head -8
+for v in "" "MDHB_TC_MC=1" "" "MDHB_TC_MC=1"; do
+  echo "M $v"; env $v timeout 120 python tools/graph_time.py matmul_fp32:tf32 10 2>&1 | tail -1 | cut -c1-100
+  echo "Mb $v"; env $v timeout 120 python tools/graph_time.py matmul_fp32:bf16 10 2>&1 | tail -1 | cut -c1-100
 done
