@@ -881,7 +881,7 @@ struct RankCombine : Routine {
   std::string describe() const override {
     std::string d = inner->describe();
     if (!d.empty() && d.back() == '}') d.pop_back();
-    return d + ", " + shard_desc + "}";
+    return d + ", " + shard_desc + ", \"nccl_allreduce\": " + (comm ? "true" : "false") + "}";
   }
   void launch(const void* const* d_in, void* const* d_out, cudaStream_t s) override {
     inner->launch(d_in, d_out, s);
@@ -934,7 +934,7 @@ std::unique_ptr<Routine> wrap_rank(std::unique_ptr<Routine> inner, const Problem
   auto r = std::make_unique<RankCombine>();
   r->inner = std::move(inner);
   r->shard_desc = desc;
-  if (pw && world > 1 && nccl_id) {
+  if (pw && nccl_id) {  // (a 1-rank communicator all-reduces as the identity: the path runs on one GPU too)
     r->op = nccl_op(fold);
     if (r->op < 0) fail("Unsupported", "NCCL has no reduction for this combine operator");
     auto& n = need_nccl();

@@ -254,3 +254,20 @@ def test_world2_rank_plans_run_the_kernels(name, sizes, split_dim):
     for p in procs:
         p.join(60)
     assert ok and all(p.exitcode == 0 for p in procs)
+
+
+@pytest.mark.gpu
+def test_rank_plan_nccl_allreduce_runs():
+    """The NCCL path of a point-wise split (dlopen'd libnccl, ncclCommInitRank,
+    in-plan ncclAllReduce(ncclMax) on packed int64 keys): on one GPU a 1-rank
+    communicator all-reduces as the identity -- the call path is real."""
+    from paper_2405_05118_b200 import mdh
+    nq, nr = 256, 8192
+    j = spec("prl_max", [nq, nr])
+    ins = prl_inputs(nq, nr, 17)
+    p = mdh.rank_plan(j, 1, 0, device=0, nccl_id=mdh.nccl_unique_id(), split_dim=2)
+    t = p.describe()["template"]
+    assert t["nccl_allreduce"] and t["shard"]["split_kind"] == "pw", t
+    (got,) = run_device(p, ins)
+    ((want, _),) = mo.execute(mo.Computation.from_json(j), ins)
+    assert np.array_equal(got, want)
