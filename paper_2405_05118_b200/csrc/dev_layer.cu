@@ -524,8 +524,12 @@ int mdh_b200_mplan_create(const char* comp_json, const char* asm_model, const ch
       if (cfg) sc = mdhb::shard_config(config_json, mp->e, mdhb::parse_md_hom(sj), mp->m, mp->split);
       o.device = mp->dev[static_cast<size_t>(g)];
       mdh_b200_plan* p = nullptr;
-      if (mdh_b200_plan_create(sj.c_str(), mp->m.name == "MultiB200" && !cfg ? "B200" : asm_model ? asm_model : "B200",
-                               cfg ? sc.c_str() : nullptr, &o, &p))
+      // shard plans: the configuration's own ASM when one is given (its GPU
+      // parts set to 1), else the single-device B200 ASM for a MultiB200 split
+      const std::string shard_asm = cfg ? (asm_model ? std::string(asm_model) : mp->m.name)
+                                        : (mp->m.name == "MultiB200" ? std::string("B200")
+                                                                     : (asm_model ? std::string(asm_model) : std::string("B200")));
+      if (mdh_b200_plan_create(sj.c_str(), shard_asm.c_str(), cfg ? sc.c_str() : nullptr, &o, &p))
         mdhb::fail("Internal", std::string("shard ") + std::to_string(g) + ": " + mdh_b200_last_error());
       mp->shard.push_back(p);
       cudaStream_t s;
