@@ -99,3 +99,32 @@ def test_world2_cpp_split_recombines_exactly(name, sizes, split_dim):
     for p in procs:
         p.join(60)
     assert all(ok) and all(p.exitcode == 0 for p in procs), ok
+
+
+def multib200_config(sizes, dim, parts):
+    """A MultiB200 configuration (ASM layers HM, DM, SM, RM, GPU, SMX, WRP, CC;
+    MDH layer l on ASM layer l): everything on HM except `parts` GPU-layer
+    parts of dimension `dim` (0-based)."""
+    L = 8
+    rows = [[1] * len(sizes) for _ in range(L)]
+    rows[0] = list(sizes)
+    rows[0][dim] //= parts
+    rows[4][dim] = parts
+    return json.dumps({"num_parts": rows})
+
+
+@pytest.mark.parametrize("dim", [0, 1])
+def test_split_from_a_multib200_configuration(dim):
+    """The GPU-layer parts of a MultiB200 configuration choose the split
+    (the reference's MultiGPU ASM, asm_model.cpp:36-37), and the shard's
+    configuration keeps every other part with GPU parts 1."""
+    from paper_2405_05118_b200 import mdh
+    j = spec("matvec_fp32", [64, 128])
+    cfg = multib200_config(j["sizes"], dim, 4)
+    assert mdh.validate_config(j, "MultiB200", cfg) == ""
+    for r in range(4):
+        sh = mdh.shard_spec(j, 4, r, config=cfg)
+        assert sh["shard"]["split_dim"] == dim + 1
+        assert sh["computation"]["sizes"][dim] == j["sizes"][dim] // 4
+        gpu_row = sh["config"]["num_parts"][4]
+        assert all(x == 1 for x in gpu_row)

@@ -271,3 +271,21 @@ def test_rank_plan_nccl_allreduce_runs():
     (got,) = run_device(p, ins)
     ((want, _),) = mo.execute(mo.Computation.from_json(j), ins)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim", [0, 1])
+def test_mplan_split_from_a_multib200_configuration(dim):
+    """A MultiB200 configuration's GPU-layer parts drive the split (the shard
+    plans run the configuration with GPU parts 1), recombined exactly."""
+    from paper_2405_05118_b200 import mdh
+    from test_dev_layer_dist import multib200_config
+    j = spec("matvec_fp32", [256, 512])
+    comp = mo.Computation.from_json(j)
+    ins = exact_inputs(comp, 8)
+    mp = mdh.MultiPlan(j, 2, device_ids=[0, 0], asm="MultiB200", config=multib200_config(j["sizes"], dim, 2))
+    d = mp.describe()
+    assert d["split_dim"] == dim + 1 and d["split_kind"] == ("cc" if dim == 0 else "pw"), d
+    (got,) = mp.run_host(ins)
+    ((want, _),) = mo.execute(comp, ins)
+    assert np.array_equal(got.astype(np.float64), want)
