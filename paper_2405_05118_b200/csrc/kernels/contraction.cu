@@ -49,6 +49,7 @@ struct GemmArgs {
   const int32_t *ak, *bk;                // per k
   int K, tilesM, tilesN;
   int sak, sbk;  // per-k strides inside one k-tile (sgemm_pipe: ak[k0 + j] = ak[k0] + j * sak)
+  int klin;      // sgemm_pipe: ak[k] = k * sak and bk[k] = k * sbk for EVERY k -- no per-k-tile table read
 };
 
 struct GemvArgs {
@@ -746,8 +747,10 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 512 / ((BM / 8) * (BN / 8
   const int nk = g.K / BKT;
   auto issue = [&](int kt) {
     const int s = kt % ST, k0 = kt * BKT;
-    const float* abase = A + __ldg(g.ak + k0);
-    const float* bbase = B + __ldg(g.bk + k0);
+    // the k-tile's base: linear in k0 when the offsets are globally affine,
+    // else one table read (its latency sits right before the copies)
+    const float* abase = A + (g.klin ? static_cast<int64_t>(k0) * g.sak : __ldg(g.ak + k0));
+    const float* bbase = B + (g.klin ? static_cast<int64_t>(k0) * g.sbk : __ldg(g.bk + k0));
     const uint32_t as = static_cast<uint32_t>(__cvta_generic_to_shared(As + s * BKT * PA + a_dst0));
     const uint32_t bs = static_cast<uint32_t>(__cvta_generic_to_shared(Bs + s * BKT * PB + b_dst0));
 #pragma unroll
@@ -1113,6 +1116,12 @@ class GemmRoutine final : public Routine {
         }
       }
       tile_affine_ = pbk_ > 0;
+      auto lin = [&](const std::vector<int64_t>& v, int stride) {
+        for (size_t k = 0; k < v.size(); ++k)
+          if (v[k] != static_cast<int64_t>(k) * stride) return false;
+        return true;
+      };
+      klin_ = tile_affine_ && lin(ak, psak_) && lin(bk, psbk_) && !std::getenv("MDHB_SGEMM_NO_KLIN");
     }
     tables(tAm, tCm, tBn, tCn, am, cm, bn, cn, ak, bk);
     if (apack_m_) {
@@ -1275,7 +1284,7 @@ class GemmRoutine final : public Routine {
       B = static_cast<const float*>(bp_);
     }
     GemmArgs a{A, B, C, tab_[0], tab_[1], tab_[2], tab_[3], tab_[4], tab_[5], tab_[6], tab_[7], tab_[8], tab_[9],
-               static_cast<int>(K_), tilesM_, tilesN_, psak_, psbk_};
+               static_cast<int>(K_), tilesM_, tilesN_, psak_, psbk_, klin_ ? 1 : 0};
     mark_begin(s);
     dispatch(a, s);
     mark_end(s);
@@ -1398,6 +1407,7 @@ class GemmRoutine final : public Routine {
   void* ap_ = nullptr;
   int64_t apack_m_ = 0;
   int psak_ = 0, psbk_ = 0, pbk_ = 0;
+  bool klin_ = false;
   float* part_ = nullptr;
   void* blob_ = nullptr;
 
