@@ -808,23 +808,16 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 512 / ((BM / 8) * (BN / 8
     }
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
-  // every C offset is loaded (read-only path, all in flight together) before
-  // the first store: the tables could alias C as far as the compiler knows,
-  // so loads interleaved with the stores would serialise on their latency
-  float* __restrict__ C = g.C + __ldg(g.tCm + tm) + __ldg(g.tCn + tn);
-  int cmr[8], cnc[2];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) cmr[i] = __ldg(g.cm + (i < 4 ? ty * 4 + i : BM / 2 + ty * 4 + (i - 4)));
-#pragma unroll
-  for (int h = 0; h < 2; ++h) cnc[h] = CVEC ? __ldg(g.cn + h * (BN / 2) + tx * 4) : 0;
+  float* __restrict__ C = g.C + g.tCm[tm] + g.tCn[tn];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    float* crow = C + cmr[i];
+    const int r = i < 4 ? ty * 4 + i : BM / 2 + ty * 4 + (i - 4);
+    float* crow = C + g.cm[r];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int c = h * (BN / 2) + tx * 4;
       if (CVEC) {
-        *reinterpret_cast<float4*>(crow + cnc[h]) =
+        *reinterpret_cast<float4*>(crow + g.cn[c]) =
             make_float4(acc[i][h * 4 + 0], acc[i][h * 4 + 1], acc[i][h * 4 + 2], acc[i][h * 4 + 3]);
       } else {
 #pragma unroll
