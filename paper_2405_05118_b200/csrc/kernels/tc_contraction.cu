@@ -627,18 +627,28 @@ __device__ __forceinline__ void tma_load_2sm_mc(void* dst, const void* tmap, uin
 // from L2 once per cluster instead of once per pair.  A stage is reused only
 // after BOTH pairs' MMAs released it (empty[s] counts two commits, each
 // multicast to all four CTAs).
-template <int BN, int STAGES, bool BF16 = false, bool B_MN = false, bool MC = false>
+//
+// WIDE: the pair's tile is 256 rows x TWO adjacent N tiles (2 * BN = 512
+// columns): each k-step lands A once for both halves (48 KB per CTA per
+// 32-deep k-step for 2^21 MACs instead of 32 KB for 2^20), so the operand
+// bytes crossing from L2 per MAC drop by a quarter.  The 512-column
+// accumulator fills TMEM, so it is single-buffered: the epilogue drains half
+// 0 then half 1, releasing each on its own tempty barrier, and the next
+// tile's first MMAs into a half wait only for that half.
+template <int BN, int STAGES, bool BF16 = false, bool B_MN = false, bool MC = false, bool WIDE = false>
 __global__ void __launch_bounds__(64 + 32 * 4, 1)
     tc_gemm_2sm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, TcArgs g, int b_row_rank) {
   constexpr int EPW = 4;
+  constexpr int NH = WIDE ? 2 : 1;  // N tiles per pair tile
+  static_assert(!WIDE || (BN == 256 && !MC && !B_MN), "WIDE: K-major B, BN 256, no multicast");
   constexpr uint32_t A_BYTES = BM * BKE * 4;
-  constexpr uint32_t B_BYTES = (BN / 2) * BKE * 4;  // this CTA's half of the B tile
-  constexpr uint32_t TMEM_COLS = 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+  constexpr uint32_t B_BYTES = (BN / 2) * BKE * 4;  // this CTA's half of one N tile of B
+  constexpr uint32_t TMEM_COLS = WIDE ? 512 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * NH * B_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -654,7 +664,7 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
   const int pair = MC ? static_cast<int>(blockIdx.x) >> 2 : static_cast<int>(blockIdx.x) >> 1;
   const int npairs = MC ? static_cast<int>(gridDim.x) >> 2 : static_cast<int>(gridDim.x) >> 1;
   const int tilesM2 = g.tilesM / 2;  // 256-row tiles
-  const int tilesNs = MC ? g.tilesN / 2 : g.tilesN;  // MC: pairs of N tiles per cluster work item
+  const int tilesNs = MC || WIDE ? g.tilesN / 2 : g.tilesN;  // MC: pairs of N tiles per cluster work item
   const int ntiles = tilesM2 * tilesNs;
   const int GROUP_M = g.group_m > 0 ? g.group_m : 8;
   auto tile_mn = [&](int x, int& tm, int& tn) {
@@ -664,6 +674,7 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
     tm = first_m + (x % per_group) % gsz;
     tn = (x % per_group) / gsz;
     if (MC) tn = 2 * tn + pp;
+    if (WIDE) tn = 2 * tn;  // first of the tile's two N tiles
   };
   if (threadIdx.x == 0) {
     tc::tma_prefetch(&tma_a);
@@ -697,11 +708,12 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
       int tm, tn;
       tile_mn(x, tm, tn);
       const int ta = 2 * tm + static_cast<int>(rank);
-      int am0[MAXR], bn0[MAXR], ka[MAXR], kb[MAXR], dig[MAXKD];
+      int am0[MAXR], bn0[MAXR], bn1[MAXR], ka[MAXR], kb[MAXR], dig[MAXKD];
 #pragma unroll
       for (int r = 0; r < MAXR; ++r) {
         am0[r] = g.a_mc[ta * MAXR + r];
         bn0[r] = g.b_nc[tn * MAXR + r] + (r == b_row_rank ? static_cast<int>(rank) * (BN / 2) : 0);
+        if (WIDE) bn1[r] = g.b_nc[(tn + 1) * MAXR + r] + (r == b_row_rank ? static_cast<int>(rank) * (BN / 2) : 0);
         ka[r] = g.ka0[r];
         kb[r] = g.kb0[r];
       }
@@ -710,7 +722,7 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
       for (int kt = 0; kt < g.nk; ++kt, ++it) {
         const uint32_t s = it % STAGES;
         if (it >= STAGES) tc::mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
-        if (leader) tc::mbar_arrive_expect_tx(&full[s], 2 * (A_BYTES + B_BYTES));
+        if (leader) tc::mbar_arrive_expect_tx(&full[s], 2 * (A_BYTES + NH * B_BYTES));
         const uint32_t fb = full_leader0 + s * 8;
         int c[MAXR];
 #pragma unroll
@@ -734,7 +746,12 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
             tma_load_2sm(sB + s * B_BYTES + j * (BKE * 128), &tma_b, fb, g.b_rank, cj);
           }
         } else {
-          tma_load_2sm(sB + s * B_BYTES, &tma_b, fb, g.b_rank, c);
+          tma_load_2sm(sB + s * NH * B_BYTES, &tma_b, fb, g.b_rank, c);
+          if (WIDE) {
+#pragma unroll
+            for (int r = 0; r < MAXR; ++r) c[r] = bn1[r] + kb[r];
+            tma_load_2sm(sB + s * NH * B_BYTES + B_BYTES, &tma_b, fb, g.b_rank, c);
+          }
         }
         for (int q = g.nkd - 1; q >= 0; --q) {
           if (++dig[q] < g.kext[q]) {
@@ -759,18 +776,24 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
     constexpr uint32_t idesc = tc::instr_desc(BF16 ? 1 : 2, 0, B_MN ? 1 : 0, 2 * BM, BN);
     uint32_t it = 0, tl = 0;
     for (int x = pair; x < ntiles; x += npairs, ++tl) {
-      const uint32_t acc = tl & 1;
-      if (tl >= 2) tc::mbar_wait_warp(&tempty[acc], ((tl / 2) - 1) & 1);
+      const uint32_t acc = WIDE ? 0u : tl & 1;
+      if (!WIDE && tl >= 2) tc::mbar_wait_warp(&tempty[acc], ((tl / 2) - 1) & 1);
       tc::tc_fence_after();
-      const uint32_t dtm = tmem + acc * BN;
       for (int kt = 0; kt < g.nk; ++kt, ++it) {
         const uint32_t s = it % STAGES;
         tc::mbar_wait_warp(&full[s], (it / STAGES) & 1);
         tc::tc_fence_after();
         const uint32_t sa = tc::smem_u32(sA + s * A_BYTES);
-        const uint32_t sb = tc::smem_u32(sB + s * B_BYTES);
 #pragma unroll
-        for (int k = 0; k < BKE / 8; ++k) {
+        for (int k = 0; k < BKE / 8; ++k)
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          if (WIDE && kt == 0 && k == 0 && tl >= 1) {  // this half drained by the previous tile's epilogue
+            tc::mbar_wait_warp(&tempty[h], (tl - 1) & 1);
+            tc::tc_fence_after();
+          }
+          const uint32_t dtm = tmem + acc * BN + h * BN;
+          const uint32_t sb = tc::smem_u32(sB + (s * NH + h) * B_BYTES);
           const uint64_t da = tc::sw128_desc(sa + k * 32, 16, 1024);
           const uint64_t db = B_MN ? tc::umma_desc(sb + k * 1024, BKE * 128, 512, 1) : tc::sw128_desc(sb + k * 32, 16, 1024);
           const uint32_t accum = (kt | k) != 0 ? 1u : 0u;
@@ -802,15 +825,19 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
       int tm, tn;
       tile_mn(x, tm, tn);
       const int ta = 2 * tm + static_cast<int>(rank);
-      const uint32_t acc = tl & 1;
-      const int64_t rowoff = static_cast<int64_t>(g.tCm[ta]) + g.cm[q * 32 + lane] + g.tCn[tn];
-      asm volatile("st.shared.s64 [%0], %1;" ::"r"(rtab + lane * 8), "l"(rowoff) : "memory");
-      tc::mbar_wait(&tfull[acc], (tl / 2) & 1);
+      const uint32_t acc = WIDE ? 0u : tl & 1;
+      tc::mbar_wait(&tfull[acc], (WIDE ? tl : tl / 2) & 1);
       tc::tc_fence_after();
+#pragma unroll 1
+      for (int h = 0; h < NH; ++h) {
+      const int64_t rowoff = static_cast<int64_t>(g.tCm[ta]) + g.cm[q * 32 + lane] + g.tCn[tn + h];
+      __syncwarp();
+      asm volatile("st.shared.s64 [%0], %1;" ::"r"(rtab + lane * 8), "l"(rowoff) : "memory");
+      __syncwarp();
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t rv[32];
-        tc::tmem_ld32(tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c0), rv);
+        tc::tmem_ld32(tmem + (acc + h) * BN + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c0), rv);
 #pragma unroll
         for (int j = 0; j < 32; ++j)
           asm volatile("st.shared.b32 [%0], %1;" ::"r"(stg + (lane * 33 + j) * 4), "r"(rv[j]) : "memory");
@@ -826,10 +853,13 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
         }
         __syncwarp();
       }
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty_leader0 + acc * 8) : "memory");
+      if (WIDE || h == NH - 1) {
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty_leader0 + (acc + h) * 8) : "memory");
+      }
+      }
     }
   }
   tc::tc_fence_before();
@@ -1017,7 +1047,7 @@ class TcRoutine final : public Routine {
   double bytes() const override { return static_cast<double>(p_.in_bytes + p_.out_bytes); }
   std::string describe() const override {
     std::ostringstream os;
- os << "{\"kernel\": \"" << (two_sm_ ? "tc_gemm_2sm<" : pers_ ? "tc_gemm_pers<" : "tc_gemm_tf32<") << BN_ << ","
+ os << "{\"kernel\": \"" << (two_sm_ ? "tc_gemm_2sm<" : pers_ ? "tc_gemm_pers<" : "tc_gemm_tf32<") << (wide_ ? 2 * BN_ : BN_) << ","
        << (two_sm_ ? st2_ : pers_ ? pstages_ : stages_) << ","
        << (va_.mn ? "A_MN" : "A_K") << "," << (vb_.mn ? "B_MN" : "B_K") << (rb_ && pers_ ? ",B_RESIDENT" : "")
        << ">\", \"math\": \"" << (bf16_ ? "bf16" : "tf32") << "\", \"M\": " << M_ << ", \"N\": " << N_ << ", \"K\": " << K_
@@ -1029,6 +1059,7 @@ class TcRoutine final : public Routine {
        << "\"";
     if (packed_) os << ", \"K_padded\": " << Kp_;
     if (two_sm_) os << ", \"cta_pair\": \"tc_gemm_2sm<" << BN_ << "," << st2_ << ">: tcgen05.mma.cta_group::2 M256xN" << BN_ << (bf16_ ? "xK16 (bf16)" : "xK8") << "\"";
+    if (wide_) os << ", \"wide\": \"256 x " << 2 * BN_ << " pair tiles: two N" << BN_ << " MMAs per k-step share one A landing, TMEM 512 columns single-buffered\"";
     if (mc_) os << ", \"a_multicast\": \"clusters of 4 (two pairs on adjacent N tiles), A halves multicast\", \"clusters\": " << mc_clusters_;
     os << ", \"raster_group_m\": " << (kn_.group > 0 ? kn_.group : 8) << ", \"k_split\": " << kn_.split
        << ", \"from_config\": " << (kn_.set ? "true" : "false");
@@ -1400,6 +1431,14 @@ class TcRoutine final : public Routine {
       vaH_ = va_;
       vaH_.box[1] = BM / 2;
     }
+    // 256 x 512 pair tiles (two adjacent N tiles, one A landing per k-step)
+    wide_ = two_sm_ && !mc_ && BN_ == 256 && tilesN_ % 2 == 0 && std::getenv("MDHB_TC_WIDE") != nullptr;
+    if (wide_) {
+      st2_ = 4;
+      smem2_ = static_cast<size_t>(st2_) * (BM + BN_) * BKE * 4 + 1024 + 256 + 4 * (32 * 33 * 4 + 32 * 8);
+      if (smem2_ > 227 * 1024) wide_ = false;
+    }
+    if (!wide_ && two_sm_) smem2_ = static_cast<size_t>(st2_) * (BM + BN_ / 2) * BKE * 4 + 1024 + 256 + 4 * (32 * 33 * 4 + 32 * 8);
   }
   bool packed() const { return packed_; }
   // the knobs of the planner's default instance (for its canonical config)
@@ -1548,7 +1587,7 @@ class TcRoutine final : public Routine {
     }
     if (two_sm_) {
       const int sms = sm_count(p_.opt.device);
-      const int pairs = std::min(sms / 2, (tilesM_ / 2) * tilesN_);
+      const int pairs = std::min(sms / 2, (tilesM_ / 2) * (wide_ ? tilesN_ / 2 : tilesN_));
       cudaLaunchConfig_t lc = {};
       lc.gridDim = dim3(static_cast<unsigned>(2 * pairs));
       lc.blockDim = dim3(64 + 32 * 4);
@@ -1562,7 +1601,8 @@ class TcRoutine final : public Routine {
       lc.attrs = at;
       lc.numAttrs = 1;
       void (*k)(const CUtensorMap, const CUtensorMap, TcArgs, int) =
-          vb_.mn ? tc_gemm_2sm<256, 6, false, true>
+          wide_ ? (bf16_ ? tc_gemm_2sm<256, 4, true, false, false, true> : tc_gemm_2sm<256, 4, false, false, false, true>)
+          : vb_.mn ? tc_gemm_2sm<256, 6, false, true>
           : bf16_ ? (BN_ == 256 ? tc_gemm_2sm<256, 6, true> : tc_gemm_2sm<128, 8, true>)
                   : (BN_ == 256 ? tc_gemm_2sm<256, 6> : tc_gemm_2sm<128, 8>);
       MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2_)));
@@ -1639,6 +1679,7 @@ class TcRoutine final : public Routine {
   int64_t Kp_ = 0, c_run_ = 1;
   bool two_sm_ = false;
   bool mc_ = false;  // CTA-pair clusters of 4 sharing A by TMA multicast
+  bool wide_ = false;  // CTA-pair tiles of 256 x 2 BN (two N tiles per A landing)
   int mc_clusters_ = 0;
   View vaH_;
   bool bf16_ = false, a_rowfast_ = false, b_rowfast_ = false;
