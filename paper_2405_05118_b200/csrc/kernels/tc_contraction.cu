@@ -1051,10 +1051,10 @@ class TcRoutine final : public Routine {
        << (two_sm_ ? st2_ : pers_ ? pstages_ : stages_) << ","
        << (va_.mn ? "A_MN" : "A_K") << "," << (vb_.mn ? "B_MN" : "B_K") << (rb_ && pers_ ? ",B_RESIDENT" : "")
        << ">\", \"math\": \"" << (bf16_ ? "bf16" : "tf32") << "\", \"M\": " << M_ << ", \"N\": " << N_ << ", \"K\": " << K_
-       << ", \"BM\": " << BM << ", \"BN\": " << BN_ << ", \"BK\": " << BKE << ", \"stages\": " << stages_
+       << ", \"BM\": " << BM << ", \"BN\": " << (wide_ ? 2 * BN_ : BN_) << ", \"BK\": " << BKE << ", \"stages\": " << stages_
        << ", \"umma\": \"tcgen05.mma.cta_group::1.kind::" << (bf16_ ? "f16 (bf16) M128xN" : "tf32 M128xN") << BN_
        << (bf16_ ? "xK16" : "xK8") << "\", \"tiles\": "
-       << static_cast<int64_t>(tilesM_) * tilesN_ << ", \"tmem_cols\": " << BN_
+       << static_cast<int64_t>(tilesM_) * tilesN_ << ", \"tmem_cols\": " << (wide_ ? 2 * BN_ : BN_)
        << ", \"b_layout\": \"" << (packed_ ? "packed K-major (pack_kmajor pre-pass, both operands)" : transposeB_ ? "K-major copy (layout_de [2,1] pre-pass)" : (vb_.mn ? "MN-major" : "K-major"))
        << "\"";
     if (packed_) os << ", \"K_padded\": " << Kp_;
@@ -1242,6 +1242,7 @@ class TcRoutine final : public Routine {
     }
     decide_2sm();
     if (kn_.set && (kn_.form == 2) != two_sm_) return *why = "CTA-pair instance unavailable for this tile", false;
+    if (kn_.set && (kn_.bn == 512) != wide_) return *why = "256 x 512 CTA-pair tile unavailable (K-major B, N % 512)", false;
     if (!pers_ && BN_ == 192) return *why = "no one-CTA-per-tile instance with BN 192", false;
     if (!pers_ && bf16_) return *why = "no one-CTA-per-tile kind::f16 instance", false;
     args_.group_m = kn_.group;
@@ -1431,8 +1432,11 @@ class TcRoutine final : public Routine {
       vaH_ = va_;
       vaH_.box[1] = BM / 2;
     }
-    // 256 x 512 pair tiles (two adjacent N tiles, one A landing per k-step)
-    wide_ = two_sm_ && !mc_ && BN_ == 256 && tilesN_ % 2 == 0 && std::getenv("MDHB_TC_WIDE") != nullptr;
+    // 256 x 512 pair tiles (two adjacent N tiles, one A landing per k-step):
+    // the default wherever they divide N; a configuration picks it by RM
+    // parts of N = 512
+    wide_ = two_sm_ && !mc_ && BN_ == 256 && tilesN_ % 2 == 0 &&
+            (kn_.set ? kn_.bn == 512 : std::getenv("MDHB_TC_NARROW") == nullptr);
     if (wide_) {
       st2_ = 4;
       smem2_ = static_cast<size_t>(st2_) * (BM + BN_) * BKE * 4 + 1024 + 256 + 4 * (32 * 33 * 4 + 32 * 8);
@@ -1445,7 +1449,7 @@ class TcRoutine final : public Routine {
   bool knobs_default(TcKnobs* k) const {
     k->set = true;
     k->form = two_sm_ ? 2 : pers_ ? 1 : 0;
-    k->bn = BN_;
+    k->bn = wide_ ? 2 * BN_ : BN_;
     k->group = k->form == 0 ? (two_sm_ ? tilesM_ / 2 : tilesM_) : 8;
     if (k->form != 0 && (two_sm_ ? tilesM_ / 2 : tilesM_) % 8) return false;
     k->split = 1;
@@ -1731,7 +1735,8 @@ TcKnobs tc_knobs(const Problem& p, const Groups& g, const Config& c) {
   const int64_t tm = below(dm_);
   if (tm != BM && tm != 2 * BM) fail("Unsupported", "tensor-core tile rows (WRP x CC x SM x RM of M) must be 128 or 256");
   k.bn = static_cast<int>(below(dn));
-  if (k.bn != 64 && k.bn != 128 && k.bn != 192 && k.bn != 256) fail("Unsupported", "tensor-core N tile must be 64, 128, 192 or 256");
+  if (k.bn != 64 && k.bn != 128 && k.bn != 192 && k.bn != 256 && !(k.bn == 512 && tm == 2 * BM))
+    fail("Unsupported", "tensor-core N tile must be 64, 128, 192 or 256 (512 for CTA-pair tiles)");
   if (below(dk) != k_tile(p)) fail("Unsupported", "tensor-core k-tile (SM x ... of K) must be one 128-byte row");
   if (at(dm, dn) != 1) fail("Unsupported", "tensor-core template rasters groups along M only (DM parts of N must be 1)");
   k.split = static_cast<int>(at(smx, dk));
@@ -1789,9 +1794,10 @@ std::vector<Config> tc_space(const Problem& p, const Groups& g) {
   if (K % ek) return out;
   const bool bf16 = p.opt.math == Math::BF16, mn = b_mn_major(g);
   for (int form = 0; form < 3; ++form)
-    for (int bn : {256, 192, 128, 64}) {
+    for (int bn : {512, 256, 192, 128, 64}) {
       if (N % bn) continue;
-      if ((form == 0 && (bn == 192 || bf16)) || (form == 2 && bn != 256 && bn != 128)) continue;
+      if ((form == 0 && (bn == 192 || bf16)) || (form == 2 && bn != 512 && bn != 256 && bn != 128)) continue;
+      if (bn == 512 && form != 2) continue;
       const int64_t tm = form == 2 ? 2 * BM : BM;
       if (M % tm) continue;
       const int64_t rows = M / tm;
@@ -1845,7 +1851,7 @@ std::unique_ptr<Routine> make_tc_contraction(const Problem& p, const Groups& g, 
   if (cfg && gemm_shaped(g)) kn = tc_knobs(p, g, *cfg);  // Unsupported when outside the template
   std::vector<int> menu = {256, 192, 128, 64};
   if (const char* f = std::getenv("MDHB_TC_BN")) menu = {std::atoi(f)};
-  if (kn.set) menu = {kn.bn};
+  if (kn.set) menu = {kn.bn == 512 ? 256 : kn.bn};  // 512: two 256-column N tiles per CTA-pair tile
   std::unique_ptr<TcRoutine> best;
   int64_t best_score = -1;
   for (int bn : menu) {

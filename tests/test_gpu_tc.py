@@ -38,8 +38,10 @@ def test_tf32_exact_mode_bit_identical(name, sizes, kernel):
     plan = plan_tf32(j)
     d = plan.describe()
     kern = d["template"]["kernel"]
+    # a 256-column tile may run as half of a 256 x 512 CTA-pair tile
     assert d["family"] == "contraction" and any(kern.startswith(kernel.replace("tc_gemm_tf32", v))
-                                                for v in ("tc_gemm_tf32", "tc_gemm_pers", "tc_gemm_2sm")), d
+                                                for v in ("tc_gemm_tf32", "tc_gemm_pers", "tc_gemm_2sm")) or (
+        kernel.endswith("<256") and kern.startswith("tc_gemm_2sm<512")), d
     assert d["family"] == "contraction" and d["template"].get("math") == "tf32", d
     ins = exact_inputs(comp, 4)
     (got,) = run_device(plan, ins)

@@ -35,7 +35,7 @@ def test_tc_space_covers_forms_tiles_groups_splits():
     rm_n = {c["num_parts"][5][1] for c in sp}        # RM parts of j = BN
     smx_k = {c["num_parts"][1][2] for c in sp}       # SMX parts of k = K split
     wrp_i = {c["num_parts"][2][0] for c in sp}       # WRP parts of i: 4 = 128-row tile, 8 = CTA pair
-    assert rm_n == {64, 128, 256} and smx_k == {1, 2, 4} and wrp_i == {4, 8}
+    assert rm_n == {64, 128, 256, 512} and smx_k == {1, 2, 4} and wrp_i == {4, 8}  # 512: CTA-pair 256 x 512
     _, small = space("matmul_fp32", [1024, 1024, 256], "contraction", math=mdh.MATH_TF32)
     assert len(small) >= 50
 
