@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(256) pack_kmajor(const float* __restrict__ src
 // epilogue warps: 2 per TMEM lane quarter (splitting the tile's columns), or
 // 1 per quarter when a resident B
 // (resident B) or a 256-wide tile's 4-stage ring leaves no room for 8 squares
-__host__ __device__ constexpr int epi_warps(bool rb, int bn) { return rb || bn >= 256 ? 4 : 8; }
+__host__ __device__ constexpr int epi_warps(bool rb, int bn) { return (rb && bn <= 128) || bn >= 256 ? 4 : 8; }
 __host__ __device__ constexpr size_t epi_bytes(bool rb, int bn) { return epi_warps(rb, bn) * (32 * 33 * 4 + 32 * 8); }
 
 // bf16 packing (MATH_BF16): the same gather, converting to bf16 (round to
@@ -394,6 +394,22 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps(RB, BN), 1)
     tm = first_m + (x % per_group) % gsz;
     tn = (x % per_group) / gsz;
   };
+  // RB: CTA b keeps N tile b % tilesN resident and walks the M tiles
+  // b / tilesN, + lanes, ... (lanes = gridDim / tilesN CTAs per N tile), so
+  // only A streams; else tiles x = b, b + gridDim, ... in raster order
+  const int lanes = RB ? static_cast<int>(gridDim.x) / g.tilesN : 1;
+  const int tn_res = RB ? static_cast<int>(blockIdx.x) % g.tilesN : 0;
+  const int sub = RB ? static_cast<int>(blockIdx.x) / g.tilesN : 0;
+  const int my_tiles = RB ? (g.tilesM - sub + lanes - 1) / lanes
+                          : (ntiles - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x);
+  auto tile_of = [&](int j, int& tm, int& tn) {
+    if (RB) {
+      tm = sub + j * lanes;
+      tn = tn_res;
+    } else {
+      tile_mn(static_cast<int>(blockIdx.x) + j * static_cast<int>(gridDim.x), tm, tn);
+    }
+  };
   if (threadIdx.x == 0) {
     tc::tma_prefetch(&tma_a);
     tc::tma_prefetch(&tma_b);
@@ -446,15 +462,15 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps(RB, BN), 1)
       for (int kt = 0; kt < g.nk; ++kt) {
         int c[MAXR];
 #pragma unroll
-        for (int r = 0; r < MAXR; ++r) c[r] = g.b_nc[r] + kb[r];
+        for (int r = 0; r < MAXR; ++r) c[r] = g.b_nc[tn_res * MAXR + r] + kb[r];
         tc::tma_load(sB + kt * B_BYTES, &tma_b, bfull, g.b_rank, c);
         kstep(dig, ka, kb);
       }
     }
     uint32_t it = 0;
-    for (int x = blockIdx.x; x < ntiles; x += gridDim.x) {
+    for (int j = 0; j < my_tiles; ++j) {
       int tm, tn;
-      tile_mn(x, tm, tn);
+      tile_of(j, tm, tn);
       int am0[MAXR], bn0[MAXR], ka[MAXR], kb[MAXR], dig[MAXKD];
 #pragma unroll
       for (int r = 0; r < MAXR; ++r) {
@@ -496,7 +512,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps(RB, BN), 1)
     constexpr uint32_t idesc = tc::instr_desc(BF16 ? 1 : 2, 0, B_MN ? 1 : 0, BM, BN);  // kind::f16 bf16 | kind::tf32
     if (RB) tc::mbar_wait_warp(bfull, 0);
     uint32_t it = 0, tl = 0;
-    for (int x = blockIdx.x; x < ntiles; x += gridDim.x, ++tl) {
+    for (int j = 0; j < my_tiles; ++j, ++tl) {
       const uint32_t acc = tl & 1;
       if (tl >= 2) tc::mbar_wait_warp(&tempty[acc], ((tl / 2) - 1) & 1);
       tc::tc_fence_after();
@@ -532,13 +548,14 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps(RB, BN), 1)
     const uint32_t rtab = stg + 32 * 33 * 4;
     constexpr int CH = (BN / 32 + NH - 1) / NH;  // 32-column chunks per column part
     uint32_t tl = 0;
-    for (int x = blockIdx.x; x < ntiles; x += gridDim.x, ++tl) {
+    for (int j = 0; j < my_tiles; ++j, ++tl) {
       int tm, tn;
-      tile_mn(x, tm, tn);
+      tile_of(j, tm, tn);
       const uint32_t acc = tl & 1;
       // row table: C offset of TMEM lane q*32 + r (tile origin folded in)
-      const int64_t rowoff = static_cast<int64_t>(g.tCm[tm]) + g.cm[q * 32 + lane] + g.tCn[tn];
-      asm volatile("st.shared.s64 [%0], %1;" ::"r"(rtab + lane * 8), "l"(rowoff) : "memory");
+      // C offset of TMEM lane q*32 + r = tile origin + cm[q*32 + r] (row table in smem)
+      const int64_t tbase = static_cast<int64_t>(g.tCm[tm]) + g.tCn[tn];
+      asm volatile("st.shared.s32 [%0], %1;" ::"r"(rtab + lane * 4), "r"(g.cm[q * 32 + lane]) : "memory");
       tc::mbar_wait(&tfull[acc], (tl / 2) & 1);
       tc::tc_fence_after();
 #pragma unroll 1
@@ -551,14 +568,21 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps(RB, BN), 1)
         for (int j = 0; j < 32; ++j)
           asm volatile("st.shared.b32 [%0], %1;" ::"r"(stg + (lane * 33 + j) * 4), "r"(r[j]) : "memory");
         __syncwarp();
-        float* cc = g.C + g.cn[c0 + lane];
+        float* cc = g.C + tbase + g.cn[c0 + lane];
+        // 8 rows per batch: 16 shared loads in flight before the 8 stores
+        // (a load -> store -> load chain per row left each warp waiting one
+        // shared-load latency per 128-byte store)
 #pragma unroll
-        for (int rr = 0; rr < 32; ++rr) {
-          int64_t ro;
-          float v;
-          asm volatile("ld.shared.s64 %0, [%1];" : "=l"(ro) : "r"(rtab + rr * 8) : "memory");
-          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(stg + (rr * 33 + lane) * 4) : "memory");
-          __stcs(cc + ro, v);
+        for (int r0 = 0; r0 < 32; r0 += 8) {
+          int ro[8];
+          float v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            asm volatile("ld.shared.s32 %0, [%1];" : "=r"(ro[u]) : "r"(rtab + (r0 + u) * 4));
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[u]) : "r"(stg + ((r0 + u) * 33 + lane) * 4));
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) __stcs(cc + ro[u], v[u]);
         }
         __syncwarp();
       }
@@ -830,10 +854,8 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
       tc::tc_fence_after();
 #pragma unroll 1
       for (int h = 0; h < NH; ++h) {
-      const int64_t rowoff = static_cast<int64_t>(g.tCm[ta]) + g.cm[q * 32 + lane] + g.tCn[tn + h];
-      __syncwarp();
-      asm volatile("st.shared.s64 [%0], %1;" ::"r"(rtab + lane * 8), "l"(rowoff) : "memory");
-      __syncwarp();
+      const int64_t tbase = static_cast<int64_t>(g.tCm[ta]) + g.tCn[tn + h];
+      if (h == 0) asm volatile("st.shared.s32 [%0], %1;" ::"r"(rtab + lane * 4), "r"(g.cm[q * 32 + lane]) : "memory");
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t rv[32];
@@ -842,14 +864,21 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
         for (int j = 0; j < 32; ++j)
           asm volatile("st.shared.b32 [%0], %1;" ::"r"(stg + (lane * 33 + j) * 4), "r"(rv[j]) : "memory");
         __syncwarp();
-        float* cc = g.C + g.cn[c0 + lane];
+        float* cc = g.C + tbase + g.cn[c0 + lane];
+        // 8 rows per batch: 16 shared loads in flight before the 8 stores
+        // (a load -> store -> load chain per row left each warp waiting one
+        // shared-load latency per 128-byte store)
 #pragma unroll
-        for (int rr = 0; rr < 32; ++rr) {
-          int64_t ro;
-          float v;
-          asm volatile("ld.shared.s64 %0, [%1];" : "=l"(ro) : "r"(rtab + rr * 8) : "memory");
-          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(stg + (rr * 33 + lane) * 4) : "memory");
-          __stcs(cc + ro, v);
+        for (int r0 = 0; r0 < 32; r0 += 8) {
+          int ro[8];
+          float v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            asm volatile("ld.shared.s32 %0, [%1];" : "=r"(ro[u]) : "r"(rtab + (r0 + u) * 4));
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[u]) : "r"(stg + ((r0 + u) * 33 + lane) * 4));
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) __stcs(cc + ro[u], v[u]);
         }
         __syncwarp();
       }
@@ -1015,6 +1044,7 @@ struct TcKnobs {
   int group = 0;      // M tiles per raster group = SMX parts of M (persistent forms), 0 = 8
   int split = 1;      // K split = SMX parts of K (SMXs combine in DM: ordered reduction)
   int transpose = -1; // B rewritten K-major (layout_de of B = [2, 1]) 1, read as stored 0
+  bool rbn = false;   // DM parts of N = every N tile: one-CTA tiles with B resident per CTA
 };
 
 // split-K combine: C += ws[0] + ws[1] + ... in split order (the k order of
@@ -1229,6 +1259,7 @@ class TcRoutine final : public Routine {
     rb_ = tilesN_ == 1 && !vb_.mn && (BN == 64 || BN == 128) && rb_bytes <= 227 * 1024;
     pstages_ = rb_ ? rb_st : pers_stages(BN);
     psmem_ = rb_ ? rb_bytes : static_cast<size_t>(pstages_) * (BM + BN) * BKE * 4 + 1024 + 256 + epi_bytes(false, BN);
+    decide_rb_multi(BN);
     pers_ = !std::getenv("MDHB_TC_NONPERSISTENT");
     return finish_knobs(why);
   }
@@ -1243,6 +1274,7 @@ class TcRoutine final : public Routine {
     decide_2sm();
     if (kn_.set && (kn_.form == 2) != two_sm_) return *why = "CTA-pair instance unavailable for this tile", false;
     if (kn_.set && (kn_.bn == 512) != wide_) return *why = "256 x 512 CTA-pair tile unavailable (K-major B, N % 512)", false;
+    if (kn_.set && kn_.rbn != (rb_ && tilesN_ > 1)) return *why = "resident-B instance unavailable (BN 192, K-major B, smem)", false;
     if (!pers_ && BN_ == 192) return *why = "no one-CTA-per-tile instance with BN 192", false;
     if (!pers_ && bf16_) return *why = "no one-CTA-per-tile kind::f16 instance", false;
     args_.group_m = kn_.group;
@@ -1388,8 +1420,35 @@ class TcRoutine final : public Routine {
     rb_ = false;
     pstages_ = pers_stages(BN);
     psmem_ = static_cast<size_t>(pstages_) * (BM + BN) * BKE * 4 + 1024 + 256 + epi_bytes(false, BN);
+    decide_rb_multi(BN);
     pers_ = !std::getenv("MDHB_TC_NONPERSISTENT");
     return finish_knobs(why);
+  }
+
+  // Many N tiles: each CTA keeps one N tile of B resident and walks M tiles,
+  // so only A crosses from L2 per tile -- when the N tiles spread over the
+  // SMs with little idle (CCSD(T): 72 tiles x 2 CTAs of 148 SMs)
+  void decide_rb_multi(int BN) {
+    if (rb_ || tilesN_ <= 1 || BN != 192 || vb_.mn) return;
+    int lanes;
+    if (kn_.set) {
+      if (!kn_.rbn || kn_.group <= 0 || tilesM_ % kn_.group) return;
+      lanes = tilesM_ / kn_.group;
+    } else {
+      if (std::getenv("MDHB_TC_NO_RBN")) return;
+      const int sms = sm_count(p_.opt.device);
+      lanes = sms / tilesN_;
+      while (lanes > 1 && tilesM_ % lanes) --lanes;
+      if (lanes < 1 || tilesM_ < 4 * lanes || (sms - lanes * tilesN_) * 16 > sms) return;
+    }
+    auto need = [&](int st) { return static_cast<size_t>(nk_) * BN * BKE * 4 + st * BM * BKE * 4 + 1024 + 256 + epi_bytes(true, BN); };
+    int st = 4;  // 5: same time, 7: slower (CCSD(T))
+    while (st > 3 && need(st) > 227 * 1024) --st;
+    if (need(st) > 227 * 1024) return;
+    rb_ = true;
+    rbn_lanes_ = lanes;
+    pstages_ = st;
+    psmem_ = need(st);
   }
 
   // CTA-pair instance: K-major B whose tile rows live in one TMA rank (the
@@ -1451,7 +1510,9 @@ class TcRoutine final : public Routine {
     k->form = two_sm_ ? 2 : pers_ ? 1 : 0;
     k->bn = wide_ ? 2 * BN_ : BN_;
     k->group = k->form == 0 ? (two_sm_ ? tilesM_ / 2 : tilesM_) : 8;
-    if (k->form != 0 && (two_sm_ ? tilesM_ / 2 : tilesM_) % 8) return false;
+    k->rbn = rb_ && tilesN_ > 1 && pers_;
+    if (k->rbn) k->group = tilesM_ / rbn_lanes_;
+    else if (k->form != 0 && (two_sm_ ? tilesM_ / 2 : tilesM_) % 8) return false;
     k->split = 1;
     k->transpose = bf16_ ? -1 : (transposeB_ ? 1 : 0);
     return true;
@@ -1615,7 +1676,7 @@ class TcRoutine final : public Routine {
     }
     if (pers_) {
       const int sms = sm_count(p_.opt.device);
-      dim3 pgrid(static_cast<unsigned>(std::min(sms, tilesM_ * tilesN_)));
+      dim3 pgrid(static_cast<unsigned>(rb_ && tilesN_ > 1 ? rbn_lanes_ * tilesN_ : std::min(sms, tilesM_ * tilesN_)));
 #define MDHB_TCP(BNV, ST, MN, RBV)                                                                           \
   if (BN_ == BNV && vb_.mn == MN && rb_ == RBV && pstages_ == ST) {                                         \
     auto k = bf16_ ? tc_gemm_pers<BNV, ST, MN, RBV, true> : tc_gemm_pers<BNV, ST, MN, RBV, false>;          \
@@ -1628,7 +1689,7 @@ class TcRoutine final : public Routine {
       MDHB_TCP(256, 4, false, false) MDHB_TCP(256, 4, true, false) MDHB_TCP(192, 4, false, false)
       MDHB_TCP(128, 5, false, false) MDHB_TCP(128, 5, true, false) MDHB_TCP(64, 6, false, false)
       MDHB_TCP(64, 4, false, true) MDHB_TCP(64, 3, false, true) MDHB_TCP(128, 4, false, true)
-      MDHB_TCP(128, 3, false, true)
+      MDHB_TCP(128, 3, false, true) MDHB_TCP(192, 4, false, true) MDHB_TCP(192, 3, false, true)
 #undef MDHB_TCP
     }
     dim3 grid(static_cast<unsigned>(tilesM_ * tilesN_));
@@ -1677,6 +1738,7 @@ class TcRoutine final : public Routine {
   int64_t tK_ = 0, tN_ = 0;
   void* bt_ = nullptr;
   bool pers_ = false, rb_ = false;
+  int rbn_lanes_ = 0;  // resident B over many N tiles: CTAs per N tile
   int pstages_ = 0;
   size_t psmem_ = 0;
   bool packed_ = false;
@@ -1738,10 +1800,20 @@ TcKnobs tc_knobs(const Problem& p, const Groups& g, const Config& c) {
   if (k.bn != 64 && k.bn != 128 && k.bn != 192 && k.bn != 256 && !(k.bn == 512 && tm == 2 * BM))
     fail("Unsupported", "tensor-core N tile must be 64, 128, 192 or 256 (512 for CTA-pair tiles)");
   if (below(dk) != k_tile(p)) fail("Unsupported", "tensor-core k-tile (SM x ... of K) must be one 128-byte row");
-  if (at(dm, dn) != 1) fail("Unsupported", "tensor-core template rasters groups along M only (DM parts of N must be 1)");
+  const int64_t cols = e.sizes[static_cast<size_t>(dn)] / k.bn;
+  if (at(dm, dn) != 1) {
+    // DM parts of N = one per N tile: each CTA keeps its N tile of B resident
+    // and walks SMX parts of M tiles (the CTAs of one N tile = DM parts of M)
+    if (tm != BM || at(dm, dn) != cols || at(smx, dn) != 1 || at(smx, dk) != 1)
+      fail("Unsupported", "tensor-core template: DM parts of N must be 1, or one per 128-row-tile N tile (resident B, no K split)");
+    k.rbn = true;
+  }
   k.split = static_cast<int>(at(smx, dk));
   const int64_t rows = e.sizes[static_cast<size_t>(dm_)] / tm;
-  if (tm == 2 * BM) {
+  if (k.rbn) {
+    k.form = 1;
+    k.group = static_cast<int>(at(smx, dm_));
+  } else if (tm == 2 * BM) {
     k.form = 2;
     k.group = static_cast<int>(at(smx, dm_));
   } else if (at(dm, dm_) > 1) {
@@ -1769,7 +1841,7 @@ Config tc_canonical(const Problem& p, const Groups& g, const TcKnobs& k) {
   std::vector<int64_t> DMv(static_cast<size_t>(D), 1), SMXv(DMv), WRPv(DMv), CCv(DMv), SMv(DMv), RMv(DMv);
   DMv[static_cast<size_t>(dm_)] = rows / grp;
   SMXv[static_cast<size_t>(dm_)] = grp;
-  SMXv[static_cast<size_t>(dn)] = cols;
+  (k.rbn ? DMv : SMXv)[static_cast<size_t>(dn)] = cols;
   SMXv[static_cast<size_t>(dk)] = k.split;
   DMv[static_cast<size_t>(dk)] = e.sizes[static_cast<size_t>(dk)] / ek / k.split;
   WRPv[static_cast<size_t>(dm_)] = tm / 32;
@@ -1804,6 +1876,20 @@ std::vector<Config> tc_space(const Problem& p, const Groups& g) {
       for (int tr : {0, 1}) {
         if (bf16 && tr) continue;
         if (!bf16 && !mn && tr) continue;
+        if (form == 1 && bn == 192 && !(mn && !tr && !bf16))  // resident-B instances: CTAs per N tile 1, 2, 4
+          for (int64_t lanes : {1, 2, 4}) {
+            if (rows % lanes || rows / lanes < 4 || N / bn < 2) continue;
+            if ((K / ek) * bn * 128 + 3 * BM * 128 + 1280 + epi_bytes(true, bn) > 227 * 1024) continue;  // B resident in smem
+            TcKnobs k;
+            k.set = true;
+            k.form = 1;
+            k.bn = bn;
+            k.group = static_cast<int>(rows / lanes);
+            k.transpose = bf16 ? -1 : (mn ? tr : 0);
+            k.rbn = true;
+            Config c = tc_canonical(p, g, k);
+            if (config_violation(c, e, p.m, true).empty()) out.push_back(c);
+          }
         if (!bf16 && mn && !tr && ((form == 2 && bn != 256) || bn == 192 || (bn == 64 && form == 1))) continue;  // no MN-major instance
         for (int split : {1, 2, 4}) {
           if ((K / ek) % split) continue;

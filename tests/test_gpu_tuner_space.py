@@ -88,3 +88,23 @@ def test_tuner_visits_fifty_distinct_instances(name, sizes, math):
     distinct = {r[1] for r in rows if r[3] == "1"}
     assert len(distinct) >= 50, len(distinct)
     assert mdh.validate_config(j, "B200", best) == "" and secs > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("math", [1, 2])
+def test_resident_b_instances_are_exact(math):
+    """DM parts of N = one per N tile: one-CTA 128 x 192 tiles whose CTA keeps
+    its N tile of B resident in shared memory and walks SMX parts of M tiles
+    (the CCSD(T) default); every such instance of the space vs the oracle."""
+    from paper_2405_05118_b200 import mdh
+    j = spec("matmul_fp32", [1024, 384, 128])
+    comp = mo.Computation.from_json(j)
+    ins = exact_inputs(comp, 6)
+    ((want, _),) = mo.execute(comp, ins)
+    sp = [c for c in mdh.tune_space(j, "contraction", math=math) if c["num_parts"][0][1] > 1]
+    assert len(sp) == 2
+    for c in sp:
+        t = mdh.Plan(j, "B200", c, math=math).describe()["template"]
+        assert "B_RESIDENT" in t["kernel"] and t["from_config"], t
+        (got,) = run_device(mdh.Plan(j, "B200", c, math=math), ins)
+        assert np.array_equal(got.astype(np.float64), want), t

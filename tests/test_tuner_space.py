@@ -43,7 +43,8 @@ def test_tc_space_covers_forms_tiles_groups_splits():
 @pytest.mark.skipif(not refbind.available(), reason="oracle/_ref not built")
 @pytest.mark.parametrize("name,sizes,family,math", [("jacobi3d_fp32", [512, 32, 128], "stencil", 0),
                                                     ("matmul_fp32", [1024, 1024, 256], "contraction", 1),
-                                                    ("matmul_fp32", [1024, 1024, 256], "contraction", 2)])
+                                                    ("matmul_fp32", [1024, 1024, 256], "contraction", 2),
+                                                    ("matmul_fp32", [1024, 384, 128], "contraction", 1)])
 def test_every_candidate_passes_the_reference_validate(name, sizes, family, math):
     from paper_2405_05118_b200 import mdh
     j, sp = space(name, sizes, family, math=math)

@@ -1,9 +1,8 @@
-# scratch A/B of an env-selected variant (development aid): MCC GPU tests,
-# then alternating timings of the default and the variant
-V=${V:-MDHB_FCONV_NOTAIL=1}
-timeout 900 python -m pytest tests/test_gpu_contraction.py tests/test_gpu_fullsize.py tests/test_gpu_tc.py -m gpu -q -x -k "mcc or conv" 2>&1 | tail -3
-for i in 1 2 3; do
-for v in "" "$V"; do
-  echo "F $v"; env $v timeout 120 python tools/graph_time.py mcc_nhwc 10 2>&1 | tail -1 | cut -c1-100
+# scratch A/B (development aid): GPU tests, then CCSD(T) / MatMul timings
+timeout 1200 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+for i in 1 2; do
+for v in "" "MDHB_TC_NO_RBN=1"; do
+  echo "C tf32 $v"; env $v timeout 120 python tools/graph_time.py ccsdt_abcdef_gdab_efgc:tf32 50 2>&1 | tail -1 | cut -c1-110
+  echo "C bf16 $v"; env $v timeout 120 python tools/graph_time.py ccsdt_abcdef_gdab_efgc:bf16 50 2>&1 | tail -1 | cut -c1-110
 done
 done

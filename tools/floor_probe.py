@@ -28,3 +28,12 @@ for mb in (8, 64):
     ys = [torch.empty(n, device="cuda") for _ in range(R)]
     us = graph_time(lambda i: ys[i % R].copy_(xs[i % R]))
     print("copy %3d MB     %.2f us  %.0f GB/s" % (mb, us, mb * 2**20 / us / 1e3))
+
+# write-only floor at CCSD(T)'s output size (729 MiB, larger than L2)
+y = torch.empty(24 ** 6, device="cuda")
+us = graph_time(lambda i: y.fill_(float(i)), steps=50)
+print("fill 729 MiB   %.2f us  %.0f GB/s" % (us, y.numel() * 4 / us / 1e3))
+x = torch.rand(24 ** 6 // 2, device="cuda")
+y2 = torch.empty(24 ** 6 // 2, device="cuda")
+us = graph_time(lambda i: y2.copy_(x), steps=50)
+print("copy 2x365 MiB %.2f us  %.0f GB/s" % (us, 2 * x.numel() * 4 / us / 1e3))
