@@ -242,6 +242,66 @@ __global__ void __launch_bounds__(256) pack_kmajor(const float* __restrict__ src
   }
 }
 
+// Epilogue store of one 32 x 32 block drained from TMEM (lane = row, r[j] =
+// column c0 + j) through this warp's staging square (stg) to C rows at
+// tbase + rtab[row] + cn[column]:
+//  * cvec (columns in aligned runs of 4): rows land in 144-byte-pitch smem
+//    rows by STS.128; lane l then reads row 4 s + l / 8, columns 4 (l % 8) ..
+//    +3 (LDS.128, conflict-free at that pitch) and stores them with one
+//    STG.128 -- each store instruction writes 4 rows x 128 contiguous bytes;
+//  * else the 33-word-pitch transpose: lane = column, one STG.32 per row.
+__device__ __forceinline__ void epi_block(const uint32_t (&r)[32], uint32_t stg, uint32_t rtab, float* C, int64_t tbase,
+                                          const int32_t* cn, int c0, int lane, bool cvec) {
+  if (cvec) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(stg + lane * 144 + j * 16), "r"(r[4 * j]),
+                   "r"(r[4 * j + 1]), "r"(r[4 * j + 2]), "r"(r[4 * j + 3])
+                   : "memory");
+    __syncwarp();
+    const int sub = lane & 7, rq = lane >> 3;
+    float* cc = C + tbase + cn[c0 + 4 * sub];
+#pragma unroll
+    for (int s0 = 0; s0 < 8; s0 += 4) {
+      int ro[4];
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int row = 4 * (s0 + u) + rq;
+        asm volatile("ld.shared.s32 %0, [%1];" : "=r"(ro[u]) : "r"(rtab + row * 4));
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(v[u].x), "=f"(v[u].y), "=f"(v[u].z), "=f"(v[u].w)
+                     : "r"(stg + row * 144 + sub * 16));
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) __stcs(reinterpret_cast<float4*>(cc + ro[u]), v[u]);
+    }
+    __syncwarp();
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(stg + (lane * 33 + j) * 4), "r"(r[j]) : "memory");
+  __syncwarp();
+  float* cc = C + tbase + cn[c0 + lane];
+  // 8 rows per batch: 16 shared loads in flight before the 8 stores (a
+  // load -> store -> load chain per row left each warp waiting one
+  // shared-load latency per 128-byte store)
+#pragma unroll
+  for (int r0 = 0; r0 < 32; r0 += 8) {
+    int ro[8];
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      asm volatile("ld.shared.s32 %0, [%1];" : "=r"(ro[u]) : "r"(rtab + (r0 + u) * 4));
+      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[u]) : "r"(stg + ((r0 + u) * 33 + lane) * 4));
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) __stcs(cc + ro[u], v[u]);
+  }
+  __syncwarp();
+}
+
 // shared-memory layout of tc_gemm_pers: A ring | B ring (or resident B) |
 // barriers (256 B) | epilogue staging (4 warps x 32 x 33 floats)
 #define EPI_OFF(ST, BNV, BSLOTS) \
@@ -250,7 +310,7 @@ __global__ void __launch_bounds__(256) pack_kmajor(const float* __restrict__ src
 // 1 per quarter when a resident B
 // (resident B) or a 256-wide tile's 4-stage ring leaves no room for 8 squares
 __host__ __device__ constexpr int epi_warps(bool rb, int bn) { return (rb && bn <= 128) || bn >= 256 ? 4 : 8; }
-__host__ __device__ constexpr size_t epi_bytes(bool rb, int bn) { return epi_warps(rb, bn) * (32 * 33 * 4 + 32 * 8); }
+__host__ __device__ constexpr size_t epi_bytes(bool rb, int bn) { return epi_warps(rb, bn) * (32 * 36 * 4 + 32 * 8); }
 
 // bf16 packing (MATH_BF16): the same gather, converting to bf16 (round to
 // nearest even).  k-fast: consecutive threads walk k (coalesced when k is the
@@ -544,8 +604,8 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps(RB, BN), 1)
     const int q = warp & 3, half = (warp - 2) >> 2;  // lane quarter, column part
     const int ew = warp - 2;
     // shared (.shared window) addresses of this warp's staging square and row table
-    const uint32_t stg = tc::smem_u32(stage_base) + static_cast<uint32_t>(ew) * (32 * 33 * 4 + 32 * 8);
-    const uint32_t rtab = stg + 32 * 33 * 4;
+    const uint32_t stg = tc::smem_u32(stage_base) + static_cast<uint32_t>(ew) * (32 * 36 * 4 + 32 * 8);
+    const uint32_t rtab = stg + 32 * 36 * 4;
     constexpr int CH = (BN / 32 + NH - 1) / NH;  // 32-column chunks per column part
     uint32_t tl = 0;
     for (int j = 0; j < my_tiles; ++j, ++tl) {
@@ -564,27 +624,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps(RB, BN), 1)
         if (c0 >= BN) break;
         uint32_t r[32];
         tc::tmem_ld32(tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c0), r);
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          asm volatile("st.shared.b32 [%0], %1;" ::"r"(stg + (lane * 33 + j) * 4), "r"(r[j]) : "memory");
-        __syncwarp();
-        float* cc = g.C + tbase + g.cn[c0 + lane];
-        // 8 rows per batch: 16 shared loads in flight before the 8 stores
-        // (a load -> store -> load chain per row left each warp waiting one
-        // shared-load latency per 128-byte store)
-#pragma unroll
-        for (int r0 = 0; r0 < 32; r0 += 8) {
-          int ro[8];
-          float v[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            asm volatile("ld.shared.s32 %0, [%1];" : "=r"(ro[u]) : "r"(rtab + (r0 + u) * 4));
-            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[u]) : "r"(stg + ((r0 + u) * 33 + lane) * 4));
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) __stcs(cc + ro[u], v[u]);
-        }
-        __syncwarp();
+        epi_block(r, stg, rtab, g.C, tbase, g.cn, c0, lane, g.cvec != 0);
       }
       tc::tc_fence_before();
       __syncwarp();
@@ -841,8 +881,8 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
   } else if (warp >= 2) {
     // ---------------- epilogue warps (both CTAs): own 128 TMEM lanes
     const int q = warp & 3;
-    const uint32_t stg = tc::smem_u32(stage_base) + static_cast<uint32_t>(warp - 2) * (32 * 33 * 4 + 32 * 8);
-    const uint32_t rtab = stg + 32 * 33 * 4;
+    const uint32_t stg = tc::smem_u32(stage_base) + static_cast<uint32_t>(warp - 2) * (32 * 36 * 4 + 32 * 8);
+    const uint32_t rtab = stg + 32 * 36 * 4;
     const uint32_t tempty_leader0 = peer_addr(tc::smem_u32(&tempty[0]), lead_rank);
     uint32_t tl = 0;
     for (int x = pair; x < ntiles; x += npairs, ++tl) {
@@ -860,27 +900,7 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t rv[32];
         tc::tmem_ld32(tmem + (acc + h) * BN + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c0), rv);
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          asm volatile("st.shared.b32 [%0], %1;" ::"r"(stg + (lane * 33 + j) * 4), "r"(rv[j]) : "memory");
-        __syncwarp();
-        float* cc = g.C + tbase + g.cn[c0 + lane];
-        // 8 rows per batch: 16 shared loads in flight before the 8 stores
-        // (a load -> store -> load chain per row left each warp waiting one
-        // shared-load latency per 128-byte store)
-#pragma unroll
-        for (int r0 = 0; r0 < 32; r0 += 8) {
-          int ro[8];
-          float v[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            asm volatile("ld.shared.s32 %0, [%1];" : "=r"(ro[u]) : "r"(rtab + (r0 + u) * 4));
-            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[u]) : "r"(stg + ((r0 + u) * 33 + lane) * 4));
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) __stcs(cc + ro[u], v[u]);
-        }
-        __syncwarp();
+        epi_block(rv, stg, rtab, g.C, tbase, g.cn, c0, lane, g.cvec != 0);
       }
       if (WIDE || h == NH - 1) {
         tc::tc_fence_before();
@@ -1250,7 +1270,7 @@ class TcRoutine final : public Routine {
     args_.nk = nk_;
     args_.tilesM = tilesM_;
     args_.tilesN = tilesN_;
-    args_.cvec = cvec_;
+    args_.cvec = cvec_ && !std::getenv("MDHB_TC_EPI32");  // dev aid: the one-row-per-store epilogue
     smem_ = static_cast<size_t>(stages_) * (BM + BN) * BKE * 4 + 1024 + 256;
     // persistent instance: resident B when the single N tile's K extent fits
     auto rb_need = [&](int st) { return static_cast<size_t>(nk_) * BN * BKE * 4 + st * BM * BKE * 4 + 1024 + 256 + epi_bytes(true, BN); };
@@ -1382,7 +1402,7 @@ class TcRoutine final : public Routine {
     args_.nk = nk_;
     args_.tilesM = tilesM_;
     args_.tilesN = tilesN_;
-    args_.cvec = cvec_;
+    args_.cvec = cvec_ && !std::getenv("MDHB_TC_EPI32");  // dev aid: the one-row-per-store epilogue
     MDHB_CUDA(cudaMalloc(&pa_, static_cast<size_t>(M_ * Kp_) * esz));
     MDHB_CUDA(cudaMalloc(&pb_, static_cast<size_t>(N_ * Kp_) * esz));
     // bf16 packing reads along the operand's unit-stride direction
@@ -1464,7 +1484,7 @@ class TcRoutine final : public Routine {
       b_row_rank_ = 0;
       vb2_ = vb_;
       st2_ = 6;
-      smem2_ = static_cast<size_t>(st2_) * (BM + BN_ / 2) * BKE * 4 + 1024 + 256 + 4 * (32 * 33 * 4 + 32 * 8);
+      smem2_ = static_cast<size_t>(st2_) * (BM + BN_ / 2) * BKE * 4 + 1024 + 256 + 4 * (32 * 36 * 4 + 32 * 8);
       two_sm_ = smem2_ <= 227 * 1024;
       return;
     }
@@ -1482,7 +1502,7 @@ class TcRoutine final : public Routine {
     vb2_ = vb_;
     vb2_.box[row_rank] = static_cast<cuuint32_t>(BN_ / 2);
     st2_ = BN_ == 256 ? 6 : 8;
-    smem2_ = static_cast<size_t>(st2_) * (BM + BN_ / 2) * BKE * 4 + 1024 + 256 + 4 * (32 * 33 * 4 + 32 * 8);
+    smem2_ = static_cast<size_t>(st2_) * (BM + BN_ / 2) * BKE * 4 + 1024 + 256 + 4 * (32 * 36 * 4 + 32 * 8);
     two_sm_ = smem2_ <= 227 * 1024;
     // clusters of two pairs sharing A by multicast (plain 2-D A views)
     mc_ = two_sm_ && BN_ == 256 && tilesN_ % 2 == 0 && va_.rank == 2 && va_.row_dims.size() <= 1 && va_.box[1] == BM &&
@@ -1498,10 +1518,10 @@ class TcRoutine final : public Routine {
             (kn_.set ? kn_.bn == 512 : std::getenv("MDHB_TC_NARROW") == nullptr);
     if (wide_) {
       st2_ = 4;
-      smem2_ = static_cast<size_t>(st2_) * (BM + BN_) * BKE * 4 + 1024 + 256 + 4 * (32 * 33 * 4 + 32 * 8);
+      smem2_ = static_cast<size_t>(st2_) * (BM + BN_) * BKE * 4 + 1024 + 256 + 4 * (32 * 36 * 4 + 32 * 8);
       if (smem2_ > 227 * 1024) wide_ = false;
     }
-    if (!wide_ && two_sm_) smem2_ = static_cast<size_t>(st2_) * (BM + BN_ / 2) * BKE * 4 + 1024 + 256 + 4 * (32 * 33 * 4 + 32 * 8);
+    if (!wide_ && two_sm_) smem2_ = static_cast<size_t>(st2_) * (BM + BN_ / 2) * BKE * 4 + 1024 + 256 + 4 * (32 * 36 * 4 + 32 * 8);
   }
   bool packed() const { return packed_; }
   // the knobs of the planner's default instance (for its canonical config)
