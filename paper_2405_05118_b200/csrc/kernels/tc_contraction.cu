@@ -329,9 +329,10 @@ __global__ void __launch_bounds__(256) pack_kmajor_bf16(const float* __restrict_
     dst[i] = __bfloat16_as_ushort(__float2bfloat16_rn(v));
   }
 }
-__global__ void __launch_bounds__(256) pack_rows_bf16(const float* __restrict__ src, uint16_t* __restrict__ dst,
-                                                      const int32_t* __restrict__ tile_off, const int32_t* __restrict__ row_off,
-                                                      const int32_t* __restrict__ k_off, int rows, int K, int Kp, int64_t n_rows) {
+template <typename OutT>
+__global__ void __launch_bounds__(256) pack_rows(const float* __restrict__ src, OutT* __restrict__ dst,
+                                                 const int32_t* __restrict__ tile_off, const int32_t* __restrict__ row_off,
+                                                 const int32_t* __restrict__ k_off, int rows, int K, int Kp, int64_t n_rows) {
   __shared__ float t[32][33];
   const int k0 = blockIdx.x * 32;
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 32;
@@ -348,7 +349,10 @@ __global__ void __launch_bounds__(256) pack_rows_bf16(const float* __restrict__ 
 #pragma unroll
   for (int rr = ty; rr < 32; rr += 8) {  // write: lanes along k
     const int64_t gr = r0 + rr;
-    if (gr < n_rows) dst[gr * Kp + k0 + tx] = __bfloat16_as_ushort(__float2bfloat16_rn(t[tx][rr]));
+    if (gr < n_rows) {
+      if constexpr (sizeof(OutT) == 2) dst[gr * Kp + k0 + tx] = __bfloat16_as_ushort(__float2bfloat16_rn(t[tx][rr]));
+      else dst[gr * Kp + k0 + tx] = t[tx][rr];
+    }
   }
 }
 
@@ -1406,8 +1410,8 @@ class TcRoutine final : public Routine {
     MDHB_CUDA(cudaMalloc(&pa_, static_cast<size_t>(M_ * Kp_) * esz));
     MDHB_CUDA(cudaMalloc(&pb_, static_cast<size_t>(N_ * Kp_) * esz));
     // bf16 packing reads along the operand's unit-stride direction
-    a_rowfast_ = bf16_ && am.size() > 1 && am[1] - am[0] == 1 && !(ak.size() > 1 && ak[1] - ak[0] == 1);
-    b_rowfast_ = bf16_ && bn.size() > 1 && bn[1] - bn[0] == 1 && !(bk.size() > 1 && bk[1] - bk[0] == 1);
+    a_rowfast_ = am.size() > 1 && am[1] - am[0] == 1 && !(ak.size() > 1 && ak[1] - ak[0] == 1);
+    b_rowfast_ = bn.size() > 1 && bn[1] - bn[0] == 1 && !(bk.size() > 1 && bk[1] - bk[0] == 1);
     // plain 2-D operands (global row r = t*rows + local at base + r*sr, k at k*sk):
     // vectorised convert (sk == 1) or 64x64 transposing convert (sr == 1)
     auto plain = [](const std::vector<int64_t>& toff, const std::vector<int64_t>& roff, const std::vector<int64_t>& koff,
@@ -1555,8 +1559,8 @@ class TcRoutine final : public Routine {
                       bool rowfast) {
         if (rowfast) {
           dim3 g(static_cast<unsigned>(Kp_ / 32), static_cast<unsigned>((n_rows + 31) / 32));
-          pack_rows_bf16<<<g, 256, 0, s>>>(static_cast<const float*>(src), static_cast<uint16_t*>(dst), t, r, k, rows,
-                                            static_cast<int>(K_), static_cast<int>(Kp_), n_rows);
+          pack_rows<uint16_t><<<g, 256, 0, s>>>(static_cast<const float*>(src), static_cast<uint16_t*>(dst), t, r, k, rows,
+                                                 static_cast<int>(K_), static_cast<int>(Kp_), n_rows);
         } else {
           const int64_t tot = n_rows * Kp_;
           pack_kmajor_bf16<<<static_cast<unsigned>(std::min<int64_t>(8 * sms, (tot + 255) / 256)), 256, 0, s>>>(
@@ -1586,15 +1590,25 @@ class TcRoutine final : public Routine {
       B = pb_;
     } else if (packed_) {
       const int sms = sm_count(p_.opt.device);
-      const int64_t ta = M_ * Kp_, tb = N_ * Kp_;
-      pack_kmajor<<<static_cast<unsigned>(std::min<int64_t>(8 * sms, (ta + 255) / 256)), 256, 0, s>>>(
-          static_cast<const float*>(A), static_cast<float*>(pa_), pk_[0], pk_[1], pk_[2], BM, static_cast<int>(K_),
-          static_cast<int>(Kp_), ta);
-      MDHB_CUDA(cudaGetLastError());
-      pack_kmajor<<<static_cast<unsigned>(std::min<int64_t>(8 * sms, (tb + 255) / 256)), 256, 0, s>>>(
-          static_cast<const float*>(B), static_cast<float*>(pb_), pk_[3], pk_[4], pk_[5], BN_, static_cast<int>(K_),
-          static_cast<int>(Kp_), tb);
-      MDHB_CUDA(cudaGetLastError());
+      // rows unit-stride (CCSD(T)'s A[g][d][a][b] along b): 32 x 32 blocks
+      // through shared memory, reads along rows and writes along k; else
+      // k-fast gathers
+      auto pack = [&](const void* src, void* dst, const int32_t* t, const int32_t* r, const int32_t* k, int rows, int64_t n_rows,
+                      bool rowfast) {
+        if (rowfast && !std::getenv("MDHB_TC_NO_ROWPACK")) {
+          dim3 g(static_cast<unsigned>(Kp_ / 32), static_cast<unsigned>((n_rows + 31) / 32));
+          pack_rows<float><<<g, 256, 0, s>>>(static_cast<const float*>(src), static_cast<float*>(dst), t, r, k, rows,
+                                              static_cast<int>(K_), static_cast<int>(Kp_), n_rows);
+        } else {
+          const int64_t tot = n_rows * Kp_;
+          pack_kmajor<<<static_cast<unsigned>(std::min<int64_t>(8 * sms, (tot + 255) / 256)), 256, 0, s>>>(
+              static_cast<const float*>(src), static_cast<float*>(dst), t, r, k, rows, static_cast<int>(K_),
+              static_cast<int>(Kp_), tot);
+        }
+        MDHB_CUDA(cudaGetLastError());
+      };
+      pack(A, pa_, pk_[0], pk_[1], pk_[2], BM, M_, a_rowfast_);
+      pack(B, pb_, pk_[3], pk_[4], pk_[5], BN_, N_, b_rowfast_);
       A = pa_;
       B = pb_;
     }
