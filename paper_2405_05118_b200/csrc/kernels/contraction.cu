@@ -771,11 +771,15 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 512 / ((BM / 8) * (BN / 8
     if (p < nk) issue(p);
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  float acc[8][8];
+  // accumulators as column pairs: acc[i][jj] = (C[i][2 jj], C[i][2 jj + 1]),
+  // updated by FFMA2 (two fma.rn per instruction, the row value broadcast
+  // from a scalar register): half the FMA instructions of scalar FFMA,
+  // bit-identical results
+  float2 acc[8][4];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
   for (int kt = 0; kt < nk; ++kt) {
     asm volatile("cp.async.wait_group %0;" ::"n"(ST - 2) : "memory");
     __syncthreads();
@@ -799,12 +803,12 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 512 / ((BM / 8) * (BN / 8
       }
       const float a[8] = {fa[cur][0].x, fa[cur][0].y, fa[cur][0].z, fa[cur][0].w,
                           fa[cur][1].x, fa[cur][1].y, fa[cur][1].z, fa[cur][1].w};
-      const float b[8] = {fb[cur][0].x, fb[cur][0].y, fb[cur][0].z, fb[cur][0].w,
-                          fb[cur][1].x, fb[cur][1].y, fb[cur][1].z, fb[cur][1].w};
+      const float2 b[4] = {make_float2(fb[cur][0].x, fb[cur][0].y), make_float2(fb[cur][0].z, fb[cur][0].w),
+                           make_float2(fb[cur][1].x, fb[cur][1].y), make_float2(fb[cur][1].z, fb[cur][1].w)};
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < 4; ++j) acc[i][j] = __ffma2_rn(make_float2(a[i], a[i]), b[j], acc[i][j]);
     }
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -818,10 +822,10 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 512 / ((BM / 8) * (BN / 8
       const int c = h * (BN / 2) + tx * 4;
       if (CVEC) {
         *reinterpret_cast<float4*>(crow + g.cn[c]) =
-            make_float4(acc[i][h * 4 + 0], acc[i][h * 4 + 1], acc[i][h * 4 + 2], acc[i][h * 4 + 3]);
+            make_float4(acc[i][h * 2].x, acc[i][h * 2].y, acc[i][h * 2 + 1].x, acc[i][h * 2 + 1].y);
       } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) crow[g.cn[c + j]] = acc[i][h * 4 + j];
+        for (int j = 0; j < 4; ++j) crow[g.cn[c + j]] = j & 1 ? acc[i][h * 2 + j / 2].y : acc[i][h * 2 + j / 2].x;
       }
     }
   }
