@@ -158,11 +158,11 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 256 / ((BM / 8) * (BN / 8
     }
   };
 
-  float acc[8][8];
+  float2 acc[8][4];  // column pairs, FFMA2 (see sgemm_pipe)
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
 
   const int nk = g.K / BK;
   load(0);
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 256 / ((BM / 8) * (BN / 8
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < 4; ++j) acc[i][j] = __ffma2_rn(make_float2(a[i], a[i]), make_float2(b[2 * j], b[2 * j + 1]), acc[i][j]);
     }
     if (kt + 1 < nk) store(buf ^ 1);
     __syncthreads();
@@ -199,10 +199,10 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 256 / ((BM / 8) * (BN / 8
       const int c = h * (BN / 2) + tx * 4;
       if (CVEC) {
         *reinterpret_cast<float4*>(crow + g.cn[c]) =
-            make_float4(acc[i][h * 4 + 0], acc[i][h * 4 + 1], acc[i][h * 4 + 2], acc[i][h * 4 + 3]);
+            make_float4(acc[i][h * 2].x, acc[i][h * 2].y, acc[i][h * 2 + 1].x, acc[i][h * 2 + 1].y);
       } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) crow[g.cn[c + j]] = acc[i][h * 4 + j];
+        for (int j = 0; j < 4; ++j) crow[g.cn[c + j]] = j & 1 ? acc[i][h * 2 + j / 2].y : acc[i][h * 2 + j / 2].x;
       }
     }
   }
@@ -612,11 +612,11 @@ __global__ void __launch_bounds__(256, TN == 8 ? 2 : 1) sgemm_async(GemmArgs g) 
     if (p < nk) issue(p);
     cp_async_commit();
   }
-  float acc[8][TN];
+  float2 acc[8][TN / 2];  // column pairs, FFMA2 (see sgemm_pipe)
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
+    for (int j = 0; j < TN / 2; ++j) acc[i][j] = make_float2(0.f, 0.f);
   for (int kt = 0; kt < nk; ++kt) {
     cp_async_wait<ST - 2>();
     __syncthreads();
@@ -655,7 +655,7 @@ __global__ void __launch_bounds__(256, TN == 8 ? 2 : 1) sgemm_async(GemmArgs g) 
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
-          for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+          for (int j = 0; j < TN / 2; ++j) acc[i][j] = __ffma2_rn(make_float2(a[i], a[i]), make_float2(b[2 * j], b[2 * j + 1]), acc[i][j]);
       }
     }
   }
@@ -670,10 +670,10 @@ __global__ void __launch_bounds__(256, TN == 8 ? 2 : 1) sgemm_async(GemmArgs g) 
       const int c = q * (BN / NQ) + tx * 4;
       if (CVEC) {
         *reinterpret_cast<float4*>(crow + g.cn[c]) =
-            make_float4(acc[i][q * 4 + 0], acc[i][q * 4 + 1], acc[i][q * 4 + 2], acc[i][q * 4 + 3]);
+            make_float4(acc[i][q * 2].x, acc[i][q * 2].y, acc[i][q * 2 + 1].x, acc[i][q * 2 + 1].y);
       } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) crow[g.cn[c + j]] = acc[i][q * 4 + j];
+        for (int j = 0; j < 4; ++j) crow[g.cn[c + j]] = j & 1 ? acc[i][q * 2 + j / 2].y : acc[i][q * 2 + j / 2].x;
       }
     }
   }
