@@ -1,7 +1,9 @@
-# scratch (development aid): ncu of the FFMA conv, default vs libmdh_b200_alt.so
-ALT=$PWD/paper_2405_05118_b200/libmdh_b200_alt.so
-M="smsp__issue_active.avg.pct_of_peak_sustained_active,sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active,smsp__inst_executed.sum,gpu__time_duration.sum,smsp__average_warp_latency_issue_stalled_dispatch_stall.ratio,smsp__average_warp_latency_issue_stalled_not_selected.ratio,smsp__average_warp_latency_issue_stalled_math_pipe_throttle.ratio,smsp__average_warp_latency_issue_stalled_short_scoreboard.ratio,smsp__average_warp_latency_issue_stalled_wait.ratio,sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_fmalite_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_fmaheavy.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_fmalite.avg.pct_of_peak_sustained_active"
-for v in "" "MDHB_LIB=$ALT"; do
-  echo "== $v"
-  env $v timeout 300 ncu --metrics $M --clock-control none -k regex:ffma_conv_tma -c 2 python tools/profile_routines.py mcc_nhwc 2>&1 | grep -E "ffma_conv_tma|smsp__|sm__|gpu__" | head -40
+# scratch A/B (development aid): 192-column FFMA instances on CCSD(T)
+for v in "MDHB_SGEMM_192=64" "MDHB_SGEMM_192=128"; do
+  env $v timeout 900 python -m pytest tests/test_gpu_contraction.py tests/test_gpu_fullsize.py -m gpu -q -x -k "ccsdt" 2>&1 | tail -1
+done
+for i in 1 2; do
+for v in "" "MDHB_SGEMM_192=64" "MDHB_SGEMM_192=128"; do
+  echo "C $v"; env $v timeout 120 python tools/graph_time.py ccsdt_abcdef_gdab_efgc 20 2>&1 | tail -1 | cut -c1-100
+done
 done
