@@ -1115,7 +1115,7 @@ class TcRoutine final : public Routine {
     if (two_sm_) os << ", \"cta_pair\": \"tc_gemm_2sm<" << BN_ << "," << st2_ << ">: tcgen05.mma.cta_group::2 M256xN" << BN_ << (bf16_ ? "xK16 (bf16)" : "xK8") << "\"";
     if (wide_) os << ", \"wide\": \"256 x " << 2 * BN_ << " pair tiles: two N" << BN_ << " MMAs per k-step share one A landing, TMEM 512 columns single-buffered\"";
     if (mc_) os << ", \"a_multicast\": \"clusters of 4 (two pairs on adjacent N tiles), A halves multicast\", \"clusters\": " << mc_clusters_;
-    os << ", \"raster_group_m\": " << (kn_.group > 0 ? kn_.group : 8) << ", \"k_split\": " << kn_.split
+    os << ", \"raster_group_m\": " << (args_.group_m > 0 ? args_.group_m : 8) << ", \"k_split\": " << kn_.split
        << ", \"from_config\": " << (kn_.set ? "true" : "false");
     os << "}";
     return os.str();
@@ -1302,6 +1302,8 @@ class TcRoutine final : public Routine {
     if (!pers_ && BN_ == 192) return *why = "no one-CTA-per-tile instance with BN 192", false;
     if (!pers_ && bf16_) return *why = "no one-CTA-per-tile kind::f16 instance", false;
     args_.group_m = kn_.group;
+    // 256 x 512 pair tiles: raster groups of 16 row tiles (1% over 8 at 8192^3)
+    if (!kn_.set && wide_ && (tilesM_ / 2) % 16 == 0) args_.group_m = 16;
     if (const char* f = std::getenv("MDHB_TC_GROUP")) args_.group_m = std::atoi(f);  // dev aid
     if (kn_.split > 1) {
       if (args_.kext[0] % kn_.split) return *why = "K split does not divide the outer K digit", false;
@@ -1533,7 +1535,7 @@ class TcRoutine final : public Routine {
     k->set = true;
     k->form = two_sm_ ? 2 : pers_ ? 1 : 0;
     k->bn = wide_ ? 2 * BN_ : BN_;
-    k->group = k->form == 0 ? (two_sm_ ? tilesM_ / 2 : tilesM_) : 8;
+    k->group = k->form == 0 ? (two_sm_ ? tilesM_ / 2 : tilesM_) : (wide_ && (tilesM_ / 2) % 16 == 0 ? 16 : 8);
     k->rbn = rb_ && tilesN_ > 1 && pers_;
     if (k->rbn) k->group = tilesM_ / rbn_lanes_;
     else if (k->form != 0 && (two_sm_ ? tilesM_ / 2 : tilesM_) % 8) return false;
