@@ -28,6 +28,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <set>
 #include <sstream>
 
 #include "../plan.hpp"
@@ -50,6 +51,7 @@ struct GemmArgs {
   int K, tilesM, tilesN;
   int sak, sbk;  // per-k strides inside one k-tile (sgemm_pipe: ak[k0 + j] = ak[k0] + j * sak)
   int klin;      // sgemm_pipe: ak[k] = k * sak and bk[k] = k * sbk for EVERY k -- no per-k-tile table read
+  int group_m;   // row tiles per raster group (Table-1: SMX parts of the innermost M dim; 0 = 8)
 };
 
 struct GemvArgs {
@@ -71,7 +73,7 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 256 / ((BM / 8) * (BN / 8
   const int tx = tid % TXN, ty = tid / TXN;
 
   // grouped raster: GROUP_M row-tiles sweep the N tiles together (L2 reuse)
-  constexpr int GROUP_M = 8;
+  const int GROUP_M = g.group_m > 0 ? g.group_m : 8;
   const int x = blockIdx.x;
   const int per_group = GROUP_M * g.tilesN;
   const int first_m = (x / per_group) * GROUP_M;
@@ -576,7 +578,7 @@ __global__ void __launch_bounds__(256, TN == 8 ? 2 : 1) sgemm_async(GemmArgs g) 
   __shared__ __align__(16) float As[ST][BM * BK];
   __shared__ __align__(16) float Bs[ST][BK * BN];
   const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
-  constexpr int GROUP_M = 8;
+  const int GROUP_M = g.group_m > 0 ? g.group_m : 8;
   const int x = blockIdx.x;
   const int per_group = GROUP_M * g.tilesN;
   const int first_m = (x / per_group) * GROUP_M;
@@ -709,7 +711,7 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 512 / ((BM / 8) * (BN / 8
   float* As = psm;                   // [ST][BKT][PA]
   float* Bs = psm + ST * BKT * PA;   // [ST][BKT][PB]
   const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
-  constexpr int GROUP_M = 8;
+  const int GROUP_M = g.group_m > 0 ? g.group_m : 8;
   const int x = blockIdx.x;
   const int per_group = GROUP_M * g.tilesN;
   const int first_m = (x / per_group) * GROUP_M;
@@ -1057,6 +1059,20 @@ class GemmRoutine final : public Routine {
     for (auto& v : tCm) v += c0;
     tilesM_ = static_cast<int>(tAm.size());
     tilesN_ = static_cast<int>(tBn.size());
+    {
+      // raster group = SMX parts of the innermost M dim's tile grid: a given
+      // group must divide that grid; the default is its largest divisor <= 8
+      const int64_t gl = gm.empty() ? 1 : gm.back();
+      if (group_ > 0 && gl % group_) return false;
+      if (group_ <= 0) {
+        group_ = 1;
+        for (int q = 8; q >= 1; --q)
+          if (gl % q == 0) {
+            group_ = q;
+            break;
+          }
+      }
+    }
     // vector load / store directions
     if (groups4(ak) && all_mod4(am) && all_mod4(tAm)) amode_ = LD_K4;
     else if (groups4(am) && all_mod4(ak) && all_mod4(tAm)) amode_ = LD_MN4;
@@ -1114,6 +1130,7 @@ class GemmRoutine final : public Routine {
       pbk_ = 0;
       for (int bkt : {32, 16, 8}) {
         if (bkt == 32 && !(BM == 128 && BN == 128)) continue;
+        if (bk_want_ && bkt != bk_want_) continue;  // the configuration's k-tile (SM parts of K)
         if (tile_aff(ak, bkt, psak_) && tile_aff(bk, bkt, psbk_)) {
           pbk_ = bkt;
           break;
@@ -1183,7 +1200,7 @@ class GemmRoutine final : public Routine {
     os << "{\"kernel\": \"" << kname << "\", \"M\": " << M_ << ", \"N\": " << N_
        << ", \"K\": " << K_ << ", \"BK\": " << (pipe_ok() ? pipe_bk() : BK) << ", \"threads\": " << (async_ok() || pipe_ok() ? 256 : (BM_ / 8) * (BN_ / 8)) << ", \"a_load\": \""
        << mn[amode_] << "\", \"b_load\": \"" << mn[bmode_] << "\", \"c_store\": \"" << (cvec_ ? "v4" : "scalar")
-       << "\", \"tiles\": " << static_cast<int64_t>(tilesM_) * tilesN_;
+       << "\", \"tiles\": " << static_cast<int64_t>(tilesM_) * tilesN_ << ", \"raster_group_m\": " << group_;
     if (!note_.empty()) os << ", \"tc_declined\": \"" << note_ << "\"";
     os << "}";
     return os.str();
@@ -1288,7 +1305,7 @@ class GemmRoutine final : public Routine {
       B = static_cast<const float*>(bp_);
     }
     GemmArgs a{A, B, C, tab_[0], tab_[1], tab_[2], tab_[3], tab_[4], tab_[5], tab_[6], tab_[7], tab_[8], tab_[9],
-               static_cast<int>(K_), tilesM_, tilesN_, psak_, psbk_, klin_ ? 1 : 0};
+               static_cast<int>(K_), tilesM_, tilesN_, psak_, psbk_, klin_ ? 1 : 0, group_};
     mark_begin(s);
     dispatch(a, s);
     mark_end(s);
@@ -1297,8 +1314,15 @@ class GemmRoutine final : public Routine {
 
   Config canonical(const Config* given) const;
   bool is_gemv() const { return gemv_; }
+  bool is_skinny() const { return skinny_ || cluster_; }
   bool uses_async() const { return async_ok(); }
   bool uses_pipe() const { return pipe_ok(); }
+  // Table-1 knobs, set before setup(): k-tile (0 = deepest affine) and raster group (0 = default)
+  void set_knobs(int bk, int group) {
+    bk_want_ = bk;
+    group_ = group;
+  }
+  int k_tile() const { return pipe_ok() ? pbk_ : BK; }
 
  private:
   void tables(const std::vector<int64_t>& t0, const std::vector<int64_t>& t1, const std::vector<int64_t>& t2,
@@ -1411,6 +1435,9 @@ class GemmRoutine final : public Routine {
   void* ap_ = nullptr;
   int64_t apack_m_ = 0;
   int psak_ = 0, psbk_ = 0, pbk_ = 0;
+  // Table-1 knobs: k-tile (SM parts of K; 0 = the deepest affine one) and
+  // raster group (SMX parts of the innermost M dim; resolved in setup)
+  int bk_want_ = 0, group_ = 0;
   bool klin_ = false;
   float* part_ = nullptr;
   void* blob_ = nullptr;
@@ -1486,9 +1513,17 @@ Config GemmRoutine::canonical(const Config* given) const {
       L[0][static_cast<size_t>(g_.Md[q])] = e.sizes[static_cast<size_t>(g_.Md[q])] / Tm_[q];
     for (size_t q = 0; q < g_.Nd.size(); ++q)
       L[0][static_cast<size_t>(g_.Nd[q])] = e.sizes[static_cast<size_t>(g_.Nd[q])] / Tn_[q];
+    if (!g_.Md.empty()) {  // raster groups: SMX = rows per group, DM = groups (innermost M dim)
+      const size_t dl = static_cast<size_t>(g_.Md.back());
+      const int64_t gl = L[0][dl];
+      if (group_ > 0 && gl % group_ == 0) {
+        L[0][dl] = group_;
+        L[1][dl] = gl / group_;
+      }
+    }
     place(Tm_, {{5, 4}, {3, BM_ / 8}, {5, 2}}, L, g_.Md, exact);
     place(Tn_, {{5, 4}, {3, BN_ / 8}, {5, 2}}, L, g_.Nd, exact);
-    int64_t bk = BK;
+    int64_t bk = pipe_ok() ? pbk_ : BK;  // the k-tile the instance runs
     for (int q = static_cast<int>(g_.Kd.size()) - 1; q >= 0; --q) {
       int d = g_.Kd[static_cast<size_t>(q)];
       int64_t g = std::gcd(bk, e.sizes[static_cast<size_t>(d)]);
@@ -1607,28 +1642,44 @@ std::unique_ptr<Routine> make_contraction(const Problem& p, const Config* cfg, C
   if (cfg) {
     // instantiate from the configuration's per-dim tile boxes
     auto P = parts_per_asm_layer(*cfg, e, p.m);
-    int smx = p.m.id("SMX"), gpu = p.m.id("GPU");
+    int smx = p.m.id("SMX"), gpu = p.m.id("GPU"), dm = p.m.id("DM"), sml = p.m.id("SM");
     if (smx < 0) fail("Unsupported", "contraction template needs an SMX layer");
+    auto at = [&](int layer, int d) { return layer > 0 ? P[static_cast<size_t>(layer - 1)][static_cast<size_t>(d)] : int64_t(1); };
     std::vector<int64_t> Tm, Tn;
     int64_t bm = 1, bn = 1;
-    for (int d : g.Md) {
-      int64_t grid = P[static_cast<size_t>(smx - 1)][static_cast<size_t>(d)] * (gpu > 0 ? P[static_cast<size_t>(gpu - 1)][static_cast<size_t>(d)] : 1);
+    // tile grid of an M / N dim = its SMX x DM (x GPU) parts; on the
+    // innermost M dim SMX = row tiles per raster group, DM = groups
+    for (size_t q = 0; q < g.Md.size(); ++q) {
+      const int d = g.Md[q];
+      if (q + 1 < g.Md.size() && at(dm, d) != 1) fail("Unsupported", "contraction template: DM parts of an outer M dim must be 1");
+      int64_t grid = at(smx, d) * at(dm, d) * at(gpu, d);
       Tm.push_back(e.sizes[static_cast<size_t>(d)] / grid);
       bm *= Tm.back();
     }
+    const int want_group = g.Md.empty() ? 0 : static_cast<int>(at(smx, g.Md.back()));
     for (int d : g.Nd) {
-      int64_t grid = P[static_cast<size_t>(smx - 1)][static_cast<size_t>(d)] * (gpu > 0 ? P[static_cast<size_t>(gpu - 1)][static_cast<size_t>(d)] : 1);
+      if (at(dm, d) != 1) fail("Unsupported", "contraction template: DM parts of an N dim must be 1");
+      int64_t grid = at(smx, d) * at(gpu, d);
       Tn.push_back(e.sizes[static_cast<size_t>(d)] / grid);
       bn *= Tn.back();
     }
-    for (int d : g.Kd)
-      if (P[static_cast<size_t>(smx - 1)][static_cast<size_t>(d)] != 1) fail("Unsupported", "contraction template does not split K across CTAs");
+    int64_t kt = 1;
+    for (int d : g.Kd) {
+      if (at(smx, d) != 1) fail("Unsupported", "contraction template does not split K across CTAs");
+      kt *= at(sml, d);
+    }
+    // the k-tile = SM parts of K (8, 16 or 32: the pipelined template's ring depth)
+    const int want_bk = kt == 8 || kt == 16 || kt == 32 ? static_cast<int>(kt) : 0;
+    if (!want_bk && kt != 1) fail("Unsupported", "contraction template: k-tile (SM parts of K) must be 8, 16 or 32");
     bool menu = (bm == 128 || bm == 64) && (bn == 128 || bn == 64);
+    r->set_knobs(want_bk, want_group);
     if (g.Nd.empty()) {
       ok = r->setup(0, 0, {}, {});
     } else if (!menu || !(ok = r->setup(static_cast<int>(bm), static_cast<int>(bn), Tm, Tn))) {
-      fail("Unsupported", "contraction template instantiates BM, BN in {64, 128} with K % 8 == 0");
+      fail("Unsupported", "contraction template instantiates BM, BN in {64, 128} with K % 8 == 0, a raster group dividing the row tiles");
     }
+    if (ok && want_bk && r->k_tile() != want_bk)
+      fail("Unsupported", "contraction template: k-tile 16 / 32 needs the pipelined 128-wide instance with affine k offsets");
   } else {
     const bool wide = std::getenv("MDHB_SGEMM_WIDE") != nullptr;
     const bool m64 = std::getenv("MDHB_PIPE_128x64") != nullptr;
@@ -1669,13 +1720,30 @@ std::vector<Config> contraction_space(const Problem& p) {
     out = tc_space(p, g);
     if (!out.empty()) return out;
   }
+  // FFMA instances: tile (BM, BN) x k-tile (SM parts of K: 8 / 16 / 32,
+  // the pipelined template's) x raster group (SMX parts of the innermost M
+  // dim, dividing its row tiles)
   const int menu[4][2] = {{128, 128}, {128, 64}, {64, 128}, {64, 64}};
+  std::set<std::string> seen;
   for (auto& t : menu) {
-    GemmRoutine r(p, g);
-    if (!r.setup(t[0], t[1], {}, {})) continue;
-    Config c = r.canonical(nullptr);
-    if (config_violation(c, p.e, p.m, true).empty()) out.push_back(c);
-    if (r.is_gemv()) break;
+    {
+      GemmRoutine r(p, g);
+      if (!r.setup(t[0], t[1], {}, {})) continue;
+      if (r.is_gemv() || r.is_skinny()) {
+        Config c = r.canonical(nullptr);
+        if (config_violation(c, p.e, p.m, true).empty()) out.push_back(c);
+        break;
+      }
+    }
+    for (int bk : {8, 16, 32})
+      for (int grp : {1, 2, 4, 8, 16, 32, 64}) {
+        GemmRoutine r(p, g);
+        r.set_knobs(bk, grp);
+        if (!r.setup(t[0], t[1], {}, {}) || r.k_tile() != bk) continue;
+        Config c = r.canonical(nullptr);
+        if (!config_violation(c, p.e, p.m, true).empty()) continue;
+        if (seen.insert(config_json(c, p.e, p.m)).second) out.push_back(c);
+      }
   }
   return out;
 }

@@ -115,3 +115,38 @@ def test_resident_b_instances_are_exact(math):
         assert "B_RESIDENT" in t["kernel"] and t["from_config"], t
         (got,) = run_device(mdh.Plan(j, "B200", c, math=math), ins)
         assert np.array_equal(got.astype(np.float64), want), t
+
+
+def layer_parts(c, name, d):
+    """Parts of dim d on the configuration's layer named `name` (num_parts rows
+    follow the configuration's own layer order: ass_de names them)."""
+    D = len(c["num_parts"][0])
+    for l in range(len(c["num_parts"])):
+        if c["ass_de"][l * D][0] == name:
+            return c["num_parts"][l][d]
+    raise KeyError(name)
+
+
+@pytest.mark.gpu
+def test_every_ffma_gemm_instance_is_exact():
+    """The FFMA contraction template's instances: tile x k-tile (SM parts of
+    K: 8 / 16 / 32) x raster group (SMX parts of the innermost M dim), each
+    run from its canonical configuration against the oracle."""
+    from paper_2405_05118_b200 import mdh
+    j = spec("matmul_fp32", [512, 512, 256])
+    comp = mo.Computation.from_json(j)
+    ins = exact_inputs(comp, 7)
+    ((want, _),) = mo.execute(comp, ins)
+    sp = mdh.tune_space(j, "contraction")
+    assert len(sp) >= 20, len(sp)  # 23 at this size; 49 at 8192^3
+    kinds = set()
+    for c in sp:
+        plan = mdh.Plan(j, "B200", c)
+        t = plan.describe()["template"]
+        k_tile = layer_parts(c, "SM", 2)         # SM parts of k
+        group = layer_parts(c, "SMX", 0)         # SMX parts of i
+        assert t["BK"] == k_tile and t["raster_group_m"] == group, (t, c["num_parts"])
+        kinds.add((t["kernel"].split("<")[0], t["BK"], group))
+        (got,) = run_device(plan, ins)
+        assert np.array_equal(got.astype(np.float64), want), t
+    assert {k[0] for k in kinds} >= {"sgemm_pipe", "sgemm_tiled"} and {k[1] for k in kinds} == {8, 16, 32}
