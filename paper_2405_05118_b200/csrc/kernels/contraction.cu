@@ -1683,6 +1683,17 @@ std::unique_ptr<Routine> make_contraction(const Problem& p, const Config* cfg, C
   } else {
     const bool wide = std::getenv("MDHB_SGEMM_WIDE") != nullptr;
     const bool m64 = std::getenv("MDHB_PIPE_128x64") != nullptr;
+    // the pipelined 128 x 64 instance first (4 CTAs of 128 threads per SM:
+    // 18.06 vs 18.65 ms for 128 x 128 at MatMul 8192^3 with FFMA2, equal on
+    // CCSD(T) -- tools/space_sweep.py), then the 128 x 128 menu
+    if (!std::getenv("MDHB_PIPE_128x128")) {
+      auto r64 = std::make_unique<GemmRoutine>(p, g);
+      r64->note_ = tc_why;
+      if (r64->setup(128, 64, {}, {}) && r64->uses_pipe()) {
+        if (cfg_out) *cfg_out = r64->canonical(cfg);
+        return r64;
+      }
+    }
     const int menu[6][2] = {{128, wide ? 256 : 128}, {128, 128}, {m64 ? 128 : 256, 64}, {128, 64}, {64, 128}, {64, 64}};
     for (auto& t : menu) {
       ok = r->setup(t[0], t[1], {}, {});

@@ -13,8 +13,8 @@ SMALL = [
     ("matmul_fp32", [128, 128, 64], "sgemm"),
     ("matmul_fp32", [256, 192, 72], "sgemm"),
     ("matmul_fp32", [64, 64, 8], "sgemm"),
-    ("matmul_fp32", [256, 2048, 96], "sgemm_pipe<128x128,V16,V16"),   # A transposed by the layout pass
-    ("matmul_fp32", [384, 2048, 40], "sgemm_pipe<128x128,V16,V16"),   # BK 8
+    ("matmul_fp32", [256, 2048, 96], "sgemm_pipe<128x64,V16,V16"),    # A transposed by the layout pass
+    ("matmul_fp32", [384, 2048, 40], "sgemm_pipe<128x64,V16,V16"),    # BK 8
     ("mcc_nhwc", [2, 8, 8, 64, 3, 3, 64], "ffma_conv"),
     ("mcc_nhwc", [4, 8, 16, 64, 3, 3, 16], "ffma_conv"),
     ("mcc_nhwc", [3, 10, 16, 64, 3, 3, 24], "ffma_conv"),      # P not a multiple of the 16-row block
