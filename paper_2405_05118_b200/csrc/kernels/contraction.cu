@@ -1063,6 +1063,7 @@ class GemmRoutine final : public Routine {
       // raster group = SMX parts of the innermost M dim's tile grid: a given
       // group must divide that grid; the default is its largest divisor <= 8
       const int64_t gl = gm.empty() ? 1 : gm.back();
+      inner_rows_ = gl;
       if (group_ > 0 && gl % group_) return false;
       if (group_ <= 0) {
         group_ = 1;
@@ -1323,6 +1324,7 @@ class GemmRoutine final : public Routine {
     group_ = group;
   }
   int k_tile() const { return pipe_ok() ? pbk_ : BK; }
+  int64_t inner_row_tiles() const { return inner_rows_; }
 
  private:
   void tables(const std::vector<int64_t>& t0, const std::vector<int64_t>& t1, const std::vector<int64_t>& t2,
@@ -1438,6 +1440,7 @@ class GemmRoutine final : public Routine {
   // Table-1 knobs: k-tile (SM parts of K; 0 = the deepest affine one) and
   // raster group (SMX parts of the innermost M dim; resolved in setup)
   int bk_want_ = 0, group_ = 0;
+  int64_t inner_rows_ = 1;  // row tiles of the innermost M dim
   bool klin_ = false;
   float* part_ = nullptr;
   void* blob_ = nullptr;
@@ -1631,8 +1634,8 @@ std::unique_ptr<Routine> make_contraction(const Problem& p, const Config* cfg, C
   if (p.opt.math != Math::FFMA) {
     auto tc = make_tc_contraction(p, g, cfg, cfg_out, &tc_why);
     if (tc) return tc;
-  } else if (!cfg) {
-    // NHWC convolutions: the patch-reuse FFMA instance (ffma_conv.cu)
+  } else if (!cfg && std::getenv("MDHB_FFMA_CONV")) {
+    // NHWC convolutions: the patch-reuse FFMA instance first (dev aid)
     std::string w;
     if (auto conv = make_ffma_conv(p, g, &w)) return conv;
   }
@@ -1694,6 +1697,14 @@ std::unique_ptr<Routine> make_contraction(const Problem& p, const Config* cfg, C
         return r64;
       }
     }
+    // NHWC convolutions the pipelined implicit GEMM cannot tile (P x Q not
+    // 128-row tiles): the patch-reuse FFMA instance (ffma_conv.cu).  Where
+    // both apply the implicit GEMM is faster since FFMA2 (MCC conv2_x:
+    // 1.133 vs 1.178 ms)
+    if (p.opt.math == Math::FFMA) {
+      std::string w;
+      if (auto conv = make_ffma_conv(p, g, &w)) return conv;
+    }
     const int menu[6][2] = {{128, wide ? 256 : 128}, {128, 128}, {m64 ? 128 : 256, 64}, {128, 64}, {64, 128}, {64, 64}};
     for (auto& t : menu) {
       ok = r->setup(t[0], t[1], {}, {});
@@ -1737,6 +1748,7 @@ std::vector<Config> contraction_space(const Problem& p) {
   const int menu[4][2] = {{128, 128}, {128, 64}, {64, 128}, {64, 64}};
   std::set<std::string> seen;
   for (auto& t : menu) {
+    std::vector<int> groups;
     {
       GemmRoutine r(p, g);
       if (!r.setup(t[0], t[1], {}, {})) continue;
@@ -1745,9 +1757,11 @@ std::vector<Config> contraction_space(const Problem& p) {
         if (config_violation(c, p.e, p.m, true).empty()) out.push_back(c);
         break;
       }
+      for (int64_t q = 1; q <= 64 && q <= r.inner_row_tiles(); ++q)  // divisors of the row tiles
+        if (r.inner_row_tiles() % q == 0) groups.push_back(static_cast<int>(q));
     }
     for (int bk : {8, 16, 32})
-      for (int grp : {1, 2, 4, 8, 16, 32, 64}) {
+      for (int grp : groups) {
         GemmRoutine r(p, g);
         r.set_knobs(bk, grp);
         if (!r.setup(t[0], t[1], {}, {}) || r.k_tile() != bk) continue;

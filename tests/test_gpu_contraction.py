@@ -15,10 +15,10 @@ SMALL = [
     ("matmul_fp32", [64, 64, 8], "sgemm"),
     ("matmul_fp32", [256, 2048, 96], "sgemm_pipe<128x64,V16,V16"),    # A transposed by the layout pass
     ("matmul_fp32", [384, 2048, 40], "sgemm_pipe<128x64,V16,V16"),    # BK 8
-    ("mcc_nhwc", [2, 8, 8, 64, 3, 3, 64], "ffma_conv"),
-    ("mcc_nhwc", [4, 8, 16, 64, 3, 3, 16], "ffma_conv"),
-    ("mcc_nhwc", [3, 10, 16, 64, 3, 3, 24], "ffma_conv"),      # P not a multiple of the 16-row block
-    ("mcc_nhwc", [2, 56, 56, 64, 3, 3, 64], "ffma_conv"),      # conv2_x images, 7 column groups
+    ("mcc_nhwc", [2, 8, 8, 64, 3, 3, 64], "sgemm_pipe<128x64"),   # implicit GEMM (FFMA2)
+    ("mcc_nhwc", [4, 8, 16, 64, 3, 3, 16], "sgemm_pipe<128x64"),
+    ("mcc_nhwc", [3, 10, 16, 64, 3, 3, 24], "ffma_conv"),      # no 128-row tiling of N x P x Q: patch-reuse conv
+    ("mcc_nhwc", [2, 56, 56, 64, 3, 3, 64], "sgemm_pipe<128x64"),  # conv2_x images
     ("ccsdt_abcdef_gdab_efgc", [4, 4, 4, 4, 4, 4, 8], "sgemm"),
     ("ccsdt_abcdef_gdab_efgc", [8, 4, 4, 4, 8, 4, 16], "sgemm"),
     ("matmul_resnet_fc", [16, 1000, 2048], "skinny_cluster<16>"),
@@ -110,16 +110,18 @@ def _full(name, slices):
 
 @pytest.mark.gpu
 def test_mcc_ffma_conv_matches_implicit_gemm(monkeypatch):
-    """The patch-reuse conv instance and the table-driven implicit GEMM it
-    replaces agree bit for bit on exact inputs (and with the oracle)."""
+    """The patch-reuse conv instance and the table-driven implicit GEMM (the
+    default where it tiles) agree bit for bit on exact inputs (and with the
+    oracle)."""
     from paper_2405_05118_b200 import mdh
-    j = spec("mcc_nhwc", [2, 12, 24, 64, 3, 3, 32])
+    j = spec("mcc_nhwc", [2, 8, 8, 64, 3, 3, 64])
     comp = mo.Computation.from_json(j)
     ins = exact_inputs(comp, 9)
+    monkeypatch.setenv("MDHB_FFMA_CONV", "1")
     p = mdh.Plan(j)
     assert "ffma_conv" in p.describe()["template"]["kernel"]
     (a,) = run_device(p, ins)
-    monkeypatch.setenv("MDHB_NO_FFMA_CONV", "1")
+    monkeypatch.delenv("MDHB_FFMA_CONV")
     q = mdh.Plan(j)
     assert "sgemm" in q.describe()["template"]["kernel"]
     (b,) = run_device(q, ins)
