@@ -708,7 +708,7 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
     tc_gemm_2sm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, TcArgs g, int b_row_rank) {
   constexpr int EPW = 4;
   constexpr int NH = WIDE ? 2 : 1;  // N tiles per pair tile
-  static_assert(!WIDE || (BN == 256 && !MC && !B_MN), "WIDE: K-major B, BN 256, no multicast");
+  static_assert(!WIDE || (BN == 256 && !MC), "WIDE: BN 256, no multicast");
   constexpr uint32_t A_BYTES = BM * BKE * 4;
   constexpr uint32_t B_BYTES = (BN / 2) * BKE * 4;  // this CTA's half of one N tile of B
   constexpr uint32_t TMEM_COLS = WIDE ? 512 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
@@ -806,12 +806,19 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
         for (int r = 0; r < MAXR; ++r) c[r] = bn0[r] + kb[r];
         if (B_MN) {  // MN-major B: this CTA's BN/2 columns as 32-column slabs (no layout pass)
 #pragma unroll
-          for (int j = 0; j < BN / 64; ++j) {
-            int cj[MAXR];
+          for (int h = 0; h < NH; ++h) {
+            if (h) {
 #pragma unroll
-            for (int r = 0; r < MAXR; ++r) cj[r] = c[r];
-            cj[0] += 32 * j;
-            tma_load_2sm(sB + s * B_BYTES + j * (BKE * 128), &tma_b, fb, g.b_rank, cj);
+              for (int r = 0; r < MAXR; ++r) c[r] = bn1[r] + kb[r];
+            }
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) {
+              int cj[MAXR];
+#pragma unroll
+              for (int r = 0; r < MAXR; ++r) cj[r] = c[r];
+              cj[0] += 32 * j;
+              tma_load_2sm(sB + (s * NH + h) * B_BYTES + j * (BKE * 128), &tma_b, fb, g.b_rank, cj);
+            }
           }
         } else {
           tma_load_2sm(sB + s * NH * B_BYTES, &tma_b, fb, g.b_rank, c);
@@ -1492,6 +1499,12 @@ class TcRoutine final : public Routine {
       st2_ = 6;
       smem2_ = static_cast<size_t>(st2_) * (BM + BN_ / 2) * BKE * 4 + 1024 + 256 + 4 * (32 * 36 * 4 + 32 * 8);
       two_sm_ = smem2_ <= 227 * 1024;
+      // 256 x 512 pair tiles reading B MN-major (dev aid)
+      wide_ = two_sm_ && tilesN_ % 2 == 0 && (kn_.set ? kn_.bn == 512 : std::getenv("MDHB_TC_WIDE_MN") != nullptr);
+      if (wide_) {
+        st2_ = 4;
+        smem2_ = static_cast<size_t>(st2_) * (BM + BN_) * BKE * 4 + 1024 + 256 + 4 * (32 * 36 * 4 + 32 * 8);
+      }
       return;
     }
     int row_rank = -1;
@@ -1702,7 +1715,8 @@ class TcRoutine final : public Routine {
       lc.attrs = at;
       lc.numAttrs = 1;
       void (*k)(const CUtensorMap, const CUtensorMap, TcArgs, int) =
-          wide_ ? (bf16_ ? tc_gemm_2sm<256, 4, true, false, false, true> : tc_gemm_2sm<256, 4, false, false, false, true>)
+          wide_ ? (bf16_ ? tc_gemm_2sm<256, 4, true, false, false, true>
+                         : vb_.mn ? tc_gemm_2sm<256, 4, false, true, false, true> : tc_gemm_2sm<256, 4, false, false, false, true>)
           : vb_.mn ? tc_gemm_2sm<256, 6, false, true>
           : bf16_ ? (BN_ == 256 ? tc_gemm_2sm<256, 6, true> : tc_gemm_2sm<128, 8, true>)
                   : (BN_ == 256 ? tc_gemm_2sm<256, 6> : tc_gemm_2sm<128, 8>);
@@ -1926,7 +1940,7 @@ std::vector<Config> tc_space(const Problem& p, const Groups& g) {
             Config c = tc_canonical(p, g, k);
             if (config_violation(c, e, p.m, true).empty()) out.push_back(c);
           }
-        if (!bf16 && mn && !tr && ((form == 2 && bn != 256) || bn == 192 || (bn == 64 && form == 1))) continue;  // no MN-major instance
+        if (!bf16 && mn && !tr && ((form == 2 && bn != 256 && bn != 512) || bn == 192 || (bn == 64 && form == 1))) continue;  // no MN-major instance
         for (int split : {1, 2, 4}) {
           if ((K / ek) % split) continue;
           std::vector<int64_t> groups;
