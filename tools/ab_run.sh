@@ -1,7 +1,7 @@
-# scratch A/B (development aid): wide CTA-pair TF32 GEMM, K-major B copy vs MN-major B
-MDHB_TC_NO_TRANSPOSE=1 MDHB_TC_WIDE_MN=1 timeout 900 python -m pytest tests/test_gpu_tc.py tests/test_gpu_fullsize.py -m gpu -q -x -k "matmul" 2>&1 | tail -1
+# scratch A/B (development aid): 24-deep k-tiles on the 128x64 FFMA instance
+MDHB_SGEMM_BK24=1 timeout 600 python -m pytest tests/test_gpu_contraction.py tests/test_gpu_fullsize.py -m gpu -q -x -k ccsdt 2>&1 | tail -1
 for i in 1 2; do
-for v in "" "MDHB_TC_NO_TRANSPOSE=1 MDHB_TC_WIDE_MN=1" "MDHB_TC_NO_TRANSPOSE=1"; do
-  echo "M tf32 $v"; env $v timeout 120 python tools/graph_time.py matmul_fp32:tf32 10 2>&1 | tail -1 | cut -c1-110
+for v in "" "MDHB_SGEMM_BK24=1"; do
+  echo "C $v"; env $v timeout 120 python tools/graph_time.py ccsdt_abcdef_gdab_efgc 20 2>&1 | tail -1 | cut -c1-100
 done
 done
