@@ -59,6 +59,10 @@ struct TcArgs {
   // (SMX parts of the K dim: split s starts at ka0 / kb0)
   int group_m;
   int ka0[MAXR], kb0[MAXR];
+  // packed operands whose K is not a multiple of the 128-byte k-tile: the
+  // last k-step lands 32- or 64-byte rows (SWIZZLE_32B / 64B) through the
+  // tail tensor maps instead of a zero-padded 128-byte step (0 = none)
+  int tail_bytes;
 };
 
 template <int BN, int STAGES, bool B_MN>
@@ -349,7 +353,7 @@ __global__ void __launch_bounds__(256) pack_rows(const float* __restrict__ src, 
 #pragma unroll
   for (int rr = ty; rr < 32; rr += 8) {  // write: lanes along k
     const int64_t gr = r0 + rr;
-    if (gr < n_rows) {
+    if (gr < n_rows && k0 + tx < Kp) {
       if constexpr (sizeof(OutT) == 2) dst[gr * Kp + k0 + tx] = __bfloat16_as_ushort(__float2bfloat16_rn(t[tx][rr]));
       else dst[gr * Kp + k0 + tx] = t[tx][rr];
     }
@@ -431,7 +435,8 @@ __global__ void __launch_bounds__(256) convert_kvec_bf16(const float* __restrict
 // shared memory -- MCC's 147 KB filter -- so only A streams from HBM.
 template <int BN, int STAGES, bool B_MN, bool RB, bool BF16 = false>
 __global__ void __launch_bounds__(64 + 32 * epi_warps(RB, BN), 1)
-    tc_gemm_pers(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, TcArgs g) {
+    tc_gemm_pers(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, TcArgs g,
+                 const __grid_constant__ CUtensorMap tma_at, const __grid_constant__ CUtensorMap tma_bt) {
   constexpr uint32_t A_BYTES = BM * BKE * 4;
   constexpr uint32_t B_BYTES = BN * BKE * 4;
   constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
@@ -474,9 +479,15 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps(RB, BN), 1)
       tile_mn(static_cast<int>(blockIdx.x) + j * static_cast<int>(gridDim.x), tm, tn);
     }
   };
+  const int tb = g.tail_bytes;  // bytes per row of the last k-step (0: full 128-byte step)
+  const int nk = g.nk;
   if (threadIdx.x == 0) {
     tc::tma_prefetch(&tma_a);
     tc::tma_prefetch(&tma_b);
+    if (tb) {
+      tc::tma_prefetch(&tma_at);
+      tc::tma_prefetch(&tma_bt);
+    }
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
@@ -522,12 +533,13 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps(RB, BN), 1)
         ka[r] = g.ka0[r];
         kb[r] = g.kb0[r];
       }
-      tc::mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(g.nk) * B_BYTES);
-      for (int kt = 0; kt < g.nk; ++kt) {
+      tc::mbar_arrive_expect_tx(bfull, tb ? static_cast<uint32_t>(nk - 1) * B_BYTES + static_cast<uint32_t>(BN * tb)
+                                          : static_cast<uint32_t>(nk) * B_BYTES);
+      for (int kt = 0; kt < nk; ++kt) {
         int c[MAXR];
 #pragma unroll
         for (int r = 0; r < MAXR; ++r) c[r] = g.b_nc[tn_res * MAXR + r] + kb[r];
-        tc::tma_load(sB + kt * B_BYTES, &tma_b, bfull, g.b_rank, c);
+        tc::tma_load(sB + kt * B_BYTES, tb && kt == nk - 1 ? &tma_bt : &tma_b, bfull, g.b_rank, c);
         kstep(dig, ka, kb);
       }
     }
@@ -545,18 +557,21 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps(RB, BN), 1)
       }
 #pragma unroll
       for (int q = 0; q < MAXKD; ++q) dig[q] = 0;
-      for (int kt = 0; kt < g.nk; ++kt, ++it) {
+      for (int kt = 0; kt < nk; ++kt, ++it) {
         const uint32_t s = it % STAGES;
+        const bool tail = tb && kt == nk - 1;
         if (it >= STAGES) tc::mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
-        tc::mbar_arrive_expect_tx(&full[s], A_BYTES + (RB ? 0u : B_BYTES));
+        tc::mbar_arrive_expect_tx(&full[s], tail ? static_cast<uint32_t>((BM + (RB ? 0 : BN)) * tb) : A_BYTES + (RB ? 0u : B_BYTES));
         int c[MAXR];
 #pragma unroll
         for (int r = 0; r < MAXR; ++r) c[r] = am0[r] + ka[r];
-        tc::tma_load(sA + s * A_BYTES, &tma_a, &full[s], g.a_rank, c);
+        tc::tma_load(sA + s * A_BYTES, tail ? &tma_at : &tma_a, &full[s], g.a_rank, c);
         if (!RB) {
 #pragma unroll
           for (int r = 0; r < MAXR; ++r) c[r] = bn0[r] + kb[r];
-          if (B_MN) {
+          if (tail) {
+            tc::tma_load(sB + s * B_BYTES, &tma_bt, &full[s], g.b_rank, c);
+          } else if (B_MN) {
             for (int j = 0; j < BN / 32; ++j) {
               int cj[MAXR];
 #pragma unroll
@@ -581,17 +596,27 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps(RB, BN), 1)
       if (tl >= 2) tc::mbar_wait_warp(&tempty[acc], ((tl / 2) - 1) & 1);
       tc::tc_fence_after();
       const uint32_t dtm = tmem + acc * BN;
-      for (int kt = 0; kt < g.nk; ++kt, ++it) {
+      for (int kt = 0; kt < nk; ++kt, ++it) {
         const uint32_t s = it % STAGES;
         tc::mbar_wait_warp(&full[s], (it / STAGES) & 1);
         tc::tc_fence_after();
         const uint32_t sa = tc::smem_u32(sA + s * A_BYTES);
         const uint32_t sb = tc::smem_u32(sB + (RB ? static_cast<uint32_t>(kt) : s) * B_BYTES);
+        if (tb && kt == nk - 1) {
+          // tail k-step: 32- / 64-byte swizzled rows (8-row atoms of 8 x tb bytes)
+          const uint32_t lt = tb == 32 ? 6u : 4u;
+          for (int k = 0; k < tb / 32; ++k) {
+            const uint64_t da = tc::umma_desc(sa + k * 32, 16, 8 * tb, lt);
+            const uint64_t db = tc::umma_desc(sb + k * 32, 16, 8 * tb, lt);
+            tc::mma_warp<!BF16>(dtm, da, db, idesc, (kt | k) != 0 ? 1u : 0u);
+          }
+        } else {
 #pragma unroll
         for (int k = 0; k < BKE / 8; ++k) {
           const uint64_t da = tc::sw128_desc(sa + k * 32, 16, 1024);
           const uint64_t db = B_MN ? tc::umma_desc(sb + k * 1024, BKE * 128, 512, 1) : tc::sw128_desc(sb + k * 32, 16, 1024);
           tc::mma_warp<!BF16>(dtm, da, db, idesc, (kt | k) != 0 ? 1u : 0u);
+        }
         }
         tc::mma_commit_warp(&empty[s]);
       }
@@ -956,6 +981,7 @@ struct View {
   std::vector<int64_t> row_box;
   bool mn = false;                    // MN-major (slabs of 32 along the inner row dim)
   bool bf16 = false;                  // packed bf16 operand (64 elements per 128-byte row)
+  int swz_bytes = 128;                // row bytes of the swizzle (tail views: 32 / 64)
   int kin = -1;                       // the K dim stepped by 32 per k-tile
   std::vector<std::vector<int64_t>> coef;  // [TMA rank][dim]
   std::vector<int64_t> c0;            // [TMA rank]
@@ -1332,6 +1358,17 @@ class TcRoutine final : public Routine {
     const int ek = bf16_ ? 2 * BKE : BKE;  // elements per 128-byte k-tile row
     const int esz = bf16_ ? 2 : 4;
     Kp_ = (K_ + ek - 1) / ek * ek;
+    // K tail: the last k-step as 32- / 64-byte rows instead of a padded
+    // 128-byte one (persistent one-CTA instances, BN 64 / 192)
+    int tail_bytes = 0;
+    // (TF32: 163-164 vs 166 us on CCSD(T); BF16 within noise, so opt-in there
+    // with MDHB_TC_KTAIL=1)
+    if (K_ % ek && K_ > ek && (BN == 192 || BN == 64) && !std::getenv("MDHB_TC_NO_KTAIL") && !std::getenv("MDHB_TC_NONPERSISTENT") &&
+        !(kn_.set && kn_.form == 0) && (!bf16_ || std::getenv("MDHB_TC_KTAIL"))) {
+      const int64_t rem = (K_ % ek) * esz;
+      tail_bytes = rem <= 32 ? 32 : rem <= 64 ? 64 : 0;
+      if (tail_bytes) Kp_ = K_ / ek * ek + tail_bytes / esz;
+    }
     if ((M_ + N_) * Kp_ * esz > (int64_t(1) << 30)) return *why = "packed operands exceed 1 GiB", false;
     auto ones = [](size_t n) { return std::vector<int64_t>(n, 1); };
     auto grid_of = [&](const std::vector<int>& dims, const std::vector<int64_t>& T, std::vector<int64_t>& gext) {
@@ -1353,7 +1390,7 @@ class TcRoutine final : public Routine {
     tilesN_ = static_cast<int>(tBn.size());
     BN_ = BN;
     stages_ = BN >= 256 ? 4 : (BN >= 128 ? 6 : 8);
-    nk_ = static_cast<int>(Kp_ / ek);
+    nk_ = static_cast<int>((Kp_ + ek - 1) / ek);
     auto view2 = [&](int buf, int64_t rows_total, int box_rows) {
       View v;
       v.buf = buf;
@@ -1370,6 +1407,14 @@ class TcRoutine final : public Routine {
     };
     va_ = view2(g_.a_buf, M_, BM);
     vb_ = view2(g_.b_buf, N_, BN);
+    tail_ = tail_bytes > 0;
+    args_.tail_bytes = tail_bytes;
+    if (tail_) {
+      vat_ = va_;
+      vbt_ = vb_;
+      vat_.box[0] = vbt_.box[0] = static_cast<cuuint32_t>(tail_bytes / esz);
+      vat_.swz_bytes = vbt_.swz_bytes = tail_bytes;
+    }
     args_.nkd = 1;
     args_.kext[0] = nk_;
     args_.kstep[0] = ek;
@@ -1573,7 +1618,7 @@ class TcRoutine final : public Routine {
       auto pack = [&](const void* src, void* dst, const int32_t* t, const int32_t* r, const int32_t* k, int rows, int64_t n_rows,
                       bool rowfast) {
         if (rowfast) {
-          dim3 g(static_cast<unsigned>(Kp_ / 32), static_cast<unsigned>((n_rows + 31) / 32));
+          dim3 g(static_cast<unsigned>((Kp_ + 31) / 32), static_cast<unsigned>((n_rows + 31) / 32));
           pack_rows<uint16_t><<<g, 256, 0, s>>>(static_cast<const float*>(src), static_cast<uint16_t*>(dst), t, r, k, rows,
                                                  static_cast<int>(K_), static_cast<int>(Kp_), n_rows);
         } else {
@@ -1611,7 +1656,7 @@ class TcRoutine final : public Routine {
       auto pack = [&](const void* src, void* dst, const int32_t* t, const int32_t* r, const int32_t* k, int rows, int64_t n_rows,
                       bool rowfast) {
         if (rowfast && !std::getenv("MDHB_TC_NO_ROWPACK")) {
-          dim3 g(static_cast<unsigned>(Kp_ / 32), static_cast<unsigned>((n_rows + 31) / 32));
+          dim3 g(static_cast<unsigned>((Kp_ + 31) / 32), static_cast<unsigned>((n_rows + 31) / 32));
           pack_rows<float><<<g, 256, 0, s>>>(static_cast<const float*>(src), static_cast<float*>(dst), t, r, k, rows,
                                               static_cast<int>(K_), static_cast<int>(Kp_), n_rows);
         } else {
@@ -1643,10 +1688,12 @@ class TcRoutine final : public Routine {
     }
     if (A != last_a_) {
       encode(mc_ ? vaH_ : va_, A, &ma_);
+      if (tail_) encode(vat_, A, &mat_);
       last_a_ = A;
     }
     if (B != last_b_) {
       encode(vb_, B, &mb_);
+      if (tail_) encode(vbt_, B, &mbt_);
       if (two_sm_) encode(vb2_, B, &mb2_);
       last_b_ = B;
     }
@@ -1731,7 +1778,7 @@ class TcRoutine final : public Routine {
   if (BN_ == BNV && vb_.mn == MN && rb_ == RBV && pstages_ == ST) {                                         \
     auto k = bf16_ ? tc_gemm_pers<BNV, ST, MN, RBV, true> : tc_gemm_pers<BNV, ST, MN, RBV, false>;          \
     MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(psmem_))); \
-    k<<<pgrid, 64 + 32 * epi_warps(RBV, BNV), psmem_, s>>>(ma_, mb_, a);                                              \
+    k<<<pgrid, 64 + 32 * epi_warps(RBV, BNV), psmem_, s>>>(ma_, mb_, a, tail_ ? mat_ : ma_, tail_ ? mbt_ : mb_);                                              \
     MDHB_CUDA(cudaGetLastError());                                                                          \
     return;                                                                                                 \
   }
@@ -1763,7 +1810,9 @@ class TcRoutine final : public Routine {
     CUresult r = encoder()(m, v.bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                            static_cast<cuuint32_t>(v.rank), const_cast<void*>(ptr),
                            v.dims, v.strides + 1, v.box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           v.mn ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                           v.mn ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                           : v.swz_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                           : v.swz_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail("CudaError", "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
@@ -1782,6 +1831,9 @@ class TcRoutine final : public Routine {
   void* blob_ = nullptr;
   TcArgs args_{};
   CUtensorMap ma_{}, mb_{};
+  CUtensorMap mat_{}, mbt_{};  // tail k-step views of packed operands
+  View vat_, vbt_;
+  bool tail_ = false;
   const void* last_a_ = nullptr;
   const void* last_b_ = nullptr;
   bool transposeB_ = false;
