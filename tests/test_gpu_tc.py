@@ -306,3 +306,22 @@ def test_matmul_random_shapes_exact_all_maths(seed):
         plan = mdh.Plan(j, math=math)
         (got,) = run_device(plan, ins)
         assert np.array_equal(got.astype(np.float64)[dfd], want[dfd]), (m, n, k, plan.describe()["template"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("math,kp", [(1, 72), (2, 80)])
+def test_k_tail_step_exact(monkeypatch, math, kp):
+    """K = 72 is not a multiple of the 128-byte k-tile: the packed operands
+    keep K (TF32) or pad to 80 (BF16) and the last k-step lands 32-byte
+    swizzled rows (SWIZZLE_32B TMA boxes, UMMA layout type 6)."""
+    from paper_2405_05118_b200 import mdh
+    monkeypatch.setenv("MDHB_TC_KTAIL", "1")
+    j = spec("ccsdt_abcdef_gdab_efgc", [4, 4, 2, 8, 8, 24, 72])
+    comp = mo.Computation.from_json(j)
+    plan = mdh.Plan(j, math=math)
+    t = plan.describe()["template"]
+    assert t["kernel"].startswith("tc_gemm_pers<192") and t.get("K_padded") == kp, t
+    ins = exact_inputs(comp, 3)
+    (got,) = run_device(plan, ins)
+    ((want, dfd),) = mo.execute(comp, ins)
+    assert np.array_equal(got.astype(np.float64)[dfd], want[dfd])
