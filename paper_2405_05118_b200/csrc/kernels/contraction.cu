@@ -746,9 +746,13 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 512 / ((BM / 8) * (BN / 8
   const int b_dst0 = BV ? (tid / (BN / 4)) * PB + (tid % (BN / 4)) * 4 : (tid % BKT) * PB + tid / BKT;
   constexpr int A_STEP = AV ? (NT / (BM / 4)) * PA : NT / BKT;  // floats between slots p and p+1
   constexpr int B_STEP = BV ? (NT / (BN / 4)) * PB : NT / BKT;
-  const int nk = g.K / BKT;
+  // K = nfull * BKT + ktail: a last, partial k-tile of ktail (a multiple of
+  // 8) rows is filled and folded without padding (CCSD(T): 72 = 4 x 16 + 8)
+  const int nfull = g.K / BKT, ktail = g.K - nfull * BKT;
+  const int nk = nfull + (ktail ? 1 : 0);
   auto issue = [&](int kt) {
     const int s = kt % ST, k0 = kt * BKT;
+    const int kcount = kt < nfull ? BKT : ktail;
     // the k-tile's base: linear in k0 when the offsets are globally affine,
     // else one table read (its latency sits right before the copies)
     const float* abase = A + (g.klin ? static_cast<int64_t>(k0) * g.sak : __ldg(g.ak + k0));
@@ -758,12 +762,14 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 512 / ((BM / 8) * (BN / 8
 #pragma unroll
     for (int p = 0; p < NA; ++p) {
       if (TA % NT && tid + NT * p >= TA) continue;
+      if ((AV ? (tid + NT * p) / (BM / 4) : (tid + NT * p) % BKT) >= kcount) continue;
       if (AV) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(as + p * A_STEP * 4), "l"(abase + a_off[p]));
       else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(as + p * A_STEP * 4), "l"(abase + a_off[p]));
     }
 #pragma unroll
     for (int p = 0; p < NB; ++p) {
       if (TB % NT && tid + NT * p >= TB) continue;
+      if ((BV ? (tid + NT * p) / (BN / 4) : (tid + NT * p) % BKT) >= kcount) continue;
       if (BV) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(bs + p * B_STEP * 4), "l"(bbase + b_off[p]));
       else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(bs + p * B_STEP * 4), "l"(bbase + b_off[p]));
     }
@@ -794,10 +800,12 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 512 / ((BM / 8) * (BN / 8
     fa[0][1] = *reinterpret_cast<const float4*>(as + BM / 2);
     fb[0][0] = *reinterpret_cast<const float4*>(bs);
     fb[0][1] = *reinterpret_cast<const float4*>(bs + BN / 2);
+    const int kcount = kt < nfull ? BKT : ktail;
 #pragma unroll
     for (int k = 0; k < BKT; ++k) {
+      if (BKT > 8 && k == 8 && kcount == 8) break;  // the partial last k-tile
       const int cur = k & 1, nxt = cur ^ 1;
-      if (k + 1 < BKT) {
+      if (k + 1 < BKT && (BKT == 8 || k + 1 != 8 || kcount != 8)) {
         fa[nxt][0] = *reinterpret_cast<const float4*>(as + (k + 1) * PA);
         fa[nxt][1] = *reinterpret_cast<const float4*>(as + (k + 1) * PA + BM / 2);
         fb[nxt][0] = *reinterpret_cast<const float4*>(bs + (k + 1) * PB);
@@ -1120,8 +1128,11 @@ class GemmRoutine final : public Routine {
       // k offsets affine inside every k-tile of the pipe template: the
       // deepest k-tile (32 for 128 x 128 tiles, else 16, else 8) that keeps
       // both operands affine and divides K
+      // a partial last k-tile of 8 (K % bkt == 8) unless a configuration
+      // names the k-tile (its Table-1 form has no partial tiles)
+      const bool ktail_ok = bk_want_ == 0 && !std::getenv("MDHB_SGEMM_NO_KTAIL");
       auto tile_aff = [&](const std::vector<int64_t>& v, int64_t bkt, int& stride) {
-        if (v.size() < 2 || K_ % bkt) return false;
+        if (v.size() < 2 || (K_ % bkt && !(ktail_ok && bkt > 8 && K_ % bkt == 8 && K_ > bkt))) return false;
         const int64_t sd = v[1] - v[0];
         for (size_t k = 0; k < v.size(); ++k)
           if (v[k] != v[k / bkt * bkt] + static_cast<int64_t>(k % bkt) * sd) return false;
