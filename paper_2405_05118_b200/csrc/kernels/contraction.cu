@@ -1697,10 +1697,14 @@ std::unique_ptr<Routine> make_contraction(const Problem& p, const Config* cfg, C
   } else {
     const bool wide = std::getenv("MDHB_SGEMM_WIDE") != nullptr;
     const bool m64 = std::getenv("MDHB_PIPE_128x64") != nullptr;
-    // the pipelined 128 x 64 instance first (4 CTAs of 128 threads per SM:
-    // 18.06 vs 18.65 ms for 128 x 128 at MatMul 8192^3 with FFMA2, equal on
-    // CCSD(T) -- tools/space_sweep.py), then the 128 x 128 menu
-    if (!std::getenv("MDHB_PIPE_128x128")) {
+    // long K: the pipelined 128 x 64 instance first (4 CTAs of 128 threads
+    // per SM: 18.06 vs 18.65 ms for 128 x 128 at MatMul 8192^3 with FFMA2 --
+    // tools/space_sweep.py); short K (a few k-tiles per output tile): the
+    // 128 x 128 menu, whose 32-deep k-tiles amortise the per-tile work
+    // (CCSD(T), K = 72: 525 vs 549 us)
+    int64_t Kall = 1;
+    for (int d : g.Kd) Kall *= e.sizes[static_cast<size_t>(d)];
+    if (!std::getenv("MDHB_PIPE_128x128") && Kall >= 512) {
       auto r64 = std::make_unique<GemmRoutine>(p, g);
       r64->note_ = tc_why;
       if (r64->setup(128, 64, {}, {}) && r64->uses_pipe()) {

@@ -13,10 +13,11 @@ SMALL = [
     ("matmul_fp32", [128, 128, 64], "sgemm"),
     ("matmul_fp32", [256, 192, 72], "sgemm"),
     ("matmul_fp32", [64, 64, 8], "sgemm"),
-    ("matmul_fp32", [256, 2048, 96], "sgemm_pipe<128x64,V16,V16"),    # A transposed by the layout pass
-    ("matmul_fp32", [384, 2048, 40], "sgemm_pipe<128x64,V16,V16"),    # BK 8
+    ("matmul_fp32", [256, 2048, 96], "sgemm_pipe<128x128,V16,V16"),   # A transposed by the layout pass; short K: 128 x 128
+    ("matmul_fp32", [384, 2048, 40], "sgemm_pipe<128x128,V16,V16"),   # K = 32 + a partial k-tile of 8
+    ("matmul_fp32", [256, 1024, 520], "sgemm_pipe<128x64,V16,V16"),   # long K: 128 x 64, 32 x 16 + 8
     ("mcc_nhwc", [2, 8, 8, 64, 3, 3, 64], "sgemm_pipe<128x64"),   # implicit GEMM (FFMA2)
-    ("mcc_nhwc", [4, 8, 16, 64, 3, 3, 16], "sgemm_pipe<128x64"),
+    ("mcc_nhwc", [4, 8, 16, 64, 3, 3, 16], ""),                   # short K: patch-reuse conv or GEMM
     ("mcc_nhwc", [3, 10, 16, 64, 3, 3, 24], "ffma_conv"),      # no 128-row tiling of N x P x Q: patch-reuse conv
     ("mcc_nhwc", [2, 56, 56, 64, 3, 3, 64], "sgemm_pipe<128x64"),  # conv2_x images
     ("ccsdt_abcdef_gdab_efgc", [4, 4, 4, 4, 4, 4, 8], "sgemm"),
