@@ -10,4 +10,4 @@ timeout 1500 compute-sanitizer --tool memcheck --print-limit 10 --error-exitcode
 timeout 1500 compute-sanitizer --tool memcheck --print-limit 10 --error-exitcode 9 python -m pytest \
   tests/test_gpu_dev_layer.py tests/test_gpu_custom_combine.py -x -q -k "not world2 and not full_size"
 timeout 1500 compute-sanitizer --tool memcheck --print-limit 10 --error-exitcode 9 python -m pytest \
-  tests/test_gpu_tuner_space.py -x -q -k "stencil or resident"
+  tests/test_gpu_tuner_space.py -x -q -k "stencil or resident or ffma"
