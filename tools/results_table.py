@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """BASELINE.md section 3's results table from a bench line (bench.py JSON) and
 the CPU table (tools/cpu_table.py JSON).  Usage:
-    python tools/results_table.py profiles/r2h_bench_line.json profiles/r2_cpu_table.json"""
+    python tools/results_table.py profiles/r2i_bench_line.json profiles/r2_cpu_table.json"""
 import json
 import sys
 
