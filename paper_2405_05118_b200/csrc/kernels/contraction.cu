@@ -841,6 +841,142 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 512 / ((BM / 8) * (BN / 8
   }
 }
 
+// sgemm_pipe with a K-contiguous A tile (MCC's implicit im2col: a k-tile is
+// 16 channels of one filter tap, 64 contiguous bytes of the NHWC input per
+// output pixel).  The tile lands row-major [BM][16] through 16-byte copies
+// along k -- 4 per thread per k-tile instead of the 16 transposing 4-byte
+// copies of the S4 form, a quarter of the L1 fill wavefronts -- and the
+// fragments are read as float4 along k (8 rows x 4 k per LDS.128 group, the
+// same LDS count per FFMA as the M-major form).  Rows are 64 bytes with the
+// 16-byte quads XOR-swizzled by (row & 3), and thread rows are interleaved
+// (ty + TY i), so one warp's four row groups read distinct bank quads (no
+// padding: 4 stages keep 4 CTAs per SM).  The k-group loop stays rolled: fully
+// unrolled, ptxas renames the accumulators across groups and pays ~170 MOVs
+// per k-tile.  Accumulation order per output (k ascending, FFMA2 column
+// pairs) is that of sgemm_pipe: bit-identical results.
+template <int BM, int BN, int BKT>
+struct PipeAkSmem {
+  static constexpr int PA = BKT, PB = BN + 4;
+  static constexpr int STAGES = 4;
+  static constexpr int FLOATS = STAGES * (BM * PA + BKT * PB);
+};
+
+template <int BM, int BN, bool BV, bool CVEC, int BKT>
+__global__ void __launch_bounds__((BM / 8) * (BN / 8), 512 / ((BM / 8) * (BN / 8))) sgemm_pipe_ak(GemmArgs g) {
+  constexpr int NT = (BM / 8) * (BN / 8);
+  using SM = PipeAkSmem<BM, BN, BKT>;
+  constexpr int PA = SM::PA, PB = SM::PB, ST = SM::STAGES, TX = BN / 8, TY = BM / 8;
+  static_assert(BKT == 16, "16-deep k-tiles: 4 swizzled quads per row (partial last tile of 8)");
+  extern __shared__ __align__(16) float psm[];
+  float* As = psm;                   // [ST][BM][PA]
+  float* Bs = psm + ST * BM * PA;    // [ST][BKT][PB]
+  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+  const int GROUP_M = g.group_m > 0 ? g.group_m : 8;
+  const int x = blockIdx.x;
+  const int per_group = GROUP_M * g.tilesN;
+  const int first_m = (x / per_group) * GROUP_M;
+  const int gsz = min(g.tilesM - first_m, GROUP_M);
+  const int tm = first_m + (x % per_group) % gsz;
+  const int tn = (x % per_group) / gsz;
+  const float* __restrict__ A = g.A + g.tAm[tm];
+  const float* __restrict__ B = g.B + g.tBn[tn];
+  // A: 16-byte chunk c = tid + NT p -> row c / (BKT/4), k quad c % (BKT/4)
+  constexpr int KQ = BKT / 4, TA = BM * KQ, NA = TA / NT;
+  static_assert(TA % NT == 0, "A chunks per thread");
+  constexpr int TB = BV ? BN * BKT / 4 : BN * BKT, NB = (TB + NT - 1) / NT;
+  int a_off[NA];
+#pragma unroll
+  for (int p = 0; p < NA; ++p) a_off[p] = g.am[(tid + NT * p) / KQ] + ((tid + NT * p) % KQ) * 4;
+  int b_off[NB];
+#pragma unroll
+  for (int p = 0; p < NB; ++p) {
+    const int c = tid + NT * p;
+    const int k = BV ? c / (BN / 4) : c % BKT, n = BV ? (c % (BN / 4)) * 4 : c / BKT;
+    b_off[p] = c < TB ? g.bn[n] + k * g.sbk : 0;
+  }
+  const int b_dst0 = BV ? (tid / (BN / 4)) * PB + (tid % (BN / 4)) * 4 : (tid % BKT) * PB + tid / BKT;
+  constexpr int B_STEP = BV ? (NT / (BN / 4)) * PB : NT / BKT;
+  const int nfull = g.K / BKT, ktail = g.K - nfull * BKT;
+  const int nk = nfull + (ktail ? 1 : 0);
+  auto issue = [&](int kt) {
+    const int s = kt % ST, k0 = kt * BKT;
+    const int kcount = kt < nfull ? BKT : ktail;
+    const float* abase = A + (g.klin ? static_cast<int64_t>(k0) : __ldg(g.ak + k0));
+    const float* bbase = B + (g.klin ? static_cast<int64_t>(k0) * g.sbk : __ldg(g.bk + k0));
+    const uint32_t as = static_cast<uint32_t>(__cvta_generic_to_shared(As + s * BM * PA));
+    const uint32_t bs = static_cast<uint32_t>(__cvta_generic_to_shared(Bs + s * BKT * PB + b_dst0));
+#pragma unroll
+    for (int p = 0; p < NA; ++p) {
+      const int c = tid + NT * p;
+      if ((c % KQ) * 4 >= kcount) continue;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(as + ((c / KQ) * PA + (((c % KQ) ^ ((c / KQ) & 3)) * 4)) * 4),
+                   "l"(abase + a_off[p]));
+    }
+#pragma unroll
+    for (int p = 0; p < NB; ++p) {
+      if (TB % NT && tid + NT * p >= TB) continue;
+      if ((BV ? (tid + NT * p) / (BN / 4) : (tid + NT * p) % BKT) >= kcount) continue;
+      if (BV) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(bs + p * B_STEP * 4), "l"(bbase + b_off[p]));
+      else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(bs + p * B_STEP * 4), "l"(bbase + b_off[p]));
+    }
+  };
+#pragma unroll
+  for (int p = 0; p < ST - 1; ++p) {
+    if (p < nk) issue(p);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  float2 acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
+  for (int kt = 0; kt < nk; ++kt) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(ST - 2) : "memory");
+    __syncthreads();
+    if (kt + ST - 1 < nk) issue(kt + ST - 1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const float* as = As + (kt % ST) * BM * PA + ty * PA;
+    const float* bs = Bs + (kt % ST) * BKT * PB + tx * 4;
+    const int kgroups = (kt < nfull ? BKT : ktail) / 4;
+#pragma unroll 1
+    for (int kg = 0; kg < kgroups; ++kg) {
+      float4 fa[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) fa[i] = *reinterpret_cast<const float4*>(as + i * TY * PA + ((kg ^ (ty & 3)) * 4));
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int k = kg * 4 + kk;
+        const float4 f0 = *reinterpret_cast<const float4*>(bs + k * PB);
+        const float4 f1 = *reinterpret_cast<const float4*>(bs + k * PB + BN / 2);
+        const float2 b[4] = {make_float2(f0.x, f0.y), make_float2(f0.z, f0.w), make_float2(f1.x, f1.y), make_float2(f1.z, f1.w)};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float a = kk == 0 ? fa[i].x : kk == 1 ? fa[i].y : kk == 2 ? fa[i].z : fa[i].w;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = __ffma2_rn(make_float2(a, a), b[j], acc[i][j]);
+        }
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  float* __restrict__ C = g.C + g.tCm[tm] + g.tCn[tn];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    float* crow = C + g.cm[ty + TY * i];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = h * (BN / 2) + tx * 4;
+      if (CVEC) {
+        *reinterpret_cast<float4*>(crow + g.cn[c]) =
+            make_float4(acc[i][h * 2].x, acc[i][h * 2].y, acc[i][h * 2 + 1].x, acc[i][h * 2 + 1].y);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) crow[g.cn[c + j]] = j & 1 ? acc[i][h * 2 + j / 2].y : acc[i][h * 2 + j / 2].x;
+      }
+    }
+  }
+}
+
 // B layout pass: Bp[k][t * BN + c] = B[tBn[t] + bn[c] + bk[k]] (n in N-tile
 // order; consecutive threads walk n).
 __global__ void __launch_bounds__(256) bpack(const float* __restrict__ B, float* __restrict__ Bp, const int32_t* __restrict__ tBn,
@@ -1205,7 +1341,7 @@ class GemmRoutine final : public Routine {
       return os.str();
     }
     const std::string kname = pipe_ok() ? "sgemm_pipe<" + std::to_string(BM_) + "x" + std::to_string(BN_) + "," +
-                                              std::string(pipe_av() ? "V16" : "S4") + "," +
+                                              std::string(pipe_av() ? "V16" : pipe_ak() ? "K16" : "S4") + "," +
                                               (pipe_bv() ? "V16" : "S4") + ",BK" + std::to_string(pipe_bk()) + ">"
                               : (async_ok() ? "sgemm_async<" : "sgemm_tiled<") + std::to_string(BM_) + "," +
                                     std::to_string(BN_) + ">";
@@ -1397,11 +1533,25 @@ class GemmRoutine final : public Routine {
   int pipe_bk() const { return pbk_; }
   bool pipe_av() const { return amode_ == LD_MN4; }
   bool pipe_bv() const { return bmode_ == LD_MN4; }
+  // K-contiguous A tile (16-byte fills along k): A is K4 with unit k stride
+  // inside 16-deep k-tiles (MCC's implicit im2col).  Opt-in (MDHB_PIPE_AK=1):
+  // bit-identical but 1186 vs 1164 us on MCC FFMA N=256 (DESIGN, dead ends)
+  bool pipe_ak() const { return amode_ == LD_K4 && psak_ == 1 && pbk_ == 16 && std::getenv("MDHB_PIPE_AK"); }
   template <int PBM, int PBN, int BKT>
   void dispatch_pipe(const GemmArgs& a, cudaStream_t s) {
     dim3 grid(static_cast<unsigned>(tilesM_ * tilesN_));
     const size_t smem = PipeSmem<PBM, PBN, BKT>::FLOATS * sizeof(float);
     void (*k)(GemmArgs) = nullptr;
+    if constexpr (BKT == 16) {
+      if (pipe_ak()) {
+        const size_t smem_ak = PipeAkSmem<PBM, PBN, 16>::FLOATS * sizeof(float);
+        if (pipe_bv()) k = cvec_ ? sgemm_pipe_ak<PBM, PBN, true, true, 16> : sgemm_pipe_ak<PBM, PBN, true, false, 16>;
+        else k = cvec_ ? sgemm_pipe_ak<PBM, PBN, false, true, 16> : sgemm_pipe_ak<PBM, PBN, false, false, 16>;
+        MDHB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_ak)));
+        k<<<grid, (PBM / 8) * (PBN / 8), smem_ak, s>>>(a);
+        return;
+      }
+    }
 #define MDHB_P(AV, BV, CV) \
   if (pipe_av() == AV && pipe_bv() == BV && cvec_ == CV) k = sgemm_pipe<PBM, PBN, AV, BV, CV, BKT>;
     MDHB_P(true, true, true) MDHB_P(true, true, false) MDHB_P(true, false, true) MDHB_P(true, false, false)

@@ -131,6 +131,33 @@ def test_mcc_ffma_conv_matches_implicit_gemm(monkeypatch):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("sizes", [[2, 8, 8, 64, 3, 3, 64], [1, 16, 8, 64, 1, 1, 40]])
+def test_mcc_k_contiguous_a_tile_bit_identical(monkeypatch, sizes):
+    """The K-contiguous A tile (sgemm_pipe_ak, opt-in) and the S4 form of the
+    implicit GEMM agree bit for bit on U(-1,1) inputs and match the oracle on
+    exact ones; the 1 x 1 filter over C = 40 gives K = 40 = 2 x 16 + 8, the
+    partial last k-tile."""
+    from paper_2405_05118_b200 import mdh
+    j = spec("mcc_nhwc", sizes)
+    comp = mo.Computation.from_json(j)
+    for ins in (exact_inputs(comp, 9), uniform_inputs(comp, 5)):
+        p = mdh.Plan(j)
+        if "sgemm_pipe" not in p.describe()["template"]["kernel"]:
+            pytest.skip(p.describe()["template"]["kernel"])
+        (a,) = run_device(p, ins)
+        monkeypatch.setenv("MDHB_PIPE_AK", "1")
+        q = mdh.Plan(j)
+        assert "K16" in q.describe()["template"]["kernel"]
+        (b,) = run_device(q, ins)
+        monkeypatch.delenv("MDHB_PIPE_AK")
+        assert np.array_equal(a, b)
+    ((want, dfd),) = mo.execute(comp, exact_inputs(comp, 9))
+    monkeypatch.setenv("MDHB_PIPE_AK", "1")  # read at launch
+    (c,) = run_device(q, exact_inputs(comp, 9))
+    assert np.array_equal(c.astype(np.float64)[dfd], want[dfd])
+
+
+@pytest.mark.gpu
 def test_matvec_full_size_exact():
     _full("matvec_fp32", [(0, 4096)])
 
