@@ -349,11 +349,17 @@ __global__ void __launch_bounds__(256) skinny_fold(SkinnyArgs g) {
 // strip's partials in slice order (deterministic, single writer) and resets
 // the counter for the next run.  CTAs that finish early leave at once (no
 // cluster barrier waits on the slowest slice).
-template <int MT, int KS, bool LAST = false, int NW = 32>
+#ifndef MDHB_FC_BISECT
+#define MDHB_FC_BISECT 0  // development bisection builds only (tools/fc_bisect.sh): 1 no FMAs, 2 no cluster fold, 4 no loads
+#endif
+template <int MT, int KS, bool LAST = false, int NW = 32, int MG = 8>
 __global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g) {
-  // NW columns per CTA strip: 256 threads = KQN k-parts x 8 m-groups x NW/4 column quads
-  constexpr int CQN = NW / 4, KQN = 256 / (8 * CQN);
-  constexpr int NSTG = 4, R = MT / 8, SL = KS / NSTG, KQ = SL / KQN, AKQ = SL / 4, AP = KS + 4;
+  // NW columns per CTA strip: 256 threads = KQN k-parts x MG m-groups x NW/4
+  // column quads; thread rows mg + MG i (i < R) -- one warp's MG row groups
+  // read distinct bank quads of the KS + 4 pitch.  MG = 4 (R = 4 rows per
+  // thread) halves the shared-memory wavefronts per FMA against MG = 8.
+  constexpr int CQN = NW / 4, KQN = 256 / (MG * CQN);
+  constexpr int NSTG = 4, R = MT / MG, SL = KS / NSTG, KQ = SL / KQN, AKQ = SL / 4, AP = KS + 4;
   static_assert(KQN >= 1 && KQ % 4 == 0, "k per thread per stage must be a multiple of 4");
   extern __shared__ __align__(16) float sm[];
   float* Bs = sm;                 // [KS][NW]
@@ -361,12 +367,12 @@ __global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g) {
   float* red = As + MT * AP;      // [KQN][MT][NW]   k-part partials
   float* inbox = red + KQN * MT * NW;  // [CS][MT*NW/CS]  slices pushed by the cluster's CTAs
   const int tid = threadIdx.x;
-  const int kq = tid / (8 * CQN), mg = (tid / CQN) % 8, cq = tid % CQN;
+  const int kq = tid / (MG * CQN), mg = (tid / CQN) % MG, cq = tid % CQN;
   const int n0 = blockIdx.x * NW;
   const int kbase = blockIdx.y * KS;
   // every CTA of the cluster must be running before anyone writes into its
   // shared memory: arrive now, wait just before the DSMEM pushes
-  if (!LAST) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  if (!LAST && !(MDHB_FC_BISECT & 2)) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   // ---- issue every stage's copies up front (NSTG commit groups).  k offsets
   // are affine (g.sak == 1, g.sbk per k), so one table read per row / column
   // precedes the copies and nothing serialises the issue on load latency.
@@ -394,28 +400,31 @@ __global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g) {
   for (int s = 0; s < NSTG; ++s) {
 #pragma unroll
     for (int i = 0; i < ACH; ++i)
-      if (tid + 256 * i < MT * AKQ)
+      if (!(MDHB_FC_BISECT & 4) && tid + 256 * i < MT * AKQ)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(As + adst[i] + s * SL))),
                      "l"(asrc[i] + s * SL), "r"(aok[i] ? 16 : 0));
 #pragma unroll
-    for (int k = s * SL + bk0; k < (s + 1) * SL; k += 256 / (NW / 4))
+    for (int k = s * SL + bk0; k < (s + 1) * SL && !(MDHB_FC_BISECT & 4); k += 256 / (NW / 4))
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(Bs + k * NW + bq * 4))),
                    "l"(bsrc + static_cast<int64_t>(k) * g.sbk), "r"(bok ? 16 : 0));
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  float acc[R][4];
+  // column pairs updated by FFMA2 (two fma.rn per instruction, bit-identical
+  // to scalar FFMA): half the FMA instructions
+  float2 acc[R][2];
 #pragma unroll
   for (int i = 0; i < R; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+    for (int j = 0; j < 2; ++j) acc[i][j] = make_float2(0.f, 0.f);
   auto stage = [&](int s) {
+    if (MDHB_FC_BISECT & 1) return;
     const int k0 = s * SL + kq * KQ;
 #pragma unroll
     for (int k = k0; k < k0 + KQ; k += 4) {
       float a[R][4];
 #pragma unroll
       for (int i = 0; i < R; ++i) {
-        const float4 v = *reinterpret_cast<const float4*>(As + (mg * R + i) * AP + k);
+        const float4 v = *reinterpret_cast<const float4*>(As + (mg + MG * i) * AP + k);
         a[i][0] = v.x; a[i][1] = v.y; a[i][2] = v.z; a[i][3] = v.w;
       }
 #pragma unroll
@@ -423,10 +432,8 @@ __global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g) {
         const float4 b = *reinterpret_cast<const float4*>(Bs + (k + kk) * NW + cq * 4);
 #pragma unroll
         for (int i = 0; i < R; ++i) {
-          acc[i][0] = fmaf(a[i][kk], b.x, acc[i][0]);
-          acc[i][1] = fmaf(a[i][kk], b.y, acc[i][1]);
-          acc[i][2] = fmaf(a[i][kk], b.z, acc[i][2]);
-          acc[i][3] = fmaf(a[i][kk], b.w, acc[i][3]);
+          acc[i][0] = __ffma2_rn(make_float2(a[i][kk], a[i][kk]), make_float2(b.x, b.y), acc[i][0]);
+          acc[i][1] = __ffma2_rn(make_float2(a[i][kk], a[i][kk]), make_float2(b.z, b.w), acc[i][1]);
         }
       }
     }
@@ -446,7 +453,7 @@ __global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g) {
   // ---- k-quarters meet in shared memory (fixed order)
 #pragma unroll
   for (int i = 0; i < R; ++i)
-    *reinterpret_cast<float4*>(red + (kq * MT + mg * R + i) * NW + cq * 4) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+    *reinterpret_cast<float4*>(red + (kq * MT + mg + MG * i) * NW + cq * 4) = make_float4(acc[i][0].x, acc[i][0].y, acc[i][1].x, acc[i][1].y);
   __syncthreads();
   if (LAST) {
     // ---- k-slices meet in global memory, the last arrival folds
@@ -478,6 +485,14 @@ __global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g) {
   // cluster; every CTA pushes its partial of o into slot [my rank] of the
   // owner's inbox (remote stores, no round trips), one cluster barrier, then
   // each owner folds its inbox in rank order -- deterministic.
+  if (MDHB_FC_BISECT & 2) {  // no cluster fold (wrong results): slice 0 writes its own partial
+    if (blockIdx.y == 0)
+      for (int o = tid; o < MT * NW; o += 256) {
+        const int m = o / NW, n = n0 + o % NW;
+        if (m < g.M && n < g.N) g.C[g.cm[m] + g.cn[n]] = red[o];
+      }
+    return;
+  }
   uint32_t rank, cs;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(cs));
@@ -1122,6 +1137,8 @@ class GemmRoutine final : public Routine {
           last_ = std::getenv("MDHB_SKINNY_LAST") != nullptr;
           if (const char* f = std::getenv("MDHB_SKINNY_NW")) nw_ = std::atoi(f);
           if (nw_ != 32 && (mt != 16 || last_ || (ks != 128 && ks != 256) || N_ % 4)) nw_ = 32;
+          // 4 m-groups x 4 rows per thread where the k-parts keep whole 4-k steps
+          mg_ = (mt == 16 && nw_ == 32 && ks >= 128 && !std::getenv("MDHB_SKINNY_MG8")) ? 4 : 8;
           if (last_) {  // workspace [strips][splits][mt * 32] + per-strip counters (zeroed once)
             const int64_t strips = (N_ + 31) / 32;
             MDHB_CUDA(cudaMalloc(&lpart_, static_cast<size_t>(strips * cs * mt * 32) * sizeof(float)));
@@ -1325,7 +1342,7 @@ class GemmRoutine final : public Routine {
     if (cluster_) {
       os << "{\"kernel\": \"skinny_cluster<" << (M_ <= 16 ? 16 : 32) << (last_ ? ",last_block>" : ">") << "\", \"M\": " << M_ << ", \"N\": " << N_
          << ", \"K\": " << K_ << ", \"k_per_cta\": " << ks_ << ", \"cluster\": " << splits_
-         << ", \"ctas\": " << (N_ + 31) / 32 * splits_ << ", \"threads\": 256}";
+         << ", \"ctas\": " << (N_ + 31) / 32 * splits_ << ", \"rows_per_thread\": " << (M_ <= 16 ? 16 : 32) / mg_ << ", \"threads\": 256}";
       return os.str();
     }
     if (skinny_) {
@@ -1362,7 +1379,7 @@ class GemmRoutine final : public Routine {
       SkinnyArgs a{A, B, lpart_, C, tab_[0], tab_[1], tab_[2], tab_[3], tab_[4], tab_[5], static_cast<int>(M_),
                    static_cast<int>(N_), static_cast<int>(K_), ks_, splits_, sak_, sbk_, lcnt_};
       const int mt = M_ <= 16 ? 16 : 32;
-      const int nw = nw_, kqn = 256 / (8 * (nw / 4));
+      const int nw = nw_, kqn = 256 / (mg_ * (nw / 4));
       const size_t smem = (static_cast<size_t>(ks_) * nw + static_cast<size_t>(mt) * (ks_ + 4) + (kqn + 1) * mt * nw) * sizeof(float);
       cudaLaunchConfig_t lc = {};
       lc.gridDim = dim3(static_cast<unsigned>((N_ + nw - 1) / nw), static_cast<unsigned>(splits_));
@@ -1381,10 +1398,16 @@ class GemmRoutine final : public Routine {
   if (ks_ == KS)                                                                                             \
     kern = last_ ? (mt == 16 ? skinny_cluster<16, KS, true> : skinny_cluster<32, KS, true>)                  \
                  : (mt == 16 ? skinny_cluster<16, KS> : skinny_cluster<32, KS>);
-      if (nw == 32) {
+#define MDHB_SK4(KS) \
+  if (ks_ == KS) kern = last_ ? skinny_cluster<16, KS, true, 32, 4> : skinny_cluster<16, KS, false, 32, 4>;
+      if (nw == 32 && mg_ == 8) {
         MDHB_SK(64) MDHB_SK(128) MDHB_SK(256) MDHB_SK(512) MDHB_SK(1024)
       }
+      if (nw == 32 && mg_ == 4) {
+        MDHB_SK4(128) MDHB_SK4(256) MDHB_SK4(512) MDHB_SK4(1024)
+      }
 #undef MDHB_SK
+#undef MDHB_SK4
       // wider column strips (longer contiguous B row segments): MT 16 only
       if (nw == 64 && mt == 16) kern = ks_ == 128 ? skinny_cluster<16, 128, false, 64> : ks_ == 256 ? skinny_cluster<16, 256, false, 64> : nullptr;
       if (nw == 128 && mt == 16) kern = ks_ == 128 ? skinny_cluster<16, 128, false, 128> : ks_ == 256 ? skinny_cluster<16, 256, false, 128> : nullptr;
@@ -1584,6 +1607,7 @@ class GemmRoutine final : public Routine {
   float* lpart_ = nullptr;
   int* lcnt_ = nullptr;
   int nw_ = 32;  // skinny_cluster column strip width
+  int mg_ = 8;   // skinny_cluster m-groups (rows per thread = MT / mg_)
   int ks_ = 0, splits_ = 0;
   int64_t sak_ = 0, sbk_ = 0;
   bool tile_affine_ = false;
