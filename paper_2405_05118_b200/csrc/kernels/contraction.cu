@@ -289,6 +289,11 @@ struct SkinnyArgs {
   int splits;
   int64_t sak, sbk;  // affine k strides of A and B (skinny_cluster)
   int* counter;      // per N strip arrival counters (skinny_cluster<..., LAST>)
+  // aff = 1: am[m] = m sam, bn[n] = n sbn, cm[m] = m scm, cn[n] = n scn -- the
+  // offsets are computed, so no table read (an L2 round trip) sits before the
+  // first copy or the last store (skinny_cluster)
+  int64_t sam, sbn, scm, scn;
+  int aff;
 };
 
 template <int MT>
@@ -378,7 +383,7 @@ __global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g) {
   // precedes the copies and nothing serialises the issue on load latency.
   const int bq = tid % (NW / 4), bk0 = tid / (NW / 4);
   const bool bok = n0 + bq * 4 < g.N;
-  const float* bsrc = g.B + (bok ? g.bn[n0 + bq * 4] + static_cast<int64_t>(kbase) * g.sbk : 0);
+  const float* bsrc = g.B + (bok ? (g.aff ? (n0 + bq * 4) * g.sbn : g.bn[n0 + bq * 4]) + static_cast<int64_t>(kbase) * g.sbk : 0);
   constexpr int ACH = (MT * AKQ + 255) / 256;
   const float* asrc[ACH];
   int adst[ACH];
@@ -388,7 +393,7 @@ __global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g) {
     const int c = tid + 256 * i, m = c / AKQ;
     aok[i] = c < MT * AKQ && m < g.M;
     adst[i] = m * AP + (c % AKQ) * 4;
-    asrc[i] = g.A + (aok[i] ? g.am[m] + kbase + (c % AKQ) * 4 : 0);
+    asrc[i] = g.A + (aok[i] ? (g.aff ? m * g.sam : g.am[m]) + kbase + (c % AKQ) * 4 : 0);
   }
   // programmatic dependent launch: everything above touches only plan-owned
   // tables; the operands may be produced by the previous kernel in the
@@ -476,7 +481,7 @@ __global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g) {
       float v = 0.f;
       for (int c = 0; c < static_cast<int>(gridDim.y); ++c) v += __ldcg(strip + c * (MT * NW) + o);
       const int m = o / NW, n = n0 + o % NW;
-      if (m < g.M && n < g.N) g.C[g.cm[m] + g.cn[n]] = v;
+      if (m < g.M && n < g.N) g.C[g.aff ? m * g.scm + n * g.scn : g.cm[m] + g.cn[n]] = v;
     }
     if (tid == 0) g.counter[blockIdx.x] = 0;  // ready for the next run (stream order)
     return;
@@ -489,7 +494,7 @@ __global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g) {
     if (blockIdx.y == 0)
       for (int o = tid; o < MT * NW; o += 256) {
         const int m = o / NW, n = n0 + o % NW;
-        if (m < g.M && n < g.N) g.C[g.cm[m] + g.cn[n]] = red[o];
+        if (m < g.M && n < g.N) g.C[g.aff ? m * g.scm + n * g.scn : g.cm[m] + g.cn[n]] = red[o];
       }
     return;
   }
@@ -514,7 +519,7 @@ __global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g) {
     for (uint32_t c = 0; c < cs; ++c) s += inbox[c * per + t];
     const int o = static_cast<int>(rank) * per + t;
     const int m = o / NW, n = n0 + o % NW;
-    if (m < g.M && n < g.N) g.C[g.cm[m] + g.cn[n]] = s;
+    if (m < g.M && n < g.N) g.C[g.aff ? m * g.scm + n * g.scn : g.cm[m] + g.cn[n]] = s;
   }
 }
 
@@ -1145,6 +1150,16 @@ class GemmRoutine final : public Routine {
             MDHB_CUDA(cudaMalloc(&lcnt_, static_cast<size_t>(strips) * sizeof(int)));
             MDHB_CUDA(cudaMemset(lcnt_, 0, static_cast<size_t>(strips) * sizeof(int)));
           }
+          {  // affine row / column offsets (the dense FC): computed in the kernel
+            auto lin = [](const std::vector<int64_t>& v, int64_t& st) {
+              st = v.size() > 1 ? v[1] - v[0] : 0;
+              for (size_t i = 0; i < v.size(); ++i)
+                if (v[i] != static_cast<int64_t>(i) * st) return false;
+              return true;
+            };
+            saff_[4] = lin(am, saff_[0]) && lin(bn, saff_[1]) && lin(cm, saff_[2]) && lin(cn, saff_[3]) &&
+                       !std::getenv("MDHB_SKINNY_TABLES");
+          }
           tables(am, ak, bk, bn, cm, cn, {}, {}, {}, {});
           return true;
         }
@@ -1377,7 +1392,8 @@ class GemmRoutine final : public Routine {
     float* C = static_cast<float*>(d_out[0]);
     if (cluster_) {
       SkinnyArgs a{A, B, lpart_, C, tab_[0], tab_[1], tab_[2], tab_[3], tab_[4], tab_[5], static_cast<int>(M_),
-                   static_cast<int>(N_), static_cast<int>(K_), ks_, splits_, sak_, sbk_, lcnt_};
+                   static_cast<int>(N_), static_cast<int>(K_), ks_, splits_, sak_, sbk_, lcnt_, saff_[0], saff_[1],
+                   saff_[2], saff_[3], static_cast<int>(saff_[4])};
       const int mt = M_ <= 16 ? 16 : 32;
       const int nw = nw_, kqn = 256 / (mg_ * (nw / 4));
       const size_t smem = (static_cast<size_t>(ks_) * nw + static_cast<size_t>(mt) * (ks_ + 4) + (kqn + 1) * mt * nw) * sizeof(float);
@@ -1608,6 +1624,7 @@ class GemmRoutine final : public Routine {
   int* lcnt_ = nullptr;
   int nw_ = 32;  // skinny_cluster column strip width
   int mg_ = 8;   // skinny_cluster m-groups (rows per thread = MT / mg_)
+  int64_t saff_[5] = {0, 0, 0, 0, 0};  // skinny_cluster: sam, sbn, scm, scn, affine flag
   int ks_ = 0, splits_ = 0;
   int64_t sak_ = 0, sbk_ = 0;
   bool tile_affine_ = false;

@@ -1,4 +1,5 @@
-# FC timing + output hash (development aid)
-python tools/bits_hash.py matmul_resnet_fc; python tools/bits_hash.py matmul_resnet_fc 5 36 512; python tools/bits_hash.py matmul_resnet_fc 24 100 256
-for i in 1 2; do python tools/graph_time.py matmul_resnet_fc 200 2>&1 | tail -1 | cut -c1-60; done
+# FC timing + output hash (development aid): computed offsets vs tables
+python tools/bits_hash.py matmul_resnet_fc; MDHB_SKINNY_TABLES=1 python tools/bits_hash.py matmul_resnet_fc
+for i in 1 2; do python tools/graph_time.py matmul_resnet_fc 200 2>&1 | tail -1 | cut -c1-60;
+MDHB_SKINNY_TABLES=1 python tools/graph_time.py matmul_resnet_fc 200 2>&1 | tail -1 | cut -c1-60; done
 timeout 300 python -m pytest tests -m gpu -q -x -k "fc or resnet or skinny" 2>&1 | tail -2
