@@ -33,6 +33,7 @@
 
 #include "../plan.hpp"
 #include "contraction_common.hpp"
+#include "tc_gemm.cuh"
 
 namespace mdhb {
 namespace {
@@ -279,6 +280,18 @@ __global__ void __launch_bounds__(128) gemv_rows(GemvArgs g) {
 // coalesced along n, the A slice is staged once in shared memory and read
 // as broadcasts.  Partial sums land in a [splits][M][N] scratch and a second
 // pass folds them in fixed split order (deterministic).
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn tensor_map_encoder() {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !p)
+    fail("CudaError", "cuTensorMapEncodeTiled unavailable");
+  return reinterpret_cast<EncodeFn>(p);
+}
+
 struct SkinnyArgs {
   const float* A;
   const float* B;
@@ -357,8 +370,11 @@ __global__ void __launch_bounds__(256) skinny_fold(SkinnyArgs g) {
 #ifndef MDHB_FC_BISECT
 #define MDHB_FC_BISECT 0  // development bisection builds only (tools/fc_bisect.sh): 1 no FMAs, 2 no cluster fold, 4 no loads
 #endif
-template <int MT, int KS, bool LAST = false, int NW = 32, int MG = 8>
-__global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g) {
+// TMAB: the B slice lands by one 2-D TMA tensor copy per stage ({32 columns,
+// KS/4 rows} boxes, zero fill past N) on an mbarrier instead of 8 16-byte
+// cp.async per thread; A keeps cp.async.
+template <int MT, int KS, bool LAST = false, int NW = 32, int MG = 8, bool TMAB = false>
+__global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g, const __grid_constant__ CUtensorMap tmb) {
   // NW columns per CTA strip: 256 threads = KQN k-parts x MG m-groups x NW/4
   // column quads; thread rows mg + MG i (i < R) -- one warp's MG row groups
   // read distinct bank quads of the KS + 4 pitch.  MG = 4 (R = 4 rows per
@@ -366,7 +382,7 @@ __global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g) {
   constexpr int CQN = NW / 4, KQN = 256 / (MG * CQN);
   constexpr int NSTG = 4, R = MT / MG, SL = KS / NSTG, KQ = SL / KQN, AKQ = SL / 4, AP = KS + 4;
   static_assert(KQN >= 1 && KQ % 4 == 0, "k per thread per stage must be a multiple of 4");
-  extern __shared__ __align__(16) float sm[];
+  extern __shared__ __align__(1024) float sm[];
   float* Bs = sm;                 // [KS][NW]
   float* As = Bs + KS * NW;       // [MT][KS + 4]
   float* red = As + MT * AP;      // [KQN][MT][NW]   k-part partials
@@ -375,6 +391,18 @@ __global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g) {
   const int kq = tid / (MG * CQN), mg = (tid / CQN) % MG, cq = tid % CQN;
   const int n0 = blockIdx.x * NW;
   const int kbase = blockIdx.y * KS;
+  constexpr bool TB = TMAB && !(MDHB_FC_BISECT & 4);
+  // stage barriers after the inbox (dynamic smem: Bs, the TMA destination,
+  // stays at the 1024-byte aligned base -- no static smem shifts it)
+  uint64_t* bbar = reinterpret_cast<uint64_t*>(inbox + MT * NW);
+  if (TB) {
+    if (tid == 0) {
+#pragma unroll
+      for (int s = 0; s < NSTG; ++s) tc::mbar_init(&bbar[s], 1);
+      tc::fence_barrier_init();
+    }
+    __syncthreads();
+  }
   // every CTA of the cluster must be running before anyone writes into its
   // shared memory: arrive now, wait just before the DSMEM pushes
   if (!LAST && !(MDHB_FC_BISECT & 2)) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
@@ -408,8 +436,13 @@ __global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g) {
       if (!(MDHB_FC_BISECT & 4) && tid + 256 * i < MT * AKQ)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(As + adst[i] + s * SL))),
                      "l"(asrc[i] + s * SL), "r"(aok[i] ? 16 : 0));
+    if (TB && tid == 0) {
+      const int c[2] = {n0, kbase + s * SL};
+      tc::mbar_arrive_expect_tx(&bbar[s], SL * NW * 4);
+      tc::tma_load(Bs + s * SL * NW, &tmb, &bbar[s], 2, c);
+    }
 #pragma unroll
-    for (int k = s * SL + bk0; k < (s + 1) * SL && !(MDHB_FC_BISECT & 4); k += 256 / (NW / 4))
+    for (int k = s * SL + bk0; k < (s + 1) * SL && !(MDHB_FC_BISECT & 4) && !TB; k += 256 / (NW / 4))
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(Bs + k * NW + bq * 4))),
                    "l"(bsrc + static_cast<int64_t>(k) * g.sbk), "r"(bok ? 16 : 0));
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -444,15 +477,19 @@ __global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g) {
     }
   };
   asm volatile("cp.async.wait_group 3;" ::: "memory");
+  if (TB) tc::mbar_wait(&bbar[0], 0);
   __syncthreads();
   stage(0);
   asm volatile("cp.async.wait_group 2;" ::: "memory");
+  if (TB) tc::mbar_wait(&bbar[1], 0);
   __syncthreads();
   stage(1);
   asm volatile("cp.async.wait_group 1;" ::: "memory");
+  if (TB) tc::mbar_wait(&bbar[2], 0);
   __syncthreads();
   stage(2);
   asm volatile("cp.async.wait_group 0;" ::: "memory");
+  if (TB) tc::mbar_wait(&bbar[3], 0);
   __syncthreads();
   stage(3);
   // ---- k-quarters meet in shared memory (fixed order)
@@ -1396,7 +1433,8 @@ class GemmRoutine final : public Routine {
                    saff_[2], saff_[3], static_cast<int>(saff_[4])};
       const int mt = M_ <= 16 ? 16 : 32;
       const int nw = nw_, kqn = 256 / (mg_ * (nw / 4));
-      const size_t smem = (static_cast<size_t>(ks_) * nw + static_cast<size_t>(mt) * (ks_ + 4) + (kqn + 1) * mt * nw) * sizeof(float);
+      const size_t smem = (static_cast<size_t>(ks_) * nw + static_cast<size_t>(mt) * (ks_ + 4) + (kqn + 1) * mt * nw) * sizeof(float) +
+                          4 * sizeof(uint64_t);  // + the TMA stage barriers
       cudaLaunchConfig_t lc = {};
       lc.gridDim = dim3(static_cast<unsigned>((N_ + nw - 1) / nw), static_cast<unsigned>(splits_));
       lc.blockDim = dim3(256);
@@ -1409,13 +1447,31 @@ class GemmRoutine final : public Routine {
       at[0].val.clusterDim.z = 1;
       lc.attrs = at;
       lc.numAttrs = last_ ? 0 : 1;  // PDL measured slower for the cluster kernel (6.6 -> 7.7 us)
-      void (*kern)(SkinnyArgs) = nullptr;
+      void (*kern)(SkinnyArgs, CUtensorMap) = nullptr;
+      // B by TMA tensor copies (opt-in MDHB_SKINNY_TMA=1: bit-identical, but
+      // 5.71 vs 5.52 us for the FC -- DESIGN, dead ends): dense FC (affine,
+      // unit column stride, 16-byte row pitch and base), 4 x 4 thread tiles
+      const bool tmab = mg_ == 4 && !last_ && saff_[4] && saff_[1] == 1 && (sbk_ * 4) % 16 == 0 && K_ % ks_ == 0 &&
+                        reinterpret_cast<uintptr_t>(B) % 16 == 0 && std::getenv("MDHB_SKINNY_TMA");
+      if (tmab && B != last_b_) {
+        static EncodeFn enc = tensor_map_encoder();
+        cuuint64_t dims[2] = {static_cast<cuuint64_t>(N_), static_cast<cuuint64_t>(K_)};
+        cuuint64_t strides[1] = {static_cast<cuuint64_t>(sbk_) * 4};
+        cuuint32_t box[2] = {32, static_cast<cuuint32_t>(ks_ / 4)};
+        cuuint32_t es[2] = {1, 1};
+        CUresult r = enc(&tmb_, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(B), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) fail("CudaError", "cuTensorMapEncodeTiled (FC B slice) failed");
+        last_b_ = B;
+      }
 #define MDHB_SK(KS)                                                                                          \
   if (ks_ == KS)                                                                                             \
     kern = last_ ? (mt == 16 ? skinny_cluster<16, KS, true> : skinny_cluster<32, KS, true>)                  \
                  : (mt == 16 ? skinny_cluster<16, KS> : skinny_cluster<32, KS>);
-#define MDHB_SK4(KS) \
-  if (ks_ == KS) kern = last_ ? skinny_cluster<16, KS, true, 32, 4> : skinny_cluster<16, KS, false, 32, 4>;
+#define MDHB_SK4(KS)                                                                                    \
+  if (ks_ == KS) kern = last_ ? skinny_cluster<16, KS, true, 32, 4>                                      \
+                       : tmab ? skinny_cluster<16, KS, false, 32, 4, true> : skinny_cluster<16, KS, false, 32, 4>;
       if (nw == 32 && mg_ == 8) {
         MDHB_SK(64) MDHB_SK(128) MDHB_SK(256) MDHB_SK(512) MDHB_SK(1024)
       }
@@ -1430,7 +1486,7 @@ class GemmRoutine final : public Routine {
       if (!kern) fail("Unsupported", "no skinny_cluster instance for this strip / slice");
       if (smem > 48 * 1024) MDHB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       if (splits_ > 8 && !last_) MDHB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      MDHB_CUDA(cudaLaunchKernelEx(&lc, kern, a));
+      MDHB_CUDA(cudaLaunchKernelEx(&lc, kern, a, tmb_));
       return;
     }
     if (skinny_) {
@@ -1624,6 +1680,8 @@ class GemmRoutine final : public Routine {
   int* lcnt_ = nullptr;
   int nw_ = 32;  // skinny_cluster column strip width
   int mg_ = 8;   // skinny_cluster m-groups (rows per thread = MT / mg_)
+  CUtensorMap tmb_{};           // skinny_cluster: B slice tensor map (TMA), re-encoded when B moves
+  const float* last_b_ = nullptr;
   int64_t saff_[5] = {0, 0, 0, 0, 0};  // skinny_cluster: sam, sbn, scm, scn, affine flag
   int ks_ = 0, splits_ = 0;
   int64_t sak_ = 0, sbk_ = 0;

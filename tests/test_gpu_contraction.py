@@ -158,17 +158,20 @@ def test_mcc_k_contiguous_a_tile_bit_identical(monkeypatch, sizes):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("sizes", [[16, 1000, 2048], [5, 36, 512], [24, 100, 256]])
-def test_fc_table_offsets_equal_computed(monkeypatch, sizes):
-    """skinny_cluster computes affine row / column offsets in the kernel; with
-    MDHB_SKINNY_TABLES=1 it reads the plan's tables: both bit-identical on
-    U(-1,1) inputs, and exact against the oracle on exact ones."""
+@pytest.mark.parametrize("env", ["MDHB_SKINNY_TABLES", "MDHB_SKINNY_TMA"])
+@pytest.mark.parametrize("sizes", [[16, 1000, 2048], [5, 36, 512], [1, 1000, 2048], [24, 100, 256]])
+def test_fc_variants_bit_identical(monkeypatch, sizes, env):
+    """skinny_cluster computes affine row / column offsets in the kernel and
+    loads B by cp.async; with MDHB_SKINNY_TABLES=1 it reads the plan's tables,
+    with MDHB_SKINNY_TMA=1 it loads the B slice by TMA tensor copies (zero
+    fill past N): all bit-identical on U(-1,1) inputs, and exact against the
+    oracle on exact ones."""
     from paper_2405_05118_b200 import mdh
     j = spec("matmul_resnet_fc", sizes)
     comp = mo.Computation.from_json(j)
     ins = uniform_inputs(comp, 4)
     (a,) = run_device(mdh.Plan(j), ins)
-    monkeypatch.setenv("MDHB_SKINNY_TABLES", "1")
+    monkeypatch.setenv(env, "1")
     q = mdh.Plan(j)
     assert "skinny_cluster" in q.describe()["template"]["kernel"]
     (b,) = run_device(q, ins)
