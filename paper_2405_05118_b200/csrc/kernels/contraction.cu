@@ -307,6 +307,11 @@ struct SkinnyArgs {
   // first copy or the last store (skinny_cluster)
   int64_t sam, sbn, scm, scn;
   int aff;
+  // txfold = 1 (opt-in MDHB_SKINNY_TXFOLD=1; 5.68 vs 5.64 us, DESIGN): the
+  // slices' pushes are st.async remote stores that complete bytes on the
+  // owner's mbarrier; each owner waits for its own inbox only (no second
+  // cluster-wide barrier)
+  int txfold;
 };
 
 template <int MT>
@@ -405,7 +410,22 @@ __global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g, const __grid
   }
   // every CTA of the cluster must be running before anyone writes into its
   // shared memory: arrive now, wait just before the DSMEM pushes
-  if (!LAST && !(MDHB_FC_BISECT & 2)) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  uint64_t* fbar = bbar + NSTG;  // txfold: this CTA's inbox barrier
+  if (!LAST && !(MDHB_FC_BISECT & 2)) {
+    if (g.txfold) {
+      if (tid == 0) {
+        uint32_t ncta;
+        asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(ncta));
+        tc::mbar_init(fbar, 1);
+        tc::fence_barrier_init();
+        tc::mbar_arrive_expect_tx(fbar, (MT * NW / ncta) * 4 * ncta);  // every slice pushes per floats
+      }
+      // release: the barrier init is visible to the cluster before any push
+      asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    } else {
+      asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    }
+  }
   // ---- issue every stage's copies up front (NSTG commit groups).  k offsets
   // are affine (g.sak == 1, g.sbk per k), so one table read per row / column
   // precedes the copies and nothing serialises the issue on load latency.
@@ -548,9 +568,21 @@ __global__ void __launch_bounds__(256) skinny_cluster(SkinnyArgs g, const __grid
     const uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(inbox + rank * per + o % per));
     uint32_t remote;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(owner));
-    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote), "f"(v) : "memory");
+    if (g.txfold) {
+      uint32_t rbar;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(tc::smem_u32(fbar)), "r"(owner));
+      asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f32 [%0], %1, [%2];" ::"r"(remote), "f"(v), "r"(rbar)
+                   : "memory");
+    } else {
+      asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote), "f"(v) : "memory");
+    }
   }
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (g.txfold) {
+    if (tid >= per) return;  // the owner's threads wait for its inbox bytes
+    tc::mbar_wait(fbar, 0);
+  } else {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
   for (int t = tid; t < per; t += 256) {
     float s = 0.f;
     for (uint32_t c = 0; c < cs; ++c) s += inbox[c * per + t];
@@ -1430,11 +1462,12 @@ class GemmRoutine final : public Routine {
     if (cluster_) {
       SkinnyArgs a{A, B, lpart_, C, tab_[0], tab_[1], tab_[2], tab_[3], tab_[4], tab_[5], static_cast<int>(M_),
                    static_cast<int>(N_), static_cast<int>(K_), ks_, splits_, sak_, sbk_, lcnt_, saff_[0], saff_[1],
-                   saff_[2], saff_[3], static_cast<int>(saff_[4])};
+                   saff_[2], saff_[3], static_cast<int>(saff_[4]), !last_ && std::getenv("MDHB_SKINNY_TXFOLD") != nullptr};  // opt-in: measured no faster
       const int mt = M_ <= 16 ? 16 : 32;
       const int nw = nw_, kqn = 256 / (mg_ * (nw / 4));
       const size_t smem = (static_cast<size_t>(ks_) * nw + static_cast<size_t>(mt) * (ks_ + 4) + (kqn + 1) * mt * nw) * sizeof(float) +
-                          4 * sizeof(uint64_t);  // + the TMA stage barriers
+                          8 * sizeof(uint64_t) +  // + the TMA stage barriers and the inbox barrier
+                          (std::getenv("MDHB_SKINNY_SMEM_PAD") ? std::atoi(std::getenv("MDHB_SKINNY_SMEM_PAD")) : 0);  // dev aid: fewer CTAs per SM
       cudaLaunchConfig_t lc = {};
       lc.gridDim = dim3(static_cast<unsigned>((N_ + nw - 1) / nw), static_cast<unsigned>(splits_));
       lc.blockDim = dim3(256);

@@ -158,14 +158,15 @@ def test_mcc_k_contiguous_a_tile_bit_identical(monkeypatch, sizes):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("env", ["MDHB_SKINNY_TABLES", "MDHB_SKINNY_TMA"])
+@pytest.mark.parametrize("env", ["MDHB_SKINNY_TABLES", "MDHB_SKINNY_TMA", "MDHB_SKINNY_TXFOLD"])
 @pytest.mark.parametrize("sizes", [[16, 1000, 2048], [5, 36, 512], [1, 1000, 2048], [24, 100, 256]])
 def test_fc_variants_bit_identical(monkeypatch, sizes, env):
     """skinny_cluster computes affine row / column offsets in the kernel and
     loads B by cp.async; with MDHB_SKINNY_TABLES=1 it reads the plan's tables,
     with MDHB_SKINNY_TMA=1 it loads the B slice by TMA tensor copies (zero
-    fill past N): all bit-identical on U(-1,1) inputs, and exact against the
-    oracle on exact ones."""
+    fill past N), with MDHB_SKINNY_TXFOLD=1 the slices meet by st.async pushes
+    on per-owner mbarriers: all bit-identical on U(-1,1) inputs, and exact
+    against the oracle on exact ones."""
     from paper_2405_05118_b200 import mdh
     j = spec("matmul_resnet_fc", sizes)
     comp = mo.Computation.from_json(j)
