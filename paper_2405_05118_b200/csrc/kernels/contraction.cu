@@ -1466,8 +1466,7 @@ class GemmRoutine final : public Routine {
       const int mt = M_ <= 16 ? 16 : 32;
       const int nw = nw_, kqn = 256 / (mg_ * (nw / 4));
       const size_t smem = (static_cast<size_t>(ks_) * nw + static_cast<size_t>(mt) * (ks_ + 4) + (kqn + 1) * mt * nw) * sizeof(float) +
-                          8 * sizeof(uint64_t) +  // + the TMA stage barriers and the inbox barrier
-                          (std::getenv("MDHB_SKINNY_SMEM_PAD") ? std::atoi(std::getenv("MDHB_SKINNY_SMEM_PAD")) : 0);  // dev aid: fewer CTAs per SM
+                          8 * sizeof(uint64_t);  // + the TMA stage barriers and the inbox barrier
       cudaLaunchConfig_t lc = {};
       lc.gridDim = dim3(static_cast<unsigned>((N_ + nw - 1) / nw), static_cast<unsigned>(splits_));
       lc.blockDim = dim3(256);
